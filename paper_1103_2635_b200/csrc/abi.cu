@@ -1,0 +1,423 @@
+// abi.cu -- the extern "C" boundary (include/rbc_b200.h).
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <vector>
+
+#include "common.cuh"
+#include "index.cuh"
+#include "kernels.cuh"
+#include "search.cuh"
+#include "tc_scan.cuh"
+
+namespace rbc {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// per-phase event pairs, recorded on the launching stream when enabled
+struct ProfRec {
+    int phase;
+    cudaEvent_t a, b;
+};
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_prof_open(kNumPhases, nullptr);
+
+void prof_mark(int phase, bool begin, cudaStream_t st) {
+    if (!g_prof_on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    if (begin) {
+        g_prof_open[phase] = e;
+    } else if (g_prof_open[phase]) {
+        g_prof.push_back({phase, g_prof_open[phase], e});
+        g_prof_open[phase] = nullptr;
+    } else {
+        cudaEventDestroy(e);
+    }
+}
+
+int gather_rows(const float *x, const int64_t *ids, int64_t rows, int d, float *out, cudaStream_t st);
+int bernoulli(int64_t n, double p, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *ids_out,
+              int64_t *count_host, cudaStream_t st);
+int build_exact(const float *x, int64_t n, int d, int metric, const int64_t *rep_ids, int64_t nr, int64_t *list_ids,
+                int64_t *offsets, float *list_dists, float *radii, cudaStream_t st);
+int build_one_shot(const float *x, int64_t n, int d, int metric, const int64_t *rep_ids, int64_t nr, int s,
+                   int64_t *lists, float *radii, cudaStream_t st);
+
+static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static int check_common(int64_t n, int d, int metric) {
+    if (metric != RBC_L2 && metric != RBC_L1) return fail(RBC_EINVAL, "metric must be 0 (l2) or 1 (l1)");
+    if (d < 1) return fail(RBC_EINVAL, "dim must be >= 1");
+    if (n < 0 || n > 0xFFFFFFFFll) return fail(RBC_EINVAL, "point count must be in [0, 2^32)");
+    return RBC_OK;
+}
+
+template <typename T>
+static int dalloc(T **p, size_t count, size_t &bytes) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RBC_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    bytes += count * sizeof(T);
+    return RBC_OK;
+}
+
+__global__ void i64_to_i32_kernel(const int64_t *__restrict__ a, int64_t n, int32_t *__restrict__ b) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        b[t] = static_cast<int32_t>(a[t]);
+}
+
+__global__ void gather_rows_i32_kernel(const float *__restrict__ x, const int32_t *__restrict__ ids, int64_t rows,
+                                       int d, float *__restrict__ out) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < rows * d;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[t] = x[static_cast<int64_t>(ids[t / d]) * d + t % d];
+}
+
+// copy list p's segment from the full CSR into the shard CSR
+__global__ void copy_segments_kernel(const int64_t *__restrict__ src_off, const int64_t *__restrict__ dst_off,
+                                     const int64_t *__restrict__ list_ids, const float *__restrict__ list_dists,
+                                     int32_t *__restrict__ perm, float *__restrict__ ldist) {
+    const int64_t p = blockIdx.x;
+    const int64_t len = dst_off[p + 1] - dst_off[p];
+    for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
+        perm[dst_off[p] + j] = static_cast<int32_t>(list_ids[src_off[p] + j]);
+        ldist[dst_off[p] + j] = list_dists[src_off[p] + j];
+    }
+}
+
+static int index_common(rbc_index *idx, const float *x, const int64_t *rep_ids, const float *radii, cudaStream_t st) {
+    RBC_CHECK(dalloc(&idx->x, idx->n * idx->d, idx->bytes));
+    RBC_CHECK(dalloc(&idx->reps, idx->nr * idx->d, idx->bytes));
+    RBC_CHECK(dalloc(&idx->rep_ids, idx->nr, idx->bytes));
+    RBC_CHECK(dalloc(&idx->radii, idx->nr, idx->bytes));
+    RBC_CUDA(cudaMemcpyAsync(idx->x, x, sizeof(float) * idx->n * idx->d, cudaMemcpyDeviceToDevice, st));
+    RBC_CUDA(cudaMemcpyAsync(idx->rep_ids, rep_ids, sizeof(int64_t) * idx->nr, cudaMemcpyDeviceToDevice, st));
+    RBC_CUDA(cudaMemcpyAsync(idx->radii, radii, sizeof(float) * idx->nr, cudaMemcpyDeviceToDevice, st));
+    RBC_CHECK(gather_rows(idx->x, idx->rep_ids, idx->nr, idx->d, idx->reps, st));
+    RBC_CUDA(cudaGetDevice(&idx->device));
+    return RBC_OK;
+}
+
+static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids, int64_t nr,
+                        const int64_t *list_ids, const int64_t *list_offsets, const float *list_dists,
+                        const float *radii, const uint8_t *owned, rbc_index **out, cudaStream_t st) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (nr < 1 || nr > n) return fail(RBC_EINVAL, "n_reps must be in [1, n]");
+    rbc_index *idx = new rbc_index();
+    idx->kind = 0;
+    idx->n = n;
+    idx->d = d;
+    idx->metric = metric;
+    idx->nr = nr;
+    idx->shard = owned != nullptr;
+    int rc = index_common(idx, x, rep_ids, radii, st);
+    std::vector<int64_t> off_full(nr + 1), off_local(nr + 1, 0);
+    if (rc == RBC_OK) rc = dalloc(&idx->offsets, nr + 1, idx->bytes);
+    if (rc == RBC_OK && cudaMemcpyAsync(off_full.data(), list_offsets, sizeof(int64_t) * (nr + 1),
+                                        cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(RBC_ECUDA, "offsets D2H");
+    if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "sync");
+    if (rc == RBC_OK) {
+        for (int64_t p = 0; p < nr; ++p) {
+            const int64_t len = off_full[p + 1] - off_full[p];
+            off_local[p + 1] = off_local[p] + ((owned == nullptr || owned[p]) ? len : 0);
+        }
+        idx->n_local = off_local[nr];
+        rc = dalloc(&idx->perm, idx->n_local, idx->bytes);
+    }
+    if (rc == RBC_OK) rc = dalloc(&idx->list_dists, idx->n_local, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->xp, idx->n_local * d, idx->bytes);
+    if (rc == RBC_OK && cudaMemcpyAsync(idx->offsets, off_local.data(), sizeof(int64_t) * (nr + 1),
+                                        cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = fail(RBC_ECUDA, "offsets H2D");
+    if (rc == RBC_OK) {
+        if (owned == nullptr) {
+            i64_to_i32_kernel<<<grid_for(n, 256, 148 * 64), 256, 0, st>>>(list_ids, n, idx->perm);
+            note_launch();
+            if (cudaMemcpyAsync(idx->list_dists, list_dists, sizeof(float) * n, cudaMemcpyDeviceToDevice, st) !=
+                cudaSuccess)
+                rc = fail(RBC_ECUDA, "list_dists copy");
+        } else {
+            DevBuf<int64_t> src_off;
+            rc = src_off.alloc(nr + 1, st);
+            if (rc == RBC_OK && cudaMemcpyAsync(src_off.get(), list_offsets, sizeof(int64_t) * (nr + 1),
+                                                cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                rc = fail(RBC_ECUDA, "offsets copy");
+            if (rc == RBC_OK) {
+                copy_segments_kernel<<<static_cast<unsigned>(nr), 256, 0, st>>>(src_off.get(), idx->offsets, list_ids,
+                                                                                  list_dists, idx->perm, idx->list_dists);
+                note_launch();
+            }
+        }
+    }
+    if (rc == RBC_OK && idx->n_local > 0) {
+        gather_rows_i32_kernel<<<grid_for(idx->n_local * d, 256, 148 * 64), 256, 0, st>>>(idx->x, idx->perm,
+                                                                                           idx->n_local, d, idx->xp);
+        note_launch();
+    }
+    if (rc == RBC_OK && cudaGetLastError() != cudaSuccess) rc = fail(RBC_ECUDA, "index kernels");
+    if (rc == RBC_OK) rc = tc_index_prepare(idx, st);
+    if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "index sync");
+    if (rc != RBC_OK) {
+        rbc_index_destroy(idx);
+        return rc;
+    }
+    *out = idx;
+    return RBC_OK;
+}
+
+}  // namespace rbc
+
+using namespace rbc;
+
+extern "C" {
+
+const char *rbc_last_error(void) { return g_last_error.c_str(); }
+int rbc_abi_version(void) { return 1; }
+int64_t rbc_launch_count(void) { return g_launches.load(); }
+
+int rbc_profile_enable(int on) {
+    for (auto &r : g_prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    g_prof_on = on != 0;
+    return RBC_OK;
+}
+
+int rbc_profile_read(double *ms, int64_t *count, int32_t n_phases) {
+    for (int p = 0; p < n_phases; ++p) {
+        ms[p] = 0;
+        count[p] = 0;
+    }
+    for (auto &r : g_prof) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return fail(RBC_ECUDA, "profile event");
+        float t = 0;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        if (r.phase < n_phases) {
+            ms[r.phase] += t;
+            count[r.phase] += 1;
+        }
+    }
+    return RBC_OK;
+}
+
+int rbc_pairwise_distances(const float *a, int64_t m, const float *b, int64_t p, int32_t d, int32_t metric,
+                           float *out, void *stream) {
+    RBC_CHECK(check_common(p, d, metric));
+    return pairwise(a, m, b, p, d, metric, out, as_stream(stream));
+}
+
+static int keys_to_output(const uint64_t *keys, int64_t count, int64_t *ids, float *dists, cudaStream_t st) {
+    return unpack_keys(keys, count, ids, dists, nullptr, st);
+}
+
+int rbc_bf_search(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric, int32_t k,
+                  int64_t *ids, float *dists, void *stream) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (k < 1 || k > n) return fail(RBC_EINVAL, "k must be in [1, n]");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<uint64_t> keys;
+    RBC_CHECK(keys.alloc(nq * k, st));
+    RBC_CHECK(bf_search_keys(q, nq, x, n, d, metric, k, keys.get(), st));
+    return keys_to_output(keys.get(), nq * k, ids, dists, st);
+}
+
+int rbc_bf_search_subsets(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric, int32_t k,
+                          const int64_t *subset_ids, const int64_t *subset_offsets, int64_t *ids, float *dists,
+                          void *stream) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (k < 1 || k > kMaxWarpK) return fail(RBC_EINVAL, "subset scan supports 1 <= k <= 64");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<uint64_t> keys;
+    RBC_CHECK(keys.alloc(nq * k, st));
+    IdSrc src{x, subset_ids, subset_offsets, d};
+    RBC_CHECK(launch_topk(q, nq, d, metric, k, src, keys.get(), st));
+    return keys_to_output(keys.get(), nq * k, ids, dists, st);
+}
+
+int rbc_merge_topk(const uint64_t *keys, int32_t parts, int64_t nq, int32_t k_in, int32_t k_out, int64_t *ids,
+                   float *dists, void *stream) {
+    if (parts < 1 || k_in < 1 || k_out < 1 || k_out > parts * k_in) return fail(RBC_EINVAL, "bad merge shape");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<uint64_t> merged;
+    RBC_CHECK(merged.alloc(nq * k_out, st));
+    RBC_CHECK(merge_parts(keys, parts, nq, k_in, k_out, merged.get(), st));
+    return keys_to_output(merged.get(), nq * k_out, ids, dists, st);
+}
+
+int rbc_bernoulli_draw(int64_t n, double p, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                       int64_t *ids_out, int64_t *count_out, void *stream) {
+    if (n < 1) return fail(RBC_EINVAL, "n must be >= 1");
+    return bernoulli(n, p, state_hi, state_lo, inc_hi, inc_lo, ids_out, count_out, as_stream(stream));
+}
+
+int rbc_build_exact(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids, int64_t n_reps,
+                    int64_t *list_ids, int64_t *list_offsets, float *list_dists, float *radii, void *stream) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (n_reps < 1 || n_reps > n) return fail(RBC_EINVAL, "n_reps must be in [1, n]");
+    return build_exact(x, n, d, metric, rep_ids, n_reps, list_ids, list_offsets, list_dists, radii, as_stream(stream));
+}
+
+int rbc_build_one_shot(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids, int64_t n_reps,
+                       int32_t s, int64_t *list_ids, float *radii, void *stream) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (s < 1 || s > n) return fail(RBC_EINVAL, "s must be in [1, n]");
+    if (n_reps < 1) return fail(RBC_EINVAL, "n_reps must be >= 1");
+    return build_one_shot(x, n, d, metric, rep_ids, n_reps, s, list_ids, radii, as_stream(stream));
+}
+
+int rbc_index_exact_create(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids,
+                           int64_t n_reps, const int64_t *list_ids, const int64_t *list_offsets,
+                           const float *list_dists, const float *radii, rbc_index **out, void *stream) {
+    return exact_create(x, n, d, metric, rep_ids, n_reps, list_ids, list_offsets, list_dists, radii, nullptr, out,
+                        as_stream(stream));
+}
+
+int rbc_index_exact_create_shard(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids,
+                                 int64_t n_reps, const int64_t *list_ids, const int64_t *list_offsets,
+                                 const float *list_dists, const float *radii, const uint8_t *owned_mask,
+                                 rbc_index **out, void *stream) {
+    if (!owned_mask) return fail(RBC_EINVAL, "owned_mask is required");
+    return exact_create(x, n, d, metric, rep_ids, n_reps, list_ids, list_offsets, list_dists, radii, owned_mask, out,
+                        as_stream(stream));
+}
+
+int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids,
+                              int64_t n_reps, const int64_t *list_ids, int32_t s, const float *radii, rbc_index **out,
+                              void *stream) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (s < 1 || s > n) return fail(RBC_EINVAL, "s must be in [1, n]");
+    cudaStream_t st = as_stream(stream);
+    rbc_index *idx = new rbc_index();
+    idx->kind = 1;
+    idx->n = n;
+    idx->d = d;
+    idx->metric = metric;
+    idx->nr = n_reps;
+    idx->s = s;
+    int rc = index_common(idx, x, rep_ids, radii, st);
+    if (rc == RBC_OK) rc = dalloc(&idx->lists, n_reps * s, idx->bytes);
+    if (rc == RBC_OK) {
+        i64_to_i32_kernel<<<grid_for(n_reps * s, 256, 148 * 64), 256, 0, st>>>(list_ids, n_reps * s, idx->lists);
+        note_launch();
+        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+            rc = fail(RBC_ECUDA, "one-shot index");
+    }
+    if (rc != RBC_OK) {
+        rbc_index_destroy(idx);
+        return rc;
+    }
+    *out = idx;
+    return RBC_OK;
+}
+
+int rbc_index_destroy(rbc_index *idx) {
+    if (!idx) return RBC_OK;
+    tc_index_release(idx);
+    void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets, idx->perm, idx->list_dists, idx->xp,
+                    idx->lists};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete idx;
+    return RBC_OK;
+}
+
+int64_t rbc_index_device_bytes(const rbc_index *idx) { return idx ? static_cast<int64_t>(idx->bytes) : 0; }
+
+int rbc_exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int32_t k, uint64_t *keys,
+                          rbc_search_stats stats, void *stream) {
+    if (!idx || idx->kind != 0) return fail(RBC_EINVAL, "not an exact index");
+    if (k < 1 || k > idx->nr || k > kMaxWarpK) return fail(RBC_EINVAL, "k must be in [1, min(|R|, 64)]");
+    return exact_search_keys(idx, q, nq, k, keys, stats, as_stream(stream));
+}
+
+int rbc_exact_search(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
+                     rbc_search_stats stats, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    DevBuf<uint64_t> keys;
+    RBC_CHECK(keys.alloc(nq * (k > 0 ? k : 1), st));
+    RBC_CHECK(rbc_exact_search_keys(idx, q, nq, k, keys.get(), stats, stream));
+    return keys_to_output(keys.get(), nq * k, ids, dists, st);
+}
+
+int rbc_one_shot_search(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
+                        float *gamma, void *stream) {
+    if (!idx || idx->kind != 1) return fail(RBC_EINVAL, "not a one-shot index");
+    if (k < 1 || k > idx->s || k > kMaxWarpK) return fail(RBC_EINVAL, "k must be in [1, min(s, 64)]");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<uint64_t> keys;
+    RBC_CHECK(keys.alloc(nq * k, st));
+    RBC_CHECK(one_shot_search_keys(idx, q, nq, k, keys.get(), gamma, st));
+    return keys_to_output(keys.get(), nq * k, ids, dists, st);
+}
+
+// ---- host-buffer (end-to-end) variants ---------------------------------------
+int rbc_exact_search_host(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
+                          rbc_search_stats stats, void *stream) {
+    if (!idx) return fail(RBC_EINVAL, "null index");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<float> dq, ddist, dgamma;
+    DevBuf<int64_t> dids, dcand;
+    DevBuf<int32_t> dpr, dp3;
+    RBC_CHECK(dq.alloc(nq * idx->d, st));
+    RBC_CHECK(dids.alloc(nq * k, st));
+    RBC_CHECK(ddist.alloc(nq * k, st));
+    rbc_search_stats ds{nullptr, nullptr, nullptr, nullptr};
+    if (stats.gamma) { RBC_CHECK(dgamma.alloc(nq, st)); ds.gamma = dgamma.get(); }
+    if (stats.candidates) { RBC_CHECK(dcand.alloc(nq, st)); ds.candidates = dcand.get(); }
+    if (stats.reps_pruned_radius) { RBC_CHECK(dpr.alloc(nq, st)); ds.reps_pruned_radius = dpr.get(); }
+    if (stats.reps_pruned_3gamma) { RBC_CHECK(dp3.alloc(nq, st)); ds.reps_pruned_3gamma = dp3.get(); }
+    RBC_CUDA(cudaMemcpyAsync(dq.get(), q, sizeof(float) * nq * idx->d, cudaMemcpyHostToDevice, st));
+    RBC_CHECK(rbc_exact_search(idx, dq.get(), nq, k, dids.get(), ddist.get(), ds, stream));
+    RBC_CUDA(cudaMemcpyAsync(ids, dids.get(), sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaMemcpyAsync(dists, ddist.get(), sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+    if (stats.gamma) RBC_CUDA(cudaMemcpyAsync(stats.gamma, ds.gamma, sizeof(float) * nq, cudaMemcpyDeviceToHost, st));
+    if (stats.candidates)
+        RBC_CUDA(cudaMemcpyAsync(stats.candidates, ds.candidates, sizeof(int64_t) * nq, cudaMemcpyDeviceToHost, st));
+    if (stats.reps_pruned_radius)
+        RBC_CUDA(cudaMemcpyAsync(stats.reps_pruned_radius, ds.reps_pruned_radius, sizeof(int32_t) * nq,
+                                 cudaMemcpyDeviceToHost, st));
+    if (stats.reps_pruned_3gamma)
+        RBC_CUDA(cudaMemcpyAsync(stats.reps_pruned_3gamma, ds.reps_pruned_3gamma, sizeof(int32_t) * nq,
+                                 cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    return RBC_OK;
+}
+
+int rbc_one_shot_search_host(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
+                             float *gamma, void *stream) {
+    if (!idx) return fail(RBC_EINVAL, "null index");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<float> dq, ddist, dgamma;
+    DevBuf<int64_t> dids;
+    RBC_CHECK(dq.alloc(nq * idx->d, st));
+    RBC_CHECK(dids.alloc(nq * k, st));
+    RBC_CHECK(ddist.alloc(nq * k, st));
+    if (gamma) RBC_CHECK(dgamma.alloc(nq, st));
+    RBC_CUDA(cudaMemcpyAsync(dq.get(), q, sizeof(float) * nq * idx->d, cudaMemcpyHostToDevice, st));
+    RBC_CHECK(rbc_one_shot_search(idx, dq.get(), nq, k, dids.get(), ddist.get(), gamma ? dgamma.get() : nullptr, stream));
+    RBC_CUDA(cudaMemcpyAsync(ids, dids.get(), sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaMemcpyAsync(dists, ddist.get(), sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+    if (gamma) RBC_CUDA(cudaMemcpyAsync(gamma, dgamma.get(), sizeof(float) * nq, cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    return RBC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// index.cuh -- the device-resident RBC index behind the opaque rbc_index.
+#pragma once
+
+#include "common.cuh"
+
+struct rbc_index {
+    int kind = 0;  // 0 = exact (RbcExactIndex), 1 = one-shot (RbcOneShotIndex)
+    int64_t n = 0;
+    int d = 0;
+    int metric = 0;
+    int64_t nr = 0;
+    int s = 0;
+    bool shard = false;
+    int device = 0;
+    size_t bytes = 0;
+
+    float *x = nullptr;        // [n, d] database, point-id order
+    float *reps = nullptr;     // [nr, d] representative rows X[rep_ids]
+    int64_t *rep_ids = nullptr;
+    float *radii = nullptr;    // [nr] list radii psi_r
+
+    // exact: lists in CSR (representative-position order), list-ordered copy
+    int64_t *offsets = nullptr;  // [nr + 1]
+    int32_t *perm = nullptr;     // [n_local] point id of each list entry
+    float *list_dists = nullptr; // [n_local] dist to the owning rep (ascending per list)
+    float *xp = nullptr;         // [n_local, d] X[perm]
+    int64_t n_local = 0;         // entries held (== n unless a shard)
+
+    // tensor-core stage-2 operands (tc_scan.cu): per list, rows centred on
+    // the list's rep, fp16, pre-swizzled for the UMMA shared-memory layout
+    void *tc = nullptr;
+
+    // one-shot: [nr, s] point ids
+    int32_t *lists = nullptr;
+};
+
+namespace rbc {
+int tc_index_prepare(rbc_index *idx, cudaStream_t st);
+void tc_index_release(rbc_index *idx);
+}  // namespace rbc

@@ -1,0 +1,268 @@
+// search.cu -- exact and one-shot RBC search (search.py:90-238).
+//
+// Exact search, per query batch:
+//   stage 1  D1 = dist(Q, R) bit-exact                 (search.py:178)
+//   prune    gamma_k by block radix-select, the fp64 survival predicate,
+//            pruned counts, and per surviving list the 4*gamma_k cutoff by
+//            binary search on the ascending list_dists  (search.py:62-82,181-198)
+//   stage 2  top-k over the surviving list prefixes    (search.py:183-186)
+// The survivor set and cutoffs are computed with exactly the reference's
+// float64 comparisons on the reference's float32 distances, so the candidate
+// set -- and therefore every result and every SearchStats field -- matches.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "index.cuh"
+#include "kernels.cuh"
+#include "search.cuh"
+#include "tc_scan.cuh"
+
+namespace rbc {
+
+// k-th smallest value of a non-negative float row (radix select over the
+// order-preserving bit pattern), computed by the whole block.
+__device__ float block_kth_smallest(const float *__restrict__ row, int64_t nr, int k, unsigned *hist, unsigned *sel) {
+    uint32_t prefix = 0, mask = 0;
+    unsigned kk = static_cast<unsigned>(k);
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+            const uint32_t bits = __float_as_uint(row[p]);
+            if ((bits & mask) == prefix) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // warp scan over the 256 bins, 8 per lane
+            const int lane = threadIdx.x;
+            unsigned local[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                local[j] = hist[lane * 8 + j];
+                tot += local[j];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            unsigned run = incl - tot;
+            const bool mine = run < kk && kk <= incl;
+            if (mine) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (run < kk && kk <= run + local[j]) {
+                        sel[0] = lane * 8 + j;
+                        sel[1] = kk - run;
+                    }
+                    run += local[j];
+                }
+            }
+        }
+        __syncthreads();
+        prefix |= sel[0] << shift;
+        mask |= 255u << shift;
+        kk = sel[1];
+        __syncthreads();
+    }
+    return __uint_as_float(prefix);
+}
+
+// #entries of an ascending f32 list <= thr, compared in f64 (search.py:77-82)
+__device__ __forceinline__ int32_t list_cutoff_dev(const float *__restrict__ l, int32_t m, double thr) {
+    int32_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (static_cast<double>(l[mid]) <= thr) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// search.py:62-74, evaluated in f64 exactly as numpy does
+__device__ __forceinline__ bool survives(float dist, float radius, double g) {
+    const double dd = dist, r = radius;
+    return (dd <= 3.0 * g) && ((dd < __dadd_rn(g, r)) || (dd <= g));
+}
+
+constexpr int kPruneThreads = 256;
+
+// pass 1: gamma_k, stats, number of non-empty surviving segments
+__global__ void __launch_bounds__(kPruneThreads) prune_count_kernel(
+    const float *__restrict__ d1, int64_t nr, int k, const float *__restrict__ radii,
+    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, float *__restrict__ gamma_out,
+    int32_t *__restrict__ nseg_out, int64_t *__restrict__ cand_out, int32_t *__restrict__ pr_out,
+    int32_t *__restrict__ p3_out) {
+    __shared__ unsigned hist[256];
+    __shared__ unsigned sel[2];
+    __shared__ unsigned long long s_cand;
+    __shared__ unsigned s_nseg, s_pr, s_p3;
+    const int64_t i = blockIdx.x;
+    const float *row = d1 + i * nr;
+    if (threadIdx.x == 0) {
+        s_cand = 0;
+        s_nseg = s_pr = s_p3 = 0;
+    }
+    const float gk = block_kth_smallest(row, nr, k, hist, sel);
+    const double g = gk, cut = 4.0 * g;
+    unsigned long long cand = 0;
+    unsigned nseg = 0, pr = 0, p3 = 0;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+        const float dist = row[p];
+        const double dd = dist;
+        pr += (dd >= __dadd_rn(g, static_cast<double>(radii[p])) && dd > g) ? 1u : 0u;  // search.py:194
+        p3 += (dd > 3.0 * g) ? 1u : 0u;                                                  // search.py:195
+        if (survives(dist, radii[p], g)) {
+            const int32_t len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
+            cand += len;
+            nseg += len > 0 ? 1u : 0u;
+        }
+    }
+    atomicAdd(&s_cand, cand);
+    atomicAdd(&s_nseg, nseg);
+    atomicAdd(&s_pr, pr);
+    atomicAdd(&s_p3, p3);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        gamma_out[i] = gk;
+        nseg_out[i] = static_cast<int32_t>(s_nseg);
+        cand_out[i] = static_cast<int64_t>(s_cand);
+        if (pr_out) pr_out[i] = static_cast<int32_t>(s_pr);
+        if (p3_out) p3_out[i] = static_cast<int32_t>(s_p3);
+    }
+}
+
+// pass 2: the surviving segments of query i in ascending rep position
+__global__ void __launch_bounds__(kPruneThreads) prune_fill_kernel(
+    const float *__restrict__ d1, int64_t nr, const float *__restrict__ gamma, const float *__restrict__ radii,
+    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, const int64_t *__restrict__ seg_off,
+    int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list) {
+    typedef cub::BlockScan<int, kPruneThreads> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int64_t base;
+    const int64_t i = blockIdx.x;
+    const float *row = d1 + i * nr;
+    const double g = gamma[i], cut = 4.0 * g;
+    if (threadIdx.x == 0) base = seg_off[i];
+    __syncthreads();
+    for (int64_t p0 = 0; p0 < nr; p0 += kPruneThreads) {
+        const int64_t p = p0 + threadIdx.x;
+        int32_t len = 0;
+        if (p < nr && survives(row[p], radii[p], g))
+            len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
+        int flag = len > 0 ? 1 : 0, pos, total;
+        Scan(scan_tmp).ExclusiveSum(flag, pos, total);
+        if (flag) {
+            seg_start[base + pos] = offsets[p];
+            seg_len[base + pos] = len;
+            if (seg_list) seg_list[base + pos] = static_cast<int32_t>(p);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) base += total;
+        __syncthreads();
+    }
+}
+
+int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &out, cudaStream_t st) {
+    RBC_CHECK(out.gamma.alloc(nq, st));
+    RBC_CHECK(out.nseg.alloc(nq, st));
+    RBC_CHECK(out.cand.alloc(nq, st));
+    RBC_CHECK(out.seg_off.alloc(nq + 1, st));
+    prune_count_kernel<<<static_cast<unsigned>(nq), kPruneThreads, 0, st>>>(
+        d1, idx->nr, k, idx->radii, idx->offsets, idx->list_dists, out.gamma.get(), out.nseg.get(), out.cand.get(),
+        out.pr, out.p3);
+    RBC_LAUNCHED();
+    // seg_off = exclusive scan of nseg (int32 -> int64)
+    RBC_CUDA(cudaMemsetAsync(out.seg_off.get(), 0, sizeof(int64_t), st));
+    size_t tb = 0;
+    cub::TransformInputIterator<int64_t, CastI64, const int32_t *> in(out.nseg.get(), CastI64());
+    cub::DeviceScan::InclusiveSum(nullptr, tb, in, out.seg_off.get() + 1, nq, st);
+    DevBuf<unsigned char> tmp;
+    RBC_CHECK(tmp.alloc(tb, st));
+    RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, in, out.seg_off.get() + 1, nq, st));
+    note_launch();
+    int64_t total = 0;
+    RBC_CUDA(cudaMemcpyAsync(&total, out.seg_off.get() + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    out.total_segs = total;
+    RBC_CHECK(out.seg_start.alloc(total, st));
+    RBC_CHECK(out.seg_len.alloc(total, st));
+    RBC_CHECK(out.seg_list.alloc(total, st));
+    prune_fill_kernel<<<static_cast<unsigned>(nq), kPruneThreads, 0, st>>>(
+        d1, idx->nr, out.gamma.get(), idx->radii, idx->offsets, idx->list_dists, out.seg_off.get(),
+        out.seg_start.get(), out.seg_len.get(), out.seg_list.get());
+    RBC_LAUNCHED();
+    return RBC_OK;
+}
+
+// ---- exact search (search.py:150-208) --------------------------------------
+int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
+                      const rbc_search_stats &stats, cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    // bound the stage-1 block to ~1 GiB per chunk
+    int64_t chunk = (int64_t(1) << 28) / (idx->nr > 0 ? idx->nr : 1);
+    if (chunk < 1) chunk = 1;
+    if (chunk > nq) chunk = nq;
+    DevBuf<float> d1;
+    RBC_CHECK(d1.alloc(chunk * idx->nr, st));
+    for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+        const int64_t m = nq - q0 < chunk ? nq - q0 : chunk;
+        const float *qc = q + q0 * idx->d;
+        {
+            ProfScope ps(kPhaseStage1, st);
+            RBC_CHECK(stage1_distances(idx, qc, m, d1.get(), st));
+        }
+        PruneOut po;
+        po.pr = stats.reps_pruned_radius ? stats.reps_pruned_radius + q0 : nullptr;
+        po.p3 = stats.reps_pruned_3gamma ? stats.reps_pruned_3gamma + q0 : nullptr;
+        {
+            ProfScope ps(kPhasePrune, st);
+            RBC_CHECK(prune(idx, d1.get(), m, k, po, st));
+        }
+        {
+            ProfScope ps(kPhaseStage2, st);
+            RBC_CHECK(stage2_scan(idx, qc, m, k, po, keys + q0 * k, st));
+        }
+        if (stats.gamma)
+            RBC_CUDA(cudaMemcpyAsync(stats.gamma + q0, po.gamma.get(), sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+        if (stats.candidates)
+            RBC_CUDA(cudaMemcpyAsync(stats.candidates + q0, po.cand.get(), sizeof(int64_t) * m,
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    return RBC_OK;
+}
+
+// exact fp64 stage 2 over the surviving segments (fallback / reference path)
+int stage2_exact(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
+                 cudaStream_t st) {
+    SegSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), idx->d};
+    return launch_topk(q, nq, idx->d, idx->metric, k, src, keys, st);
+}
+
+// ---- one-shot search (search.py:90-141) -------------------------------------
+__global__ void argmin_row_kernel(const uint64_t *__restrict__ keys, int64_t nq, int32_t *__restrict__ row,
+                                  float *__restrict__ gamma) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nq) return;
+    const uint64_t key = keys[i];
+    row[i] = static_cast<int32_t>(key_id(key));
+    if (gamma) gamma[i] = key_dist(key);
+}
+
+int one_shot_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, float *gamma,
+                         cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    DevBuf<uint64_t> nearest;
+    DevBuf<int32_t> row;
+    RBC_CHECK(nearest.alloc(nq, st));
+    RBC_CHECK(row.alloc(nq, st));
+    // nearest representative by key64 argmin (lowest position on ties)
+    RBC_CHECK(nearest_rows(q, nq, idx->reps, idx->nr, idx->d, idx->metric, nearest.get(), st));
+    argmin_row_kernel<<<grid_for(nq, 256), 256, 0, st>>>(nearest.get(), nq, row.get(), gamma);
+    RBC_LAUNCHED();
+    RowSrc src{idx->x, idx->lists, row.get(), idx->s, idx->d};
+    return launch_topk(q, nq, idx->d, idx->metric, k, src, keys, st);
+}
+
+}  // namespace rbc

@@ -1,0 +1,35 @@
+// search.cuh -- internal interfaces of the search pipeline.
+#pragma once
+
+#include "common.cuh"
+#include "index.cuh"
+
+namespace rbc {
+
+struct CastI64 {
+    __host__ __device__ __forceinline__ int64_t operator()(const int32_t &v) const { return v; }
+};
+
+// Output of stage 1 + pruning for a query chunk.
+struct PruneOut {
+    DevBuf<float> gamma;       // [nq] gamma_k
+    DevBuf<int32_t> nseg;      // [nq] non-empty surviving segments
+    DevBuf<int64_t> cand;      // [nq] candidates_examined
+    DevBuf<int64_t> seg_off;   // [nq+1] CSR over segments
+    DevBuf<int64_t> seg_start; // [total] first list-order position
+    DevBuf<int32_t> seg_len;   // [total] cutoff length
+    DevBuf<int32_t> seg_list;  // [total] rep position of the segment
+    int64_t total_segs = 0;
+    int32_t *pr = nullptr;     // optional stats outputs (caller memory)
+    int32_t *p3 = nullptr;
+};
+
+int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &out, cudaStream_t st);
+int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
+                      const rbc_search_stats &stats, cudaStream_t st);
+int stage2_exact(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
+                 cudaStream_t st);
+int one_shot_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, float *gamma,
+                         cudaStream_t st);
+
+}  // namespace rbc

@@ -1,0 +1,28 @@
+// tc_scan.cuh -- the filtered distance scans (tensor-core filter + exact
+// fp64 re-rank) that carry the heavy work of every hot call.
+#pragma once
+
+#include "common.cuh"
+#include "index.cuh"
+
+namespace rbc {
+
+struct PruneOut;
+
+// k=1 key64 argmin of every q row over the rows of x (build assignment,
+// one-shot nearest rep, bf_search k=1).  keys[i] = (f32 bits(dist) << 32) | j.
+int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
+                 cudaStream_t st);
+
+// bf_search core: k nearest keys per query row over all of x, sorted.
+int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
+                   cudaStream_t st);
+
+// stage 1 of the searches: bit-exact dist(q_i, r_p) -> d1[nq, nr]
+int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1, cudaStream_t st);
+
+// stage 2 of the exact search over the pruned segments
+int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
+                cudaStream_t st);
+
+}  // namespace rbc

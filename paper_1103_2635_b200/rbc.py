@@ -1,0 +1,283 @@
+"""Random ball cover index: sampling, builds, parameter formulas (reference rbc.py).
+
+Both builds run on the GPU through the C-ABI and return the reference
+dataclasses (``RbcExactIndex`` / ``RbcOneShotIndex``) with host numpy fields,
+plus a device-resident index handle (``index._dev``) that the searches use
+without re-uploading anything.  An index constructed by hand (e.g. from saved
+arrays) is uploaded on first search.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .dataset import DataMatrix
+from .metric import MetricSpec
+
+BERNOULLI = "bernoulli"
+FIXED_COUNT = "fixed-count"
+_MODES = (BERNOULLI, FIXED_COUNT)
+
+
+@dataclass(frozen=True)
+class RepSet:
+    """The sampled representative ids (sorted ascending) and how they were drawn (rbc.py:44-54)."""
+
+    rep_ids: np.ndarray
+    sampling_mode: str
+    seed: int
+
+    @property
+    def size(self) -> int:
+        return len(self.rep_ids)
+
+
+def _pcg64_words(seed: int):
+    """128-bit PCG64 state/increment of numpy's default_rng(seed) (SeedSequence seeding, host)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m = (1 << 64) - 1
+    return s >> 64, s & m, inc >> 64, inc & m
+
+
+def _bernoulli_draw(n: int, p: float, seed: int) -> np.ndarray:
+    """rbc.py:57-59 on the device: ids i with default_rng(seed).random(n)[i] < p."""
+    t = _lib.require_cuda()
+    out = _lib.empty((n,), t.int64)
+    count = ctypes.c_int64(0)
+    _lib.check(_lib.lib.rbc_bernoulli_draw(n, float(p), *_pcg64_words(seed), _lib.ptr(out), ctypes.byref(count),
+                                           _lib.stream_ptr()), "bernoulli draw")
+    return _lib.to_host(out[: count.value])
+
+
+def sample_representatives(n: int, n_r: int, seed: int, mode: str = BERNOULLI) -> RepSet:
+    """Draw the representative set (rbc.py:62-84)."""
+    if not 1 <= n_r <= n:
+        raise ValueError(f"n_r must be in [1, {n}], got {n_r}")
+    if mode not in _MODES:
+        raise ValueError(f"unknown sampling mode {mode!r}; expected one of {_MODES}")
+    if seed < 0:
+        raise ValueError("seed must be non-negative")
+    if mode == BERNOULLI:
+        ids = _bernoulli_draw(n, n_r / n, seed)
+        if ids.size == 0:
+            ids = _bernoulli_draw(n, n_r / n, seed + 1)
+        if ids.size == 0:
+            raise ValueError(f"bernoulli sampling produced an empty set twice (n={n}, n_r={n_r})")
+    else:
+        # O(n_r) host draw without replacement, identical to the reference's generator call
+        rng = np.random.default_rng(seed)
+        ids = np.sort(rng.choice(n, size=n_r, replace=False))
+    return RepSet(np.asarray(ids, dtype=np.int64), mode, seed)
+
+
+class DeviceIndex:
+    """Owner of an rbc_index* handle (device-resident index)."""
+
+    def __init__(self, handle: ctypes.c_void_p, device: int):
+        self.handle = handle
+        self.device = device
+
+    @property
+    def nbytes(self) -> int:
+        return int(_lib.lib.rbc_index_device_bytes(self.handle))
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h is not None and h.value:
+            try:
+                _lib.lib.rbc_index_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
+
+@dataclass
+class RbcExactIndex:
+    """Disjoint ownership partition for exact search (rbc.py:87-115)."""
+
+    data: DataMatrix
+    metric: MetricSpec
+    reps: RepSet
+    list_ids: list[np.ndarray]
+    list_dists: list[np.ndarray]
+    radii: np.ndarray
+
+    @property
+    def rep_points(self) -> np.ndarray:
+        return np.ascontiguousarray(self.data.values[self.reps.rep_ids])
+
+    def owner_positions(self) -> np.ndarray:
+        owner = np.empty(self.data.n, dtype=np.int64)
+        for pos, ids in enumerate(self.list_ids):
+            owner[ids] = pos
+        return owner
+
+    def flat_lists(self):
+        """(list_ids, offsets, list_dists) as flat CSR arrays."""
+        lengths = np.array([len(a) for a in self.list_ids], np.int64)
+        offsets = np.zeros(len(lengths) + 1, np.int64)
+        np.cumsum(lengths, out=offsets[1:])
+        ids = np.concatenate(self.list_ids).astype(np.int64) if len(self.list_ids) else np.empty(0, np.int64)
+        dists = np.concatenate(self.list_dists).astype(np.float32) if len(self.list_dists) else np.empty(0, np.float32)
+        return ids, offsets, dists
+
+
+@dataclass
+class RbcOneShotIndex:
+    """Overlapping fixed-size ownership lists for one-shot search (rbc.py:118-137)."""
+
+    data: DataMatrix
+    metric: MetricSpec
+    reps: RepSet
+    list_ids: np.ndarray
+    s: int
+    radii: np.ndarray
+
+    @property
+    def rep_points(self) -> np.ndarray:
+        return np.ascontiguousarray(self.data.values[self.reps.rep_ids])
+
+
+def _resolve_reps(n: int, n_r: int, seed: int, mode: str, rep_ids) -> RepSet:
+    if rep_ids is not None:
+        ids = np.sort(np.asarray(rep_ids, dtype=np.int64))
+        return RepSet(ids, mode, seed)
+    return sample_representatives(n, n_r, seed, mode)
+
+
+def _split(flat: np.ndarray, offsets: np.ndarray) -> list[np.ndarray]:
+    return [flat[offsets[p]: offsets[p + 1]] for p in range(len(offsets) - 1)]
+
+
+def _create_exact_device(x_dev, n, spec, rep_dev, nr, ids_dev, off_dev, ld_dev, radii_dev, owned=None):
+    handle = ctypes.c_void_p()
+    if owned is None:
+        rc = _lib.lib.rbc_index_exact_create(_lib.ptr(x_dev), n, spec.dim, spec.code, _lib.ptr(rep_dev), nr,
+                                             _lib.ptr(ids_dev), _lib.ptr(off_dev), _lib.ptr(ld_dev),
+                                             _lib.ptr(radii_dev), ctypes.byref(handle), _lib.stream_ptr())
+    else:
+        mask = np.ascontiguousarray(owned, dtype=np.uint8)
+        rc = _lib.lib.rbc_index_exact_create_shard(_lib.ptr(x_dev), n, spec.dim, spec.code, _lib.ptr(rep_dev), nr,
+                                                   _lib.ptr(ids_dev), _lib.ptr(off_dev), _lib.ptr(ld_dev),
+                                                   _lib.ptr(radii_dev), mask.ctypes.data_as(ctypes.c_void_p),
+                                                   ctypes.byref(handle), _lib.stream_ptr())
+    _lib.check(rc, "index create")
+    return DeviceIndex(handle, _lib.torch().cuda.current_device())
+
+
+def build_exact(
+    data: DataMatrix,
+    n_r: int,
+    spec: MetricSpec,
+    seed: int,
+    mode: str = BERNOULLI,
+    rep_ids=None,
+    workers: int | None = None,
+) -> RbcExactIndex:
+    """Build the exact-search index on the GPU (rbc.py:147-180)."""
+    t = _lib.require_cuda()
+    reps = _resolve_reps(data.n, n_r, seed, mode, rep_ids)
+    if data.d != spec.dim:
+        raise ValueError(f"dimension mismatch: data d={data.d}, metric dim={spec.dim}")
+    n, nr = data.n, reps.size
+    x_dev = _lib.to_device(data.values)
+    rep_dev = _lib.to_device(reps.rep_ids)
+    ids_dev = _lib.empty((n,), t.int64)
+    off_dev = _lib.empty((nr + 1,), t.int64)
+    ld_dev = _lib.empty((n,), t.float32)
+    radii_dev = _lib.empty((nr,), t.float32)
+    _lib.check(_lib.lib.rbc_build_exact(_lib.ptr(x_dev), n, spec.dim, spec.code, _lib.ptr(rep_dev), nr,
+                                        _lib.ptr(ids_dev), _lib.ptr(off_dev), _lib.ptr(ld_dev), _lib.ptr(radii_dev),
+                                        _lib.stream_ptr()), "build_exact")
+    dev = _create_exact_device(x_dev, n, spec, rep_dev, nr, ids_dev, off_dev, ld_dev, radii_dev)
+    flat_ids, offsets, flat_d = _lib.to_host(ids_dev), _lib.to_host(off_dev), _lib.to_host(ld_dev)
+    index = RbcExactIndex(data, spec, reps, _split(flat_ids, offsets), _split(flat_d, offsets),
+                          _lib.to_host(radii_dev))
+    index._dev = dev
+    return index
+
+
+def build_one_shot(
+    data: DataMatrix,
+    n_r: int,
+    s: int,
+    spec: MetricSpec,
+    seed: int,
+    mode: str = BERNOULLI,
+    rep_ids=None,
+    workers: int | None = None,
+) -> RbcOneShotIndex:
+    """Build the one-shot index on the GPU (rbc.py:183-200)."""
+    if not 1 <= s <= data.n:
+        raise ValueError(f"s must be in [1, {data.n}], got {s}")
+    t = _lib.require_cuda()
+    reps = _resolve_reps(data.n, n_r, seed, mode, rep_ids)
+    if data.d != spec.dim:
+        raise ValueError(f"dimension mismatch: data d={data.d}, metric dim={spec.dim}")
+    n, nr = data.n, reps.size
+    x_dev = _lib.to_device(data.values)
+    rep_dev = _lib.to_device(reps.rep_ids)
+    lists_dev = _lib.empty((nr, s), t.int64)
+    radii_dev = _lib.empty((nr,), t.float32)
+    _lib.check(_lib.lib.rbc_build_one_shot(_lib.ptr(x_dev), n, spec.dim, spec.code, _lib.ptr(rep_dev), nr, s,
+                                           _lib.ptr(lists_dev), _lib.ptr(radii_dev), _lib.stream_ptr()),
+               "build_one_shot")
+    handle = ctypes.c_void_p()
+    _lib.check(_lib.lib.rbc_index_one_shot_create(_lib.ptr(x_dev), n, spec.dim, spec.code, _lib.ptr(rep_dev), nr,
+                                                  _lib.ptr(lists_dev), s, _lib.ptr(radii_dev), ctypes.byref(handle),
+                                                  _lib.stream_ptr()), "one-shot index")
+    index = RbcOneShotIndex(data, spec, reps, _lib.to_host(lists_dev), s, _lib.to_host(radii_dev))
+    index._dev = DeviceIndex(handle, t.cuda.current_device())
+    return index
+
+
+def device_index(index) -> DeviceIndex:
+    """The index's device handle, uploading a hand-made / loaded index on first use."""
+    t = _lib.require_cuda()
+    dev = getattr(index, "_dev", None)
+    if dev is not None and dev.handle is not None and dev.device == t.cuda.current_device():
+        return dev
+    spec = index.metric
+    x_dev = _lib.to_device(index.data.values)
+    rep_dev = _lib.to_device(index.reps.rep_ids)
+    radii_dev = _lib.to_device(np.asarray(index.radii, np.float32))
+    if isinstance(index, RbcExactIndex):
+        ids, offsets, dists = index.flat_lists()
+        dev = _create_exact_device(x_dev, index.data.n, spec, rep_dev, index.reps.size, _lib.to_device(ids),
+                                   _lib.to_device(offsets), _lib.to_device(dists), radii_dev)
+    else:
+        handle = ctypes.c_void_p()
+        lists_dev = _lib.to_device(np.asarray(index.list_ids, np.int64))
+        _lib.check(_lib.lib.rbc_index_one_shot_create(_lib.ptr(x_dev), index.data.n, spec.dim, spec.code,
+                                                      _lib.ptr(rep_dev), index.reps.size, _lib.ptr(lists_dev),
+                                                      index.s, _lib.ptr(radii_dev), ctypes.byref(handle),
+                                                      _lib.stream_ptr()), "one-shot index")
+        dev = DeviceIndex(handle, t.cuda.current_device())
+    index._dev = dev
+    return dev
+
+
+def standard_params_exact(n: int, c: float) -> int:
+    """Representative count ceil(c^1.5 sqrt(n)) (rbc.py:203-209)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if c < 1:
+        raise ValueError(f"expansion-rate estimate must be >= 1, got {c}")
+    return int(min(n, max(1, math.ceil(c**1.5 * math.sqrt(n)))))
+
+
+def one_shot_params(n: int, c: float, delta: float) -> tuple[int, int]:
+    """n_r = s = ceil(c sqrt(n) sqrt(ln(1/delta))) (rbc.py:212-225)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if c < 1:
+        raise ValueError(f"expansion-rate estimate must be >= 1, got {c}")
+    if not 0 < delta < 1:
+        raise ValueError(f"delta must be in (0, 1), got {delta}")
+    value = int(min(n, max(1, math.ceil(c * math.sqrt(n) * math.sqrt(math.log(1.0 / delta))))))
+    return value, value
