@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 
 import numpy as np
 
@@ -124,7 +125,9 @@ def to_device(a: np.ndarray, dtype=None):
     """Upload a host array through pinned memory."""
     t = require_cuda()
     a = np.ascontiguousarray(a, dtype=dtype)
-    host = t.from_numpy(a)
+    with warnings.catch_warnings():  # read-only DataMatrix values: the tensor is only read
+        warnings.simplefilter("ignore")
+        host = t.from_numpy(a)
     if a.nbytes >= (1 << 20):
         host = host.pin_memory()
     return host.to("cuda", non_blocking=True)

@@ -46,8 +46,9 @@ def prune_representatives(rep_dists: np.ndarray, radii: np.ndarray, gamma_k: flo
         return np.empty(0, np.int64)
     t = _lib.require_cuda()
     mask = _lib.empty((d.size,), t.uint8)
-    _lib.check(_lib.lib.rbc_prune_representatives(_lib.ptr(_lib.to_device(d)), _lib.ptr(_lib.to_device(r)), d.size,
-                                                  float(gamma_k), _lib.ptr(mask), _lib.stream_ptr()), "prune")
+    d_dev, r_dev = _lib.to_device(d), _lib.to_device(r)  # keep alive until the kernel has run
+    _lib.check(_lib.lib.rbc_prune_representatives(_lib.ptr(d_dev), _lib.ptr(r_dev), d.size, float(gamma_k),
+                                                  _lib.ptr(mask), _lib.stream_ptr()), "prune")
     return np.flatnonzero(_lib.to_host(mask))
 
 
@@ -59,7 +60,8 @@ def list_cutoff(sorted_rep_dists: np.ndarray, threshold: float) -> int:
     t = _lib.require_cuda()
     out = _lib.empty((1,), t.int64)
     thr = _lib.to_device(np.array([np.float64(threshold)]))
-    _lib.check(_lib.lib.rbc_list_cutoff(_lib.ptr(_lib.to_device(a)), a.size, _lib.ptr(thr), 1, _lib.ptr(out),
+    a_dev = _lib.to_device(a)
+    _lib.check(_lib.lib.rbc_list_cutoff(_lib.ptr(a_dev), a.size, _lib.ptr(thr), 1, _lib.ptr(out),
                                         _lib.stream_ptr()), "list_cutoff")
     return int(_lib.to_host(out)[0])
 
