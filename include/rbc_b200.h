@@ -69,6 +69,14 @@ int64_t rbc_launch_count(void);
 int rbc_profile_enable(int on);
 int rbc_profile_read(double *ms, int64_t *count, int32_t n_phases);
 
+/* Engine selection for the heavy scans: 0 = auto (tcgen05 filter + exact
+ * fp64 re-rank where supported, the default), 1 = exact fp64 SIMT only.
+ * Both produce identical results; 1 exists for A/B checks. */
+int rbc_set_engine(int mode);
+/* Queries of the last exact search whose candidate buffer overflowed and
+ * were recomputed by the exact SIMT scan (diagnostic). */
+int64_t rbc_stage2_overflows(void);
+
 /* metric.py:57-76 pairwise_distances (and brute_force.py:220-251
  * distance_rows): out[m,p] = dist(a[i], b[j]), bit-exact. */
 int rbc_pairwise_distances(const float *a, int64_t m, const float *b, int64_t p, int32_t d, int32_t metric,
@@ -166,6 +174,11 @@ int rbc_prune_representatives(const double *rep_dists, const double *radii, int6
  * leading entries of the ascending list that are <= thresholds[t]. */
 int rbc_list_cutoff(const double *sorted, int64_t m, const double *thresholds, int64_t n_thresholds, int64_t *out,
                     void *stream);
+
+/* Diagnostic: one 128 x n x 64 f16 tcgen05.mma tile (A [128][64], B [n][64]
+ * row-major f16, device) -> c [128][n] f32, through the same UMMA
+ * descriptor / TMEM path as the stage-2 engine.  n in {16, 32, ..., 256}. */
+int rbc_tc_selftest(const void *a, const void *b, float *c, int32_t n, void *stream);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,9 @@ EXPORTS = {
     "rbc_range_query_host": ([_p, _p, ctypes.c_double, _i64, _p, _p, ctypes.POINTER(_i64), _p], ctypes.c_int),
     "rbc_prune_representatives": ([_p, _p, _i64, ctypes.c_double, _p, _p], ctypes.c_int),
     "rbc_list_cutoff": ([_p, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "rbc_tc_selftest": ([_p, _p, _p, _i32, _p], ctypes.c_int),
+    "rbc_set_engine": ([ctypes.c_int], ctypes.c_int),
+    "rbc_stage2_overflows": ([], _i64),
 }
 for _name, (_args, _res) in EXPORTS.items():
     _sig(_name, _args, _res)

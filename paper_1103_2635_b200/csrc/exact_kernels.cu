@@ -128,6 +128,7 @@ template int launch_topk<AllSrc>(const float *, int64_t, int, int, int, const Al
 template int launch_topk<IdSrc>(const float *, int64_t, int, int, int, const IdSrc &, uint64_t *, cudaStream_t);
 template int launch_topk<SegSrc>(const float *, int64_t, int, int, int, const SegSrc &, uint64_t *, cudaStream_t);
 template int launch_topk<RowSrc>(const float *, int64_t, int, int, int, const RowSrc &, uint64_t *, cudaStream_t);
+template int launch_topk<SegSubSrc>(const float *, int64_t, int, int, int, const SegSubSrc &, uint64_t *, cudaStream_t);
 
 // ---- key64 rows -> (ids, dists) -------------------------------------------
 __global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t count, int64_t *__restrict__ ids,

@@ -75,6 +75,27 @@ struct SegSrc {
     }
 };
 
+// segments of a query subset (overflow fallback of the tensor-core scan):
+// query i of the subset is qmap[i] of the segment CSR
+struct SegSubSrc {
+    const float *xp;
+    const int32_t *perm;
+    const int64_t *seg_start;
+    const int32_t *seg_len;
+    const int64_t *seg_off;
+    const int32_t *qmap;
+    int d;
+    template <class F>
+    __device__ __forceinline__ void for_each(int64_t i, int lane, F &&f) const {
+        const int64_t qi = qmap[i];
+        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) {
+            const int64_t st = seg_start[s];
+            const int32_t len = seg_len[s];
+            for (int32_t j = lane; j < len; j += 32) f(xp + (st + j) * d, static_cast<uint32_t>(perm[st + j]));
+        }
+    }
+};
+
 int pairwise(const float *a, int64_t m, const float *b, int64_t p, int d, int metric, float *out, cudaStream_t st);
 
 template <class Src>

@@ -93,36 +93,43 @@ __global__ void __launch_bounds__(kPruneThreads) prune_count_kernel(
     const float *__restrict__ d1, int64_t nr, int k, const float *__restrict__ radii,
     const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, float *__restrict__ gamma_out,
     int32_t *__restrict__ nseg_out, int64_t *__restrict__ cand_out, int32_t *__restrict__ pr_out,
-    int32_t *__restrict__ p3_out) {
+    int32_t *__restrict__ p3_out, uint64_t *__restrict__ order_key) {
     __shared__ unsigned hist[256];
     __shared__ unsigned sel[2];
-    __shared__ unsigned long long s_cand;
-    __shared__ unsigned s_nseg, s_pr, s_p3;
+    __shared__ unsigned long long s_cand, s_near;
+    __shared__ unsigned s_nseg, s_pr, s_p3, s_first;
     const int64_t i = blockIdx.x;
     const float *row = d1 + i * nr;
     if (threadIdx.x == 0) {
         s_cand = 0;
+        s_near = ~0ull;
         s_nseg = s_pr = s_p3 = 0;
+        s_first = 0xFFFFFFFFu;
     }
     const float gk = block_kth_smallest(row, nr, k, hist, sel);
     const double g = gk, cut = 4.0 * g;
-    unsigned long long cand = 0;
-    unsigned nseg = 0, pr = 0, p3 = 0;
+    unsigned long long cand = 0, near = ~0ull;
+    unsigned nseg = 0, pr = 0, p3 = 0, first = 0xFFFFFFFFu;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
         const float dist = row[p];
         const double dd = dist;
+        const unsigned long long key = pack_key(dist, static_cast<uint32_t>(p));
+        near = key < near ? key : near;
         pr += (dd >= __dadd_rn(g, static_cast<double>(radii[p])) && dd > g) ? 1u : 0u;  // search.py:194
         p3 += (dd > 3.0 * g) ? 1u : 0u;                                                  // search.py:195
         if (survives(dist, radii[p], g)) {
             const int32_t len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
             cand += len;
             nseg += len > 0 ? 1u : 0u;
+            if (len > 0 && static_cast<unsigned>(p) < first) first = static_cast<unsigned>(p);
         }
     }
     atomicAdd(&s_cand, cand);
     atomicAdd(&s_nseg, nseg);
     atomicAdd(&s_pr, pr);
     atomicAdd(&s_p3, p3);
+    atomicMin(&s_near, near);
+    atomicMin(&s_first, first);
     __syncthreads();
     if (threadIdx.x == 0) {
         gamma_out[i] = gk;
@@ -130,6 +137,8 @@ __global__ void __launch_bounds__(kPruneThreads) prune_count_kernel(
         cand_out[i] = static_cast<int64_t>(s_cand);
         if (pr_out) pr_out[i] = static_cast<int32_t>(s_pr);
         if (p3_out) p3_out[i] = static_cast<int32_t>(s_p3);
+        // group queries with the same surviving lists: (first surviving list, nearest rep)
+        if (order_key) order_key[i] = (static_cast<uint64_t>(s_first & 0xFFFFFFu) << 24) | (key_id(s_near) & 0xFFFFFFu);
     }
 }
 
@@ -169,9 +178,11 @@ int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &ou
     RBC_CHECK(out.nseg.alloc(nq, st));
     RBC_CHECK(out.cand.alloc(nq, st));
     RBC_CHECK(out.seg_off.alloc(nq + 1, st));
+    RBC_CHECK(out.order_key.alloc(nq, st));
+    out.d1 = d1;
     prune_count_kernel<<<static_cast<unsigned>(nq), kPruneThreads, 0, st>>>(
         d1, idx->nr, k, idx->radii, idx->offsets, idx->list_dists, out.gamma.get(), out.nseg.get(), out.cand.get(),
-        out.pr, out.p3);
+        out.pr, out.p3, out.order_key.get());
     RBC_LAUNCHED();
     // seg_off = exclusive scan of nseg (int32 -> int64)
     RBC_CUDA(cudaMemsetAsync(out.seg_off.get(), 0, sizeof(int64_t), st));

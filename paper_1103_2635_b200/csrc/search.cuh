@@ -19,6 +19,8 @@ struct PruneOut {
     DevBuf<int64_t> seg_start; // [total] first list-order position
     DevBuf<int32_t> seg_len;   // [total] cutoff length
     DevBuf<int32_t> seg_list;  // [total] rep position of the segment
+    DevBuf<uint64_t> order_key; // [nq] (first surviving list << 24) | nearest rep: query grouping key
+    const float *d1 = nullptr; // stage-1 distances [nq, nr] (owned by the caller)
     int64_t total_segs = 0;
     int32_t *pr = nullptr;     // optional stats outputs (caller memory)
     int32_t *p3 = nullptr;

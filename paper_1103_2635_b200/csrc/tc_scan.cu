@@ -1,4 +1,5 @@
-// tc_scan.cu -- dispatch of the hot scans.
+// tc_scan.cu -- dispatch of the hot scans between the tensor-core engine and
+// the exact SIMT kernels.
 #include "common.cuh"
 #include "index.cuh"
 #include "kernels.cuh"
@@ -6,6 +7,10 @@
 #include "tc_scan.cuh"
 
 namespace rbc {
+
+static int g_engine = 0;  // 0 = auto (tensor cores where supported), 1 = exact SIMT only
+
+bool force_exact_engine() { return g_engine == 1; }
 
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
                  cudaStream_t st) {
@@ -26,10 +31,17 @@ int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1
 
 int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                 cudaStream_t st) {
+    if (!force_exact_engine() && tc_stage2_supported(idx, k)) return tc_stage2(idx, q, nq, k, po, keys, st);
+    last_overflow_count() = 0;
     return stage2_exact(idx, q, nq, k, po, keys, st);
 }
 
-int tc_index_prepare(rbc_index *, cudaStream_t) { return RBC_OK; }
-void tc_index_release(rbc_index *) {}
-
 }  // namespace rbc
+
+extern "C" int rbc_set_engine(int mode) {
+    if (mode != 0 && mode != 1) return rbc::fail(RBC_EINVAL, "engine must be 0 (auto) or 1 (exact)");
+    rbc::g_engine = mode;
+    return RBC_OK;
+}
+
+extern "C" int64_t rbc_stage2_overflows(void) { return rbc::last_overflow_count(); }

@@ -25,4 +25,13 @@ int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1
 int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                 cudaStream_t st);
 
+// tcgen05 stage 2 (tc_stage2.cu)
+bool tc_stage2_supported(const rbc_index *idx, int k);
+int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
+              cudaStream_t st);
+int64_t &last_overflow_count();
+
+// engine selection (RBC_ENGINE env: "auto" (default) | "exact")
+bool force_exact_engine();
+
 }  // namespace rbc

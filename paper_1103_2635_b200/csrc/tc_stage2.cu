@@ -1,0 +1,730 @@
+// tc_stage2.cu -- exact-search stage 2 on the 5th-generation tensor cores.
+//
+// Work unit: a TILE of 128 queries that share (mostly) the same surviving
+// ownership lists (queries are grouped by (first surviving list, nearest
+// rep)).  For every list p in the union of the tile's survivors, and every
+// 256-row chunk of p's scanned prefix:
+//
+//   A_p = f16((q_i - r_p) * sA)   128 x 64, K-major SWIZZLE_128B, built by 4 "prep" warps
+//   B   = f16((x_j - r_p) * sB_p) N x 64 rows, pre-swizzled in HBM, one cp.async.bulk per chunk
+//   D   = A_p . B^T               tcgen05.mma kind::f16 into TMEM (fp32), double-buffered
+//
+// Centering both operands on the list's representative keeps |a|,|b| at the
+// scale of the query->rep and point->rep distances, so the expanded form
+//   d^2 = |q - r_p|^2 + |x - r_p|^2 - 2 (q - r_p).(x - r_p)
+// (the first term is stage 1's exact distance) has an error bound
+//   E <= C1 |a||b| + C2 (|a|^2 + |b|^2) + ...
+// small enough that only a handful of points per query need the exact
+// re-rank.  The epilogue (4 warps, one TMEM lane = one query row per thread)
+// tests every element against the row's running k-th best upper bound with
+// one FFMA + one max per element; survivors of the filter are appended to a
+// per-query candidate buffer.  At the end of the tile each row re-ranks its
+// buffered candidates with the reference's exact fp64 arithmetic
+// (common.cuh exact_dist) and emits key64 = (f32 dist, id), so results are
+// bit-identical to the reference.  A query whose buffer overflows is
+// recomputed by the exact SIMT scan.
+//
+// Roles (320 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0      producer: cp.async.bulk of B chunks into a 4-stage ring
+//   warp 1      MMA issuer + TMEM owner (512 columns = 2 x 256 fp32 accumulators)
+//   warps 2..5  epilogue / candidate filter / exact re-rank
+//   warps 6..9  A-operand prep (query rows centred on the current list's rep)
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "common.cuh"
+#include "index.cuh"
+#include "kernels.cuh"
+#include "search.cuh"
+#include "sm100.cuh"
+#include "tc_scan.cuh"
+
+namespace rbc {
+
+namespace {
+
+constexpr int kRows = 128;       // queries per tile = UMMA M = TMEM lanes
+constexpr int kNmax = 256;       // max UMMA N per chunk
+constexpr int kStages = 4;       // B ring depth
+constexpr int kThreads = 320;    // 10 warps
+constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
+
+// error-bound constants (see header comment; factor 2 safety on each term)
+constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 64.0f / 4194304.0f);  // f16 rounding of a and b, fp32 accumulate
+constexpr float kC2 = 1.0f / 1048576.0f;                             // fp32 rounding of norms / epilogue
+constexpr float kC4 = 1.0f / 262144.0f;                              // f16 subnormal flush (absolute, scaled)
+constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                      // rounding-up factor for norms
+constexpr float kTie = 1.0f + 1.0f / 524288.0f;                      // tie slack: 8 fp32 ulps of the distance
+
+struct TcIndex {
+    int64_t npad = 0;
+    __half *xh = nullptr;    // [npad + tail][64] f16 residual rows, SW128 pre-swizzled
+    float *gcol = nullptr;   // [npad + tail] (|x - r_p|^2 / 2) * sB_p
+    int64_t *poff = nullptr; // [nr + 1] padded (8-row aligned) list offsets
+    float *sB = nullptr;     // [nr] per-list power-of-two scale
+};
+
+struct S2Params {
+    const __half *xh;
+    const float *gcol;
+    const int64_t *poff;
+    const float *sB;
+    const int64_t *offsets;
+    const float *radii;
+    const float *reps;
+    const float *xp;
+    const int32_t *perm;
+    int d;
+    int64_t nr;
+    const float *q;
+    const float *d1;
+    const float *gamma;
+    int k;
+    int ntiles;
+    const int32_t *tile_rows;
+    const int64_t *work_off;
+    const int32_t *work_p;
+    const int32_t *work_ext;
+    const float *work_sA;
+    const int32_t *cut;
+    float *cand_lb;
+    int32_t *cand_pos;
+    int cap;
+    uint64_t *out_keys;
+    int32_t *overflow_list;
+    int32_t *overflow_count;
+    int32_t *tile_counter;
+};
+
+__device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
+
+// ---- index preparation ----------------------------------------------------------
+__global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, float *__restrict__ sB) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p >= nr) return;
+    const float r = radii[p];
+    int e = 0;
+    if (r > 0.f) frexpf(r, &e);  // r = m * 2^e, m in [0.5, 1)  ->  r * 2^-e < 1
+    sB[p] = r > 0.f ? ldexpf(1.0f, -e) : 1.0f;
+}
+
+// one block per list: f16 residual rows (pre-swizzled) + (|b|^2 / 2) * sB
+__global__ void residual_rows_kernel(const float *__restrict__ xp, const float *__restrict__ reps,
+                                     const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff,
+                                     const float *__restrict__ sB, int d, __half *__restrict__ xh,
+                                     float *__restrict__ gcol) {
+    const int64_t p = blockIdx.x;
+    const int64_t len = offsets[p + 1] - offsets[p];
+    const float s = sB[p];
+    const float *r = reps + p * d;
+    for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
+        const float *x = xp + (offsets[p] + j) * d;
+        const int64_t row = poff[p] + j;
+        double h = 0.0;
+        uint8_t *dst = reinterpret_cast<uint8_t *>(xh) + row * 128;
+        for (int c = 0; c < 8; ++c) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k0 = c * 8 + 2 * e, k1 = k0 + 1;
+                const float b0 = k0 < d ? __fsub_rn(x[k0], r[k0]) : 0.f;
+                const float b1 = k1 < d ? __fsub_rn(x[k1], r[k1]) : 0.f;
+                h += static_cast<double>(b0) * b0 + static_cast<double>(b1) * b1;
+                w[e] = sm100::pack_f16x2_sat(b0 * s, b1 * s);
+            }
+            *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        gcol[row] = static_cast<float>(h) * 0.5f * s;
+    }
+}
+
+// ---- tile preparation -----------------------------------------------------------------
+__global__ void tile_rows_kernel(const int32_t *__restrict__ order, int64_t nq, int64_t total, int32_t *__restrict__ rows) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < total) rows[t] = t < nq ? order[t] : -1;
+}
+
+__global__ void iota_kernel(int32_t *v, int64_t n) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < n) v[t] = static_cast<int32_t>(t);
+}
+
+// union of the tile's surviving lists: count
+__global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__restrict__ rows,
+                                                           const int64_t *__restrict__ seg_off,
+                                                           const int32_t *__restrict__ seg_list, int64_t nr,
+                                                           int64_t *__restrict__ nwork) {
+    extern __shared__ int32_t present[];
+    __shared__ int s_count;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) present[p] = 0;
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
+    if (qi >= 0)
+        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) present[seg_list[s]] = 1;
+    __syncthreads();
+    int c = 0;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) c += present[p];
+    atomicAdd(&s_count, c);
+    __syncthreads();
+    if (threadIdx.x == 0) nwork[blockIdx.x] = s_count;
+}
+
+// union of the tile's surviving lists: work entries (list, extent, A scale) and per-row cutoffs
+__global__ void __launch_bounds__(kRows) tile_fill_kernel(
+    const int32_t *__restrict__ rows, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_list,
+    const int32_t *__restrict__ seg_len, const uint64_t *__restrict__ order_key, const float *__restrict__ d1,
+    int64_t nr, const int64_t *__restrict__ work_off, int32_t *__restrict__ work_p, int32_t *__restrict__ work_ext,
+    float *__restrict__ work_sA, int32_t *__restrict__ cut) {
+    extern __shared__ int32_t sm[];
+    int32_t *maxlen = sm;           // [nr]
+    int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
+    int32_t *nearcnt = sm + 2 * nr; // [nr]
+    typedef cub::BlockScan<int, kRows> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_base;
+    __shared__ unsigned long long s_front;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) maxlen[p] = maxd1[p] = nearcnt[p] = 0;
+    if (threadIdx.x == 0) {
+        s_base = 0;
+        s_front = ~0ull;
+    }
+    __syncthreads();
+    const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
+    if (qi >= 0) {
+        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) {
+            const int32_t p = seg_list[s];
+            atomicMax(&maxlen[p], seg_len[s]);
+            atomicMax(&maxd1[p], __float_as_int(d1[static_cast<int64_t>(qi) * nr + p]));
+        }
+        atomicAdd(&nearcnt[order_key[qi] & 0xFFFFFF], 1);
+    }
+    __syncthreads();
+    // front list = the most common nearest rep of the tile (ties: lowest position)
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x)
+        if (maxlen[p] > 0 && nearcnt[p] > 0)
+            atomicMin(&s_front, (static_cast<unsigned long long>(kRows - nearcnt[p]) << 32) | static_cast<uint64_t>(p));
+    __syncthreads();
+    const int32_t front = s_front == ~0ull ? -1 : static_cast<int32_t>(s_front & 0xFFFFFFFFu);
+    const int64_t w0 = work_off[blockIdx.x];
+    // ordered compaction: front first, then the others ascending
+    for (int64_t p0 = 0; p0 < nr; p0 += kRows) {
+        const int64_t p = p0 + threadIdx.x;
+        const int flag = (p < nr && maxlen[p] > 0 && p != front) ? 1 : 0;
+        int pos, total;
+        Scan(scan_tmp).ExclusiveSum(flag, pos, total);
+        if (flag) nearcnt[p] = s_base + pos + (front >= 0 ? 1 : 0);  // reuse as list -> work index
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += total;
+        __syncthreads();
+    }
+    if (front >= 0 && threadIdx.x == 0) nearcnt[front] = 0;
+    __syncthreads();
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+        if (maxlen[p] > 0) {
+            const int64_t w = w0 + nearcnt[p];
+            work_p[w] = static_cast<int32_t>(p);
+            work_ext[w] = maxlen[p];
+            int e = 0;
+            const float m = __int_as_float(maxd1[p]);
+            if (m > 0.f) frexpf(m, &e);
+            work_sA[w] = m > 0.f ? ldexpf(1.0f, -e) : 1.0f;
+        }
+    }
+    __syncthreads();
+    if (qi >= 0)
+        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s)
+            cut[(w0 + nearcnt[seg_list[s]]) * kRows + threadIdx.x] = seg_len[s];
+}
+
+// ---- the stage-2 kernel -----------------------------------------------------------------
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *sB = smem;                                   // kStages x kNmax x 128 B
+    uint8_t *sA = sB + kStages * kNmax * 128;             // 2 x 128 x 128 B
+    float *gbuf = reinterpret_cast<float *>(sA + 2 * kRows * 128);  // 4 epilogue warps x kNmax
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 4 * kNmax);
+    uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
+    uint64_t *afull = tempty + 2, *aempty = afull + 2;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(aempty + 2);
+    int *s_tile = reinterpret_cast<int *>(s_tmem + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            sm100::mbar_init(&full[s], 1);
+            sm100::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            sm100::mbar_init(&tfull[b], 1);
+            sm100::mbar_init(&tempty[b], 4);
+            sm100::mbar_init(&afull[b], 4);
+            sm100::mbar_init(&aempty[b], 1);
+        }
+        sm100::fence_barrier_init();
+    }
+    if (warp == 1) sm100::tmem_alloc<512>(s_tmem);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *s_tmem;
+
+    uint32_t bi = 0, ti = 0, ai = 0;  // ring counters (identical sequence in every role)
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;  // TMEM lane / tile row owned by this thread (epilogue + prep)
+
+    for (;;) {
+        if (tid == 0) *s_tile = atomicAdd(P.tile_counter, 1);
+        __syncthreads();
+        const int tile = *s_tile;
+        if (tile >= P.ntiles) break;
+        const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
+
+        if (warp == 0) {
+            // ===== producer =====
+            if (lane == 0) {
+                for (int64_t w = w0; w < w1; ++w) {
+                    const int ext = P.work_ext[w];
+                    const int64_t base = P.poff[P.work_p[w]];
+                    for (int off = 0; off < ext; off += kNmax) {
+                        const int n = min(kNmax, roundup16(ext - off));
+                        const uint32_t s = bi % kStages;
+                        sm100::mbar_wait(&empty[s], ((bi / kStages) & 1) ^ 1);
+                        const uint32_t bytes = static_cast<uint32_t>(n) * 128u;
+                        sm100::mbar_arrive_expect_tx(&full[s], bytes);
+                        sm100::bulk_g2s(sB + s * (kNmax * 128), P.xh + (base + off) * 64, bytes, &full[s]);
+                        ++bi;
+                    }
+                }
+            }
+        } else if (warp == 1) {
+            // ===== MMA issuer =====
+            if (lane == 0) {
+                for (int64_t w = w0; w < w1; ++w) {
+                    const int ext = P.work_ext[w];
+                    const uint32_t a = ai & 1;
+                    sm100::mbar_wait(&afull[a], (ai >> 1) & 1);
+                    sm100::tc_fence_after();
+                    const uint32_t a_base = sm100::smem_u32(sA + a * (kRows * 128));
+                    for (int off = 0; off < ext; off += kNmax) {
+                        const int n = min(kNmax, roundup16(ext - off));
+                        const uint32_t s = bi % kStages, tb = ti & 1;
+                        sm100::mbar_wait(&full[s], (bi / kStages) & 1);
+                        sm100::mbar_wait(&tempty[tb], ((ti >> 1) & 1) ^ 1);
+                        sm100::tc_fence_after();
+                        const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
+                        const uint32_t b_base = sm100::smem_u32(sB + s * (kNmax * 128));
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            sm100::umma_f16(tmem + tb * kNmax, sm100::umma_desc_sw128(a_base + kk * 32),
+                                            sm100::umma_desc_sw128(b_base + kk * 32), idesc, kk > 0);
+                        sm100::umma_commit(&empty[s]);
+                        sm100::umma_commit(&tfull[tb]);
+                        ++bi;
+                        ++ti;
+                    }
+                    sm100::umma_commit(&aempty[a]);
+                    ++ai;
+                }
+            }
+        } else if (warp >= 6) {
+            // ===== A-operand prep: row i = f16((q_i - r_p) * sA) =====
+            const int32_t qi = P.tile_rows[tile * kRows + row];
+            const float *qrow = P.q + static_cast<int64_t>(qi < 0 ? 0 : qi) * P.d;
+            for (int64_t w = w0; w < w1; ++w) {
+                const uint32_t a = ai & 1;
+                sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
+                const float sa = P.work_sA[w];
+                const float *rep = P.reps + static_cast<int64_t>(P.work_p[w]) * P.d;
+                uint8_t *dst = sA + a * (kRows * 128) + row * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int k0 = c * 8 + 2 * e, k1 = k0 + 1;
+                        float v0 = 0.f, v1 = 0.f;
+                        if (qi >= 0 && k0 < P.d) v0 = fmaf(qrow[k0], sa, -(rep[k0] * sa));
+                        if (qi >= 0 && k1 < P.d) v1 = fmaf(qrow[k1], sa, -(rep[k1] * sa));
+                        wv[e] = sm100::pack_f16x2_sat(v0, v1);
+                    }
+                    *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                sm100::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(&afull[a]);
+                ++ai;
+            }
+        } else {
+            // ===== epilogue: filter, candidate buffer, exact re-rank =====
+            float *g = gbuf + (warp - 2) * kNmax;
+            const int32_t qi = P.tile_rows[tile * kRows + row];
+            const bool live = qi >= 0;
+            float ubk[KT];
+#pragma unroll
+            for (int j = 0; j < KT; ++j) ubk[j] = __int_as_float(0x7f800000);
+            const float gk = live ? P.gamma[qi] : 0.f;
+            const float u_init = gk * gk * kUp * kUp;
+            float U = u_init;  // running upper bound of the k-th smallest candidate d^2
+            int count = 0;
+            bool overflow = false;
+            float *clb = P.cand_lb + static_cast<int64_t>(live ? qi : 0) * P.cap;
+            int32_t *cpos = P.cand_pos + static_cast<int64_t>(live ? qi : 0) * P.cap;
+
+            for (int64_t w = w0; w < w1; ++w) {
+                const int32_t p = P.work_p[w];
+                const int ext = P.work_ext[w];
+                const int cutv = live ? P.cut[w * kRows + row] : 0;
+                const float sa = P.work_sA[w];
+                const float sb = P.sB[p];
+                const float scale = sa * sb;
+                const int64_t poff = P.poff[p];
+                const int64_t csr = P.offsets[p];
+                float A2 = 0.f, E = 0.f;
+                if (cutv > 0) {
+                    const float dq = P.d1[static_cast<int64_t>(qi) * P.nr + p];
+                    const float na = dq * kUp, rb = P.radii[p] * kUp;
+                    A2 = dq * dq;
+                    E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
+                }
+                auto threshold = [&]() {
+                    // V >= T  <=>  lb = A2 - E - 2 V / scale <= U * kTie   (loosened by 2^-18 relative)
+                    const float t = 0.5f * scale * (A2 - E - U * kTie);
+                    return t - fabsf(t) * (1.0f / 262144.0f) - 1e-30f;
+                };
+                float T = cutv > 0 ? threshold() : __int_as_float(0x7f800000);
+                for (int off = 0; off < ext; off += kNmax) {
+                    const int n = min(kNmax, roundup16(ext - off));
+                    // per-column (|b|^2 / 2) * sB for this chunk -> warp-private smem
+                    {
+                        const float *src = P.gcol + poff + off;
+                        float4 g0 = make_float4(0, 0, 0, 0), g1 = g0;
+                        if (lane * 8 < n) {
+                            g0 = *reinterpret_cast<const float4 *>(src + lane * 8);
+                            g1 = *reinterpret_cast<const float4 *>(src + lane * 8 + 4);
+                        }
+                        reinterpret_cast<float4 *>(g)[lane * 2] = g0;
+                        reinterpret_cast<float4 *>(g)[lane * 2 + 1] = g1;
+                    }
+                    const uint32_t tb = ti & 1;
+                    sm100::mbar_wait(&tfull[tb], (ti >> 1) & 1);
+                    sm100::tc_fence_after();
+                    __syncwarp();
+                    const int lim = min(cutv - off, n);  // valid columns of this row in the chunk
+                    const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
+                    for (int c0 = 0; c0 < wlim; c0 += 32) {
+                        float v[32];
+                        sm100::tmem_ld32(tmem + tb * kNmax + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
+                        float m = -__int_as_float(0x7f800000);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            v[j] = fmaf(-sa, g[c0 + j], v[j]);
+                            m = fmaxf(m, v[j]);
+                        }
+                        if (m >= T && c0 < lim) {
+                            // slow path: push every element that passes the exact-bound test
+                            float vv[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) vv[j] = v[j];
+#pragma unroll 1
+                            for (int j = 0; j < 32; ++j) {
+                                if (c0 + j >= lim || !(vv[j] >= T)) continue;
+                                const float lb = A2 - E - 2.0f * vv[j] / scale;
+                                if (!(lb <= U * kTie)) continue;
+                                const float ub = lb + 2.0f * E;
+                                if (count == P.cap && !overflow) {
+                                    // compact: drop entries that can no longer qualify
+                                    int c2 = 0;
+                                    for (int e = 0; e < count; ++e) {
+                                        const float l2 = clb[e];
+                                        if (l2 <= U * kTie) {
+                                            clb[c2] = l2;
+                                            cpos[c2] = cpos[e];
+                                            ++c2;
+                                        }
+                                    }
+                                    count = c2;
+                                    if (count == P.cap) overflow = true;
+                                }
+                                if (!overflow) {
+                                    clb[count] = lb;
+                                    cpos[count] = static_cast<int32_t>(csr + off + c0 + j);
+                                    ++count;
+                                }
+                                // running k-th best upper bound
+                                if (KT == 1) {
+                                    U = fminf(U, ub);
+                                } else {
+                                    float x = ub;
+#pragma unroll
+                                    for (int t = 0; t < KT; ++t) {
+                                        const float lo = fminf(ubk[t], x), hi = fmaxf(ubk[t], x);
+                                        ubk[t] = lo;
+                                        x = hi;
+                                    }
+                                    float kth = ubk[0];
+#pragma unroll
+                                    for (int t = 0; t < KT; ++t)
+                                        if (t == P.k - 1) kth = ubk[t];
+                                    U = fminf(u_init, kth);
+                                }
+                                T = threshold();
+                            }
+                        }
+                    }
+                    sm100::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) sm100::mbar_arrive(&tempty[tb]);
+                    ++ti;
+                }
+            }
+            // ---- exact re-rank of the buffered candidates (reference arithmetic) ----
+            if (live) {
+                if (overflow) {
+                    P.overflow_list[atomicAdd(P.overflow_count, 1)] = qi;
+                } else {
+                    uint64_t best[KT];
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+                    const float ufin = U * kTie;
+                    const float *qrow = P.q + static_cast<int64_t>(qi) * P.d;
+                    for (int e = 0; e < count; ++e) {
+                        if (!(clb[e] <= ufin)) continue;
+                        const int32_t pos = cpos[e];
+                        const float dist = exact_dist<RBC_L2>(qrow, P.xp + static_cast<int64_t>(pos) * P.d, P.d);
+                        const uint64_t key = pack_key(dist, static_cast<uint32_t>(P.perm[pos]));
+                        if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+                    }
+                    uint64_t *out = P.out_keys + static_cast<int64_t>(qi) * P.k;
+#pragma unroll
+                    for (int j = 0; j < KT; ++j)
+                        if (j < P.k) out[j] = best[j];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) sm100::tmem_dealloc<512>(tmem);
+}
+
+__global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
+                                         float *__restrict__ out) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < m * d;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[t] = q[static_cast<int64_t>(ids[t / d]) * d + t % d];
+}
+
+__global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int32_t *__restrict__ ids, int64_t m, int k,
+                                    uint64_t *__restrict__ dst) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < m * k) dst[static_cast<int64_t>(ids[t / k]) * k + t % k] = src[t];
+}
+
+}  // namespace
+
+int64_t &last_overflow_count() {
+    static int64_t v = 0;
+    return v;
+}
+
+// ---- index-side preparation ----------------------------------------------------------------
+int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
+    if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->n_local == 0) return RBC_OK;
+    TcIndex *tc = new TcIndex();
+    std::vector<int64_t> off(idx->nr + 1), poff(idx->nr + 1, 0);
+    RBC_CUDA(cudaMemcpyAsync(off.data(), idx->offsets, sizeof(int64_t) * (idx->nr + 1), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    for (int64_t p = 0; p < idx->nr; ++p) poff[p + 1] = poff[p] + ((off[p + 1] - off[p] + 7) & ~int64_t(7));
+    tc->npad = poff[idx->nr];
+    const int64_t rows = tc->npad + kTailRows;
+    auto cleanup = [&](int rc) {
+        cudaFree(tc->xh);
+        cudaFree(tc->gcol);
+        cudaFree(tc->poff);
+        cudaFree(tc->sB);
+        delete tc;
+        return rc;
+    };
+    if (cudaMalloc(&tc->xh, rows * 128) != cudaSuccess || cudaMalloc(&tc->gcol, rows * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&tc->poff, (idx->nr + 1) * sizeof(int64_t)) != cudaSuccess ||
+        cudaMalloc(&tc->sB, idx->nr * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return cleanup(fail(RBC_ENOMEM, "tc index allocation"));
+    }
+    idx->bytes += rows * (128 + sizeof(float)) + (idx->nr + 1) * sizeof(int64_t) + idx->nr * sizeof(float);
+    if (cudaMemsetAsync(tc->xh, 0, rows * 128, st) != cudaSuccess ||
+        cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
+        cudaMemcpyAsync(tc->poff, poff.data(), sizeof(int64_t) * (idx->nr + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return cleanup(fail(RBC_ECUDA, "tc index init"));
+    list_scale_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->radii, idx->nr, tc->sB);
+    residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(idx->xp, idx->reps, idx->offsets, tc->poff,
+                                                                        tc->sB, idx->d, tc->xh, tc->gcol);
+    note_launch(2);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+        return cleanup(fail(RBC_ECUDA, "tc index kernels"));
+    idx->tc = tc;
+    return RBC_OK;
+}
+
+void tc_index_release(rbc_index *idx) {
+    TcIndex *tc = static_cast<TcIndex *>(idx->tc);
+    if (!tc) return;
+    cudaFree(tc->xh);
+    cudaFree(tc->gcol);
+    cudaFree(tc->poff);
+    cudaFree(tc->sB);
+    delete tc;
+    idx->tc = nullptr;
+}
+
+bool tc_stage2_supported(const rbc_index *idx, int k) {
+    return idx->tc != nullptr && k <= 16 && idx->nr < (1 << 24);
+}
+
+static int g_num_sms = 0;
+
+int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
+              cudaStream_t st) {
+    const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
+    const int64_t nr = idx->nr;
+    const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
+    // 1. group queries: sort by (first surviving list, nearest rep)
+    DevBuf<uint64_t> skey;
+    DevBuf<int32_t> ids, order, rows;
+    RBC_CHECK(skey.alloc(nq, st));
+    RBC_CHECK(ids.alloc(nq, st));
+    RBC_CHECK(order.alloc(nq, st));
+    RBC_CHECK(rows.alloc(static_cast<int64_t>(ntiles) * kRows, st));
+    iota_kernel<<<grid_for(nq, 256), 256, 0, st>>>(ids.get(), nq);
+    RBC_LAUNCHED();
+    {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq, 0, 48, st);
+        DevBuf<unsigned char> tmp;
+        RBC_CHECK(tmp.alloc(tb, st));
+        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, po.order_key.get(), skey.get(), ids.get(), order.get(),
+                                                 nq, 0, 48, st));
+        note_launch();
+    }
+    tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
+        order.get(), nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
+    RBC_LAUNCHED();
+    // 2. union of surviving lists per tile
+    DevBuf<int64_t> nwork, work_off;
+    RBC_CHECK(nwork.alloc(ntiles, st));
+    RBC_CHECK(work_off.alloc(ntiles + 1, st));
+    const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
+    if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
+    cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
+    cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
+    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), nr, nwork.get());
+    RBC_LAUNCHED();
+    RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
+    {
+        size_t tb = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tb, nwork.get(), work_off.get() + 1, ntiles, st);
+        DevBuf<unsigned char> tmp;
+        RBC_CHECK(tmp.alloc(tb, st));
+        RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, nwork.get(), work_off.get() + 1, ntiles, st));
+        note_launch();
+    }
+    int64_t total_work = 0;
+    RBC_CUDA(cudaMemcpyAsync(&total_work, work_off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    DevBuf<int32_t> work_p, work_ext, cut;
+    DevBuf<float> work_sA;
+    RBC_CHECK(work_p.alloc(total_work, st));
+    RBC_CHECK(work_ext.alloc(total_work, st));
+    RBC_CHECK(work_sA.alloc(total_work, st));
+    RBC_CHECK(cut.alloc(total_work * kRows, st));
+    RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
+    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), po.seg_len.get(),
+                                                   po.order_key.get(), po.d1, nr, work_off.get(), work_p.get(),
+                                                   work_ext.get(), work_sA.get(), cut.get());
+    RBC_LAUNCHED();
+    // 3. the tensor-core scan
+    const int cap = 64 + 32 * k;
+    DevBuf<float> cand_lb;
+    DevBuf<int32_t> cand_pos, ovf_list, counters;
+    RBC_CHECK(cand_lb.alloc(nq * cap, st));
+    RBC_CHECK(cand_pos.alloc(nq * cap, st));
+    RBC_CHECK(ovf_list.alloc(nq, st));
+    RBC_CHECK(counters.alloc(2, st));
+    RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
+    S2Params P;
+    P.xh = tc->xh;
+    P.gcol = tc->gcol;
+    P.poff = tc->poff;
+    P.sB = tc->sB;
+    P.offsets = idx->offsets;
+    P.radii = idx->radii;
+    P.reps = idx->reps;
+    P.xp = idx->xp;
+    P.perm = idx->perm;
+    P.d = idx->d;
+    P.nr = nr;
+    P.q = q;
+    P.d1 = po.d1;
+    P.gamma = po.gamma.get();
+    P.k = k;
+    P.ntiles = ntiles;
+    P.tile_rows = rows.get();
+    P.work_off = work_off.get();
+    P.work_p = work_p.get();
+    P.work_ext = work_ext.get();
+    P.work_sA = work_sA.get();
+    P.cut = cut.get();
+    P.cand_lb = cand_lb.get();
+    P.cand_pos = cand_pos.get();
+    P.cap = cap;
+    P.out_keys = keys;
+    P.overflow_list = ovf_list.get();
+    P.overflow_count = counters.get();
+    P.tile_counter = counters.get() + 1;
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = 1024 + kStages * kNmax * 128 + 2 * kRows * 128 + 4 * kNmax * sizeof(float) + 256;
+    const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kThreads, smem, st>>>(P);
+    };
+    {
+        ProfScope ps(kPhaseScan, st);
+        if (k == 1) launch(stage2_tc_kernel<1>);
+        else if (k <= 4) launch(stage2_tc_kernel<4>);
+        else if (k <= 8) launch(stage2_tc_kernel<8>);
+        else launch(stage2_tc_kernel<16>);
+    }
+    RBC_LAUNCHED();
+    // 4. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
+    int32_t n_ovf = 0;
+    RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    if (n_ovf > 0) {
+        DevBuf<float> qsub;
+        DevBuf<uint64_t> ksub;
+        RBC_CHECK(qsub.alloc(static_cast<int64_t>(n_ovf) * idx->d, st));
+        RBC_CHECK(ksub.alloc(static_cast<int64_t>(n_ovf) * k, st));
+        gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
+            q, ovf_list.get(), n_ovf, idx->d, qsub.get());
+        RBC_LAUNCHED();
+        SegSubSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), ovf_list.get(), idx->d};
+        RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
+        scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
+                                                                                         n_ovf, k, keys);
+        RBC_LAUNCHED();
+    }
+    last_overflow_count() = n_ovf;
+    return RBC_OK;
+}
+
+}  // namespace rbc

@@ -324,3 +324,71 @@ def test_prune_and_cutoff_kats(rbc):
     assert rbc.list_cutoff(np.array([0.0, 1.0, 2.0, 5.0, 7.0]), 4.0) == 3
     assert rbc.list_cutoff(np.array([0.0, 1.0, 1.0, 2.0]), 1.0) == 3
     assert rbc.list_cutoff(np.array([0.1], np.float32), 0.1) == 0
+
+
+# ---- tcgen05 building block --------------------------------------------------------------
+@pytest.mark.parametrize("n", [16, 48, 128, 256])
+def test_tc_selftest_tile(rbc, n):
+    import torch
+
+    from paper_1103_2635_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(n)
+    a = torch.randn(128, 64, device="cuda", generator=g).half()
+    b = torch.randn(n, 64, device="cuda", generator=g).half()
+    c = torch.empty(128, n, device="cuda", dtype=torch.float32)
+    _lib.check(_lib.lib.rbc_tc_selftest(_lib.ptr(a), _lib.ptr(b), _lib.ptr(c), n, _lib.stream_ptr()))
+    ref = a.double() @ b.double().T
+    err = (c.double() - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item(), err
+
+
+def _both_engines(rbc, idx, q, k):
+    from paper_1103_2635_b200 import _lib
+
+    try:
+        _lib.lib.rbc_set_engine(1)
+        exact = rbc.exact_query_arrays(idx, q, k)
+    finally:
+        _lib.lib.rbc_set_engine(0)
+    fast = rbc.exact_query_arrays(idx, q, k)
+    return fast, exact
+
+
+@pytest.mark.parametrize("k", [1, 2, 10, 16])
+def test_tc_engine_matches_exact_engine(rbc, oracle, k):
+    full = oracle.gen_clusters(100_000 + 2_000, 64, 1, n_clusters=32, cluster_sigma=0.05)
+    x, q = full[:100_000], full[100_000:]
+    idx = rbc.build_exact(rbc.DataMatrix(x), 316, rbc.MetricSpec("l2", 64), seed=0)
+    fast, exact = _both_engines(rbc, idx, q, k)
+    for a, b in zip(fast, exact):
+        assert np.array_equal(a, b)
+    li, off, ld = idx.flat_lists()
+    want = oracle.exact_query(x, idx.reps.rep_ids, li, off, ld, idx.radii, q[:300], k)
+    assert np.array_equal(fast[0][:300], want[0]) and np.array_equal(fast[1][:300], want[1])
+
+
+@pytest.mark.parametrize("d", [3, 17, 40, 64])
+def test_tc_engine_scales_and_offsets(rbc, oracle, d):
+    # large coordinate offsets and mixed scales stress the centred f16 operands and the error bound
+    rng = np.random.default_rng(d)
+    x = (rng.standard_normal((30_000, d)) * rng.choice([0.001, 1.0, 300.0], size=(30_000, 1)) + 1000.0).astype(np.float32)
+    q = (x[rng.integers(0, 30_000, 400)] + rng.standard_normal((400, d)).astype(np.float32) * 0.01).astype(np.float32)
+    idx = rbc.build_exact(rbc.DataMatrix(x), 173, rbc.MetricSpec("l2", d), seed=1)
+    for k in (1, 5):
+        fast, exact = _both_engines(rbc, idx, q, k)
+        for a, b in zip(fast, exact):
+            assert np.array_equal(a, b)
+
+
+def test_tc_engine_overflow_fallback(rbc):
+    from paper_1103_2635_b200 import _lib
+
+    base = np.repeat(uniform(40, 8, 3), 300, axis=0)  # 300 exact copies of each point
+    idx = rbc.build_exact(rbc.DataMatrix(base), 30, rbc.MetricSpec("l2", 8), seed=0)
+    q = base[::997][:12]
+    fast, exact = _both_engines(rbc, idx, q, 1)
+    for a, b in zip(fast, exact):
+        assert np.array_equal(a, b)
+    rbc.exact_query_arrays(idx, q, 1)
+    assert _lib.lib.rbc_stage2_overflows() > 0
