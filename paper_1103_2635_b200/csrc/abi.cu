@@ -22,6 +22,18 @@ int fail(int code, const std::string &msg) {
 }
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+void retain_pool_memory() {
+    static thread_local int done_for = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_for) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_for = dev;
+}
+
 // per-phase event pairs, recorded on the launching stream when enabled
 struct ProfRec {
     int phase;

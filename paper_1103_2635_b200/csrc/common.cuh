@@ -49,6 +49,11 @@ struct ProfScope {
         if (_rc != RBC_OK) return _rc;                                                          \
     } while (0)
 
+// Keep freed blocks in the device's default stream-ordered pool (otherwise
+// every synchronisation returns them to the OS and the next search re-maps
+// hundreds of MB).
+void retain_pool_memory();
+
 // Stream-ordered scratch allocation (cudaMallocAsync pool).
 template <typename T>
 struct DevBuf {
@@ -63,6 +68,7 @@ struct DevBuf {
     int alloc(size_t count, cudaStream_t s) {
         stream = s;
         if (count == 0) count = 1;
+        retain_pool_memory();
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&ptr), count * sizeof(T), s);
         if (e != cudaSuccess) {
             ptr = nullptr;

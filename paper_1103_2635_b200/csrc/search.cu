@@ -173,6 +173,118 @@ __global__ void __launch_bounds__(kPruneThreads) prune_fill_kernel(
     }
 }
 
+// ---- warp-per-query pruning (k <= 16) ----------------------------------------------
+// gamma_k = k-th smallest row value: each lane keeps its KT smallest values
+// (sorted, registers), then k rounds of warp-minimum extraction.
+template <int KT>
+__global__ void __launch_bounds__(256) prune_count_warp_kernel(
+    const float *__restrict__ d1, int64_t nq, int64_t nr, int k, const float *__restrict__ radii,
+    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, float *__restrict__ gamma_out,
+    int32_t *__restrict__ nseg_out, int64_t *__restrict__ cand_out, int32_t *__restrict__ pr_out,
+    int32_t *__restrict__ p3_out, uint64_t *__restrict__ order_key) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (i >= nq) return;
+    const float *row = d1 + i * nr;
+    float best[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) best[j] = __int_as_float(0x7f800000);
+    unsigned long long near = ~0ull;
+    for (int64_t p = lane; p < nr; p += 32) {
+        float x = row[p];
+        const unsigned long long key = pack_key(x, static_cast<uint32_t>(p));
+        near = key < near ? key : near;
+        if (x < best[KT - 1]) {
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {
+                const float lo = fminf(best[j], x), hi = fmaxf(best[j], x);
+                best[j] = lo;
+                x = hi;
+            }
+        }
+    }
+    float gk = best[0];
+    for (int r = 0; r < k; ++r) {
+        unsigned long long h = (static_cast<unsigned long long>(__float_as_uint(best[0])) << 32) | lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long w = __shfl_xor_sync(0xffffffffu, h, o);
+            h = w < h ? w : h;
+        }
+        gk = __uint_as_float(static_cast<uint32_t>(h >> 32));
+        if (static_cast<int>(h & 31) == lane) {
+#pragma unroll
+            for (int j = 0; j < KT - 1; ++j) best[j] = best[j + 1];
+            best[KT - 1] = __int_as_float(0x7f800000);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, near, o);
+        near = w < near ? w : near;
+    }
+    const double g = gk, cut = 4.0 * g;
+    long long cand = 0;
+    int nseg = 0, pr = 0, p3 = 0;
+    unsigned first = 0xFFFFFFFFu;
+    for (int64_t p = lane; p < nr; p += 32) {
+        const float dist = row[p];
+        const double dd = dist;
+        pr += (dd >= __dadd_rn(g, static_cast<double>(radii[p])) && dd > g) ? 1 : 0;  // search.py:194
+        p3 += (dd > 3.0 * g) ? 1 : 0;                                                  // search.py:195
+        if (survives(dist, radii[p], g)) {
+            const int32_t len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
+            cand += len;
+            nseg += len > 0 ? 1 : 0;
+            if (len > 0 && static_cast<unsigned>(p) < first) first = static_cast<unsigned>(p);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cand += __shfl_xor_sync(0xffffffffu, cand, o);
+        nseg += __shfl_xor_sync(0xffffffffu, nseg, o);
+        pr += __shfl_xor_sync(0xffffffffu, pr, o);
+        p3 += __shfl_xor_sync(0xffffffffu, p3, o);
+        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    }
+    if (lane == 0) {
+        gamma_out[i] = gk;
+        nseg_out[i] = nseg;
+        cand_out[i] = cand;
+        if (pr_out) pr_out[i] = pr;
+        if (p3_out) p3_out[i] = p3;
+        if (order_key) order_key[i] = (static_cast<uint64_t>(first & 0xFFFFFFu) << 24) | (key_id(near) & 0xFFFFFFu);
+    }
+}
+
+// surviving segments of query i in ascending rep position (warp ballot compaction)
+__global__ void __launch_bounds__(256) prune_fill_warp_kernel(
+    const float *__restrict__ d1, int64_t nq, int64_t nr, const float *__restrict__ gamma,
+    const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
+    const int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len,
+    int32_t *__restrict__ seg_list) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (i >= nq) return;
+    const float *row = d1 + i * nr;
+    const double g = gamma[i], cut = 4.0 * g;
+    int64_t base = seg_off[i];
+    for (int64_t p0 = 0; p0 < nr; p0 += 32) {
+        const int64_t p = p0 + lane;
+        int32_t len = 0;
+        if (p < nr && survives(row[p], radii[p], g))
+            len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
+        const unsigned bal = __ballot_sync(0xffffffffu, len > 0);
+        if (len > 0) {
+            const int64_t at = base + __popc(bal & ((1u << lane) - 1u));
+            seg_start[at] = offsets[p];
+            seg_len[at] = len;
+            seg_list[at] = static_cast<int32_t>(p);
+        }
+        base += __popc(bal);
+    }
+}
+
 int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &out, cudaStream_t st) {
     RBC_CHECK(out.gamma.alloc(nq, st));
     RBC_CHECK(out.nseg.alloc(nq, st));
@@ -180,9 +292,19 @@ int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &ou
     RBC_CHECK(out.seg_off.alloc(nq + 1, st));
     RBC_CHECK(out.order_key.alloc(nq, st));
     out.d1 = d1;
-    prune_count_kernel<<<static_cast<unsigned>(nq), kPruneThreads, 0, st>>>(
-        d1, idx->nr, k, idx->radii, idx->offsets, idx->list_dists, out.gamma.get(), out.nseg.get(), out.cand.get(),
-        out.pr, out.p3, out.order_key.get());
+    const unsigned wgrid = grid_for(nq * 32, 256);
+#define RBC_PRUNE_WARP(KT)                                                                                       \
+    prune_count_warp_kernel<KT><<<wgrid, 256, 0, st>>>(d1, nq, idx->nr, k, idx->radii, idx->offsets,             \
+                                                       idx->list_dists, out.gamma.get(), out.nseg.get(),          \
+                                                       out.cand.get(), out.pr, out.p3, out.order_key.get())
+    if (k == 1) RBC_PRUNE_WARP(1);
+    else if (k <= 4) RBC_PRUNE_WARP(4);
+    else if (k <= 16) RBC_PRUNE_WARP(16);
+    else
+        prune_count_kernel<<<static_cast<unsigned>(nq), kPruneThreads, 0, st>>>(
+            d1, idx->nr, k, idx->radii, idx->offsets, idx->list_dists, out.gamma.get(), out.nseg.get(), out.cand.get(),
+            out.pr, out.p3, out.order_key.get());
+#undef RBC_PRUNE_WARP
     RBC_LAUNCHED();
     // seg_off = exclusive scan of nseg (int32 -> int64)
     RBC_CUDA(cudaMemsetAsync(out.seg_off.get(), 0, sizeof(int64_t), st));
@@ -200,9 +322,9 @@ int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &ou
     RBC_CHECK(out.seg_start.alloc(total, st));
     RBC_CHECK(out.seg_len.alloc(total, st));
     RBC_CHECK(out.seg_list.alloc(total, st));
-    prune_fill_kernel<<<static_cast<unsigned>(nq), kPruneThreads, 0, st>>>(
-        d1, idx->nr, out.gamma.get(), idx->radii, idx->offsets, idx->list_dists, out.seg_off.get(),
-        out.seg_start.get(), out.seg_len.get(), out.seg_list.get());
+    prune_fill_warp_kernel<<<wgrid, 256, 0, st>>>(d1, nq, idx->nr, out.gamma.get(), idx->radii, idx->offsets,
+                                                  idx->list_dists, out.seg_off.get(), out.seg_start.get(),
+                                                  out.seg_len.get(), out.seg_list.get());
     RBC_LAUNCHED();
     return RBC_OK;
 }

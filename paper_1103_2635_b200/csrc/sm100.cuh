@@ -88,6 +88,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// K-major operand in the canonical SWIZZLE_32B layout: rows of 32 bytes
+// (16 f16 = one K=16 step), 8-row (256 B) atoms stacked with SBO = 256 B.
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(256 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(6) << 61;  // SWIZZLE_32B
+    return d;
+}
+
 // kind::f16 instruction descriptor: A,B = f16, D = f32, both K-major.
 __device__ __forceinline__ uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
     return (1u << 4)             // D format f32

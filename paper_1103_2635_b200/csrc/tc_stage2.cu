@@ -5,26 +5,31 @@
 // rep)).  For every list p in the union of the tile's survivors, and every
 // 256-row chunk of p's scanned prefix:
 //
-//   A_p = f16((q_i - r_p) * sA)   128 x 64, K-major SWIZZLE_128B, built by 4 "prep" warps
-//   B   = f16((x_j - r_p) * sB_p) N x 64 rows, pre-swizzled in HBM, one cp.async.bulk per chunk
+//   A_p = f16((q_i - r_p) * sA)   128 x 64 (+16), K-major, built by 4 "prep" warps
+//   B   = f16((x_j - r_p) * sB_p) N x 64 (+16) rows, pre-swizzled in HBM, cp.async.bulk per chunk
 //   D   = A_p . B^T               tcgen05.mma kind::f16 into TMEM (fp32), double-buffered
 //
 // Centering both operands on the list's representative keeps |a|,|b| at the
 // scale of the query->rep and point->rep distances, so the expanded form
 //   d^2 = |q - r_p|^2 + |x - r_p|^2 - 2 (q - r_p).(x - r_p)
-// (the first term is stage 1's exact distance) has an error bound
-//   E <= C1 |a||b| + C2 (|a|^2 + |b|^2) + ...
+// (the first term is stage 1's exact distance) has a rigorous error bound
+//   E <= C1 |a||b| + C2 (|a|^2 + |b|^2) + C4 |b| / sA
 // small enough that only a handful of points per query need the exact
-// re-rank.  The epilogue (4 warps, one TMEM lane = one query row per thread)
-// tests every element against the row's running k-th best upper bound with
-// one FFMA + one max per element; survivors of the filter are appended to a
-// per-query candidate buffer.  At the end of the tile each row re-ranks its
-// buffered candidates with the reference's exact fp64 arithmetic
+// re-rank.  The per-column term |x - r_p|^2 / 2 is folded into the MMA as
+// two extra K columns (hi/lo f16 split; A side = -sA/sB), so the
+// accumulator is directly V = sA sB ((q-r).(x-r) - |x-r|^2/2), and
+//   lb = |q - r_p|^2 - E - 2 V / (sA sB)  <=  d^2  <=  lb + 2E.
+// The epilogue (4 warps, one TMEM lane = one query row per thread) reduces
+// each 32-column chunk to its maximum V (3-input FMNMX), updates the row's
+// running best upper bound from it (k = 1) and only drops to the slow path
+// when some element can still beat the k-th best; there candidates are
+// appended to a per-query buffer.  At the end of the tile each row re-ranks
+// its buffered candidates with the reference's exact fp64 arithmetic
 // (common.cuh exact_dist) and emits key64 = (f32 dist, id), so results are
 // bit-identical to the reference.  A query whose buffer overflows is
 // recomputed by the exact SIMT scan.
 //
-// Roles (320 threads, 1 CTA per SM, persistent over tiles):
+// Roles (320 threads, 1 CTA per SM, persistent over tiles in LPT order):
 //   warp 0      producer: cp.async.bulk of B chunks into a 4-stage ring
 //   warp 1      MMA issuer + TMEM owner (512 columns = 2 x 256 fp32 accumulators)
 //   warps 2..5  epilogue / candidate filter / exact re-rank
@@ -49,24 +54,31 @@ constexpr int kNmax = 256;       // max UMMA N per chunk
 constexpr int kStages = 4;       // B ring depth
 constexpr int kThreads = 320;    // 10 warps
 constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
+constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
+constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
+constexpr int kStageBytes = kNmax * (kP0 + kP1);
+constexpr int kABytes = kRows * (kP0 + kP1);
 
-// error-bound constants (see header comment; factor 2 safety on each term)
-constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 64.0f / 4194304.0f);  // f16 rounding of a and b, fp32 accumulate
-constexpr float kC2 = 1.0f / 1048576.0f;                             // fp32 rounding of norms / epilogue
-constexpr float kC4 = 1.0f / 262144.0f;                              // f16 subnormal flush (absolute, scaled)
-constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                      // rounding-up factor for norms
-constexpr float kTie = 1.0f + 1.0f / 524288.0f;                      // tie slack: 8 fp32 ulps of the distance
+// error-bound constants (factor-2 safety on each term; K <= 80 accumulated products)
+constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 128.0f / 4194304.0f);  // f16 rounding of a and b, fp32 accumulate
+constexpr float kC2 = 1.0f / 1048576.0f;                              // norms, aug split, epilogue rounding
+constexpr float kC4 = 1.0f / 262144.0f;                               // f16 subnormal flush (absolute, scaled)
+constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                       // rounding-up factor for norms
+constexpr float kTie = 1.0f + 1.0f / 524288.0f;                       // tie slack: 8 fp32 ulps of the distance
 
 struct TcIndex {
     int64_t npad = 0;
-    __half *xh = nullptr;    // [npad + tail][64] f16 residual rows, SW128 pre-swizzled
-    float *gcol = nullptr;   // [npad + tail] (|x - r_p|^2 / 2) * sB_p
-    int64_t *poff = nullptr; // [nr + 1] padded (8-row aligned) list offsets
-    float *sB = nullptr;     // [nr] per-list power-of-two scale
+    bool plane1 = false;      // aug columns in a separate 16-wide plane (d > 62)
+    uint8_t *xh0 = nullptr;   // [npad + tail][128 B] f16 residual rows (+aug when d <= 62), SW128 pre-swizzled
+    uint8_t *xh1 = nullptr;   // [npad + tail][32 B] aug plane, SW32 pre-swizzled (d > 62 only)
+    float *gcol = nullptr;    // [npad + tail] (|x - r_p|^2 / 2) * sB_p (fallback when -sA/sB is not an f16 normal)
+    int64_t *poff = nullptr;  // [nr + 1] padded (8-row aligned) list offsets
+    float *sB = nullptr;      // [nr] per-list power-of-two scale
 };
 
 struct S2Params {
-    const __half *xh;
+    const uint8_t *xh0;
+    const uint8_t *xh1;
     const float *gcol;
     const int64_t *poff;
     const float *sB;
@@ -76,12 +88,14 @@ struct S2Params {
     const float *xp;
     const int32_t *perm;
     int d;
+    int plane1;
     int64_t nr;
     const float *q;
     const float *d1;
     const float *gamma;
     int k;
     int ntiles;
+    const int32_t *tile_order;
     const int32_t *tile_rows;
     const int64_t *work_off;
     const int32_t *work_p;
@@ -99,6 +113,16 @@ struct S2Params {
 
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
 
+// A-side coefficient of the folded |b|^2 term: -sA / sB when that is an f16 normal, else 0 (epilogue subtracts)
+__device__ __forceinline__ float aug_coeff(float sa, float sb) {
+    const float c = sa / sb;  // exact: both powers of two
+    return (c >= 6.103515625e-05f && c <= 32768.0f) ? -c : 0.0f;
+}
+
+__device__ __forceinline__ float max8(const float *v) {
+    return fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+}
+
 // ---- index preparation ----------------------------------------------------------
 __global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, float *__restrict__ sB) {
     const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -109,11 +133,11 @@ __global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, f
     sB[p] = r > 0.f ? ldexpf(1.0f, -e) : 1.0f;
 }
 
-// one block per list: f16 residual rows (pre-swizzled) + (|b|^2 / 2) * sB
+// one block per list: f16 residual rows (pre-swizzled), folded-norm columns, fallback column
 __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *__restrict__ reps,
                                      const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff,
-                                     const float *__restrict__ sB, int d, __half *__restrict__ xh,
-                                     float *__restrict__ gcol) {
+                                     const float *__restrict__ sB, int d, int plane1, uint8_t *__restrict__ xh0,
+                                     uint8_t *__restrict__ xh1, float *__restrict__ gcol) {
     const int64_t p = blockIdx.x;
     const int64_t len = offsets[p + 1] - offsets[p];
     const float s = sB[p];
@@ -122,7 +146,17 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
         const float *x = xp + (offsets[p] + j) * d;
         const int64_t row = poff[p] + j;
         double h = 0.0;
-        uint8_t *dst = reinterpret_cast<uint8_t *>(xh) + row * 128;
+        for (int k = 0; k < d; ++k) {
+            const double b = __fsub_rn(x[k], r[k]);
+            h += b * b;
+        }
+        const float hf = static_cast<float>(h);
+        const float gp = hf * 0.5f * s * s;  // (|b|^2 / 2) sB^2, < 0.5
+        const __half ghi = __float2half_rn(gp);
+        const __half glo = __float2half_rn(gp - __half2float(ghi));
+        const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ghi)) |
+                             (static_cast<uint32_t>(__half_as_ushort(glo)) << 16);
+        uint8_t *dst = xh0 + row * kP0;
         for (int c = 0; c < 8; ++c) {
             uint32_t w[4];
 #pragma unroll
@@ -130,12 +164,18 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
                 const int k0 = c * 8 + 2 * e, k1 = k0 + 1;
                 const float b0 = k0 < d ? __fsub_rn(x[k0], r[k0]) : 0.f;
                 const float b1 = k1 < d ? __fsub_rn(x[k1], r[k1]) : 0.f;
-                h += static_cast<double>(b0) * b0 + static_cast<double>(b1) * b1;
                 w[e] = sm100::pack_f16x2_sat(b0 * s, b1 * s);
             }
+            if (!plane1 && c == 7) w[3] = aug;  // columns 62, 63
             *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        gcol[row] = static_cast<float>(h) * 0.5f * s;
+        if (plane1) {
+            uint8_t *d1p = xh1 + row * kP1;
+            const int sw = static_cast<int>((row >> 2) & 1);
+            *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
+            *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
+        }
+        gcol[row] = hf * 0.5f * s;
     }
 }
 
@@ -171,12 +211,13 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     if (threadIdx.x == 0) nwork[blockIdx.x] = s_count;
 }
 
-// union of the tile's surviving lists: work entries (list, extent, A scale) and per-row cutoffs
+// union of the tile's surviving lists: work entries (list, extent, A scale), per-row
+// cutoffs, and the tile's total work (for the LPT order)
 __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int32_t *__restrict__ rows, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_list,
     const int32_t *__restrict__ seg_len, const uint64_t *__restrict__ order_key, const float *__restrict__ d1,
     int64_t nr, const int64_t *__restrict__ work_off, int32_t *__restrict__ work_p, int32_t *__restrict__ work_ext,
-    float *__restrict__ work_sA, int32_t *__restrict__ cut) {
+    float *__restrict__ work_sA, int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key) {
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
@@ -184,11 +225,12 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     typedef cub::BlockScan<int, kRows> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int s_base;
-    __shared__ unsigned long long s_front;
+    __shared__ unsigned long long s_front, s_work;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) maxlen[p] = maxd1[p] = nearcnt[p] = 0;
     if (threadIdx.x == 0) {
         s_base = 0;
         s_front = ~0ull;
+        s_work = 0;
     }
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
@@ -202,9 +244,13 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     __syncthreads();
     // front list = the most common nearest rep of the tile (ties: lowest position)
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x)
+    unsigned long long wsum = 0;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+        wsum += maxlen[p];
         if (maxlen[p] > 0 && nearcnt[p] > 0)
             atomicMin(&s_front, (static_cast<unsigned long long>(kRows - nearcnt[p]) << 32) | static_cast<uint64_t>(p));
+    }
+    atomicAdd(&s_work, wsum);
     __syncthreads();
     const int32_t front = s_front == ~0ull ? -1 : static_cast<int32_t>(s_front & 0xFFFFFFFFu);
     const int64_t w0 = work_off[blockIdx.x];
@@ -236,6 +282,11 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     if (qi >= 0)
         for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s)
             cut[(w0 + nearcnt[seg_list[s]]) * kRows + threadIdx.x] = seg_len[s];
+    // LPT: heavier tiles first
+    if (threadIdx.x == 0) {
+        const unsigned long long wk = s_work < 0xFFFFFFFFFFull ? s_work : 0xFFFFFFFFFFull;
+        tile_key[blockIdx.x] = 0xFFFFFFFFFFull - wk;
+    }
 }
 
 // ---- the stage-2 kernel -----------------------------------------------------------------
@@ -243,9 +294,10 @@ template <int KT>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t *sB = smem;                                   // kStages x kNmax x 128 B
-    uint8_t *sA = sB + kStages * kNmax * 128;             // 2 x 128 x 128 B
-    float *gbuf = reinterpret_cast<float *>(sA + 2 * kRows * 128);  // 4 epilogue warps x kNmax
+    uint8_t *sB = smem;                                   // kStages x (plane 0 | plane 1)
+    uint8_t *sA = sB + kStages * kStageBytes;             // 2 x (plane 0 | plane 1)
+    float *scratch = reinterpret_cast<float *>(sA + 2 * kABytes);  // 128 threads x 32 floats
+    float *gbuf = scratch + kRows * 32;                   // 4 epilogue warps x kNmax (fallback column)
     uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 4 * kNmax);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
     uint64_t *afull = tempty + 2, *aempty = afull + 2;
@@ -277,10 +329,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     const int row = quad * 32 + lane;  // TMEM lane / tile row owned by this thread (epilogue + prep)
 
     for (;;) {
-        if (tid == 0) *s_tile = atomicAdd(P.tile_counter, 1);
+        if (tid == 0) {
+            const int t = atomicAdd(P.tile_counter, 1);
+            *s_tile = t < P.ntiles ? P.tile_order[t] : -1;
+        }
         __syncthreads();
         const int tile = *s_tile;
-        if (tile >= P.ntiles) break;
+        if (tile < 0) break;
         const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
 
         if (warp == 0) {
@@ -293,9 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         const int n = min(kNmax, roundup16(ext - off));
                         const uint32_t s = bi % kStages;
                         sm100::mbar_wait(&empty[s], ((bi / kStages) & 1) ^ 1);
-                        const uint32_t bytes = static_cast<uint32_t>(n) * 128u;
-                        sm100::mbar_arrive_expect_tx(&full[s], bytes);
-                        sm100::bulk_g2s(sB + s * (kNmax * 128), P.xh + (base + off) * 64, bytes, &full[s]);
+                        uint8_t *dst = sB + s * kStageBytes;
+                        const uint32_t b0 = static_cast<uint32_t>(n) * kP0;
+                        const uint32_t b1 = P.plane1 ? static_cast<uint32_t>(n) * kP1 : 0u;
+                        sm100::mbar_arrive_expect_tx(&full[s], b0 + b1);
+                        sm100::bulk_g2s(dst, P.xh0 + (base + off) * kP0, b0, &full[s]);
+                        if (b1) sm100::bulk_g2s(dst + kNmax * kP0, P.xh1 + (base + off) * kP1, b1, &full[s]);
                         ++bi;
                     }
                 }
@@ -308,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     const uint32_t a = ai & 1;
                     sm100::mbar_wait(&afull[a], (ai >> 1) & 1);
                     sm100::tc_fence_after();
-                    const uint32_t a_base = sm100::smem_u32(sA + a * (kRows * 128));
+                    const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
                     for (int off = 0; off < ext; off += kNmax) {
                         const int n = min(kNmax, roundup16(ext - off));
                         const uint32_t s = bi % kStages, tb = ti & 1;
@@ -316,11 +374,15 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         sm100::mbar_wait(&tempty[tb], ((ti >> 1) & 1) ^ 1);
                         sm100::tc_fence_after();
                         const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
-                        const uint32_t b_base = sm100::smem_u32(sB + s * (kNmax * 128));
+                        const uint32_t b0 = sm100::smem_u32(sB + s * kStageBytes);
+                        const uint32_t d_tmem = tmem + tb * kNmax;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
-                            sm100::umma_f16(tmem + tb * kNmax, sm100::umma_desc_sw128(a_base + kk * 32),
-                                            sm100::umma_desc_sw128(b_base + kk * 32), idesc, kk > 0);
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32),
+                                            sm100::umma_desc_sw128(b0 + kk * 32), idesc, kk > 0);
+                        if (P.plane1)
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(a0 + kRows * kP0),
+                                            sm100::umma_desc_sw32(b0 + kNmax * kP0), idesc, 1);
                         sm100::umma_commit(&empty[s]);
                         sm100::umma_commit(&tfull[tb]);
                         ++bi;
@@ -331,15 +393,18 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 }
             }
         } else if (warp >= 6) {
-            // ===== A-operand prep: row i = f16((q_i - r_p) * sA) =====
+            // ===== A-operand prep: row i = f16((q_i - r_p) * sA), aug columns = -sA/sB =====
             const int32_t qi = P.tile_rows[tile * kRows + row];
             const float *qrow = P.q + static_cast<int64_t>(qi < 0 ? 0 : qi) * P.d;
             for (int64_t w = w0; w < w1; ++w) {
                 const uint32_t a = ai & 1;
                 sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
+                const int32_t p = P.work_p[w];
                 const float sa = P.work_sA[w];
-                const float *rep = P.reps + static_cast<int64_t>(P.work_p[w]) * P.d;
-                uint8_t *dst = sA + a * (kRows * 128) + row * 128;
+                const float *rep = P.reps + static_cast<int64_t>(p) * P.d;
+                const __half ac = __float2half_rn(aug_coeff(sa, P.sB[p]));
+                const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
+                uint8_t *dst = sA + a * kABytes + row * kP0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     uint32_t wv[4];
@@ -351,7 +416,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         if (qi >= 0 && k1 < P.d) v1 = fmaf(qrow[k1], sa, -(rep[k1] * sa));
                         wv[e] = sm100::pack_f16x2_sat(v0, v1);
                     }
+                    if (!P.plane1 && c == 7) wv[3] = aug;
                     *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                if (P.plane1) {
+                    uint8_t *d1p = sA + a * kABytes + kRows * kP0 + row * kP1;
+                    const int sw = (row >> 2) & 1;
+                    *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
                 }
                 sm100::fence_proxy_async_smem();
                 __syncwarp();
@@ -361,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         } else {
             // ===== epilogue: filter, candidate buffer, exact re-rank =====
             float *g = gbuf + (warp - 2) * kNmax;
+            float *scr = scratch + row * 32;
             const int32_t qi = P.tile_rows[tile * kRows + row];
             const bool live = qi >= 0;
             float ubk[KT];
@@ -380,7 +453,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const int cutv = live ? P.cut[w * kRows + row] : 0;
                 const float sa = P.work_sA[w];
                 const float sb = P.sB[p];
-                const float scale = sa * sb;
+                const bool noaug = aug_coeff(sa, sb) == 0.0f;  // warp-uniform (per work item)
+                const float scale = sa * sb, inv2s = 2.0f / scale;
                 const int64_t poff = P.poff[p];
                 const int64_t csr = P.offsets[p];
                 float A2 = 0.f, E = 0.f;
@@ -390,16 +464,17 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     A2 = dq * dq;
                     E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
+                // V >= T  <=>  lb = A2 - E - 2 V / scale <= U * kTie   (loosened by 2^-18 relative)
                 auto threshold = [&]() {
-                    // V >= T  <=>  lb = A2 - E - 2 V / scale <= U * kTie   (loosened by 2^-18 relative)
                     const float t = 0.5f * scale * (A2 - E - U * kTie);
                     return t - fabsf(t) * (1.0f / 262144.0f) - 1e-30f;
                 };
                 float T = cutv > 0 ? threshold() : __int_as_float(0x7f800000);
+                float vbest = -__int_as_float(0x7f800000);
                 for (int off = 0; off < ext; off += kNmax) {
                     const int n = min(kNmax, roundup16(ext - off));
-                    // per-column (|b|^2 / 2) * sB for this chunk -> warp-private smem
-                    {
+                    if (noaug) {
+                        // rare: per-column norm term subtracted in the epilogue instead of the MMA
                         const float *src = P.gcol + poff + off;
                         float4 g0 = make_float4(0, 0, 0, 0), g1 = g0;
                         if (lane * 8 < n) {
@@ -418,21 +493,39 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     for (int c0 = 0; c0 < wlim; c0 += 32) {
                         float v[32];
                         sm100::tmem_ld32(tmem + tb * kNmax + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
-                        float m = -__int_as_float(0x7f800000);
+                        if (noaug) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            v[j] = fmaf(-sa, g[c0 + j], v[j]);
-                            m = fmaxf(m, v[j]);
+                            for (int j = 0; j < 32; ++j) v[j] = fmaf(-sa, g[c0 + j], v[j]);
                         }
-                        if (m >= T && c0 < lim) {
-                            // slow path: push every element that passes the exact-bound test
-                            float vv[32];
+                        if (c0 + 32 > lim) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) vv[j] = v[j];
-#pragma unroll 1
-                            for (int j = 0; j < 32; ++j) {
-                                if (c0 + j >= lim || !(vv[j] >= T)) continue;
-                                const float lb = A2 - E - 2.0f * vv[j] / scale;
+                            for (int j = 0; j < 32; ++j)
+                                if (c0 + j >= lim) v[j] = -__int_as_float(0x7f800000);
+                        }
+                        const float m0 = max8(v), m1 = max8(v + 8), m2 = max8(v + 16), m3 = max8(v + 24);
+                        const float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+                        if (KT == 1 && m > vbest) {
+                            // k = 1: the chunk's best element bounds the nearest candidate
+                            vbest = m;
+                            const float ub = A2 + E - m * inv2s;
+                            if (ub < U) {
+                                U = ub;
+                                T = threshold();
+                            }
+                        }
+                        if (m >= T) {
+                            // slow path: stage the chunk, visit only elements that pass
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                *reinterpret_cast<float4 *>(scr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            unsigned mask = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
+                            while (mask) {
+                                const int j = __ffs(mask) - 1;
+                                mask &= mask - 1;
+                                const float vj = scr[j];
+                                const float lb = A2 - E - vj * inv2s;
                                 if (!(lb <= U * kTie)) continue;
                                 const float ub = lb + 2.0f * E;
                                 if (count == P.cap && !overflow) {
@@ -454,7 +547,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                     cpos[count] = static_cast<int32_t>(csr + off + c0 + j);
                                     ++count;
                                 }
-                                // running k-th best upper bound
                                 if (KT == 1) {
                                     U = fminf(U, ub);
                                 } else {
@@ -525,6 +617,9 @@ __global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int3
     if (t < m * k) dst[static_cast<int64_t>(ids[t / k]) * k + t % k] = src[t];
 }
 
+constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kRows * 32 * sizeof(float) +
+                              4 * kNmax * sizeof(float) + 256;
+
 }  // namespace
 
 int64_t &last_overflow_count() {
@@ -536,6 +631,7 @@ int64_t &last_overflow_count() {
 int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
     if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->n_local == 0) return RBC_OK;
     TcIndex *tc = new TcIndex();
+    tc->plane1 = idx->d > 62;
     std::vector<int64_t> off(idx->nr + 1), poff(idx->nr + 1, 0);
     RBC_CUDA(cudaMemcpyAsync(off.data(), idx->offsets, sizeof(int64_t) * (idx->nr + 1), cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaStreamSynchronize(st));
@@ -543,27 +639,33 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
     tc->npad = poff[idx->nr];
     const int64_t rows = tc->npad + kTailRows;
     auto cleanup = [&](int rc) {
-        cudaFree(tc->xh);
+        cudaFree(tc->xh0);
+        cudaFree(tc->xh1);
         cudaFree(tc->gcol);
         cudaFree(tc->poff);
         cudaFree(tc->sB);
         delete tc;
         return rc;
     };
-    if (cudaMalloc(&tc->xh, rows * 128) != cudaSuccess || cudaMalloc(&tc->gcol, rows * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&tc->poff, (idx->nr + 1) * sizeof(int64_t)) != cudaSuccess ||
-        cudaMalloc(&tc->sB, idx->nr * sizeof(float)) != cudaSuccess) {
+    bool ok = cudaMalloc(&tc->xh0, rows * kP0) == cudaSuccess &&
+              (!tc->plane1 || cudaMalloc(&tc->xh1, rows * kP1) == cudaSuccess) &&
+              cudaMalloc(&tc->gcol, rows * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&tc->poff, (idx->nr + 1) * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&tc->sB, idx->nr * sizeof(float)) == cudaSuccess;
+    if (!ok) {
         cudaGetLastError();
         return cleanup(fail(RBC_ENOMEM, "tc index allocation"));
     }
-    idx->bytes += rows * (128 + sizeof(float)) + (idx->nr + 1) * sizeof(int64_t) + idx->nr * sizeof(float);
-    if (cudaMemsetAsync(tc->xh, 0, rows * 128, st) != cudaSuccess ||
+    idx->bytes += rows * (kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (idx->nr + 1) * sizeof(int64_t) +
+                  idx->nr * sizeof(float);
+    if (cudaMemsetAsync(tc->xh0, 0, rows * kP0, st) != cudaSuccess ||
+        (tc->plane1 && cudaMemsetAsync(tc->xh1, 0, rows * kP1, st) != cudaSuccess) ||
         cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
         cudaMemcpyAsync(tc->poff, poff.data(), sizeof(int64_t) * (idx->nr + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
         return cleanup(fail(RBC_ECUDA, "tc index init"));
     list_scale_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->radii, idx->nr, tc->sB);
-    residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(idx->xp, idx->reps, idx->offsets, tc->poff,
-                                                                        tc->sB, idx->d, tc->xh, tc->gcol);
+    residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(
+        idx->xp, idx->reps, idx->offsets, tc->poff, tc->sB, idx->d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol);
     note_launch(2);
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
         return cleanup(fail(RBC_ECUDA, "tc index kernels"));
@@ -574,7 +676,8 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
 void tc_index_release(rbc_index *idx) {
     TcIndex *tc = static_cast<TcIndex *>(idx->tc);
     if (!tc) return;
-    cudaFree(tc->xh);
+    cudaFree(tc->xh0);
+    cudaFree(tc->xh1);
     cudaFree(tc->gcol);
     cudaFree(tc->poff);
     cudaFree(tc->sB);
@@ -594,136 +697,148 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     const int64_t nr = idx->nr;
     const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
     // 1. group queries: sort by (first surviving list, nearest rep)
-    DevBuf<uint64_t> skey;
-    DevBuf<int32_t> ids, order, rows;
+    DevBuf<uint64_t> skey, tkey, tkey_sorted;
+    DevBuf<int32_t> ids, order, rows, tids, tile_order;
     RBC_CHECK(skey.alloc(nq, st));
     RBC_CHECK(ids.alloc(nq, st));
     RBC_CHECK(order.alloc(nq, st));
     RBC_CHECK(rows.alloc(static_cast<int64_t>(ntiles) * kRows, st));
+    RBC_CHECK(tkey.alloc(ntiles, st));
+    RBC_CHECK(tkey_sorted.alloc(ntiles, st));
+    RBC_CHECK(tids.alloc(ntiles, st));
+    RBC_CHECK(tile_order.alloc(ntiles, st));
     iota_kernel<<<grid_for(nq, 256), 256, 0, st>>>(ids.get(), nq);
     RBC_LAUNCHED();
+    iota_kernel<<<grid_for(ntiles, 256), 256, 0, st>>>(tids.get(), ntiles);
+    RBC_LAUNCHED();
     {
-        size_t tb = 0;
+        size_t tb = 0, tb2 = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq, 0, 48, st);
+        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles,
+                                        0, 40, st);
         DevBuf<unsigned char> tmp;
-        RBC_CHECK(tmp.alloc(tb, st));
+        RBC_CHECK(tmp.alloc(tb > tb2 ? tb : tb2, st));
         RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, po.order_key.get(), skey.get(), ids.get(), order.get(),
                                                  nq, 0, 48, st));
         note_launch();
-    }
-    tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
-        order.get(), nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
-    RBC_LAUNCHED();
-    // 2. union of surviving lists per tile
-    DevBuf<int64_t> nwork, work_off;
-    RBC_CHECK(nwork.alloc(ntiles, st));
-    RBC_CHECK(work_off.alloc(ntiles + 1, st));
-    const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
-    if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
-    cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
-    cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
-    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), nr, nwork.get());
-    RBC_LAUNCHED();
-    RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
-    {
-        size_t tb = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tb, nwork.get(), work_off.get() + 1, ntiles, st);
-        DevBuf<unsigned char> tmp;
-        RBC_CHECK(tmp.alloc(tb, st));
-        RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, nwork.get(), work_off.get() + 1, ntiles, st));
+        tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
+            order.get(), nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
+        RBC_LAUNCHED();
+        // 2. union of surviving lists per tile
+        DevBuf<int64_t> nwork;
+        RBC_CHECK(nwork.alloc(ntiles, st));
+        const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
+        if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
+        cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
+        cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
+        tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), nr, nwork.get());
+        RBC_LAUNCHED();
+        DevBuf<int64_t> work_off;
+        RBC_CHECK(work_off.alloc(ntiles + 1, st));
+        RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
+        size_t tb3 = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tb3, nwork.get(), work_off.get() + 1, ntiles, st);
+        DevBuf<unsigned char> tmp3;
+        RBC_CHECK(tmp3.alloc(tb3, st));
+        RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp3.get(), tb3, nwork.get(), work_off.get() + 1, ntiles, st));
         note_launch();
-    }
-    int64_t total_work = 0;
-    RBC_CUDA(cudaMemcpyAsync(&total_work, work_off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    RBC_CUDA(cudaStreamSynchronize(st));
-    DevBuf<int32_t> work_p, work_ext, cut;
-    DevBuf<float> work_sA;
-    RBC_CHECK(work_p.alloc(total_work, st));
-    RBC_CHECK(work_ext.alloc(total_work, st));
-    RBC_CHECK(work_sA.alloc(total_work, st));
-    RBC_CHECK(cut.alloc(total_work * kRows, st));
-    RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
-    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), po.seg_len.get(),
-                                                   po.order_key.get(), po.d1, nr, work_off.get(), work_p.get(),
-                                                   work_ext.get(), work_sA.get(), cut.get());
-    RBC_LAUNCHED();
-    // 3. the tensor-core scan
-    const int cap = 64 + 32 * k;
-    DevBuf<float> cand_lb;
-    DevBuf<int32_t> cand_pos, ovf_list, counters;
-    RBC_CHECK(cand_lb.alloc(nq * cap, st));
-    RBC_CHECK(cand_pos.alloc(nq * cap, st));
-    RBC_CHECK(ovf_list.alloc(nq, st));
-    RBC_CHECK(counters.alloc(2, st));
-    RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
-    S2Params P;
-    P.xh = tc->xh;
-    P.gcol = tc->gcol;
-    P.poff = tc->poff;
-    P.sB = tc->sB;
-    P.offsets = idx->offsets;
-    P.radii = idx->radii;
-    P.reps = idx->reps;
-    P.xp = idx->xp;
-    P.perm = idx->perm;
-    P.d = idx->d;
-    P.nr = nr;
-    P.q = q;
-    P.d1 = po.d1;
-    P.gamma = po.gamma.get();
-    P.k = k;
-    P.ntiles = ntiles;
-    P.tile_rows = rows.get();
-    P.work_off = work_off.get();
-    P.work_p = work_p.get();
-    P.work_ext = work_ext.get();
-    P.work_sA = work_sA.get();
-    P.cut = cut.get();
-    P.cand_lb = cand_lb.get();
-    P.cand_pos = cand_pos.get();
-    P.cap = cap;
-    P.out_keys = keys;
-    P.overflow_list = ovf_list.get();
-    P.overflow_count = counters.get();
-    P.tile_counter = counters.get() + 1;
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const size_t smem = 1024 + kStages * kNmax * 128 + 2 * kRows * 128 + 4 * kNmax * sizeof(float) + 256;
-    const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
-    auto launch = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        kern<<<grid, kThreads, smem, st>>>(P);
-    };
-    {
-        ProfScope ps(kPhaseScan, st);
-        if (k == 1) launch(stage2_tc_kernel<1>);
-        else if (k <= 4) launch(stage2_tc_kernel<4>);
-        else if (k <= 8) launch(stage2_tc_kernel<8>);
-        else launch(stage2_tc_kernel<16>);
-    }
-    RBC_LAUNCHED();
-    // 4. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
-    int32_t n_ovf = 0;
-    RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    RBC_CUDA(cudaStreamSynchronize(st));
-    if (n_ovf > 0) {
-        DevBuf<float> qsub;
-        DevBuf<uint64_t> ksub;
-        RBC_CHECK(qsub.alloc(static_cast<int64_t>(n_ovf) * idx->d, st));
-        RBC_CHECK(ksub.alloc(static_cast<int64_t>(n_ovf) * k, st));
-        gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
-            q, ovf_list.get(), n_ovf, idx->d, qsub.get());
+        int64_t total_work = 0;
+        RBC_CUDA(cudaMemcpyAsync(&total_work, work_off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        RBC_CUDA(cudaStreamSynchronize(st));
+        DevBuf<int32_t> work_p, work_ext, cut;
+        DevBuf<float> work_sA;
+        RBC_CHECK(work_p.alloc(total_work, st));
+        RBC_CHECK(work_ext.alloc(total_work, st));
+        RBC_CHECK(work_sA.alloc(total_work, st));
+        RBC_CHECK(cut.alloc(total_work * kRows, st));
+        RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
+        tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), po.seg_len.get(),
+                                                       po.order_key.get(), po.d1, nr, work_off.get(), work_p.get(),
+                                                       work_ext.get(), work_sA.get(), cut.get(), tkey.get());
         RBC_LAUNCHED();
-        SegSubSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), ovf_list.get(), idx->d};
-        RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
-        scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
-                                                                                         n_ovf, k, keys);
+        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
+                                                 tile_order.get(), ntiles, 0, 40, st));
+        note_launch();
+        // 3. the tensor-core scan
+        const int cap = 64 + 32 * k;
+        DevBuf<float> cand_lb;
+        DevBuf<int32_t> cand_pos, ovf_list, counters;
+        RBC_CHECK(cand_lb.alloc(nq * cap, st));
+        RBC_CHECK(cand_pos.alloc(nq * cap, st));
+        RBC_CHECK(ovf_list.alloc(nq, st));
+        RBC_CHECK(counters.alloc(2, st));
+        RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
+        S2Params P;
+        P.xh0 = tc->xh0;
+        P.xh1 = tc->xh1;
+        P.gcol = tc->gcol;
+        P.poff = tc->poff;
+        P.sB = tc->sB;
+        P.offsets = idx->offsets;
+        P.radii = idx->radii;
+        P.reps = idx->reps;
+        P.xp = idx->xp;
+        P.perm = idx->perm;
+        P.d = idx->d;
+        P.plane1 = tc->plane1 ? 1 : 0;
+        P.nr = nr;
+        P.q = q;
+        P.d1 = po.d1;
+        P.gamma = po.gamma.get();
+        P.k = k;
+        P.ntiles = ntiles;
+        P.tile_order = tile_order.get();
+        P.tile_rows = rows.get();
+        P.work_off = work_off.get();
+        P.work_p = work_p.get();
+        P.work_ext = work_ext.get();
+        P.work_sA = work_sA.get();
+        P.cut = cut.get();
+        P.cand_lb = cand_lb.get();
+        P.cand_pos = cand_pos.get();
+        P.cap = cap;
+        P.out_keys = keys;
+        P.overflow_list = ovf_list.get();
+        P.overflow_count = counters.get();
+        P.tile_counter = counters.get() + 1;
+        if (g_num_sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
+        auto launch = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+            kern<<<grid, kThreads, kSmemBytes, st>>>(P);
+        };
+        {
+            ProfScope ps(kPhaseScan, st);
+            if (k == 1) launch(stage2_tc_kernel<1>);
+            else if (k <= 4) launch(stage2_tc_kernel<4>);
+            else if (k <= 8) launch(stage2_tc_kernel<8>);
+            else launch(stage2_tc_kernel<16>);
+        }
         RBC_LAUNCHED();
+        // 4. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
+        int32_t n_ovf = 0;
+        RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        RBC_CUDA(cudaStreamSynchronize(st));
+        if (n_ovf > 0) {
+            DevBuf<float> qsub;
+            DevBuf<uint64_t> ksub;
+            RBC_CHECK(qsub.alloc(static_cast<int64_t>(n_ovf) * idx->d, st));
+            RBC_CHECK(ksub.alloc(static_cast<int64_t>(n_ovf) * k, st));
+            gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
+                q, ovf_list.get(), n_ovf, idx->d, qsub.get());
+            RBC_LAUNCHED();
+            SegSubSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), ovf_list.get(), idx->d};
+            RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
+            scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
+                                                                                             n_ovf, k, keys);
+            RBC_LAUNCHED();
+        }
+        last_overflow_count() = n_ovf;
     }
-    last_overflow_count() = n_ovf;
     return RBC_OK;
 }
 

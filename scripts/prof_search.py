@@ -1,0 +1,37 @@
+"""Profiling driver: build the cfg2 index, run `--iters` exact searches (for ncu / launch lists)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--k", type=int, default=1)
+    args = ap.parse_args()
+    import ctypes
+
+    import torch
+
+    import paper_1103_2635_b200 as rbc
+    from paper_1103_2635_b200 import _lib
+
+    x, q = bench.gen_inputs(0)
+    index = rbc.build_exact(rbc.DataMatrix(x), bench.NR, rbc.MetricSpec("l2", bench.D), seed=bench.REP_SEED)
+    q_dev = _lib.to_device(q)
+    keys = torch.empty((bench.NQ, args.k), dtype=torch.int64, device="cuda")
+    stats = _lib.SearchStatsC(None, None, None, None)
+    sptr = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(args.iters):
+        _lib.check(_lib.lib.rbc_exact_search_keys(index._dev.handle, _lib.ptr(q_dev), bench.NQ, args.k,
+                                                  _lib.ptr(keys), stats, sptr))
+    torch.cuda.synchronize()
+    print("overflows", _lib.lib.rbc_stage2_overflows(), file=sys.stderr)
+
+
+if __name__ == "__main__":
+    main()
