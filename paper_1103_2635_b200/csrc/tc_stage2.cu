@@ -74,6 +74,7 @@ struct TcIndex {
     float *gcol = nullptr;    // [npad + tail] (|x - r_p|^2 / 2) * sB_p (fallback when -sA/sB is not an f16 normal)
     int64_t *poff = nullptr;  // [nr + 1] padded (8-row aligned) list offsets
     float *sB = nullptr;      // [nr] per-list power-of-two scale
+    float *reps64 = nullptr;  // [nr][64] representatives, zero padded
 };
 
 struct S2Params {
@@ -91,9 +92,13 @@ struct S2Params {
     int plane1;
     int64_t nr;
     const float *q;
+    const float *q64;     // queries, rows padded to 64 floats (16-byte aligned)
+    const float *reps64;  // representatives, rows padded to 64 floats
     const float *d1;
     const float *gamma;
     int k;
+    int32_t *cand_count;  // [nq] buffered candidates, -1 = overflow
+    float *cand_ufin;     // [nq] final k-th best upper bound (with tie slack)
     int ntiles;
     const int32_t *tile_order;
     const int32_t *tile_rows;
@@ -394,26 +399,40 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             }
         } else if (warp >= 6) {
             // ===== A-operand prep: row i = f16((q_i - r_p) * sA), aug columns = -sA/sB =====
+            // the row's query stays in registers for the whole tile (padded rep rows
+            // are zero beyond d, so no per-element bounds checks)
             const int32_t qi = P.tile_rows[tile * kRows + row];
-            const float *qrow = P.q + static_cast<int64_t>(qi < 0 ? 0 : qi) * P.d;
+            float qv[64];
+            {
+                const float4 *src = reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(qi < 0 ? 0 : qi) * 64);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const float4 t = qi >= 0 ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    qv[4 * c] = t.x;
+                    qv[4 * c + 1] = t.y;
+                    qv[4 * c + 2] = t.z;
+                    qv[4 * c + 3] = t.w;
+                }
+            }
             for (int64_t w = w0; w < w1; ++w) {
                 const uint32_t a = ai & 1;
-                sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
                 const int32_t p = P.work_p[w];
                 const float sa = P.work_sA[w];
-                const float *rep = P.reps + static_cast<int64_t>(p) * P.d;
+                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(p) * 64);
                 const __half ac = __float2half_rn(aug_coeff(sa, P.sB[p]));
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
+                sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
+                    const float4 r0 = __ldg(rep4 + 2 * c), r1 = __ldg(rep4 + 2 * c + 1);
+                    const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
                     uint32_t wv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int k0 = c * 8 + 2 * e, k1 = k0 + 1;
-                        float v0 = 0.f, v1 = 0.f;
-                        if (qi >= 0 && k0 < P.d) v0 = fmaf(qrow[k0], sa, -(rep[k0] * sa));
-                        if (qi >= 0 && k1 < P.d) v1 = fmaf(qrow[k1], sa, -(rep[k1] * sa));
+                        const int k0 = c * 8 + 2 * e;
+                        const float v0 = fmaf(qv[k0], sa, -(rr[2 * e] * sa));
+                        const float v1 = fmaf(qv[k0 + 1], sa, -(rr[2 * e + 1] * sa));
                         wv[e] = sm100::pack_f16x2_sat(v0, v1);
                     }
                     if (!P.plane1 && c == 7) wv[3] = aug;
@@ -573,28 +592,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     ++ti;
                 }
             }
-            // ---- exact re-rank of the buffered candidates (reference arithmetic) ----
+            // ---- hand the buffered candidates to the exact re-rank kernel ----
             if (live) {
-                if (overflow) {
-                    P.overflow_list[atomicAdd(P.overflow_count, 1)] = qi;
-                } else {
-                    uint64_t best[KT];
-#pragma unroll
-                    for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-                    const float ufin = U * kTie;
-                    const float *qrow = P.q + static_cast<int64_t>(qi) * P.d;
-                    for (int e = 0; e < count; ++e) {
-                        if (!(clb[e] <= ufin)) continue;
-                        const int32_t pos = cpos[e];
-                        const float dist = exact_dist<RBC_L2>(qrow, P.xp + static_cast<int64_t>(pos) * P.d, P.d);
-                        const uint64_t key = pack_key(dist, static_cast<uint32_t>(P.perm[pos]));
-                        if (key < best[KT - 1]) sorted_insert<KT>(best, key);
-                    }
-                    uint64_t *out = P.out_keys + static_cast<int64_t>(qi) * P.k;
-#pragma unroll
-                    for (int j = 0; j < KT; ++j)
-                        if (j < P.k) out[j] = best[j];
-                }
+                P.cand_count[qi] = overflow ? -1 : count;
+                P.cand_ufin[qi] = U * kTie;
+                if (overflow) P.overflow_list[atomicAdd(P.overflow_count, 1)] = qi;
             }
         }
         __syncthreads();
@@ -602,6 +604,44 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 1) sm100::tmem_dealloc<512>(tmem);
+}
+
+// Exact re-rank (reference arithmetic) of the buffered candidates: one warp per
+// query, one candidate per lane, warp merge of the lanes' sorted key64 lists.
+template <int KT>
+__global__ void __launch_bounds__(256) rerank_kernel(const float *__restrict__ cand_lb,
+                                                     const int32_t *__restrict__ cand_pos,
+                                                     const int32_t *__restrict__ cand_count,
+                                                     const float *__restrict__ cand_ufin, int cap, int64_t nq,
+                                                     const float *__restrict__ q, const float *__restrict__ xp,
+                                                     const int32_t *__restrict__ perm, int d, int k,
+                                                     uint64_t *__restrict__ out_keys) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (i >= nq) return;
+    const int cnt = cand_count[i];
+    if (cnt < 0) return;  // overflowed: recomputed by the exact scan
+    const float ufin = cand_ufin[i];
+    const float *qrow = q + i * d;
+    uint64_t best[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+    for (int e = lane; e < cnt; e += 32) {
+        if (!(cand_lb[i * cap + e] <= ufin)) continue;
+        const int32_t pos = cand_pos[i * cap + e];
+        const float dist = exact_dist<RBC_L2>(qrow, xp + static_cast<int64_t>(pos) * d, d);
+        const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos]));
+        if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+    }
+    warp_merge_sorted<KT>(best, k, out_keys + i * k);
+}
+
+__global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= rows * 64) return;
+    const int64_t r = t >> 6;
+    const int c = static_cast<int>(t & 63);
+    dst[t] = c < d ? src[r * d + c] : 0.f;
 }
 
 __global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
@@ -644,6 +684,7 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaFree(tc->gcol);
         cudaFree(tc->poff);
         cudaFree(tc->sB);
+        cudaFree(tc->reps64);
         delete tc;
         return rc;
     };
@@ -651,7 +692,8 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
               (!tc->plane1 || cudaMalloc(&tc->xh1, rows * kP1) == cudaSuccess) &&
               cudaMalloc(&tc->gcol, rows * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&tc->poff, (idx->nr + 1) * sizeof(int64_t)) == cudaSuccess &&
-              cudaMalloc(&tc->sB, idx->nr * sizeof(float)) == cudaSuccess;
+              cudaMalloc(&tc->sB, idx->nr * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&tc->reps64, idx->nr * 64 * sizeof(float)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         return cleanup(fail(RBC_ENOMEM, "tc index allocation"));
@@ -664,6 +706,8 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaMemcpyAsync(tc->poff, poff.data(), sizeof(int64_t) * (idx->nr + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
         return cleanup(fail(RBC_ECUDA, "tc index init"));
     list_scale_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->radii, idx->nr, tc->sB);
+    pad64_rows_kernel<<<grid_for(idx->nr * 64, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, tc->reps64);
+    note_launch();
     residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(
         idx->xp, idx->reps, idx->offsets, tc->poff, tc->sB, idx->d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol);
     note_launch(2);
@@ -681,6 +725,7 @@ void tc_index_release(rbc_index *idx) {
     cudaFree(tc->gcol);
     cudaFree(tc->poff);
     cudaFree(tc->sB);
+    cudaFree(tc->reps64);
     delete tc;
     idx->tc = nullptr;
 }
@@ -766,6 +811,17 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         RBC_CHECK(cand_lb.alloc(nq * cap, st));
         RBC_CHECK(cand_pos.alloc(nq * cap, st));
         RBC_CHECK(ovf_list.alloc(nq, st));
+        DevBuf<int32_t> cand_count;
+        DevBuf<float> cand_ufin, q64buf;
+        RBC_CHECK(cand_count.alloc(nq, st));
+        RBC_CHECK(cand_ufin.alloc(nq, st));
+        const float *q64 = q;
+        if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
+            RBC_CHECK(q64buf.alloc(nq * 64, st));
+            pad64_rows_kernel<<<grid_for(nq * 64, 256), 256, 0, st>>>(q, nq, idx->d, q64buf.get());
+            RBC_LAUNCHED();
+            q64 = q64buf.get();
+        }
         RBC_CHECK(counters.alloc(2, st));
         RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
         S2Params P;
@@ -783,6 +839,10 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         P.plane1 = tc->plane1 ? 1 : 0;
         P.nr = nr;
         P.q = q;
+        P.q64 = q64;
+        P.reps64 = tc->reps64;
+        P.cand_count = cand_count.get();
+        P.cand_ufin = cand_ufin.get();
         P.d1 = po.d1;
         P.gamma = po.gamma.get();
         P.k = k;
@@ -819,7 +879,20 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
             else launch(stage2_tc_kernel<16>);
         }
         RBC_LAUNCHED();
-        // 4. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
+        // 4. exact re-rank of the buffered candidates
+        {
+            const unsigned rgrid = grid_for(nq * 32, 256);
+#define RBC_RERANK(KT)                                                                                          \
+    rerank_kernel<KT><<<rgrid, 256, 0, st>>>(cand_lb.get(), cand_pos.get(), cand_count.get(), cand_ufin.get(), cap, \
+                                             nq, q, idx->xp, idx->perm, idx->d, k, keys)
+            if (k == 1) RBC_RERANK(1);
+            else if (k <= 4) RBC_RERANK(4);
+            else if (k <= 8) RBC_RERANK(8);
+            else RBC_RERANK(16);
+#undef RBC_RERANK
+            RBC_LAUNCHED();
+        }
+        // 5. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
         int32_t n_ovf = 0;
         RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         RBC_CUDA(cudaStreamSynchronize(st));
