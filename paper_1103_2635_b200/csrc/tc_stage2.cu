@@ -23,16 +23,18 @@
 // each 32-column chunk to its maximum V (3-input FMNMX), updates the row's
 // running best upper bound from it (k = 1) and only drops to the slow path
 // when some element can still beat the k-th best; there candidates are
-// appended to a per-query buffer.  At the end of the tile each row re-ranks
-// its buffered candidates with the reference's exact fp64 arithmetic
+// appended to a per-query buffer.  A separate kernel then re-ranks every
+// buffered candidate with the reference's exact fp64 arithmetic
 // (common.cuh exact_dist) and emits key64 = (f32 dist, id), so results are
 // bit-identical to the reference.  A query whose buffer overflows is
 // recomputed by the exact SIMT scan.
 //
-// Roles (320 threads, 1 CTA per SM, persistent over tiles in LPT order):
-//   warp 0      producer: cp.async.bulk of B chunks into a 4-stage ring
+// Roles (320 threads, 1 CTA per SM, persistent, no CTA-wide barrier in the
+// steady state; tiles come from an LPT-ordered global queue through a
+// 2-slot shared-memory ring):
+//   warp 0      scheduler + producer: cp.async.bulk of B chunks, 4-stage ring
 //   warp 1      MMA issuer + TMEM owner (512 columns = 2 x 256 fp32 accumulators)
-//   warps 2..5  epilogue / candidate filter / exact re-rank
+//   warps 2..5  epilogue / candidate filter
 //   warps 6..9  A-operand prep (query rows centred on the current list's rep)
 #include <cub/cub.cuh>
 
@@ -77,52 +79,45 @@ struct TcIndex {
     float *reps64 = nullptr;  // [nr][64] representatives, zero padded
 };
 
+// one (tile, list) work item, 32 bytes
+struct __align__(16) WorkItem {
+    int32_t p;       // list (rep position)
+    int32_t ext;     // scanned prefix: max cutoff over the tile's rows
+    float sA;        // A scale (power of two)
+    float sB;        // B scale of the list
+    float radius;    // list radius psi_p
+    float aug;       // A-side folded-norm coefficient -sA/sB (0 = subtract in the epilogue)
+    int32_t poff;    // padded row offset of the list in xh0/xh1/gcol
+    int32_t csr;     // CSR offset of the list (positions into xp / perm)
+};
+
 struct S2Params {
     const uint8_t *xh0;
     const uint8_t *xh1;
     const float *gcol;
-    const int64_t *poff;
-    const float *sB;
-    const int64_t *offsets;
-    const float *radii;
-    const float *reps;
-    const float *xp;
-    const int32_t *perm;
-    int d;
+    const float *reps64;
     int plane1;
-    int64_t nr;
-    const float *q;
-    const float *q64;     // queries, rows padded to 64 floats (16-byte aligned)
-    const float *reps64;  // representatives, rows padded to 64 floats
-    const float *d1;
-    const float *gamma;
+    const float *q64;           // queries, rows padded to 64 floats
+    const float *gamma;         // [nq] gamma_k
     int k;
-    int32_t *cand_count;  // [nq] buffered candidates, -1 = overflow
-    float *cand_ufin;     // [nq] final k-th best upper bound (with tie slack)
     int ntiles;
-    const int32_t *tile_order;
-    const int32_t *tile_rows;
-    const int64_t *work_off;
-    const int32_t *work_p;
-    const int32_t *work_ext;
-    const float *work_sA;
-    const int32_t *cut;
+    const int32_t *tile_order;  // LPT order
+    const int32_t *tile_rows;   // [ntiles][128] query ids (-1 = padding)
+    const int64_t *work_off;    // [ntiles + 1]
+    const WorkItem *work;       // [total work]
+    const int32_t *cut;         // [total work][128] per-row cutoff (0 = list not a survivor for the row)
+    const float *rowd1;         // [total work][128] per-row exact dist(q, r_p)
     float *cand_lb;
     int32_t *cand_pos;
     int cap;
-    uint64_t *out_keys;
+    int32_t *cand_count;        // [nq] buffered candidates, -1 = overflow
+    float *cand_ufin;           // [nq] final k-th best upper bound (with tie slack)
     int32_t *overflow_list;
     int32_t *overflow_count;
     int32_t *tile_counter;
 };
 
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
-
-// A-side coefficient of the folded |b|^2 term: -sA / sB when that is an f16 normal, else 0 (epilogue subtracts)
-__device__ __forceinline__ float aug_coeff(float sa, float sb) {
-    const float c = sa / sb;  // exact: both powers of two
-    return (c >= 6.103515625e-05f && c <= 32768.0f) ? -c : 0.0f;
-}
 
 __device__ __forceinline__ float max8(const float *v) {
     return fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
@@ -184,6 +179,14 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
     }
 }
 
+__global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= rows * 64) return;
+    const int64_t r = t >> 6;
+    const int c = static_cast<int>(t & 63);
+    dst[t] = c < d ? src[r * d + c] : 0.f;
+}
+
 // ---- tile preparation -----------------------------------------------------------------
 __global__ void tile_rows_kernel(const int32_t *__restrict__ order, int64_t nq, int64_t total, int32_t *__restrict__ rows) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -216,13 +219,14 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     if (threadIdx.x == 0) nwork[blockIdx.x] = s_count;
 }
 
-// union of the tile's surviving lists: work entries (list, extent, A scale), per-row
-// cutoffs, and the tile's total work (for the LPT order)
+// union of the tile's surviving lists: work items, per-row cutoffs and stage-1
+// distances, and the tile's total work (for the LPT order)
 __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int32_t *__restrict__ rows, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_list,
     const int32_t *__restrict__ seg_len, const uint64_t *__restrict__ order_key, const float *__restrict__ d1,
-    int64_t nr, const int64_t *__restrict__ work_off, int32_t *__restrict__ work_p, int32_t *__restrict__ work_ext,
-    float *__restrict__ work_sA, int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key) {
+    int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
+    const int64_t *__restrict__ offsets, const int64_t *__restrict__ work_off, WorkItem *__restrict__ work,
+    int32_t *__restrict__ cut, float *__restrict__ rowd1, uint64_t *__restrict__ tile_key) {
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
@@ -274,19 +278,30 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     __syncthreads();
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
         if (maxlen[p] > 0) {
-            const int64_t w = w0 + nearcnt[p];
-            work_p[w] = static_cast<int32_t>(p);
-            work_ext[w] = maxlen[p];
+            WorkItem it;
+            it.p = static_cast<int32_t>(p);
+            it.ext = maxlen[p];
             int e = 0;
             const float m = __int_as_float(maxd1[p]);
             if (m > 0.f) frexpf(m, &e);
-            work_sA[w] = m > 0.f ? ldexpf(1.0f, -e) : 1.0f;
+            it.sA = m > 0.f ? ldexpf(1.0f, -e) : 1.0f;
+            it.sB = sB[p];
+            it.radius = radii[p];
+            const float c = it.sA / it.sB;  // exact: both powers of two
+            it.aug = (c >= 6.103515625e-05f && c <= 32768.0f) ? -c : 0.0f;
+            it.poff = static_cast<int32_t>(poff[p]);
+            it.csr = static_cast<int32_t>(offsets[p]);
+            work[w0 + nearcnt[p]] = it;
         }
     }
     __syncthreads();
     if (qi >= 0)
-        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s)
-            cut[(w0 + nearcnt[seg_list[s]]) * kRows + threadIdx.x] = seg_len[s];
+        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) {
+            const int32_t p = seg_list[s];
+            const int64_t at = (w0 + nearcnt[p]) * kRows + threadIdx.x;
+            cut[at] = seg_len[s];
+            rowd1[at] = d1[static_cast<int64_t>(qi) * nr + p];
+        }
     // LPT: heavier tiles first
     if (threadIdx.x == 0) {
         const unsigned long long wk = s_work < 0xFFFFFFFFFFull ? s_work : 0xFFFFFFFFFFull;
@@ -305,9 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     float *gbuf = scratch + kRows * 32;                   // 4 epilogue warps x kNmax (fallback column)
     uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 4 * kNmax);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
-    uint64_t *afull = tempty + 2, *aempty = afull + 2;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(aempty + 2);
-    int *s_tile = reinterpret_cast<int *>(s_tmem + 1);
+    uint64_t *afull = tempty + 2, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
+    int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);  // 2-slot ring of tile ids
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -320,6 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             sm100::mbar_init(&tempty[b], 4);
             sm100::mbar_init(&afull[b], 4);
             sm100::mbar_init(&aempty[b], 1);
+            sm100::mbar_init(&tile_full[b], 1);
+            sm100::mbar_init(&tile_empty[b], 9);  // MMA lane + 4 prep warps + 4 epilogue warps
         }
         sm100::fence_barrier_init();
     }
@@ -329,45 +346,62 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     sm100::tc_fence_after();
     const uint32_t tmem = *s_tmem;
 
-    uint32_t bi = 0, ti = 0, ai = 0;  // ring counters (identical sequence in every role)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;  // TMEM lane / tile row owned by this thread (epilogue + prep)
 
-    for (;;) {
-        if (tid == 0) {
-            const int t = atomicAdd(P.tile_counter, 1);
-            *s_tile = t < P.ntiles ? P.tile_order[t] : -1;
-        }
-        __syncthreads();
-        const int tile = *s_tile;
-        if (tile < 0) break;
-        const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
+    // consumer side of the tile ring: returns the next tile id (-1 = done)
+    auto next_tile = [&](uint32_t it) {
+        const uint32_t slot = it & 1;
+        sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
+        const int t = s_tiles[slot];
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&tile_empty[slot]);
+        return t;
+    };
 
-        if (warp == 0) {
-            // ===== producer =====
-            if (lane == 0) {
-                for (int64_t w = w0; w < w1; ++w) {
-                    const int ext = P.work_ext[w];
-                    const int64_t base = P.poff[P.work_p[w]];
-                    for (int off = 0; off < ext; off += kNmax) {
-                        const int n = min(kNmax, roundup16(ext - off));
+    if (warp == 0) {
+        // ===== scheduler + producer =====
+        if (lane == 0) {
+            uint32_t bi = 0;
+            for (uint32_t it = 0;; ++it) {
+                const uint32_t slot = it & 1;
+                sm100::mbar_wait(&tile_empty[slot], ((it >> 1) & 1) ^ 1);
+                const int t = atomicAdd(P.tile_counter, 1);
+                const int tile = t < P.ntiles ? P.tile_order[t] : -1;
+                s_tiles[slot] = tile;
+                sm100::mbar_arrive(&tile_full[slot]);
+                if (tile < 0) break;
+                for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
+                    const WorkItem wi = P.work[w];
+                    for (int off = 0; off < wi.ext; off += kNmax) {
+                        const int n = min(kNmax, roundup16(wi.ext - off));
                         const uint32_t s = bi % kStages;
                         sm100::mbar_wait(&empty[s], ((bi / kStages) & 1) ^ 1);
                         uint8_t *dst = sB + s * kStageBytes;
                         const uint32_t b0 = static_cast<uint32_t>(n) * kP0;
                         const uint32_t b1 = P.plane1 ? static_cast<uint32_t>(n) * kP1 : 0u;
                         sm100::mbar_arrive_expect_tx(&full[s], b0 + b1);
-                        sm100::bulk_g2s(dst, P.xh0 + (base + off) * kP0, b0, &full[s]);
-                        if (b1) sm100::bulk_g2s(dst + kNmax * kP0, P.xh1 + (base + off) * kP1, b1, &full[s]);
+                        sm100::bulk_g2s(dst, P.xh0 + (static_cast<int64_t>(wi.poff) + off) * kP0, b0, &full[s]);
+                        if (b1)
+                            sm100::bulk_g2s(dst + kNmax * kP0, P.xh1 + (static_cast<int64_t>(wi.poff) + off) * kP1, b1,
+                                            &full[s]);
                         ++bi;
                     }
                 }
             }
-        } else if (warp == 1) {
-            // ===== MMA issuer =====
-            if (lane == 0) {
-                for (int64_t w = w0; w < w1; ++w) {
-                    const int ext = P.work_ext[w];
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            uint32_t bi = 0, ti = 0, ai = 0;
+            for (uint32_t it = 0;; ++it) {
+                const uint32_t slot = it & 1;
+                sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
+                const int tile = s_tiles[slot];
+                sm100::mbar_arrive(&tile_empty[slot]);
+                if (tile < 0) break;
+                for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
+                    const int ext = P.work[w].ext;
                     const uint32_t a = ai & 1;
                     sm100::mbar_wait(&afull[a], (ai >> 1) & 1);
                     sm100::tc_fence_after();
@@ -397,10 +431,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     ++ai;
                 }
             }
-        } else if (warp >= 6) {
-            // ===== A-operand prep: row i = f16((q_i - r_p) * sA), aug columns = -sA/sB =====
-            // the row's query stays in registers for the whole tile (padded rep rows
-            // are zero beyond d, so no per-element bounds checks)
+        }
+    } else if (warp >= 6) {
+        // ===== A-operand prep: row i = f16((q_i - r_p) * sA), aug columns = -sA/sB =====
+        uint32_t ai = 0;
+        for (uint32_t it = 0;; ++it) {
+            const int tile = next_tile(it);
+            if (tile < 0) break;
+            // the row's query stays in registers for the whole tile (rows padded to 64 with zeros)
             const int32_t qi = P.tile_rows[tile * kRows + row];
             float qv[64];
             {
@@ -414,19 +452,22 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     qv[4 * c + 3] = t.w;
                 }
             }
-            for (int64_t w = w0; w < w1; ++w) {
+            for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
                 const uint32_t a = ai & 1;
-                const int32_t p = P.work_p[w];
-                const float sa = P.work_sA[w];
-                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(p) * 64);
-                const __half ac = __float2half_rn(aug_coeff(sa, P.sB[p]));
+                const WorkItem wi = P.work[w];
+                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64);
+                const __half ac = __float2half_rn(wi.aug);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
+                const float sa = wi.sA;
+                float4 rr4[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) rr4[c] = __ldg(rep4 + c);
                 sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const float4 r0 = __ldg(rep4 + 2 * c), r1 = __ldg(rep4 + 2 * c + 1);
-                    const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                    const float rr[8] = {rr4[2 * c].x, rr4[2 * c].y, rr4[2 * c].z, rr4[2 * c].w,
+                                         rr4[2 * c + 1].x, rr4[2 * c + 1].y, rr4[2 * c + 1].z, rr4[2 * c + 1].w};
                     uint32_t wv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -449,10 +490,15 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 if (lane == 0) sm100::mbar_arrive(&afull[a]);
                 ++ai;
             }
-        } else {
-            // ===== epilogue: filter, candidate buffer, exact re-rank =====
-            float *g = gbuf + (warp - 2) * kNmax;
-            float *scr = scratch + row * 32;
+        }
+    } else {
+        // ===== epilogue: filter and candidate buffer =====
+        float *g = gbuf + (warp - 2) * kNmax;
+        float *scr = scratch + row * 32;
+        uint32_t ti = 0;
+        for (uint32_t it = 0;; ++it) {
+            const int tile = next_tile(it);
+            if (tile < 0) break;
             const int32_t qi = P.tile_rows[tile * kRows + row];
             const bool live = qi >= 0;
             float ubk[KT];
@@ -465,21 +511,28 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             bool overflow = false;
             float *clb = P.cand_lb + static_cast<int64_t>(live ? qi : 0) * P.cap;
             int32_t *cpos = P.cand_pos + static_cast<int64_t>(live ? qi : 0) * P.cap;
-
+            const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
+            // per-list row data, prefetched one list ahead
+            int cut_n = 0;
+            float dq_n = 0.f;
+            if (w0 < w1) {
+                cut_n = P.cut[w0 * kRows + row];
+                dq_n = P.rowd1[w0 * kRows + row];
+            }
             for (int64_t w = w0; w < w1; ++w) {
-                const int32_t p = P.work_p[w];
-                const int ext = P.work_ext[w];
-                const int cutv = live ? P.cut[w * kRows + row] : 0;
-                const float sa = P.work_sA[w];
-                const float sb = P.sB[p];
-                const bool noaug = aug_coeff(sa, sb) == 0.0f;  // warp-uniform (per work item)
-                const float scale = sa * sb, inv2s = 2.0f / scale;
-                const int64_t poff = P.poff[p];
-                const int64_t csr = P.offsets[p];
+                const WorkItem wi = P.work[w];
+                const int cutv = live ? cut_n : 0;
+                const float dq = dq_n;
+                if (w + 1 < w1) {
+                    cut_n = P.cut[(w + 1) * kRows + row];
+                    dq_n = P.rowd1[(w + 1) * kRows + row];
+                }
+                const bool noaug = wi.aug == 0.0f;  // warp-uniform (per work item)
+                const float sa = wi.sA;
+                const float scale = sa * wi.sB, inv2s = 2.0f / scale;
                 float A2 = 0.f, E = 0.f;
                 if (cutv > 0) {
-                    const float dq = P.d1[static_cast<int64_t>(qi) * P.nr + p];
-                    const float na = dq * kUp, rb = P.radii[p] * kUp;
+                    const float na = dq * kUp, rb = wi.radius * kUp;
                     A2 = dq * dq;
                     E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
@@ -490,11 +543,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 };
                 float T = cutv > 0 ? threshold() : __int_as_float(0x7f800000);
                 float vbest = -__int_as_float(0x7f800000);
-                for (int off = 0; off < ext; off += kNmax) {
-                    const int n = min(kNmax, roundup16(ext - off));
+                for (int off = 0; off < wi.ext; off += kNmax) {
+                    const int n = min(kNmax, roundup16(wi.ext - off));
                     if (noaug) {
                         // rare: per-column norm term subtracted in the epilogue instead of the MMA
-                        const float *src = P.gcol + poff + off;
+                        const float *src = P.gcol + wi.poff + off;
                         float4 g0 = make_float4(0, 0, 0, 0), g1 = g0;
                         if (lane * 8 < n) {
                             g0 = *reinterpret_cast<const float4 *>(src + lane * 8);
@@ -563,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                 }
                                 if (!overflow) {
                                     clb[count] = lb;
-                                    cpos[count] = static_cast<int32_t>(csr + off + c0 + j);
+                                    cpos[count] = wi.csr + off + c0 + j;
                                     ++count;
                                 }
                                 if (KT == 1) {
@@ -592,14 +645,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     ++ti;
                 }
             }
-            // ---- hand the buffered candidates to the exact re-rank kernel ----
+            // hand the buffered candidates to the exact re-rank kernel
             if (live) {
                 P.cand_count[qi] = overflow ? -1 : count;
                 P.cand_ufin[qi] = U * kTie;
                 if (overflow) P.overflow_list[atomicAdd(P.overflow_count, 1)] = qi;
             }
         }
-        __syncthreads();
     }
     sm100::tc_fence_before();
     __syncthreads();
@@ -636,14 +688,6 @@ __global__ void __launch_bounds__(256) rerank_kernel(const float *__restrict__ c
     warp_merge_sorted<KT>(best, k, out_keys + i * k);
 }
 
-__global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t >= rows * 64) return;
-    const int64_t r = t >> 6;
-    const int c = static_cast<int>(t & 63);
-    dst[t] = c < d ? src[r * d + c] : 0.f;
-}
-
 __global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
                                          float *__restrict__ out) {
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < m * d;
@@ -670,6 +714,7 @@ int64_t &last_overflow_count() {
 // ---- index-side preparation ----------------------------------------------------------------
 int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
     if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->n_local == 0) return RBC_OK;
+    if (idx->n_local + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 work offsets
     TcIndex *tc = new TcIndex();
     tc->plane1 = idx->d > 62;
     std::vector<int64_t> off(idx->nr + 1), poff(idx->nr + 1, 0);
@@ -699,7 +744,7 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
         return cleanup(fail(RBC_ENOMEM, "tc index allocation"));
     }
     idx->bytes += rows * (kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (idx->nr + 1) * sizeof(int64_t) +
-                  idx->nr * sizeof(float);
+                  idx->nr * (65 * sizeof(float));
     if (cudaMemsetAsync(tc->xh0, 0, rows * kP0, st) != cudaSuccess ||
         (tc->plane1 && cudaMemsetAsync(tc->xh1, 0, rows * kP1, st) != cudaSuccess) ||
         cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
@@ -707,10 +752,9 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
         return cleanup(fail(RBC_ECUDA, "tc index init"));
     list_scale_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->radii, idx->nr, tc->sB);
     pad64_rows_kernel<<<grid_for(idx->nr * 64, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, tc->reps64);
-    note_launch();
     residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(
         idx->xp, idx->reps, idx->offsets, tc->poff, tc->sB, idx->d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol);
-    note_launch(2);
+    note_launch(3);
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
         return cleanup(fail(RBC_ECUDA, "tc index kernels"));
     idx->tc = tc;
@@ -756,162 +800,145 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_LAUNCHED();
     iota_kernel<<<grid_for(ntiles, 256), 256, 0, st>>>(tids.get(), ntiles);
     RBC_LAUNCHED();
+    size_t tb = 0, tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq, 0, 48, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles, 0,
+                                    40, st);
+    DevBuf<unsigned char> tmp;
+    RBC_CHECK(tmp.alloc(tb > tb2 ? tb : tb2, st));
+    RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq,
+                                             0, 48, st));
+    note_launch();
+    tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
+        order.get(), nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
+    RBC_LAUNCHED();
+    // 2. union of surviving lists per tile
+    DevBuf<int64_t> nwork, work_off;
+    RBC_CHECK(nwork.alloc(ntiles, st));
+    RBC_CHECK(work_off.alloc(ntiles + 1, st));
+    const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
+    if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
+    cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
+    cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
+    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), nr, nwork.get());
+    RBC_LAUNCHED();
+    RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
+    size_t tb3 = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb3, nwork.get(), work_off.get() + 1, ntiles, st);
+    DevBuf<unsigned char> tmp3;
+    RBC_CHECK(tmp3.alloc(tb3, st));
+    RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp3.get(), tb3, nwork.get(), work_off.get() + 1, ntiles, st));
+    note_launch();
+    int64_t total_work = 0;
+    RBC_CUDA(cudaMemcpyAsync(&total_work, work_off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    DevBuf<WorkItem> work;
+    DevBuf<int32_t> cut;
+    DevBuf<float> rowd1;
+    RBC_CHECK(work.alloc(total_work, st));
+    RBC_CHECK(cut.alloc(total_work * kRows, st));
+    RBC_CHECK(rowd1.alloc(total_work * kRows, st));
+    RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
+    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), po.seg_len.get(),
+                                                   po.order_key.get(), po.d1, nr, tc->sB, idx->radii, tc->poff,
+                                                   idx->offsets, work_off.get(), work.get(), cut.get(), rowd1.get(),
+                                                   tkey.get());
+    RBC_LAUNCHED();
+    RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
+                                             tile_order.get(), ntiles, 0, 40, st));
+    note_launch();
+    // 3. the tensor-core scan
+    const int cap = 64 + 32 * k;
+    DevBuf<float> cand_lb, cand_ufin, q64buf;
+    DevBuf<int32_t> cand_pos, cand_count, ovf_list, counters;
+    RBC_CHECK(cand_lb.alloc(nq * cap, st));
+    RBC_CHECK(cand_pos.alloc(nq * cap, st));
+    RBC_CHECK(cand_count.alloc(nq, st));
+    RBC_CHECK(cand_ufin.alloc(nq, st));
+    RBC_CHECK(ovf_list.alloc(nq, st));
+    RBC_CHECK(counters.alloc(2, st));
+    RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
+    const float *q64 = q;
+    if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
+        RBC_CHECK(q64buf.alloc(nq * 64, st));
+        pad64_rows_kernel<<<grid_for(nq * 64, 256), 256, 0, st>>>(q, nq, idx->d, q64buf.get());
+        RBC_LAUNCHED();
+        q64 = q64buf.get();
+    }
+    S2Params P;
+    P.xh0 = tc->xh0;
+    P.xh1 = tc->xh1;
+    P.gcol = tc->gcol;
+    P.reps64 = tc->reps64;
+    P.plane1 = tc->plane1 ? 1 : 0;
+    P.q64 = q64;
+    P.gamma = po.gamma.get();
+    P.k = k;
+    P.ntiles = ntiles;
+    P.tile_order = tile_order.get();
+    P.tile_rows = rows.get();
+    P.work_off = work_off.get();
+    P.work = work.get();
+    P.cut = cut.get();
+    P.rowd1 = rowd1.get();
+    P.cand_lb = cand_lb.get();
+    P.cand_pos = cand_pos.get();
+    P.cap = cap;
+    P.cand_count = cand_count.get();
+    P.cand_ufin = cand_ufin.get();
+    P.overflow_list = ovf_list.get();
+    P.overflow_count = counters.get();
+    P.tile_counter = counters.get() + 1;
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+        kern<<<grid, kThreads, kSmemBytes, st>>>(P);
+    };
     {
-        size_t tb = 0, tb2 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq, 0, 48, st);
-        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles,
-                                        0, 40, st);
-        DevBuf<unsigned char> tmp;
-        RBC_CHECK(tmp.alloc(tb > tb2 ? tb : tb2, st));
-        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, po.order_key.get(), skey.get(), ids.get(), order.get(),
-                                                 nq, 0, 48, st));
-        note_launch();
-        tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
-            order.get(), nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
-        RBC_LAUNCHED();
-        // 2. union of surviving lists per tile
-        DevBuf<int64_t> nwork;
-        RBC_CHECK(nwork.alloc(ntiles, st));
-        const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
-        if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
-        cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
-        cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
-        tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), nr, nwork.get());
-        RBC_LAUNCHED();
-        DevBuf<int64_t> work_off;
-        RBC_CHECK(work_off.alloc(ntiles + 1, st));
-        RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
-        size_t tb3 = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tb3, nwork.get(), work_off.get() + 1, ntiles, st);
-        DevBuf<unsigned char> tmp3;
-        RBC_CHECK(tmp3.alloc(tb3, st));
-        RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp3.get(), tb3, nwork.get(), work_off.get() + 1, ntiles, st));
-        note_launch();
-        int64_t total_work = 0;
-        RBC_CUDA(cudaMemcpyAsync(&total_work, work_off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        RBC_CUDA(cudaStreamSynchronize(st));
-        DevBuf<int32_t> work_p, work_ext, cut;
-        DevBuf<float> work_sA;
-        RBC_CHECK(work_p.alloc(total_work, st));
-        RBC_CHECK(work_ext.alloc(total_work, st));
-        RBC_CHECK(work_sA.alloc(total_work, st));
-        RBC_CHECK(cut.alloc(total_work * kRows, st));
-        RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
-        tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), po.seg_len.get(),
-                                                       po.order_key.get(), po.d1, nr, work_off.get(), work_p.get(),
-                                                       work_ext.get(), work_sA.get(), cut.get(), tkey.get());
-        RBC_LAUNCHED();
-        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
-                                                 tile_order.get(), ntiles, 0, 40, st));
-        note_launch();
-        // 3. the tensor-core scan
-        const int cap = 64 + 32 * k;
-        DevBuf<float> cand_lb;
-        DevBuf<int32_t> cand_pos, ovf_list, counters;
-        RBC_CHECK(cand_lb.alloc(nq * cap, st));
-        RBC_CHECK(cand_pos.alloc(nq * cap, st));
-        RBC_CHECK(ovf_list.alloc(nq, st));
-        DevBuf<int32_t> cand_count;
-        DevBuf<float> cand_ufin, q64buf;
-        RBC_CHECK(cand_count.alloc(nq, st));
-        RBC_CHECK(cand_ufin.alloc(nq, st));
-        const float *q64 = q;
-        if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
-            RBC_CHECK(q64buf.alloc(nq * 64, st));
-            pad64_rows_kernel<<<grid_for(nq * 64, 256), 256, 0, st>>>(q, nq, idx->d, q64buf.get());
-            RBC_LAUNCHED();
-            q64 = q64buf.get();
-        }
-        RBC_CHECK(counters.alloc(2, st));
-        RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
-        S2Params P;
-        P.xh0 = tc->xh0;
-        P.xh1 = tc->xh1;
-        P.gcol = tc->gcol;
-        P.poff = tc->poff;
-        P.sB = tc->sB;
-        P.offsets = idx->offsets;
-        P.radii = idx->radii;
-        P.reps = idx->reps;
-        P.xp = idx->xp;
-        P.perm = idx->perm;
-        P.d = idx->d;
-        P.plane1 = tc->plane1 ? 1 : 0;
-        P.nr = nr;
-        P.q = q;
-        P.q64 = q64;
-        P.reps64 = tc->reps64;
-        P.cand_count = cand_count.get();
-        P.cand_ufin = cand_ufin.get();
-        P.d1 = po.d1;
-        P.gamma = po.gamma.get();
-        P.k = k;
-        P.ntiles = ntiles;
-        P.tile_order = tile_order.get();
-        P.tile_rows = rows.get();
-        P.work_off = work_off.get();
-        P.work_p = work_p.get();
-        P.work_ext = work_ext.get();
-        P.work_sA = work_sA.get();
-        P.cut = cut.get();
-        P.cand_lb = cand_lb.get();
-        P.cand_pos = cand_pos.get();
-        P.cap = cap;
-        P.out_keys = keys;
-        P.overflow_list = ovf_list.get();
-        P.overflow_count = counters.get();
-        P.tile_counter = counters.get() + 1;
-        if (g_num_sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
-        auto launch = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-            kern<<<grid, kThreads, kSmemBytes, st>>>(P);
-        };
-        {
-            ProfScope ps(kPhaseScan, st);
-            if (k == 1) launch(stage2_tc_kernel<1>);
-            else if (k <= 4) launch(stage2_tc_kernel<4>);
-            else if (k <= 8) launch(stage2_tc_kernel<8>);
-            else launch(stage2_tc_kernel<16>);
-        }
-        RBC_LAUNCHED();
-        // 4. exact re-rank of the buffered candidates
-        {
-            const unsigned rgrid = grid_for(nq * 32, 256);
-#define RBC_RERANK(KT)                                                                                          \
+        ProfScope ps(kPhaseScan, st);
+        if (k == 1) launch(stage2_tc_kernel<1>);
+        else if (k <= 4) launch(stage2_tc_kernel<4>);
+        else if (k <= 8) launch(stage2_tc_kernel<8>);
+        else launch(stage2_tc_kernel<16>);
+    }
+    RBC_LAUNCHED();
+    // 4. exact re-rank of the buffered candidates
+    {
+        const unsigned rgrid = grid_for(nq * 32, 256);
+#define RBC_RERANK(KT)                                                                                              \
     rerank_kernel<KT><<<rgrid, 256, 0, st>>>(cand_lb.get(), cand_pos.get(), cand_count.get(), cand_ufin.get(), cap, \
                                              nq, q, idx->xp, idx->perm, idx->d, k, keys)
-            if (k == 1) RBC_RERANK(1);
-            else if (k <= 4) RBC_RERANK(4);
-            else if (k <= 8) RBC_RERANK(8);
-            else RBC_RERANK(16);
+        if (k == 1) RBC_RERANK(1);
+        else if (k <= 4) RBC_RERANK(4);
+        else if (k <= 8) RBC_RERANK(8);
+        else RBC_RERANK(16);
 #undef RBC_RERANK
-            RBC_LAUNCHED();
-        }
-        // 5. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
-        int32_t n_ovf = 0;
-        RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        RBC_CUDA(cudaStreamSynchronize(st));
-        if (n_ovf > 0) {
-            DevBuf<float> qsub;
-            DevBuf<uint64_t> ksub;
-            RBC_CHECK(qsub.alloc(static_cast<int64_t>(n_ovf) * idx->d, st));
-            RBC_CHECK(ksub.alloc(static_cast<int64_t>(n_ovf) * k, st));
-            gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
-                q, ovf_list.get(), n_ovf, idx->d, qsub.get());
-            RBC_LAUNCHED();
-            SegSubSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), ovf_list.get(), idx->d};
-            RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
-            scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
-                                                                                             n_ovf, k, keys);
-            RBC_LAUNCHED();
-        }
-        last_overflow_count() = n_ovf;
+        RBC_LAUNCHED();
     }
+    // 5. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
+    int32_t n_ovf = 0;
+    RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    if (n_ovf > 0) {
+        DevBuf<float> qsub;
+        DevBuf<uint64_t> ksub;
+        RBC_CHECK(qsub.alloc(static_cast<int64_t>(n_ovf) * idx->d, st));
+        RBC_CHECK(ksub.alloc(static_cast<int64_t>(n_ovf) * k, st));
+        gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
+            q, ovf_list.get(), n_ovf, idx->d, qsub.get());
+        RBC_LAUNCHED();
+        SegSubSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), ovf_list.get(), idx->d};
+        RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
+        scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
+                                                                                         n_ovf, k, keys);
+        RBC_LAUNCHED();
+    }
+    last_overflow_count() = n_ovf;
     return RBC_OK;
 }
 
