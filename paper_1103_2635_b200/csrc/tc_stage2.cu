@@ -34,8 +34,9 @@
 // 2-slot shared-memory ring):
 //   warp 0      scheduler + producer: cp.async.bulk of B chunks, 4-stage ring
 //   warp 1      MMA issuer + TMEM owner (512 columns = 2 x 256 fp32 accumulators)
-//   warps 2..5  epilogue / candidate filter
-//   warps 6..9  A-operand prep (query rows centred on the current list's rep)
+//   warps 2..9  epilogue, two warps per TMEM lane quadrant (one per 128-column
+//               half of each chunk): A-operand prep for the next list (each warp
+//               its half of K), candidate filter, per-half candidate buffers
 #include <cub/cub.cuh>
 
 #include <vector>
@@ -54,7 +55,8 @@ namespace {
 constexpr int kRows = 128;       // queries per tile = UMMA M = TMEM lanes
 constexpr int kNmax = 256;       // max UMMA N per chunk
 constexpr int kStages = 4;       // B ring depth
-constexpr int kThreads = 320;    // 10 warps
+constexpr int kThreads = 320;    // 10 warps: producer, MMA, 8 epilogue
+constexpr int kEpiWarps = 8;
 constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
 constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
 constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
@@ -310,15 +312,32 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
 }
 
 // ---- the stage-2 kernel -----------------------------------------------------------------
+// v[j] for a runtime j in [0, 32) without local memory (select tree)
+__device__ __forceinline__ float pick32(const float (&v)[32], int j) {
+    float t16[16], t8[8], t4[4], t2[2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t16[i] = (j & 16) ? v[i + 16] : v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t8[i] = (j & 8) ? t16[i + 8] : t16[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[i + 4] : t8[i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) t2[i] = (j & 2) ? t4[i + 2] : t4[i];
+    return (j & 1) ? t2[1] : t2[0];
+}
+
+__device__ __forceinline__ float max32(const float (&v)[32]) {
+    return fmaxf(fmaxf(max8(v), max8(v + 8)), fmaxf(max8(v + 16), max8(v + 24)));
+}
+
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *sB = smem;                                   // kStages x (plane 0 | plane 1)
     uint8_t *sA = sB + kStages * kStageBytes;             // 2 x (plane 0 | plane 1)
-    float *scratch = reinterpret_cast<float *>(sA + 2 * kABytes);  // 128 threads x 32 floats
-    float *gbuf = scratch + kRows * 32;                   // 4 epilogue warps x kNmax (fallback column)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 4 * kNmax);
+    float *gbuf = reinterpret_cast<float *>(sA + 2 * kABytes);  // 8 epilogue warps x 128 (fallback column)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + kEpiWarps * (kNmax / 2));
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
     uint64_t *afull = tempty + 2, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
@@ -332,11 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         }
         for (int b = 0; b < 2; ++b) {
             sm100::mbar_init(&tfull[b], 1);
-            sm100::mbar_init(&tempty[b], 4);
-            sm100::mbar_init(&afull[b], 4);
+            sm100::mbar_init(&tempty[b], kEpiWarps);
+            sm100::mbar_init(&afull[b], kEpiWarps);
             sm100::mbar_init(&aempty[b], 1);
             sm100::mbar_init(&tile_full[b], 1);
-            sm100::mbar_init(&tile_empty[b], 9);  // MMA lane + 4 prep warps + 4 epilogue warps
+            sm100::mbar_init(&tile_empty[b], 1 + kEpiWarps);  // MMA lane + epilogue warps
         }
         sm100::fence_barrier_init();
     }
@@ -345,19 +364,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *s_tmem;
-
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;  // TMEM lane / tile row owned by this thread (epilogue + prep)
-
-    // consumer side of the tile ring: returns the next tile id (-1 = done)
-    auto next_tile = [&](uint32_t it) {
-        const uint32_t slot = it & 1;
-        sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
-        const int t = s_tiles[slot];
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&tile_empty[slot]);
-        return t;
-    };
 
     if (warp == 0) {
         // ===== scheduler + producer =====
@@ -432,40 +438,54 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 }
             }
         }
-    } else if (warp >= 6) {
-        // ===== A-operand prep: row i = f16((q_i - r_p) * sA), aug columns = -sA/sB =====
-        uint32_t ai = 0;
+    } else {
+        // ===== epilogue warps (2 per TMEM lane quadrant): A prep + filter + candidate buffer =====
+        // warp pair (quad, half): rows quad*32 .. +31, columns [half*128, half*128+128) of every
+        // 256-column chunk, K range [half*32, half*32+32) of the A operand.
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row = quad * 32 + lane;
+        float *g = gbuf + (warp - 2) * (kNmax / 2);
+        uint32_t ti = 0, ai = 0;
         for (uint32_t it = 0;; ++it) {
-            const int tile = next_tile(it);
+            const uint32_t slot = it & 1;
+            sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
+            const int tile = s_tiles[slot];
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&tile_empty[slot]);
             if (tile < 0) break;
-            // the row's query stays in registers for the whole tile (rows padded to 64 with zeros)
             const int32_t qi = P.tile_rows[tile * kRows + row];
-            float qv[64];
+            const bool live = qi >= 0;
+            // this thread's half of the query row (rows padded to 64 floats with zeros)
+            float qv[32];
             {
-                const float4 *src = reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(qi < 0 ? 0 : qi) * 64);
+                const float4 *src =
+                    reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(live ? qi : 0) * 64 + half * 32);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const float4 t = qi >= 0 ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int c = 0; c < 8; ++c) {
+                    const float4 t = live ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                     qv[4 * c] = t.x;
                     qv[4 * c + 1] = t.y;
                     qv[4 * c + 2] = t.z;
                     qv[4 * c + 3] = t.w;
                 }
             }
-            for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
-                const uint32_t a = ai & 1;
+            const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
+            // A operand of list w: this thread's 64 bytes of row `row` (+ the aug columns on half 1)
+            auto prep_a = [&](int64_t w) {
                 const WorkItem wi = P.work[w];
-                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64);
+                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64 + half * 32);
+                float4 rr4[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) rr4[c] = __ldg(rep4 + c);
                 const __half ac = __float2half_rn(wi.aug);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 const float sa = wi.sA;
-                float4 rr4[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) rr4[c] = __ldg(rep4 + c);
+                const uint32_t a = ai & 1;
                 sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < 4; ++c) {
                     const float rr[8] = {rr4[2 * c].x, rr4[2 * c].y, rr4[2 * c].z, rr4[2 * c].w,
                                          rr4[2 * c + 1].x, rr4[2 * c + 1].y, rr4[2 * c + 1].z, rr4[2 * c + 1].w};
                     uint32_t wv[4];
@@ -476,10 +496,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         const float v1 = fmaf(qv[k0 + 1], sa, -(rr[2 * e + 1] * sa));
                         wv[e] = sm100::pack_f16x2_sat(v0, v1);
                     }
-                    if (!P.plane1 && c == 7) wv[3] = aug;
-                    *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                    const int cc = half * 4 + c;
+                    if (!P.plane1 && cc == 7) wv[3] = aug;
+                    *reinterpret_cast<uint4 *>(dst + ((cc ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                 }
-                if (P.plane1) {
+                if (P.plane1 && half == 1) {
                     uint8_t *d1p = sA + a * kABytes + kRows * kP0 + row * kP1;
                     const int sw = (row >> 2) & 1;
                     *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
@@ -489,18 +510,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(&afull[a]);
                 ++ai;
-            }
-        }
-    } else {
-        // ===== epilogue: filter and candidate buffer =====
-        float *g = gbuf + (warp - 2) * kNmax;
-        float *scr = scratch + row * 32;
-        uint32_t ti = 0;
-        for (uint32_t it = 0;; ++it) {
-            const int tile = next_tile(it);
-            if (tile < 0) break;
-            const int32_t qi = P.tile_rows[tile * kRows + row];
-            const bool live = qi >= 0;
+            };
+            if (w0 < w1) prep_a(w0);
+
             float ubk[KT];
 #pragma unroll
             for (int j = 0; j < KT; ++j) ubk[j] = __int_as_float(0x7f800000);
@@ -509,9 +521,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             float U = u_init;  // running upper bound of the k-th smallest candidate d^2
             int count = 0;
             bool overflow = false;
-            float *clb = P.cand_lb + static_cast<int64_t>(live ? qi : 0) * P.cap;
-            int32_t *cpos = P.cand_pos + static_cast<int64_t>(live ? qi : 0) * P.cap;
-            const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
+            const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * 2 + half);
+            float *clb = P.cand_lb + slot_id * P.cap;
+            int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
             int cut_n = 0;
             float dq_n = 0.f;
@@ -520,6 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 dq_n = P.rowd1[w0 * kRows + row];
             }
             for (int64_t w = w0; w < w1; ++w) {
+                if (w + 1 < w1) prep_a(w + 1);  // next list's A while this list's MMAs run
                 const WorkItem wi = P.work[w];
                 const int cutv = live ? cut_n : 0;
                 const float dq = dq_n;
@@ -543,101 +556,109 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 };
                 float T = cutv > 0 ? threshold() : __int_as_float(0x7f800000);
                 float vbest = -__int_as_float(0x7f800000);
+                // push every element of a 32-column group that passes the exact-bound test
+                auto slow32 = [&](const float (&v)[32], int col0, int lim) {
+                    unsigned mask = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
+                    if (col0 + 32 > lim) mask &= lim > col0 ? (0xFFFFFFFFu >> (32 - (lim - col0))) : 0u;
+                    while (mask) {
+                        const int j = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        const float vj = pick32(v, j);
+                        const float lb = A2 - E - vj * inv2s;
+                        if (!(lb <= U * kTie)) continue;
+                        const float ub = lb + 2.0f * E;
+                        if (count == P.cap && !overflow) {
+                            // compact: drop entries that can no longer qualify
+                            int c2 = 0;
+                            for (int e = 0; e < count; ++e) {
+                                const float l2 = clb[e];
+                                if (l2 <= U * kTie) {
+                                    clb[c2] = l2;
+                                    cpos[c2] = cpos[e];
+                                    ++c2;
+                                }
+                            }
+                            count = c2;
+                            if (count == P.cap) overflow = true;
+                        }
+                        if (!overflow) {
+                            clb[count] = lb;
+                            cpos[count] = wi.csr + col0 + j;
+                            ++count;
+                        }
+                        if (KT == 1) {
+                            U = fminf(U, ub);
+                        } else {
+                            float x = ub;
+#pragma unroll
+                            for (int t = 0; t < KT; ++t) {
+                                const float lo = fminf(ubk[t], x), hi = fmaxf(ubk[t], x);
+                                ubk[t] = lo;
+                                x = hi;
+                            }
+                            float kth = ubk[0];
+#pragma unroll
+                            for (int t = 0; t < KT; ++t)
+                                if (t == P.k - 1) kth = ubk[t];
+                            U = fminf(u_init, kth);
+                        }
+                        T = threshold();
+                    }
+                };
                 for (int off = 0; off < wi.ext; off += kNmax) {
                     const int n = min(kNmax, roundup16(wi.ext - off));
+                    const int hb = half * (kNmax / 2);  // this warp's first column in the chunk
                     if (noaug) {
-                        // rare: per-column norm term subtracted in the epilogue instead of the MMA
-                        const float *src = P.gcol + wi.poff + off;
-                        float4 g0 = make_float4(0, 0, 0, 0), g1 = g0;
-                        if (lane * 8 < n) {
-                            g0 = *reinterpret_cast<const float4 *>(src + lane * 8);
-                            g1 = *reinterpret_cast<const float4 *>(src + lane * 8 + 4);
-                        }
-                        reinterpret_cast<float4 *>(g)[lane * 2] = g0;
-                        reinterpret_cast<float4 *>(g)[lane * 2 + 1] = g1;
+                        // rare: per-column norm term subtracted here instead of in the MMA
+                        const float *src = P.gcol + wi.poff + off + hb;
+                        float4 g0 = make_float4(0, 0, 0, 0);
+                        if (hb + lane * 4 < n) g0 = *reinterpret_cast<const float4 *>(src + lane * 4);
+                        reinterpret_cast<float4 *>(g)[lane] = g0;
                     }
                     const uint32_t tb = ti & 1;
                     sm100::mbar_wait(&tfull[tb], (ti >> 1) & 1);
                     sm100::tc_fence_after();
                     __syncwarp();
-                    const int lim = min(cutv - off, n);  // valid columns of this row in the chunk
+                    // valid columns of this row, relative to this warp's half of the chunk
+                    const int lim = min(cutv - off, n) - hb;
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
-                    for (int c0 = 0; c0 < wlim; c0 += 32) {
-                        float v[32];
-                        sm100::tmem_ld32(tmem + tb * kNmax + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
+                    const uint32_t tbase = tmem + tb * kNmax + hb + (static_cast<uint32_t>(quad * 32) << 16);
+                    for (int c0 = 0; c0 < wlim; c0 += 64) {
+                        uint32_t ra[32], rb[32];
+                        sm100::tmem_ld32_async(tbase + c0, ra);
+                        sm100::tmem_ld32_async(tbase + c0 + 32, rb);
+                        sm100::tmem_wait_ld(ra);
+                        sm100::tmem_tie(rb);
+                        float va[32], vb[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            va[j] = __uint_as_float(ra[j]);
+                            vb[j] = __uint_as_float(rb[j]);
+                        }
                         if (noaug) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] = fmaf(-sa, g[c0 + j], v[j]);
-                        }
-                        if (c0 + 32 > lim) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (c0 + j >= lim) v[j] = -__int_as_float(0x7f800000);
-                        }
-                        const float m0 = max8(v), m1 = max8(v + 8), m2 = max8(v + 16), m3 = max8(v + 24);
-                        const float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-                        if (KT == 1 && m > vbest) {
-                            // k = 1: the chunk's best element bounds the nearest candidate
-                            vbest = m;
-                            const float ub = A2 + E - m * inv2s;
-                            if (ub < U) {
-                                U = ub;
-                                T = threshold();
+                            for (int j = 0; j < 32; ++j) {
+                                va[j] = fmaf(-sa, g[c0 + j], va[j]);
+                                vb[j] = fmaf(-sa, g[c0 + 32 + j], vb[j]);
                             }
                         }
-                        if (m >= T) {
-                            // slow path: stage the chunk, visit only elements that pass
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4)
-                                *reinterpret_cast<float4 *>(scr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                            unsigned mask = 0;
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
-                            while (mask) {
-                                const int j = __ffs(mask) - 1;
-                                mask &= mask - 1;
-                                const float vj = scr[j];
-                                const float lb = A2 - E - vj * inv2s;
-                                if (!(lb <= U * kTie)) continue;
-                                const float ub = lb + 2.0f * E;
-                                if (count == P.cap && !overflow) {
-                                    // compact: drop entries that can no longer qualify
-                                    int c2 = 0;
-                                    for (int e = 0; e < count; ++e) {
-                                        const float l2 = clb[e];
-                                        if (l2 <= U * kTie) {
-                                            clb[c2] = l2;
-                                            cpos[c2] = cpos[e];
-                                            ++c2;
-                                        }
-                                    }
-                                    count = c2;
-                                    if (count == P.cap) overflow = true;
+                        const float ma = max32(va), mb = max32(vb);
+                        if (KT == 1) {
+                            // k = 1: a fully valid group's best element bounds the nearest candidate
+                            const float mv = c0 + 64 <= lim ? fmaxf(ma, mb) : (c0 + 32 <= lim ? ma : -__int_as_float(0x7f800000));
+                            if (mv > vbest) {
+                                vbest = mv;
+                                const float ub = A2 + E - mv * inv2s;
+                                if (ub < U) {
+                                    U = ub;
+                                    T = threshold();
                                 }
-                                if (!overflow) {
-                                    clb[count] = lb;
-                                    cpos[count] = wi.csr + off + c0 + j;
-                                    ++count;
-                                }
-                                if (KT == 1) {
-                                    U = fminf(U, ub);
-                                } else {
-                                    float x = ub;
-#pragma unroll
-                                    for (int t = 0; t < KT; ++t) {
-                                        const float lo = fminf(ubk[t], x), hi = fmaxf(ubk[t], x);
-                                        ubk[t] = lo;
-                                        x = hi;
-                                    }
-                                    float kth = ubk[0];
-#pragma unroll
-                                    for (int t = 0; t < KT; ++t)
-                                        if (t == P.k - 1) kth = ubk[t];
-                                    U = fminf(u_init, kth);
-                                }
-                                T = threshold();
                             }
                         }
+                        if (ma >= T) slow32(va, off + hb + c0, off + hb + lim);
+                        if (mb >= T) slow32(vb, off + hb + c0 + 32, off + hb + lim);
                     }
                     sm100::tc_fence_before();
                     __syncwarp();
@@ -647,8 +668,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             }
             // hand the buffered candidates to the exact re-rank kernel
             if (live) {
-                P.cand_count[qi] = overflow ? -1 : count;
-                P.cand_ufin[qi] = U * kTie;
+                P.cand_count[slot_id] = overflow ? -1 : count;
+                P.cand_ufin[slot_id] = U * kTie;
                 if (overflow) P.overflow_list[atomicAdd(P.overflow_count, 1)] = qi;
             }
         }
@@ -658,8 +679,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     if (warp == 1) sm100::tmem_dealloc<512>(tmem);
 }
 
-// Exact re-rank (reference arithmetic) of the buffered candidates: one warp per
-// query, one candidate per lane, warp merge of the lanes' sorted key64 lists.
+// Exact re-rank (reference arithmetic) of the buffered candidates of both column
+// halves: one warp per query, one candidate per lane, warp merge of the lanes'
+// sorted key64 lists.
 template <int KT>
 __global__ void __launch_bounds__(256) rerank_kernel(const float *__restrict__ cand_lb,
                                                      const int32_t *__restrict__ cand_pos,
@@ -671,23 +693,23 @@ __global__ void __launch_bounds__(256) rerank_kernel(const float *__restrict__ c
     const int lane = threadIdx.x & 31;
     const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     if (i >= nq) return;
-    const int cnt = cand_count[i];
-    if (cnt < 0) return;  // overflowed: recomputed by the exact scan
-    const float ufin = cand_ufin[i];
+    const int c0 = cand_count[2 * i], c1 = cand_count[2 * i + 1];
+    if (c0 < 0 || c1 < 0) return;  // overflowed: recomputed by the exact scan
+    const float ufin = fminf(cand_ufin[2 * i], cand_ufin[2 * i + 1]);
     const float *qrow = q + i * d;
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-    for (int e = lane; e < cnt; e += 32) {
-        if (!(cand_lb[i * cap + e] <= ufin)) continue;
-        const int32_t pos = cand_pos[i * cap + e];
+    for (int e = lane; e < c0 + c1; e += 32) {
+        const int64_t at = e < c0 ? (2 * i) * cap + e : (2 * i + 1) * cap + (e - c0);
+        if (!(cand_lb[at] <= ufin)) continue;
+        const int32_t pos = cand_pos[at];
         const float dist = exact_dist<RBC_L2>(qrow, xp + static_cast<int64_t>(pos) * d, d);
         const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos]));
         if (key < best[KT - 1]) sorted_insert<KT>(best, key);
     }
     warp_merge_sorted<KT>(best, k, out_keys + i * k);
 }
-
 __global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
                                          float *__restrict__ out) {
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < m * d;
@@ -701,8 +723,7 @@ __global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int3
     if (t < m * k) dst[static_cast<int64_t>(ids[t / k]) * k + t % k] = src[t];
 }
 
-constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kRows * 32 * sizeof(float) +
-                              4 * kNmax * sizeof(float) + 256;
+constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kEpiWarps * (kNmax / 2) * sizeof(float) + 256;
 
 }  // namespace
 
@@ -848,14 +869,15 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                              tile_order.get(), ntiles, 0, 40, st));
     note_launch();
     // 3. the tensor-core scan
-    const int cap = 64 + 32 * k;
+    const int cap = 48 + 16 * k;  // per query and column half
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, cand_count, ovf_list, counters;
-    RBC_CHECK(cand_lb.alloc(nq * cap, st));
-    RBC_CHECK(cand_pos.alloc(nq * cap, st));
-    RBC_CHECK(cand_count.alloc(nq, st));
-    RBC_CHECK(cand_ufin.alloc(nq, st));
-    RBC_CHECK(ovf_list.alloc(nq, st));
+    RBC_CHECK(cand_lb.alloc(nq * 2 * cap, st));
+    RBC_CHECK(cand_pos.alloc(nq * 2 * cap, st));
+    RBC_CHECK(cand_count.alloc(nq * 2, st));
+    RBC_CHECK(cand_ufin.alloc(nq * 2, st));
+    RBC_CUDA(cudaMemsetAsync(cand_count.get(), 0, sizeof(int32_t) * nq * 2, st));
+    RBC_CHECK(ovf_list.alloc(nq * 2, st));
     RBC_CHECK(counters.alloc(2, st));
     RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
     const float *q64 = q;
