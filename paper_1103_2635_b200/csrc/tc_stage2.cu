@@ -312,22 +312,12 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
 }
 
 // ---- the stage-2 kernel -----------------------------------------------------------------
-// v[j] for a runtime j in [0, 32) without local memory (select tree)
-__device__ __forceinline__ float pick32(const float (&v)[32], int j) {
-    float t16[16], t8[8], t4[4], t2[2];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) t16[i] = (j & 16) ? v[i + 16] : v[i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) t8[i] = (j & 8) ? t16[i + 8] : t16[i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[i + 4] : t8[i];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) t2[i] = (j & 2) ? t4[i + 2] : t4[i];
-    return (j & 1) ? t2[1] : t2[0];
-}
-
-__device__ __forceinline__ float max32(const float (&v)[32]) {
-    return fmaxf(fmaxf(max8(v), max8(v + 8)), fmaxf(max8(v + 16), max8(v + 24)));
+// v[j] for a runtime j in [0, 8) without local memory (select tree)
+__device__ __forceinline__ float pick8(const float *v, int j) {
+    const float a0 = (j & 4) ? v[4] : v[0], a1 = (j & 4) ? v[5] : v[1];
+    const float a2 = (j & 4) ? v[6] : v[2], a3 = (j & 4) ? v[7] : v[3];
+    const float b0 = (j & 2) ? a2 : a0, b1 = (j & 2) ? a3 : a1;
+    return (j & 1) ? b1 : b0;
 }
 
 template <int KT>
@@ -556,16 +546,16 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 };
                 float T = cutv > 0 ? threshold() : __int_as_float(0x7f800000);
                 float vbest = -__int_as_float(0x7f800000);
-                // push every element of a 32-column group that passes the exact-bound test
-                auto slow32 = [&](const float (&v)[32], int col0, int lim) {
+                // push every element of an 8-column group that passes the exact-bound test
+                auto slow8 = [&](const float *v, int col0, int lim) {
                     unsigned mask = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
-                    if (col0 + 32 > lim) mask &= lim > col0 ? (0xFFFFFFFFu >> (32 - (lim - col0))) : 0u;
+                    for (int j = 0; j < 8; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
+                    if (col0 + 8 > lim) mask &= lim > col0 ? (0xFFu >> (8 - (lim - col0))) : 0u;
                     while (mask) {
                         const int j = __ffs(mask) - 1;
                         mask &= mask - 1;
-                        const float vj = pick32(v, j);
+                        const float vj = pick8(v, j);
                         const float lb = A2 - E - vj * inv2s;
                         if (!(lb <= U * kTie)) continue;
                         const float ub = lb + 2.0f * E;
@@ -622,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     sm100::tc_fence_after();
                     __syncwarp();
                     // valid columns of this row, relative to this warp's half of the chunk
-                    const int lim = min(cutv - off, n) - hb;
+                    const int lim = min(min(cutv - off, n) - hb, kNmax / 2);
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
                     const uint32_t tbase = tmem + tb * kNmax + hb + (static_cast<uint32_t>(quad * 32) << 16);
                     for (int c0 = 0; c0 < wlim; c0 += 64) {
@@ -644,7 +634,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                 vb[j] = fmaf(-sa, g[c0 + 32 + j], vb[j]);
                             }
                         }
-                        const float ma = max32(va), mb = max32(vb);
+                        float m8[8];
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            m8[s] = max8(va + 8 * s);
+                            m8[4 + s] = max8(vb + 8 * s);
+                        }
+                        const float ma = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3]));
+                        const float mb = fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]));
                         if (KT == 1) {
                             // k = 1: a fully valid group's best element bounds the nearest candidate
                             const float mv = c0 + 64 <= lim ? fmaxf(ma, mb) : (c0 + 32 <= lim ? ma : -__int_as_float(0x7f800000));
@@ -657,8 +654,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                 }
                             }
                         }
-                        if (ma >= T) slow32(va, off + hb + c0, off + hb + lim);
-                        if (mb >= T) slow32(vb, off + hb + c0 + 32, off + hb + lim);
+                        if (fmaxf(ma, mb) >= T) {
+                            const int base = off + hb + c0, llim = off + hb + lim;
+#pragma unroll
+                            for (int s = 0; s < 4; ++s) {
+                                if (m8[s] >= T) slow8(va + 8 * s, base + 8 * s, llim);
+                                if (m8[4 + s] >= T) slow8(vb + 8 * s, base + 32 + 8 * s, llim);
+                            }
+                        }
                     }
                     sm100::tc_fence_before();
                     __syncwarp();
