@@ -184,6 +184,7 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
     }
     if (rc == RBC_OK && cudaGetLastError() != cudaSuccess) rc = fail(RBC_ECUDA, "index kernels");
     if (rc == RBC_OK) rc = tc_index_prepare(idx, st);
+    if (rc == RBC_OK) rc = tc1_index_prepare(idx, st);
     if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "index sync");
     if (rc != RBC_OK) {
         rbc_index_destroy(idx);
@@ -343,6 +344,7 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
 int rbc_index_destroy(rbc_index *idx) {
     if (!idx) return RBC_OK;
     tc_index_release(idx);
+    tc1_index_release(idx);
     void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets, idx->perm, idx->list_dists, idx->xp,
                     idx->lists};
     for (void *p : ptrs)

@@ -29,6 +29,9 @@ struct rbc_index {
     // tensor-core stage-2 operands (tc_scan.cu): per list, rows centred on
     // the list's rep, fp16, pre-swizzled for the UMMA shared-memory layout
     void *tc = nullptr;
+    // tensor-core stage-1 operands (tc_stage1.cu): representatives centred on
+    // their mean, f16, pre-swizzled
+    void *tc1 = nullptr;
 
     // one-shot: [nr, s] point ids
     int32_t *lists = nullptr;
@@ -37,4 +40,6 @@ struct rbc_index {
 namespace rbc {
 int tc_index_prepare(rbc_index *idx, cudaStream_t st);
 void tc_index_release(rbc_index *idx);
+int tc1_index_prepare(rbc_index *idx, cudaStream_t st);
+void tc1_index_release(rbc_index *idx);
 }  // namespace rbc

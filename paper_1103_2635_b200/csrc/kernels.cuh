@@ -56,7 +56,7 @@ struct RowSrc {
 };
 
 // ranges of the list-ordered point copy (exact search stage 2,
-// search.py:183-186): query i scans segments seg_off[i]..seg_off[i+1],
+// search.py:183-186): query i scans segments seg_off[i] .. seg_off[i]+seg_cnt[i],
 // segment s = rows [start[s], start[s]+len[s]) of xp whose ids are perm[].
 struct SegSrc {
     const float *xp;
@@ -64,10 +64,11 @@ struct SegSrc {
     const int64_t *seg_start;
     const int32_t *seg_len;
     const int64_t *seg_off;
+    const int32_t *seg_cnt;
     int d;
     template <class F>
     __device__ __forceinline__ void for_each(int64_t i, int lane, F &&f) const {
-        for (int64_t s = seg_off[i]; s < seg_off[i + 1]; ++s) {
+        for (int64_t s = seg_off[i]; s < seg_off[i] + seg_cnt[i]; ++s) {
             const int64_t st = seg_start[s];
             const int32_t len = seg_len[s];
             for (int32_t j = lane; j < len; j += 32) f(xp + (st + j) * d, static_cast<uint32_t>(perm[st + j]));
@@ -83,12 +84,13 @@ struct SegSubSrc {
     const int64_t *seg_start;
     const int32_t *seg_len;
     const int64_t *seg_off;
+    const int32_t *seg_cnt;
     const int32_t *qmap;
     int d;
     template <class F>
     __device__ __forceinline__ void for_each(int64_t i, int lane, F &&f) const {
         const int64_t qi = qmap[i];
-        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) {
+        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) {
             const int64_t st = seg_start[s];
             const int32_t len = seg_len[s];
             for (int32_t j = lane; j < len; j += 32) f(xp + (st + j) * d, static_cast<uint32_t>(perm[st + j]));

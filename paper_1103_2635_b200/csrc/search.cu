@@ -11,9 +11,12 @@
 // set -- and therefore every result and every SearchStats field -- matches.
 #include <cub/cub.cuh>
 
+#include <memory>
+
 #include "common.cuh"
 #include "index.cuh"
 #include "kernels.cuh"
+#include "prune_math.cuh"
 #include "search.cuh"
 #include "tc_scan.cuh"
 
@@ -69,23 +72,6 @@ __device__ float block_kth_smallest(const float *__restrict__ row, int64_t nr, i
     return __uint_as_float(prefix);
 }
 
-// #entries of an ascending f32 list <= thr, compared in f64 (search.py:77-82)
-__device__ __forceinline__ int32_t list_cutoff_dev(const float *__restrict__ l, int32_t m, double thr) {
-    int32_t lo = 0, hi = m;
-    while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        if (static_cast<double>(l[mid]) <= thr) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// search.py:62-74, evaluated in f64 exactly as numpy does
-__device__ __forceinline__ bool survives(float dist, float radius, double g) {
-    const double dd = dist, r = radius;
-    return (dd <= 3.0 * g) && ((dd < __dadd_rn(g, r)) || (dd <= g));
-}
-
 constexpr int kPruneThreads = 256;
 
 // pass 1: gamma_k, stats, number of non-empty surviving segments
@@ -139,37 +125,6 @@ __global__ void __launch_bounds__(kPruneThreads) prune_count_kernel(
         if (p3_out) p3_out[i] = static_cast<int32_t>(s_p3);
         // group queries with the same surviving lists: (first surviving list, nearest rep)
         if (order_key) order_key[i] = (static_cast<uint64_t>(s_first & 0xFFFFFFu) << 24) | (key_id(s_near) & 0xFFFFFFu);
-    }
-}
-
-// pass 2: the surviving segments of query i in ascending rep position
-__global__ void __launch_bounds__(kPruneThreads) prune_fill_kernel(
-    const float *__restrict__ d1, int64_t nr, const float *__restrict__ gamma, const float *__restrict__ radii,
-    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, const int64_t *__restrict__ seg_off,
-    int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list) {
-    typedef cub::BlockScan<int, kPruneThreads> Scan;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ int64_t base;
-    const int64_t i = blockIdx.x;
-    const float *row = d1 + i * nr;
-    const double g = gamma[i], cut = 4.0 * g;
-    if (threadIdx.x == 0) base = seg_off[i];
-    __syncthreads();
-    for (int64_t p0 = 0; p0 < nr; p0 += kPruneThreads) {
-        const int64_t p = p0 + threadIdx.x;
-        int32_t len = 0;
-        if (p < nr && survives(row[p], radii[p], g))
-            len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
-        int flag = len > 0 ? 1 : 0, pos, total;
-        Scan(scan_tmp).ExclusiveSum(flag, pos, total);
-        if (flag) {
-            seg_start[base + pos] = offsets[p];
-            seg_len[base + pos] = len;
-            if (seg_list) seg_list[base + pos] = static_cast<int32_t>(p);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) base += total;
-        __syncthreads();
     }
 }
 
@@ -262,7 +217,7 @@ __global__ void __launch_bounds__(256) prune_fill_warp_kernel(
     const float *__restrict__ d1, int64_t nq, int64_t nr, const float *__restrict__ gamma,
     const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
     const int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len,
-    int32_t *__restrict__ seg_list) {
+    int32_t *__restrict__ seg_list, float *__restrict__ seg_d1) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     if (i >= nq) return;
@@ -280,6 +235,7 @@ __global__ void __launch_bounds__(256) prune_fill_warp_kernel(
             seg_start[at] = offsets[p];
             seg_len[at] = len;
             seg_list[at] = static_cast<int32_t>(p);
+            seg_d1[at] = row[p];
         }
         base += __popc(bal);
     }
@@ -322,9 +278,10 @@ int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &ou
     RBC_CHECK(out.seg_start.alloc(total, st));
     RBC_CHECK(out.seg_len.alloc(total, st));
     RBC_CHECK(out.seg_list.alloc(total, st));
+    RBC_CHECK(out.seg_d1.alloc(total, st));
     prune_fill_warp_kernel<<<wgrid, 256, 0, st>>>(d1, nq, idx->nr, out.gamma.get(), idx->radii, idx->offsets,
                                                   idx->list_dists, out.seg_off.get(), out.seg_start.get(),
-                                                  out.seg_len.get(), out.seg_list.get());
+                                                  out.seg_len.get(), out.seg_list.get(), out.seg_d1.get());
     RBC_LAUNCHED();
     return RBC_OK;
 }
@@ -333,34 +290,47 @@ int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &ou
 int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
                       const rbc_search_stats &stats, cudaStream_t st) {
     if (nq == 0) return RBC_OK;
-    // bound the stage-1 block to ~1 GiB per chunk
-    int64_t chunk = (int64_t(1) << 28) / (idx->nr > 0 ? idx->nr : 1);
+    const bool fused = !force_exact_engine() && tc_stage1_supported(idx, k);
+    // bound the stage-1 block to ~1 GiB per chunk (the fused path holds no |Q| x |R| block)
+    int64_t chunk = fused ? (int64_t(1) << 20) : (int64_t(1) << 28) / (idx->nr > 0 ? idx->nr : 1);
     if (chunk < 1) chunk = 1;
     if (chunk > nq) chunk = nq;
     DevBuf<float> d1;
-    RBC_CHECK(d1.alloc(chunk * idx->nr, st));
     for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
         const int64_t m = nq - q0 < chunk ? nq - q0 : chunk;
         const float *qc = q + q0 * idx->d;
-        {
+        std::unique_ptr<PruneOut> po(new PruneOut());
+        po->pr = stats.reps_pruned_radius ? stats.reps_pruned_radius + q0 : nullptr;
+        po->p3 = stats.reps_pruned_3gamma ? stats.reps_pruned_3gamma + q0 : nullptr;
+        bool done = false;
+        if (fused) {
+            // tensor-core stage 1 + pruning (tc_stage1.cu); a buffer overflow falls back below
+            bool fallback = false;
             ProfScope ps(kPhaseStage1, st);
-            RBC_CHECK(stage1_distances(idx, qc, m, d1.get(), st));
+            RBC_CHECK(tc_stage1(idx, qc, m, k, *po, &fallback, st));
+            done = !fallback;
         }
-        PruneOut po;
-        po.pr = stats.reps_pruned_radius ? stats.reps_pruned_radius + q0 : nullptr;
-        po.p3 = stats.reps_pruned_3gamma ? stats.reps_pruned_3gamma + q0 : nullptr;
-        {
+        if (!done) {
+            int32_t *pr = po->pr, *p3 = po->p3;
+            po.reset(new PruneOut());
+            po->pr = pr;
+            po->p3 = p3;
+            if (!d1.get()) RBC_CHECK(d1.alloc(chunk * idx->nr, st));
+            {
+                ProfScope ps(kPhaseStage1, st);
+                RBC_CHECK(stage1_distances(idx, qc, m, d1.get(), st));
+            }
             ProfScope ps(kPhasePrune, st);
-            RBC_CHECK(prune(idx, d1.get(), m, k, po, st));
+            RBC_CHECK(prune(idx, d1.get(), m, k, *po, st));
         }
         {
             ProfScope ps(kPhaseStage2, st);
-            RBC_CHECK(stage2_scan(idx, qc, m, k, po, keys + q0 * k, st));
+            RBC_CHECK(stage2_scan(idx, qc, m, k, *po, keys + q0 * k, st));
         }
         if (stats.gamma)
-            RBC_CUDA(cudaMemcpyAsync(stats.gamma + q0, po.gamma.get(), sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+            RBC_CUDA(cudaMemcpyAsync(stats.gamma + q0, po->gamma.get(), sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
         if (stats.candidates)
-            RBC_CUDA(cudaMemcpyAsync(stats.candidates + q0, po.cand.get(), sizeof(int64_t) * m,
+            RBC_CUDA(cudaMemcpyAsync(stats.candidates + q0, po->cand.get(), sizeof(int64_t) * m,
                                      cudaMemcpyDeviceToDevice, st));
     }
     return RBC_OK;
@@ -369,7 +339,7 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
 // exact fp64 stage 2 over the surviving segments (fallback / reference path)
 int stage2_exact(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                  cudaStream_t st) {
-    SegSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), idx->d};
+    SegSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), po.nseg.get(), idx->d};
     return launch_topk(q, nq, idx->d, idx->metric, k, src, keys, st);
 }
 

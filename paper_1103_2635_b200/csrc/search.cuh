@@ -15,10 +15,11 @@ struct PruneOut {
     DevBuf<float> gamma;       // [nq] gamma_k
     DevBuf<int32_t> nseg;      // [nq] non-empty surviving segments
     DevBuf<int64_t> cand;      // [nq] candidates_examined
-    DevBuf<int64_t> seg_off;   // [nq+1] CSR over segments
+    DevBuf<int64_t> seg_off;   // [nq+1] first segment of query i (its segments: seg_off[i] .. +nseg[i])
     DevBuf<int64_t> seg_start; // [total] first list-order position
     DevBuf<int32_t> seg_len;   // [total] cutoff length
     DevBuf<int32_t> seg_list;  // [total] rep position of the segment
+    DevBuf<float> seg_d1;      // [total] exact dist(q, r_p) of the segment's list
     DevBuf<uint64_t> order_key; // [nq] (first surviving list << 24) | nearest rep: query grouping key
     const float *d1 = nullptr; // stage-1 distances [nq, nr] (owned by the caller)
     int64_t total_segs = 0;

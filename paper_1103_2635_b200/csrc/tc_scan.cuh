@@ -25,6 +25,14 @@ int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1
 int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                 cudaStream_t st);
 
+// tcgen05 stage 1 + pruning (tc_stage1.cu); *fallback = true when a buffer
+// overflowed and the caller must use the exact path for this batch
+bool tc_stage1_supported(const rbc_index *idx, int k);
+int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut &out, bool *fallback,
+              cudaStream_t st);
+// rows of src [rows][d] -> dst [rows][64], zero padded
+void pad_rows64(const float *src, int64_t rows, int d, float *dst, cudaStream_t st);
+
 // tcgen05 stage 2 (tc_stage2.cu)
 bool tc_stage2_supported(const rbc_index *idx, int k);
 int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,

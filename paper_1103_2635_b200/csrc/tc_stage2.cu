@@ -203,8 +203,9 @@ __global__ void iota_kernel(int32_t *v, int64_t n) {
 // union of the tile's surviving lists: count
 __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__restrict__ rows,
                                                            const int64_t *__restrict__ seg_off,
+                                                           const int32_t *__restrict__ seg_cnt,
                                                            const int32_t *__restrict__ seg_list, int64_t nr,
-                                                           int64_t *__restrict__ nwork) {
+                                                           int64_t *__restrict__ nwork, int warm) {
     extern __shared__ int32_t present[];
     __shared__ int s_count;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) present[p] = 0;
@@ -212,23 +213,25 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
     if (qi >= 0)
-        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) present[seg_list[s]] = 1;
+        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) present[seg_list[s]] = 1;
     __syncthreads();
     int c = 0;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) c += present[p];
     atomicAdd(&s_count, c);
     __syncthreads();
-    if (threadIdx.x == 0) nwork[blockIdx.x] = s_count;
+    // + 1 warm-up (max-only) copy of the first list when warm
+    if (threadIdx.x == 0) nwork[blockIdx.x] = s_count + (warm && s_count > 0 ? 1 : 0);
 }
 
 // union of the tile's surviving lists: work items, per-row cutoffs and stage-1
 // distances, and the tile's total work (for the LPT order)
 __global__ void __launch_bounds__(kRows) tile_fill_kernel(
-    const int32_t *__restrict__ rows, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_list,
-    const int32_t *__restrict__ seg_len, const uint64_t *__restrict__ order_key, const float *__restrict__ d1,
+    const int32_t *__restrict__ rows, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
+    const int32_t *__restrict__ seg_list, const int32_t *__restrict__ seg_len, const float *__restrict__ seg_d1,
+    const uint64_t *__restrict__ order_key,
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
     const int64_t *__restrict__ offsets, const int64_t *__restrict__ work_off, WorkItem *__restrict__ work,
-    int32_t *__restrict__ cut, float *__restrict__ rowd1, uint64_t *__restrict__ tile_key) {
+    int32_t *__restrict__ cut, float *__restrict__ rowd1, uint64_t *__restrict__ tile_key, int warm) {
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
@@ -246,10 +249,10 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
     if (qi >= 0) {
-        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) {
+        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) {
             const int32_t p = seg_list[s];
             atomicMax(&maxlen[p], seg_len[s]);
-            atomicMax(&maxd1[p], __float_as_int(d1[static_cast<int64_t>(qi) * nr + p]));
+            atomicMax(&maxd1[p], __float_as_int(seg_d1[s]));
         }
         atomicAdd(&nearcnt[order_key[qi] & 0xFFFFFF], 1);
     }
@@ -264,7 +267,10 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     atomicAdd(&s_work, wsum);
     __syncthreads();
     const int32_t front = s_front == ~0ull ? -1 : static_cast<int32_t>(s_front & 0xFFFFFFFFu);
-    const int64_t w0 = work_off[blockIdx.x];
+    // with warm-up, slot w0 is a max-only copy of the first list (k = 1: it
+    // tightens the running bound before any candidate is buffered)
+    const int64_t wbase = work_off[blockIdx.x];
+    const int64_t w0 = wbase + ((warm && work_off[blockIdx.x + 1] > wbase) ? 1 : 0);
     // ordered compaction: front first, then the others ascending
     for (int64_t p0 = 0; p0 < nr; p0 += kRows) {
         const int64_t p = p0 + threadIdx.x;
@@ -298,12 +304,22 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     __syncthreads();
     if (qi >= 0)
-        for (int64_t s = seg_off[qi]; s < seg_off[qi + 1]; ++s) {
+        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) {
             const int32_t p = seg_list[s];
             const int64_t at = (w0 + nearcnt[p]) * kRows + threadIdx.x;
             cut[at] = seg_len[s];
-            rowd1[at] = d1[static_cast<int64_t>(qi) * nr + p];
+            rowd1[at] = seg_d1[s];
         }
+    if (w0 > wbase) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            WorkItem it = work[w0];
+            it.csr = -1;  // max-only marker
+            work[wbase] = it;
+        }
+        cut[wbase * kRows + threadIdx.x] = cut[w0 * kRows + threadIdx.x];
+        rowd1[wbase * kRows + threadIdx.x] = rowd1[w0 * kRows + threadIdx.x];
+    }
     // LPT: heavier tiles first
     if (threadIdx.x == 0) {
         const unsigned long long wk = s_work < 0xFFFFFFFFFFull ? s_work : 0xFFFFFFFFFFull;
@@ -544,7 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     const float t = 0.5f * scale * (A2 - E - U * kTie);
                     return t - fabsf(t) * (1.0f / 262144.0f) - 1e-30f;
                 };
-                float T = cutv > 0 ? threshold() : __int_as_float(0x7f800000);
+                const bool maxonly = wi.csr < 0;  // warm-up copy: bound only, no candidates
+                float T = (cutv > 0 && !maxonly) ? threshold() : __int_as_float(0x7f800000);
                 float vbest = -__int_as_float(0x7f800000);
                 // push every element of an 8-column group that passes the exact-bound test
                 auto slow8 = [&](const float *v, int col0, int lim) {
@@ -650,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                 const float ub = A2 + E - mv * inv2s;
                                 if (ub < U) {
                                     U = ub;
-                                    T = threshold();
+                                    if (!maxonly) T = threshold();
                                 }
                             }
                         }
@@ -733,6 +750,11 @@ constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kEpiW
 int64_t &last_overflow_count() {
     static int64_t v = 0;
     return v;
+}
+
+void pad_rows64(const float *src, int64_t rows, int d, float *dst, cudaStream_t st) {
+    pad64_rows_kernel<<<grid_for(rows * 64, 256), 256, 0, st>>>(src, rows, d, dst);
+    note_launch();
 }
 
 // ---- index-side preparation ----------------------------------------------------------------
@@ -844,7 +866,9 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
     cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
     cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
-    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), nr, nwork.get());
+    const int warm = k == 1 ? 1 : 0;
+    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.nseg.get(), po.seg_list.get(), nr,
+                                                    nwork.get(), warm);
     RBC_LAUNCHED();
     RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
     size_t tb3 = 0;
@@ -863,10 +887,11 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(cut.alloc(total_work * kRows, st));
     RBC_CHECK(rowd1.alloc(total_work * kRows, st));
     RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
-    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.seg_list.get(), po.seg_len.get(),
-                                                   po.order_key.get(), po.d1, nr, tc->sB, idx->radii, tc->poff,
+    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.nseg.get(), po.seg_list.get(),
+                                                   po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
+                                                   idx->radii, tc->poff,
                                                    idx->offsets, work_off.get(), work.get(), cut.get(), rowd1.get(),
-                                                   tkey.get());
+                                                   tkey.get(), warm);
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
                                              tile_order.get(), ntiles, 0, 40, st));
@@ -957,7 +982,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
             q, ovf_list.get(), n_ovf, idx->d, qsub.get());
         RBC_LAUNCHED();
-        SegSubSrc src{idx->xp, idx->perm, po.seg_start.get(), po.seg_len.get(), po.seg_off.get(), ovf_list.get(), idx->d};
+        SegSubSrc src{idx->xp, idx->perm,     po.seg_start.get(), po.seg_len.get(),
+                      po.seg_off.get(), po.nseg.get(), ovf_list.get(), idx->d};
         RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
         scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
                                                                                          n_ovf, k, keys);
