@@ -15,7 +15,7 @@ import warnings
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librbc_b200.so")
+LIB_PATH = os.environ.get("RBC_B200_LIB") or os.path.join(_HERE, "librbc_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -5,22 +5,23 @@
 // k-th smallest as gamma_k (:181), and keeps r iff
 //   d <= 3 gamma  and  (d < gamma + psi_r  or  d <= gamma)      (:62-74)
 // counting the two pruning tests (:194-195).  Here each 128-query tile is
-// multiplied against all representatives with tcgen05.mma (f16 operands
-// centred on the representatives' mean c; |r - c|^2 / 2 folded into the MMA
-// as in tc_stage2.cu), giving every d^2 inside a rigorous interval [lb, ub].
+// multiplied against all representatives with tcgen05.mma.  Operands are
+// centred on the representatives' mean c and split into f16 hi + lo parts
+// (three MMAs: hi.hi + hi.lo + lo.hi, ~2^-20 relative precision); the
+// per-rep term |r - c|^2 / 2 is folded into the MMA as in tc_stage2.cu.  Every
+// d^2 is thereby known inside a rigorous interval [lb, ub]:
 //   pass 1: the k smallest upper bounds give a bound U_k; every rep with
 //           lb <= U_k is evaluated exactly (fp64, reference arithmetic), so
 //           gamma_k and the nearest rep are exact;
 //   pass 2: every rep is classified against 3 gamma, gamma and gamma + psi_r
-//           using its interval; reps whose class is certain (almost all:
-//           far away) are only counted, the rest -- possible survivors and
+//           with its interval; reps whose class is certain (almost all: far
+//           away) are only counted, the rest -- possible survivors and
 //           interval straddles -- are recorded for the fix-up kernel, which
 //           decides them with exact distances, computes the 4 gamma cutoff by
 //           binary search and emits the surviving segments.
-// No |Q| x |R| distance matrix is materialised.  Any row that exhausts its
-// candidate or record buffer raises a flag and the caller recomputes the
-// batch with the exact path (search.cu), so the result is always the
-// reference's.
+// No |Q| x |R| distance matrix is materialised.  Any row that exhausts a
+// buffer raises a flag and the caller recomputes the batch with the exact
+// path (search.cu), so the result is always the reference's.
 #include <cub/cub.cuh>
 
 #include <vector>
@@ -38,17 +39,19 @@ namespace rbc {
 namespace {
 
 constexpr int kRows = 128;
-constexpr int kN = 256;
-constexpr int kStages = 4;
+constexpr int kN = 128;       // representatives per chunk (UMMA N)
+constexpr int kStages = 3;
 constexpr int kThreads = 192;  // producer, MMA, 4 epilogue warps
 constexpr int kP0 = 128, kP1 = 32;
-constexpr int kStageBytes = kN * (kP0 + kP1);
-constexpr int kABytes = kRows * (kP0 + kP1);
+// per row: hi plane (SW128) | lo plane (SW128) | aug plane (SW32, d > 62 only)
+constexpr int kStageBytes = kN * (2 * kP0 + kP1);
+constexpr int kABytes = kRows * (2 * kP0 + kP1);
 constexpr int kMaxRepsSmem = 6144;  // radii staged in shared memory
 
-constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 128.0f / 4194304.0f);
+// hi/lo split: per-product error 3 * 2^-22, fp32 accumulation of <= 208 terms; factor-2 safety, x2 for d^2
+constexpr float kC1 = 4.0f * (3.0f / 4194304.0f + 208.0f / 8388608.0f);
 constexpr float kC2 = 1.0f / 1048576.0f;
-constexpr float kC4 = 1.0f / 262144.0f;
+constexpr float kC4 = 1.0f / 1073741824.0f;  // subnormal flush of the lo parts (absolute, scaled)
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;
 constexpr float kTie = 1.0f + 1.0f / 524288.0f;
 constexpr float kEps = 1.0f / 262144.0f;  // relative slack of the interval classification
@@ -56,18 +59,17 @@ constexpr float kEps = 1.0f / 262144.0f;  // relative slack of the interval clas
 struct Tc1Index {
     int64_t nrpad = 0;
     bool plane1 = false;
-    uint8_t *rh0 = nullptr;  // [nrpad][128 B] f16 (r - c) * sG (+aug when d <= 62), SW128 pre-swizzled
-    uint8_t *rh1 = nullptr;  // [nrpad][32 B] aug plane (d > 62)
+    uint8_t *rb = nullptr;   // [nrpad] rows of (hi 128 B | lo 128 B | aug 32 B), pre-swizzled
     float *c64 = nullptr;    // [64] centre (mean of the reps), zero padded
     float *stat = nullptr;   // [2] sG, rmax (max |r - c|, rounded up)
     float sG = 1.f, rmax = 0.f;
 };
 
 struct S1Params {
-    const uint8_t *rh0;
-    const uint8_t *rh1;
+    const uint8_t *rb;
     int plane1;
     int64_t nr;
+    int64_t nrpad;
     float sG;
     float rmax;
     const float *c64;
@@ -105,6 +107,31 @@ __device__ __forceinline__ float pick8(const float *v, int j) {
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// f16 hi/lo split of x: hi = f16(x), lo = f16(x - hi)
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t &hi, uint32_t &lo) {
+    hi = sm100::pack_f16x2_sat(x0, x1);
+    const __half2 h = *reinterpret_cast<const __half2 *>(&hi);
+    lo = sm100::pack_f16x2_sat(x0 - __low2float(h), x1 - __high2float(h));
+}
+
+// one 128-byte row (64 f16) of hi and lo planes + aug word at column 62/63 when d <= 62
+__device__ __forceinline__ void write_split_row(uint8_t *hi_row, uint8_t *lo_row, int row, const float *v, float s,
+                                                bool aug_in_row, uint32_t aug) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        uint32_t wh[4], wl[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_f16x2(v[c * 8 + 2 * e] * s, v[c * 8 + 2 * e + 1] * s, wh[e], wl[e]);
+        if (aug_in_row && c == 7) {
+            wh[3] = aug;
+            wl[3] = 0;
+        }
+        const uint32_t o = (c ^ (row & 7)) << 4;
+        *reinterpret_cast<uint4 *>(hi_row + o) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        *reinterpret_cast<uint4 *>(lo_row + o) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+    }
+}
+
 // ---- index preparation ------------------------------------------------------------
 __global__ void rep_centre_kernel(const float *__restrict__ reps, int64_t nr, int d, float *__restrict__ c64) {
     const int k = threadIdx.x;
@@ -135,40 +162,33 @@ __global__ void rep_scale_kernel(const unsigned *__restrict__ rmax_bits, float *
     stat[1] = r;
 }
 
-// B operand rows: f16 (r - c) * sG, SW128 pre-swizzled, aug = (|r - c|^2 / 2) sG^2 hi/lo
+// B operand rows: f16 hi/lo of (r - c) * sG, aug = (|r - c|^2 / 2) sG^2 hi/lo
 __global__ void rep_rows_kernel(const float *__restrict__ reps, int64_t nr, int d, const float *__restrict__ c64,
-                                const float *__restrict__ stat, int plane1, uint8_t *__restrict__ rh0,
-                                uint8_t *__restrict__ rh1) {
+                                const float *__restrict__ stat, int plane1, uint8_t *__restrict__ rb) {
     const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (p >= nr) return;
     const float s = stat[0];
-    const float *x = reps + p * d;
+    float v[64];
     double h = 0.0;
-    for (int k = 0; k < d; ++k) {
-        const double b = __fsub_rn(x[k], c64[k]);
-        h += b * b;
+#pragma unroll
+    for (int k = 0; k < 64; ++k) {
+        v[k] = k < d ? __fsub_rn(reps[p * d + k], c64[k]) : 0.f;
+        h += static_cast<double>(v[k]) * v[k];
     }
     const float gp = static_cast<float>(h) * 0.5f * s * s;
     const __half ghi = __float2half_rn(gp);
     const __half glo = __float2half_rn(gp - __half2float(ghi));
     const uint32_t aug =
         static_cast<uint32_t>(__half_as_ushort(ghi)) | (static_cast<uint32_t>(__half_as_ushort(glo)) << 16);
-    uint8_t *dst = rh0 + p * kP0;
-    for (int c = 0; c < 8; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int k0 = c * 8 + 2 * e, k1 = k0 + 1;
-            const float b0 = k0 < d ? __fsub_rn(x[k0], c64[k0]) : 0.f;
-            const float b1 = k1 < d ? __fsub_rn(x[k1], c64[k1]) : 0.f;
-            w[e] = sm100::pack_f16x2_sat(b0 * s, b1 * s);
-        }
-        if (!plane1 && c == 7) w[3] = aug;
-        *reinterpret_cast<uint4 *>(dst + ((c ^ (p & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-    }
+    uint8_t *row = rb + p * (2 * kP0 + kP1);
+    // rows are grouped in kN-row chunks: chunk base | hi plane (kN x 128) | lo plane | aug plane
+    const int64_t ch = p / kN, r = p % kN;
+    uint8_t *base = rb + ch * static_cast<int64_t>(kStageBytes);
+    (void)row;
+    write_split_row(base + r * kP0, base + kN * kP0 + r * kP0, static_cast<int>(r), v, s, !plane1, aug);
     if (plane1) {
-        uint8_t *d1p = rh1 + p * kP1;
-        const int sw = static_cast<int>((p >> 2) & 1);
+        uint8_t *d1p = base + 2 * kN * kP0 + r * kP1;
+        const int sw = static_cast<int>((r >> 2) & 1);
         *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
         *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
     }
@@ -206,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
         }
         sm100::fence_barrier_init();
     }
-    if (warp == 1) sm100::tmem_alloc<512>(s_tmem);
+    if (warp == 1) sm100::tmem_alloc<256>(s_tmem);
     sm100::tc_fence_before();
     __syncthreads();
     sm100::tc_fence_after();
@@ -225,24 +245,20 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                 s_tiles[slot] = tile;
                 sm100::mbar_arrive(&tile_full[slot]);
                 if (tile < 0) break;
+                const uint32_t bytes = P.plane1 ? kStageBytes : 2 * kN * kP0;
                 for (int pass = 0; pass < 2; ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
-                        const int off = ch * kN;
-                        const int n = min(kN, roundup16(static_cast<int>(P.nr) - off));
                         const uint32_t s = bi % kStages;
                         sm100::mbar_wait(&empty[s], ((bi / kStages) & 1) ^ 1);
-                        uint8_t *dst = sB + s * kStageBytes;
-                        const uint32_t b0 = static_cast<uint32_t>(n) * kP0;
-                        const uint32_t b1 = P.plane1 ? static_cast<uint32_t>(n) * kP1 : 0u;
-                        sm100::mbar_arrive_expect_tx(&full[s], b0 + b1);
-                        sm100::bulk_g2s(dst, P.rh0 + static_cast<int64_t>(off) * kP0, b0, &full[s]);
-                        if (b1) sm100::bulk_g2s(dst + kN * kP0, P.rh1 + static_cast<int64_t>(off) * kP1, b1, &full[s]);
+                        sm100::mbar_arrive_expect_tx(&full[s], bytes);
+                        sm100::bulk_g2s(sB + s * kStageBytes, P.rb + static_cast<int64_t>(ch) * kStageBytes, bytes,
+                                        &full[s]);
                         ++bi;
                     }
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
+        // ===== MMA issuer: hi.hi + hi.lo + lo.hi (+ aug plane) =====
         if (lane == 0) {
             uint32_t bi = 0, ti = 0, ai = 0;
             for (uint32_t it = 0;; ++it) {
@@ -254,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                 const uint32_t a = ai & 1;
                 sm100::mbar_wait(&afull[a], (ai >> 1) & 1);
                 sm100::tc_fence_after();
-                const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
+                const uint32_t ah = sm100::smem_u32(sA + a * kABytes), al = ah + kRows * kP0;
                 for (int pass = 0; pass < 2; ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
                         const int n = min(kN, roundup16(static_cast<int>(P.nr) - ch * kN));
@@ -263,15 +279,23 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                         sm100::mbar_wait(&tempty[tb], ((ti >> 1) & 1) ^ 1);
                         sm100::tc_fence_after();
                         const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
-                        const uint32_t b0 = sm100::smem_u32(sB + s * kStageBytes);
+                        const uint32_t bh = sm100::smem_u32(sB + s * kStageBytes), bl = bh + kN * kP0;
                         const uint32_t d_tmem = tmem + tb * kN;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32),
-                                            sm100::umma_desc_sw128(b0 + kk * 32), idesc, kk > 0);
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(ah + kk * 32), sm100::umma_desc_sw128(bh + kk * 32),
+                                            idesc, kk > 0);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(ah + kk * 32), sm100::umma_desc_sw128(bl + kk * 32),
+                                            idesc, 1);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(al + kk * 32), sm100::umma_desc_sw128(bh + kk * 32),
+                                            idesc, 1);
                         if (P.plane1)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(a0 + kRows * kP0),
-                                            sm100::umma_desc_sw32(b0 + kN * kP0), idesc, 1);
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(al + kRows * kP0),
+                                            sm100::umma_desc_sw32(bl + kN * kP0), idesc, 1);
                         sm100::umma_commit(&empty[s]);
                         sm100::umma_commit(&tfull[tb]);
                         ++bi;
@@ -285,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
         // ===== epilogue: one query row per thread =====
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
         uint32_t ti = 0, ai = 0;
         for (uint32_t it = 0;; ++it) {
             const uint32_t slot = it & 1;
@@ -303,8 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                 const float4 *cc = reinterpret_cast<const float4 *>(P.c64);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    const float4 t = live ? __ldg(src + c) : __ldg(cc + c);
                     const float4 m = __ldg(cc + c);
+                    const float4 t = live ? __ldg(src + c) : m;
                     qv[4 * c] = __fsub_rn(t.x, m.x);
                     qv[4 * c + 1] = __fsub_rn(t.y, m.y);
                     qv[4 * c + 2] = __fsub_rn(t.z, m.z);
@@ -328,24 +353,18 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             const float scale = sa * P.sG, inv2s = 2.0f / scale;
             const float cf = sa / P.sG;
             const float acoef = (cf >= 6.103515625e-05f && cf <= 32768.0f) ? -cf : 0.0f;
-            // A operand (f16, SW128 K-major) + aug columns
+            bool fail = acoef == 0.0f;
+            // A operand: hi | lo | aug planes
             {
                 const uint32_t a = ai & 1;
                 sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
                 const __half ac = __float2half_rn(acoef);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
-                uint8_t *dst = sA + a * kABytes + row * kP0;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t wv[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        wv[e] = sm100::pack_f16x2_sat(qv[c * 8 + 2 * e] * sa, qv[c * 8 + 2 * e + 1] * sa);
-                    if (!P.plane1 && c == 7) wv[3] = aug;
-                    *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                }
+                uint8_t *abuf = sA + a * kABytes;
+                write_split_row(abuf + row * kP0, abuf + kRows * kP0 + row * kP0, row, qv, sa, !P.plane1, aug);
                 if (P.plane1) {
-                    uint8_t *d1p = sA + a * kABytes + kRows * kP0 + row * kP1;
+                    // the aug pairs with the B aug plane through the lo-plane descriptor slot
+                    uint8_t *d1p = abuf + 2 * kRows * kP0 + row * kP1;
                     const int sw = (row >> 2) & 1;
                     *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
                     *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
@@ -357,9 +376,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             }
             const float rb = P.rmax;
             const float E = kC1 * nqv * rb + kC2 * (qn + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
-            const float *gcol = nullptr;  // (acoef == 0 only for degenerate scales; handled by the fail flag)
-            (void)gcol;
-            bool fail = acoef == 0.0f;
 
             // ---------- pass 1: bound and collect the k nearest representatives ----------
             float ubk[KT];
@@ -374,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                 const float t = 0.5f * scale * (qn - E - U * kTie);
                 return t - fabsf(t) * (1.0f / 262144.0f) - 1e-30f;
             };
-            float T = -__int_as_float(0x7f800000);
+            float T = live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
             float vbest = -__int_as_float(0x7f800000);
             auto slow8 = [&](const float *v, int col0) {
                 unsigned mask = 0;
@@ -415,11 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
 #pragma unroll
                     for (int t = 0; t < KT; ++t)
                         if (t == P.k - 1) kth = ubk[t];
-                    U = kth;
+                    U = fminf(U, kth);
                     T = threshold();
                 }
             };
-            const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
             for (int ch = 0; ch < nchunks; ++ch) {
                 const int off = ch * kN;
                 const int lim = min(kN, static_cast<int>(P.nr) - off);
@@ -441,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     float m8[8];
 #pragma unroll
                     for (int s = 0; s < 8; ++s) m8[s] = max8(v + 8 * s);
-                    if (KT == 1) {
+                    if (KT == 1 && live) {
                         float mv = -__int_as_float(0x7f800000);
 #pragma unroll
                         for (int s = 0; s < 8; ++s)
@@ -483,8 +498,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
 #pragma unroll
             for (int t = 0; t < KT; ++t)
                 if (t == P.k - 1) kth_key = best[t];
-            if (kth_key == kEmptyKey) fail = true;
-            const float g = key_dist(kth_key);
+            if (live && kth_key == kEmptyKey) fail = true;
+            const float g = live ? key_dist(kth_key) : 0.f;
             const float g2 = g * g;
             const float t3 = 9.0f * g2;
 
@@ -501,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     uint32_t ra[32];
                     sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0, ra);
                     sm100::tmem_wait_ld(ra);
+                    if (!live) continue;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const int p = off + c0 + j;
@@ -508,19 +524,20 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                         const float dt = qn - __uint_as_float(ra[j]) * inv2s;
                         const float lb = dt - E, ub = dt + E;
                         if (lb > t3 * (1.0f + kEps)) {
-                            // certainly d > 3 gamma (and d > gamma): pruned by both when d >= gamma + psi
-                            ++p3;
+                            // certainly d > 3 gamma (and d > gamma); radius test decides pr
                             const float tp = g + s_radii[p];
                             const float tp2 = tp * tp;
                             if (lb > tp2 * (1.0f + kEps)) {
+                                ++p3;
                                 ++pr;
-                            } else if (!(ub < tp2 * (1.0f - kEps))) {
-                                --p3;  // undecided radius test: the fix-up decides this rep entirely
-                                if (rc < P.cap_rec) rec[rc] = p;
+                            } else if (ub < tp2 * (1.0f - kEps)) {
+                                ++p3;
+                            } else {
+                                if (rc < P.cap_rec) rec[rc] = p;  // undecided radius test
                                 ++rc;
                             }
                         } else {
-                            if (rc < P.cap_rec) rec[rc] = p;
+                            if (rc < P.cap_rec) rec[rc] = p;  // possible survivor / straddle
                             ++rc;
                         }
                     }
@@ -543,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
     }
     sm100::tc_fence_before();
     __syncthreads();
-    if (warp == 1) sm100::tmem_dealloc<512>(tmem);
+    if (warp == 1) sm100::tmem_dealloc<256>(tmem);
 }
 
 // Fix-up, one warp per query: exact decisions for the recorded reps, the
@@ -552,7 +569,7 @@ __global__ void __launch_bounds__(256) stage1_fixup_kernel(
     const float *__restrict__ q, const float *__restrict__ reps, int d, int64_t nq, const float *__restrict__ radii,
     const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, const float *__restrict__ gamma,
     const int32_t *__restrict__ nearest, const int32_t *__restrict__ rec_cnt, const int32_t *__restrict__ rec,
-    int cap_rec, int32_t *__restrict__ pr_io, int32_t *__restrict__ p3_io, int32_t *__restrict__ nseg,
+    int cap_rec, const int32_t *__restrict__ pr_in, const int32_t *__restrict__ p3_in, int32_t *__restrict__ nseg,
     int64_t *__restrict__ cand, int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start,
     int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list, float *__restrict__ seg_d1,
     uint64_t *__restrict__ order_key, int32_t *__restrict__ pr_out, int32_t *__restrict__ p3_out) {
@@ -599,9 +616,8 @@ __global__ void __launch_bounds__(256) stage1_fixup_kernel(
         first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
     }
     if (lane == 0) {
-        const int prt = pr_io[i] + pr, p3t = p3_io[i] + p3;
-        if (pr_out) pr_out[i] = prt;
-        if (p3_out) p3_out[i] = p3t;
+        if (pr_out) pr_out[i] = pr_in[i] + pr;
+        if (p3_out) p3_out[i] = p3_in[i] + p3;
         nseg[i] = ns;
         cand[i] = cs;
         seg_off[i] = base;
@@ -617,16 +633,15 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->nr > kMaxRepsSmem) return RBC_OK;
     Tc1Index *t = new Tc1Index();
     t->plane1 = idx->d > 62;
-    t->nrpad = ((idx->nr + 15) & ~int64_t(15)) + kN;
+    const int64_t nchunks = (idx->nr + kN - 1) / kN;
+    t->nrpad = nchunks * kN;
     unsigned *rmax_bits = nullptr;
-    bool ok = cudaMalloc(&t->rh0, t->nrpad * kP0) == cudaSuccess &&
-              (!t->plane1 || cudaMalloc(&t->rh1, t->nrpad * kP1) == cudaSuccess) &&
+    bool ok = cudaMalloc(&t->rb, nchunks * kStageBytes) == cudaSuccess &&
               cudaMalloc(&t->c64, 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->stat, 2 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&rmax_bits, sizeof(unsigned)) == cudaSuccess;
     auto cleanup = [&](int rc) {
-        cudaFree(t->rh0);
-        cudaFree(t->rh1);
+        cudaFree(t->rb);
         cudaFree(t->c64);
         cudaFree(t->stat);
         cudaFree(rmax_bits);
@@ -637,14 +652,13 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaGetLastError();
         return cleanup(fail(RBC_ENOMEM, "tc1 index allocation"));
     }
-    cudaMemsetAsync(t->rh0, 0, t->nrpad * kP0, st);
-    if (t->plane1) cudaMemsetAsync(t->rh1, 0, t->nrpad * kP1, st);
+    cudaMemsetAsync(t->rb, 0, nchunks * kStageBytes, st);
     cudaMemsetAsync(rmax_bits, 0, sizeof(unsigned), st);
     rep_centre_kernel<<<1, 64, 0, st>>>(idx->reps, idx->nr, idx->d, t->c64);
     rep_extent_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, t->c64, rmax_bits);
     rep_scale_kernel<<<1, 1, 0, st>>>(rmax_bits, t->stat);
     rep_rows_kernel<<<grid_for(idx->nr, 128), 128, 0, st>>>(idx->reps, idx->nr, idx->d, t->c64, t->stat,
-                                                          t->plane1 ? 1 : 0, t->rh0, t->rh1);
+                                                          t->plane1 ? 1 : 0, t->rb);
     note_launch(4);
     float stat[2] = {1.f, 0.f};
     if (cudaMemcpyAsync(stat, t->stat, sizeof(stat), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -654,7 +668,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     rmax_bits = nullptr;
     t->sG = stat[0];
     t->rmax = stat[1];
-    idx->bytes += t->nrpad * (kP0 + (t->plane1 ? kP1 : 0)) + 66 * sizeof(float);
+    idx->bytes += nchunks * kStageBytes + 66 * sizeof(float);
     idx->tc1 = t;
     return RBC_OK;
 }
@@ -662,8 +676,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
 void tc1_index_release(rbc_index *idx) {
     Tc1Index *t = static_cast<Tc1Index *>(idx->tc1);
     if (!t) return;
-    cudaFree(t->rh0);
-    cudaFree(t->rh1);
+    cudaFree(t->rb);
     cudaFree(t->c64);
     cudaFree(t->stat);
     delete t;
@@ -709,10 +722,10 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(out.seg_d1.alloc(nq * cap_rec, st));
     RBC_CUDA(cudaMemsetAsync(flags.get(), 0, 2 * sizeof(int32_t), st));
     S1Params P;
-    P.rh0 = t->rh0;
-    P.rh1 = t->rh1;
+    P.rb = t->rb;
     P.plane1 = t->plane1 ? 1 : 0;
     P.nr = idx->nr;
+    P.nrpad = t->nrpad;
     P.sG = t->sG;
     P.rmax = t->rmax;
     P.c64 = t->c64;
