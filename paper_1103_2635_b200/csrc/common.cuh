@@ -102,7 +102,21 @@ __device__ __forceinline__ double l1_term(float a, float b) {
 template <int METRIC>
 __device__ __forceinline__ float exact_dist(const float *__restrict__ a, const float *__restrict__ b, int d) {
     double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(a[k], b[k]) : l1_term(a[k], b[k]));
+    int k = 0;
+    // loads batched 8 at a time (independent, in flight together); the
+    // accumulation itself stays strictly in coordinate order
+    for (; k + 8 <= d; k += 8) {
+        float av[8], bv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            av[j] = a[k + j];
+            bv[j] = b[k + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(av[j], bv[j]) : l1_term(av[j], bv[j]));
+    }
+    for (; k < d; ++k) acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(a[k], b[k]) : l1_term(a[k], b[k]));
     if (METRIC == RBC_L2) return __double2float_rn(__dsqrt_rn(acc));
     return __double2float_rn(acc);
 }

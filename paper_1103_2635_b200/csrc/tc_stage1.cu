@@ -62,6 +62,7 @@ struct Tc1Index {
     uint8_t *rb = nullptr;   // [nrpad] rows of (hi 128 B | lo 128 B | aug 32 B), pre-swizzled
     float *c64 = nullptr;    // [64] centre (mean of the reps), zero padded
     float *stat = nullptr;   // [2] sG, rmax (max |r - c|, rounded up)
+    float *psimax = nullptr; // [nchunks] largest list radius of each rep chunk
     float sG = 1.f, rmax = 0.f;
 };
 
@@ -73,6 +74,7 @@ struct S1Params {
     float sG;
     float rmax;
     const float *c64;
+    const float *psimax;
     const float *q64;
     const float *q;
     const float *reps;
@@ -106,6 +108,18 @@ __device__ __forceinline__ float pick8(const float *v, int j) {
     return (j & 1) ? b1 : b0;
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// r[j] for a runtime j in [0, 32) without local memory (select tree)
+__device__ __forceinline__ uint32_t pick32u(const uint32_t (&r)[32], int j) {
+    uint32_t t16[16], t8[8], t4[4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t16[i] = (j & 16) ? r[i + 16] : r[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t8[i] = (j & 8) ? t16[i + 8] : t16[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[i + 4] : t8[i];
+    const uint32_t a = (j & 2) ? t4[2] : t4[0], b = (j & 2) ? t4[3] : t4[1];
+    return (j & 1) ? b : a;
+}
 
 // f16 hi/lo split of x: hi = f16(x), lo = f16(x - hi)
 __device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t &hi, uint32_t &lo) {
@@ -152,6 +166,14 @@ __global__ void rep_extent_kernel(const float *__restrict__ reps, int64_t nr, in
         h += b * b;
     }
     atomicMax(rmax_bits, __float_as_uint(static_cast<float>(sqrt(h)) * kUp));
+}
+
+__global__ void chunk_psimax_kernel(const float *__restrict__ radii, int64_t nr, float *__restrict__ psimax) {
+    const int64_t ch = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (ch * kN >= nr) return;
+    float m = 0.f;
+    for (int64_t p = ch * kN; p < nr && p < (ch + 1) * kN; ++p) m = fmaxf(m, radii[p]);
+    psimax[ch] = m * kUp;
 }
 
 __global__ void rep_scale_kernel(const unsigned *__restrict__ rmax_bits, float *__restrict__ stat) {
@@ -510,6 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                 const int off = ch * kN;
                 const int lim = min(kN, static_cast<int>(P.nr) - off);
                 const uint32_t tb = ti & 1;
+                // reps farther than max(3 gamma, gamma + max psi of the chunk) are pruned by both tests
+                const float tpm = g + P.psimax[ch];
+                const float thr_far = fmaxf(t3, tpm * tpm) * (1.0f + kEps) + E;  // on dt = d^2 estimate
                 sm100::mbar_wait(&tfull[tb], (ti >> 1) & 1);
                 sm100::tc_fence_after();
                 for (int c0 = 0; c0 < lim; c0 += 32) {
@@ -517,11 +542,21 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0, ra);
                     sm100::tmem_wait_ld(ra);
                     if (!live) continue;
+                    const int nvalid = min(32, lim - c0);
+                    const unsigned valid = nvalid == 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+                    unsigned nearm = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
+                    for (int j = 0; j < 32; ++j)
+                        nearm |= ((qn - __uint_as_float(ra[j]) * inv2s) > thr_far ? 0u : 1u) << j;
+                    nearm &= valid;
+                    const int nfar = nvalid - __popc(nearm);
+                    pr += nfar;
+                    p3 += nfar;
+                    while (nearm) {
+                        const int j = __ffs(nearm) - 1;
+                        nearm &= nearm - 1;
                         const int p = off + c0 + j;
-                        if (p >= P.nr) break;
-                        const float dt = qn - __uint_as_float(ra[j]) * inv2s;
+                        const float dt = qn - __uint_as_float(pick32u(ra, j)) * inv2s;
                         const float lb = dt - E, ub = dt + E;
                         if (lb > t3 * (1.0f + kEps)) {
                             // certainly d > 3 gamma (and d > gamma); radius test decides pr
@@ -637,11 +672,13 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     t->nrpad = nchunks * kN;
     unsigned *rmax_bits = nullptr;
     bool ok = cudaMalloc(&t->rb, nchunks * kStageBytes) == cudaSuccess &&
+              cudaMalloc(&t->psimax, nchunks * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->c64, 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->stat, 2 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&rmax_bits, sizeof(unsigned)) == cudaSuccess;
     auto cleanup = [&](int rc) {
         cudaFree(t->rb);
+        cudaFree(t->psimax);
         cudaFree(t->c64);
         cudaFree(t->stat);
         cudaFree(rmax_bits);
@@ -659,7 +696,8 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     rep_scale_kernel<<<1, 1, 0, st>>>(rmax_bits, t->stat);
     rep_rows_kernel<<<grid_for(idx->nr, 128), 128, 0, st>>>(idx->reps, idx->nr, idx->d, t->c64, t->stat,
                                                           t->plane1 ? 1 : 0, t->rb);
-    note_launch(4);
+    chunk_psimax_kernel<<<grid_for(nchunks, 64), 64, 0, st>>>(idx->radii, idx->nr, t->psimax);
+    note_launch(5);
     float stat[2] = {1.f, 0.f};
     if (cudaMemcpyAsync(stat, t->stat, sizeof(stat), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -677,6 +715,7 @@ void tc1_index_release(rbc_index *idx) {
     Tc1Index *t = static_cast<Tc1Index *>(idx->tc1);
     if (!t) return;
     cudaFree(t->rb);
+    cudaFree(t->psimax);
     cudaFree(t->c64);
     cudaFree(t->stat);
     delete t;
@@ -729,6 +768,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     P.sG = t->sG;
     P.rmax = t->rmax;
     P.c64 = t->c64;
+    P.psimax = t->psimax;
     P.q64 = q64;
     P.q = q;
     P.reps = idx->reps;
