@@ -63,8 +63,45 @@ struct Tc1Index {
     float *c64 = nullptr;    // [64] centre (mean of the reps), zero padded
     float *stat = nullptr;   // [2] sG, rmax (max |r - c|, rounded up)
     float *psimax = nullptr; // [nchunks] largest list radius of each rep chunk
+    float *lskip = nullptr;  // [nr][32] list_dists at the end of each of 32 equal blocks (cutoff skip table)
     float sG = 1.f, rmax = 0.f;
 };
+
+// skip table: sample i of list p = list_dists at position min(len, (i+1) * s) - 1, s = ceil(len / 32)
+__global__ void list_skip_kernel(const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, int64_t nr,
+                                 float *__restrict__ lskip) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= nr * 32) return;
+    const int64_t p = t >> 5, i = t & 31;
+    const int64_t len = offsets[p + 1] - offsets[p];
+    const int64_t s = (len + 31) / 32;
+    const int64_t pos = min(len, (i + 1) * s) - 1;
+    lskip[t] = (len > 0 && pos >= 0) ? list_dists[offsets[p] + pos] : __int_as_float(0x7f800000);
+}
+
+// list_cutoff (search.py:77-82) through the skip table: #entries <= thr, f64 compares
+__device__ __forceinline__ int32_t list_cutoff_skip(const float *__restrict__ l, int32_t len,
+                                                    const float *__restrict__ skip, double thr) {
+    if (len == 0) return 0;
+    const int32_t s = (len + 31) / 32;
+    const float4 *s4 = reinterpret_cast<const float4 *>(skip);
+    int b = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float4 v = __ldg(s4 + c);
+        b += (static_cast<double>(v.x) <= thr) + (static_cast<double>(v.y) <= thr) + (static_cast<double>(v.z) <= thr) +
+             (static_cast<double>(v.w) <= thr);
+    }
+    // blocks 0..b-1 lie entirely at or below thr; search block b
+    int32_t lo = b * s, hi = min(len, (b + 1) * s);
+    if (lo >= len) return len;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (static_cast<double>(l[mid]) <= thr) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
 
 struct S1Params {
     const uint8_t *rb;
@@ -602,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
 // 4 gamma cutoffs, the surviving segments (ascending rep position) and stats.
 __global__ void __launch_bounds__(256) stage1_fixup_kernel(
     const float *__restrict__ q, const float *__restrict__ reps, int d, int64_t nq, const float *__restrict__ radii,
-    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, const float *__restrict__ gamma,
+    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, const float *__restrict__ lskip,
+    const float *__restrict__ gamma,
     const int32_t *__restrict__ nearest, const int32_t *__restrict__ rec_cnt, const int32_t *__restrict__ rec,
     int cap_rec, const int32_t *__restrict__ pr_in, const int32_t *__restrict__ p3_in, int32_t *__restrict__ nseg,
     int64_t *__restrict__ cand, int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start,
@@ -629,7 +667,8 @@ __global__ void __launch_bounds__(256) stage1_fixup_kernel(
             pr += pruned_radius(dist, radii[p], g) ? 1 : 0;
             p3 += pruned_3gamma(dist, g) ? 1 : 0;
             if (survives(dist, radii[p], g))
-                len = list_cutoff_dev(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]), cut);
+                len = list_cutoff_skip(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]),
+                                       lskip + static_cast<int64_t>(p) * 32, cut);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, len > 0);
         if (len > 0) {
@@ -673,12 +712,14 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     unsigned *rmax_bits = nullptr;
     bool ok = cudaMalloc(&t->rb, nchunks * kStageBytes) == cudaSuccess &&
               cudaMalloc(&t->psimax, nchunks * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&t->lskip, idx->nr * 32 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->c64, 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->stat, 2 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&rmax_bits, sizeof(unsigned)) == cudaSuccess;
     auto cleanup = [&](int rc) {
         cudaFree(t->rb);
         cudaFree(t->psimax);
+        cudaFree(t->lskip);
         cudaFree(t->c64);
         cudaFree(t->stat);
         cudaFree(rmax_bits);
@@ -697,7 +738,8 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     rep_rows_kernel<<<grid_for(idx->nr, 128), 128, 0, st>>>(idx->reps, idx->nr, idx->d, t->c64, t->stat,
                                                           t->plane1 ? 1 : 0, t->rb);
     chunk_psimax_kernel<<<grid_for(nchunks, 64), 64, 0, st>>>(idx->radii, idx->nr, t->psimax);
-    note_launch(5);
+    list_skip_kernel<<<grid_for(idx->nr * 32, 256), 256, 0, st>>>(idx->offsets, idx->list_dists, idx->nr, t->lskip);
+    note_launch(6);
     float stat[2] = {1.f, 0.f};
     if (cudaMemcpyAsync(stat, t->stat, sizeof(stat), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -716,6 +758,7 @@ void tc1_index_release(rbc_index *idx) {
     if (!t) return;
     cudaFree(t->rb);
     cudaFree(t->psimax);
+    cudaFree(t->lskip);
     cudaFree(t->c64);
     cudaFree(t->stat);
     delete t;
@@ -805,7 +848,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     else launch(stage1_tc_kernel<16>);
     RBC_LAUNCHED();
     stage1_fixup_kernel<<<grid_for(nq * 32, 256), 256, 0, st>>>(
-        q, idx->reps, idx->d, nq, idx->radii, idx->offsets, idx->list_dists, out.gamma.get(), nearest.get(),
+        q, idx->reps, idx->d, nq, idx->radii, idx->offsets, idx->list_dists, t->lskip, out.gamma.get(), nearest.get(),
         rec_cnt.get(), rec.get(), cap_rec, pr0.get(), p30.get(), out.nseg.get(), out.cand.get(), out.seg_off.get(),
         out.seg_start.get(), out.seg_len.get(), out.seg_list.get(), out.seg_d1.get(), out.order_key.get(), out.pr,
         out.p3);
