@@ -100,9 +100,33 @@ __device__ __forceinline__ double l1_term(float a, float b) {
 }
 
 template <int METRIC>
+__device__ __forceinline__ double exact_acc4(double acc, const float4 &x, const float4 &y) {
+    acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(x.x, y.x) : l1_term(x.x, y.x));
+    acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(x.y, y.y) : l1_term(x.y, y.y));
+    acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(x.z, y.z) : l1_term(x.z, y.z));
+    acc = __dadd_rn(acc, METRIC == RBC_L2 ? l2_term(x.w, y.w) : l1_term(x.w, y.w));
+    return acc;
+}
+
+template <int METRIC>
 __device__ __forceinline__ float exact_dist(const float *__restrict__ a, const float *__restrict__ b, int d) {
     double acc = 0.0;
     int k = 0;
+    if (((d & 3) | ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)) == 0) {
+        // 16-byte rows: 16 coordinates (4+4 vector loads) in flight per step
+        const float4 *a4 = reinterpret_cast<const float4 *>(a), *b4 = reinterpret_cast<const float4 *>(b);
+        for (; k + 16 <= d; k += 16) {
+            float4 x[4], y[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                x[j] = a4[(k >> 2) + j];
+                y[j] = b4[(k >> 2) + j];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc = exact_acc4<METRIC>(acc, x[j], y[j]);
+        }
+        for (; k + 4 <= d; k += 4) acc = exact_acc4<METRIC>(acc, a4[k >> 2], b4[k >> 2]);
+    }
     // loads batched 8 at a time (independent, in flight together); the
     // accumulation itself stays strictly in coordinate order
     for (; k + 8 <= d; k += 8) {
