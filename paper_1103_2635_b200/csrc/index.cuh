@@ -35,6 +35,9 @@ struct rbc_index {
 
     // one-shot: [nr, s] point ids
     int32_t *lists = nullptr;
+
+    // stage-2 work-item capacity learned from previous searches (tile unions)
+    mutable int64_t s2_work_per_tile = 24;
 };
 
 namespace rbc {

@@ -304,11 +304,38 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
         po->p3 = stats.reps_pruned_3gamma ? stats.reps_pruned_3gamma + q0 : nullptr;
         bool done = false;
         if (fused) {
-            // tensor-core stage 1 + pruning (tc_stage1.cu); a buffer overflow falls back below
-            bool fallback = false;
-            ProfScope ps(kPhaseStage1, st);
-            RBC_CHECK(tc_stage1(idx, qc, m, k, *po, &fallback, st));
-            done = !fallback;
+            // tensor-core stage 1 + pruning (tc_stage1.cu) and stage 2 (tc_stage2.cu),
+            // stream-ordered with a single host round trip; rare buffer overflows re-run below
+            DevBuf<int32_t> s1fail;
+            DevBuf<int64_t> s2status;
+            RBC_CHECK(s1fail.alloc(1, st));
+            RBC_CHECK(s2status.alloc(2, st));
+            RBC_CUDA(cudaMemsetAsync(s1fail.get(), 0, sizeof(int32_t), st));
+            {
+                ProfScope ps(kPhaseStage1, st);
+                RBC_CHECK(tc_stage1(idx, qc, m, k, *po, s1fail.get(), st));
+            }
+            const bool tc2 = tc_stage2_supported(idx, k);
+            const int64_t cap = stage2_work_capacity(idx, m);
+            if (tc2) {
+                ProfScope ps(kPhaseStage2, st);
+                RBC_CHECK(tc_stage2(idx, qc, m, k, *po, keys + q0 * k, cap, s2status.get(), st));
+            }
+            int32_t f = 0;
+            int64_t s2[2] = {0, 0};
+            RBC_CUDA(cudaMemcpyAsync(&f, s1fail.get(), sizeof(f), cudaMemcpyDeviceToHost, st));
+            if (tc2) RBC_CUDA(cudaMemcpyAsync(s2, s2status.get(), sizeof(s2), cudaMemcpyDeviceToHost, st));
+            RBC_CUDA(cudaStreamSynchronize(st));
+            if (!f) {
+                if (!tc2 || s2[0] > cap) {
+                    if (tc2) stage2_note_work(idx, m, s2[0]);
+                    ProfScope ps(kPhaseStage2, st);
+                    RBC_CHECK(stage2_scan(idx, qc, m, k, *po, keys + q0 * k, st));
+                } else {
+                    last_overflow_count() = s2[1];
+                }
+                done = true;
+            }
         }
         if (!done) {
             int32_t *pr = po->pr, *p3 = po->p3;
@@ -320,10 +347,10 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
                 ProfScope ps(kPhaseStage1, st);
                 RBC_CHECK(stage1_distances(idx, qc, m, d1.get(), st));
             }
-            ProfScope ps(kPhasePrune, st);
-            RBC_CHECK(prune(idx, d1.get(), m, k, *po, st));
-        }
-        {
+            {
+                ProfScope ps(kPhasePrune, st);
+                RBC_CHECK(prune(idx, d1.get(), m, k, *po, st));
+            }
             ProfScope ps(kPhaseStage2, st);
             RBC_CHECK(stage2_scan(idx, qc, m, k, *po, keys + q0 * k, st));
         }

@@ -29,9 +29,33 @@ int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1
     return pairwise(q, nq, idx->reps, idx->nr, idx->d, idx->metric, d1, st);
 }
 
+int64_t stage2_work_capacity(const rbc_index *idx, int64_t nq) {
+    const int64_t ntiles = (nq + 127) / 128;
+    return ntiles * idx->s2_work_per_tile + 64;
+}
+
+void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed) {
+    const int64_t ntiles = (nq + 127) / 128;
+    const int64_t per = (needed + ntiles - 1) / (ntiles > 0 ? ntiles : 1) + 4;
+    if (per > idx->s2_work_per_tile) idx->s2_work_per_tile = per;
+}
+
 int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                 cudaStream_t st) {
-    if (!force_exact_engine() && tc_stage2_supported(idx, k)) return tc_stage2(idx, q, nq, k, po, keys, st);
+    if (!force_exact_engine() && tc_stage2_supported(idx, k)) {
+        DevBuf<int64_t> status;
+        RBC_CHECK(status.alloc(2, st));
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            const int64_t cap = stage2_work_capacity(idx, nq);
+            RBC_CHECK(tc_stage2(idx, q, nq, k, po, keys, cap, status.get(), st));
+            int64_t h[2] = {0, 0};
+            RBC_CUDA(cudaMemcpyAsync(h, status.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+            RBC_CUDA(cudaStreamSynchronize(st));
+            last_overflow_count() = h[1];
+            if (h[0] <= cap) return RBC_OK;
+            stage2_note_work(idx, nq, h[0]);
+        }
+    }
     last_overflow_count() = 0;
     return stage2_exact(idx, q, nq, k, po, keys, st);
 }

@@ -21,23 +21,31 @@ int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d,
 // stage 1 of the searches: bit-exact dist(q_i, r_p) -> d1[nq, nr]
 int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1, cudaStream_t st);
 
-// stage 2 of the exact search over the pruned segments
+// stage 2 of the exact search over the pruned segments (synchronising wrapper
+// around tc_stage2 / stage2_exact)
 int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                 cudaStream_t st);
 
-// tcgen05 stage 1 + pruning (tc_stage1.cu); *fallback = true when a buffer
-// overflowed and the caller must use the exact path for this batch
+// tcgen05 stage 1 + pruning (tc_stage1.cu), stream-ordered, no host sync;
+// *fail_dev (device int) becomes nonzero when a buffer overflowed and the
+// caller must redo the batch with the exact path
 bool tc_stage1_supported(const rbc_index *idx, int k);
-int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut &out, bool *fallback,
+int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut &out, int32_t *fail_dev,
               cudaStream_t st);
 // rows of src [rows][d] -> dst [rows][64], zero padded
 void pad_rows64(const float *src, int64_t rows, int d, float *dst, cudaStream_t st);
 
 // tcgen05 stage 2 (tc_stage2.cu)
 bool tc_stage2_supported(const rbc_index *idx, int k);
+// stream-ordered, no host sync: work arrays sized cap_work; writes
+// status_dev[0] = work items needed (> cap_work: results invalid, re-run),
+// status_dev[1] = queries recomputed by the exact overflow scan
 int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
-              cudaStream_t st);
+              int64_t cap_work, int64_t *status_dev, cudaStream_t st);
 int64_t &last_overflow_count();
+// stage-2 work-item capacity for nq queries, and its update from a measured need
+int64_t stage2_work_capacity(const rbc_index *idx, int64_t nq);
+void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed);
 
 // engine selection (RBC_ENGINE env: "auto" (default) | "exact")
 bool force_exact_engine();

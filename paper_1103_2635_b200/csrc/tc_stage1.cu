@@ -771,7 +771,7 @@ static int g_num_sms1 = 0;
 
 // Fused stage 1 + pruning.  Returns RBC_OK with *fallback = true when some
 // row exhausted a buffer (the caller then runs the exact path).
-int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut &out, bool *fallback,
+int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut &out, int32_t *fail_dev,
               cudaStream_t st) {
     const Tc1Index *t = static_cast<const Tc1Index *>(idx->tc1);
     const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
@@ -830,7 +830,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     P.rec_cnt = rec_cnt.get();
     P.rec = rec.get();
     P.cap_rec = cap_rec;
-    P.fail = flags.get();
+    P.fail = fail_dev;
     P.tile_counter = flags.get() + 1;
     if (g_num_sms1 == 0) {
         int dev = 0;
@@ -853,10 +853,6 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
         out.seg_start.get(), out.seg_len.get(), out.seg_list.get(), out.seg_d1.get(), out.order_key.get(), out.pr,
         out.p3);
     RBC_LAUNCHED();
-    int32_t f = 0;
-    RBC_CUDA(cudaMemcpyAsync(&f, flags.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    RBC_CUDA(cudaStreamSynchronize(st));
-    *fallback = f != 0;
     return RBC_OK;
 }
 

@@ -117,6 +117,7 @@ struct S2Params {
     int32_t *overflow_list;
     int32_t *overflow_count;
     int32_t *tile_counter;
+    int64_t cap_work;
 };
 
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
@@ -231,7 +232,9 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const uint64_t *__restrict__ order_key,
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
     const int64_t *__restrict__ offsets, const int64_t *__restrict__ work_off, WorkItem *__restrict__ work,
-    int32_t *__restrict__ cut, float *__restrict__ rowd1, uint64_t *__restrict__ tile_key, int warm) {
+    int32_t *__restrict__ cut, float *__restrict__ rowd1, uint64_t *__restrict__ tile_key, int warm,
+    int64_t cap_work) {
+    if (work_off[gridDim.x] > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
@@ -338,6 +341,7 @@ __device__ __forceinline__ float pick8(const float *v, int j) {
 
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
+    if (P.work_off[P.ntiles] > P.cap_work) return;  // work arrays incomplete (see tile_fill_kernel)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *sB = smem;                                   // kStages x (plane 0 | plane 1)
@@ -745,6 +749,39 @@ __global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int3
 
 constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kEpiWarps * (kNmax / 2) * sizeof(float) + 256;
 
+// Exact SIMT scan for the queries whose candidate buffer overflowed; the count
+// lives on the device (no host round trip).  One warp per entry, grid-stride.
+template <int KT>
+__global__ void __launch_bounds__(256) overflow_scan_kernel(const float *__restrict__ q, int d,
+                                                            const int32_t *__restrict__ ovf_list,
+                                                            const int32_t *__restrict__ ovf_count, SegSubSrc src, int k,
+                                                            uint64_t *__restrict__ keys) {
+    __shared__ float qs_all[8 * 64];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = *ovf_count;
+    for (int64_t i = blockIdx.x * 8 + w; i < n; i += static_cast<int64_t>(gridDim.x) * 8) {
+        const int64_t qi = ovf_list[i];
+        float *qs = qs_all + w * 64;
+        for (int c = lane; c < d; c += 32) qs[c] = q[qi * d + c];
+        __syncwarp();
+        uint64_t best[KT];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+        src.for_each(i, lane, [&](const float *__restrict__ row, uint32_t id) {
+            const uint64_t key = pack_key(exact_dist<RBC_L2>(qs, row, d), id);
+            if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+        });
+        warp_merge_sorted<KT>(best, k, keys + qi * k);
+        __syncwarp();
+    }
+}
+
+__global__ void stage2_status_kernel(const int64_t *__restrict__ work_off, int ntiles,
+                                     const int32_t *__restrict__ ovf_count, int64_t *__restrict__ status) {
+    status[0] = work_off[ntiles];
+    status[1] = *ovf_count;
+}
+
 }  // namespace
 
 int64_t &last_overflow_count() {
@@ -827,8 +864,13 @@ bool tc_stage2_supported(const rbc_index *idx, int k) {
 static int g_num_sms = 0;
 
 int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
-              cudaStream_t st) {
+              int64_t cap_work, int64_t *status_dev, cudaStream_t st) {
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     const int64_t nr = idx->nr;
     const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
     // 1. group queries: sort by (first surviving list, nearest rep)
@@ -877,9 +919,10 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(tmp3.alloc(tb3, st));
     RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp3.get(), tb3, nwork.get(), work_off.get() + 1, ntiles, st));
     note_launch();
-    int64_t total_work = 0;
-    RBC_CUDA(cudaMemcpyAsync(&total_work, work_off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    RBC_CUDA(cudaStreamSynchronize(st));
+    // work arrays sized from the caller's capacity (no host round trip); an
+    // undersized capacity makes every consumer kernel bail out and the caller
+    // re-runs with the size reported in status[0]
+    const int64_t total_work = cap_work;
     DevBuf<WorkItem> work;
     DevBuf<int32_t> cut;
     DevBuf<float> rowd1;
@@ -891,7 +934,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
                                                    idx->radii, tc->poff,
                                                    idx->offsets, work_off.get(), work.get(), cut.get(), rowd1.get(),
-                                                   tkey.get(), warm);
+                                                   tkey.get(), warm, cap_work);
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
                                              tile_order.get(), ntiles, 0, 40, st));
@@ -939,6 +982,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.overflow_list = ovf_list.get();
     P.overflow_count = counters.get();
     P.tile_counter = counters.get() + 1;
+    P.cap_work = cap_work;
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -970,26 +1014,20 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
 #undef RBC_RERANK
         RBC_LAUNCHED();
     }
-    // 5. overflow fallback: exact SIMT scan for the few queries whose buffer filled up
-    int32_t n_ovf = 0;
-    RBC_CUDA(cudaMemcpyAsync(&n_ovf, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    RBC_CUDA(cudaStreamSynchronize(st));
-    if (n_ovf > 0) {
-        DevBuf<float> qsub;
-        DevBuf<uint64_t> ksub;
-        RBC_CHECK(qsub.alloc(static_cast<int64_t>(n_ovf) * idx->d, st));
-        RBC_CHECK(ksub.alloc(static_cast<int64_t>(n_ovf) * k, st));
-        gather_query_rows_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * idx->d, 256, 4096), 256, 0, st>>>(
-            q, ovf_list.get(), n_ovf, idx->d, qsub.get());
-        RBC_LAUNCHED();
+    // 5. overflow fallback: exact SIMT scan for the few queries whose buffer filled
+    //    up (device-side count; the queries' segments are still in `po`)
+    {
         SegSubSrc src{idx->xp, idx->perm,     po.seg_start.get(), po.seg_len.get(),
                       po.seg_off.get(), po.nseg.get(), ovf_list.get(), idx->d};
-        RBC_CHECK(launch_topk(qsub.get(), n_ovf, idx->d, idx->metric, k, src, ksub.get(), st));
-        scatter_keys_kernel<<<grid_for(static_cast<int64_t>(n_ovf) * k, 256), 256, 0, st>>>(ksub.get(), ovf_list.get(),
-                                                                                         n_ovf, k, keys);
+        const unsigned ogrid = static_cast<unsigned>(g_num_sms * 4);
+        if (k == 1) overflow_scan_kernel<1><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
+        else if (k <= 4) overflow_scan_kernel<4><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
+        else if (k <= 8) overflow_scan_kernel<8><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
+        else overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
         RBC_LAUNCHED();
     }
-    last_overflow_count() = n_ovf;
+    stage2_status_kernel<<<1, 1, 0, st>>>(work_off.get(), ntiles, counters.get(), status_dev);
+    RBC_LAUNCHED();
     return RBC_OK;
 }
 

@@ -381,6 +381,21 @@ def test_tc_engine_scales_and_offsets(rbc, oracle, d):
             assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("k", [1, 10])
+def test_tc_engine_wide_tile_unions(rbc, oracle, k):
+    # few clusters, many representatives: every tile's surviving-list union is large,
+    # which exercises the stage-2 work-capacity re-run path on the first search
+    full = oracle.gen_clusters(40_000 + 600, 32, 5, n_clusters=2, cluster_sigma=0.05)
+    x, q = full[:40_000], full[40_000:]
+    idx = rbc.build_exact(rbc.DataMatrix(x), 400, rbc.MetricSpec("l2", 32), seed=2)
+    fast, exact = _both_engines(rbc, idx, q, k)
+    for a, b in zip(fast, exact):
+        assert np.array_equal(a, b)
+    again = rbc.exact_query_arrays(idx, q, k)
+    for a, b in zip(again, exact):
+        assert np.array_equal(a, b)
+
+
 def test_tc_engine_overflow_fallback(rbc):
     from paper_1103_2635_b200 import _lib
 
