@@ -621,11 +621,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             }
             if (rc > P.cap_rec) fail = true;
             if (live) {
-                P.gamma[qi] = g;
-                P.nearest[qi] = static_cast<int32_t>(key_id(best[0]));
+                // a failed row gets inert, in-range outputs: the batch is re-run on the
+                // exact path, but stage 2 is already queued behind this kernel
+                P.gamma[qi] = fail ? 0.0f : g;
+                P.nearest[qi] = fail ? 0 : static_cast<int32_t>(key_id(best[0]));
                 P.pr[qi] = pr;
                 P.p3[qi] = p3;
-                P.rec_cnt[qi] = rc < P.cap_rec ? rc : P.cap_rec;
+                P.rec_cnt[qi] = fail ? 0 : rc;
                 if (fail) atomicExch(P.fail, 1);
             }
         }
