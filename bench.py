@@ -85,6 +85,13 @@ class ClockSampler:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # NVML start-up takes driver locks that stall CUDA calls: keep it out of the
+        # timed region by waiting for the first sample
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+            time.sleep(0.02)
+        time.sleep(0.05)
 
     def stop(self):
         if self.proc is None:
@@ -168,7 +175,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -319,7 +326,9 @@ def main():
                 "config": {"workload": "cfg2: exact RBC 1-NN L2, clusters n=1M d=64 C=64 sigma=0.05, |R|=1016",
                            "queries_per_rank": NQ, "k": K, "n_reps": n_reps, "parallelism": f"query-shard x{world}",
                            "l2_flush": "256 MiB write between timed steps", "index_build_s": build_s,
-                           "mean_candidates": float(cand_h.mean()), "flops_per_step": flops_per_step},
+                           "mean_candidates": float(cand_h.mean()), "flops_per_step": flops_per_step,
+                           "step_ms_min": min(times), "step_ms_median": sorted(times)[len(times) // 2],
+                           "arith": "f32 inputs; f16 tcgen05 filter; exact re-rank in f64 (reference rule)"},
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "gpu_bruteforce": bf, "clocks": clk}
         print(json.dumps(line), flush=True)
