@@ -10,8 +10,11 @@ ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Met
 agg = defaultdict(lambda: [0, 0.0])
 for r in data:
     v = float(r[vi].replace(",", ""))
-    v = {"nsecond": v / 1e3, "usecond": v, "msecond": v * 1e3, "second": v * 1e6}.get(r[ui], v)
+    v = {"ns": v / 1e3, "nsecond": v / 1e3, "us": v, "usecond": v, "ms": v * 1e3, "msecond": v * 1e3,
+         "s": v * 1e6, "second": v * 1e6}.get(r[ui], v)
     agg[r[ki][:80]][0] += 1
     agg[r[ki][:80]][1] += v
+tot = sum(t for _, t in agg.values()) or 1.0
+print(f"{'us/launch':>10} {'launches':>8} {'share':>6}  kernel")
 for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 20]:
-    print(f"{t / c:10.1f} us x{c:3d}  {k}")
+    print(f"{t / c:10.1f} {c:8d} {100 * t / tot:5.1f}%  {k}")
