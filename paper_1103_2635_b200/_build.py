@@ -19,14 +19,17 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "librbc_b200.so")
+# diagnostic variants: RBC_BUILD_TAG=timing RBC_BUILD_DEFINES=-DRBC_S2_TIMING builds
+# librbc_b200_timing.so (load it with RBC_B200_LIB=...); the default build is untouched
+_TAG = os.environ.get("RBC_BUILD_TAG", "")
+OBJ = os.path.join(PKG, "build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, "librbc_b200" + (f"_{_TAG}" if _TAG else "") + ".so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
     "-I", os.path.join(ROOT, "include"), "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("RBC_BUILD_DEFINES", "").split()
 
 
 def nvcc() -> str:

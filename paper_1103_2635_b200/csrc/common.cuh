@@ -108,22 +108,24 @@ __device__ __forceinline__ double exact_acc4(double acc, const float4 &x, const 
     return acc;
 }
 
-template <int METRIC>
+// B4 = float4 loads of each row in flight per step (4: 16 coordinates; 8 for
+// latency-bound callers with registers to spare)
+template <int METRIC, int B4 = 4>
 __device__ __forceinline__ float exact_dist(const float *__restrict__ a, const float *__restrict__ b, int d) {
     double acc = 0.0;
     int k = 0;
     if (((d & 3) | ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)) == 0) {
-        // 16-byte rows: 16 coordinates (4+4 vector loads) in flight per step
+        // 16-byte rows: 4*B4 coordinates (B4+B4 vector loads) in flight per step
         const float4 *a4 = reinterpret_cast<const float4 *>(a), *b4 = reinterpret_cast<const float4 *>(b);
-        for (; k + 16 <= d; k += 16) {
-            float4 x[4], y[4];
+        for (; k + 4 * B4 <= d; k += 4 * B4) {
+            float4 x[B4], y[B4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < B4; ++j) {
                 x[j] = a4[(k >> 2) + j];
                 y[j] = b4[(k >> 2) + j];
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc = exact_acc4<METRIC>(acc, x[j], y[j]);
+            for (int j = 0; j < B4; ++j) acc = exact_acc4<METRIC>(acc, x[j], y[j]);
         }
         for (; k + 4 <= d; k += 4) acc = exact_acc4<METRIC>(acc, a4[k >> 2], b4[k >> 2]);
     }

@@ -30,8 +30,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 // try_wait with a suspend-time hint: a waiting thread is parked by the
 // hardware until the phase completes (or the hint expires) instead of
 // spinning, so idle roles do not steal issue slots from busy warps.
+// RBC_MBAR_NOHINT builds the plain form (hardware-chosen time slice).
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
+#ifdef RBC_MBAR_NOHINT
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -39,6 +49,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "=r"(ok)
         : "r"(addr), "r"(parity), "r"(0x989680u)
         : "memory");
+#endif
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
@@ -189,6 +200,18 @@ __device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
+}
+
+// three-input max (sm_100: one FMNMX3); NaN-free inputs assumed
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// max of 8 values in 4 ALU instructions
+__device__ __forceinline__ float max8(const float *v) {
+    return fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmaxf(v[6], v[7]));
 }
 
 }  // namespace sm100

@@ -5,25 +5,31 @@
 // k-th smallest as gamma_k (:181), and keeps r iff
 //   d <= 3 gamma  and  (d < gamma + psi_r  or  d <= gamma)      (:62-74)
 // counting the two pruning tests (:194-195).  Here each 128-query tile is
-// multiplied against all representatives with tcgen05.mma.  Operands are
-// centred on the representatives' mean c and split into f16 hi + lo parts
-// (three MMAs: hi.hi + hi.lo + lo.hi, ~2^-20 relative precision); the
-// per-rep term |r - c|^2 / 2 is folded into the MMA as in tc_stage2.cu.  Every
-// d^2 is thereby known inside a rigorous interval [lb, ub]:
-//   pass 1: the k smallest upper bounds give a bound U_k; every rep with
-//           lb <= U_k is evaluated exactly (fp64, reference arithmetic), so
-//           gamma_k and the nearest rep are exact;
-//   pass 2: every rep is classified against 3 gamma, gamma and gamma + psi_r
-//           with its interval; reps whose class is certain (almost all: far
-//           away) are only counted, the rest -- possible survivors and
-//           interval straddles -- are recorded for the fix-up kernel, which
-//           decides them with exact distances, computes the 4 gamma cutoff by
-//           binary search and emits the surviving segments.
-// No |Q| x |R| distance matrix is materialised.  Any row that exhausts a
-// buffer raises a flag and the caller recomputes the batch with the exact
-// path (search.cu), so the result is always the reference's.
+// multiplied against all representatives with one tcgen05.mma kind::f16 per
+// K=16 slice: operands centred on the representatives' mean c, the per-rep
+// term |r - c|^2 / 2 folded into the MMA as two extra K columns (as in
+// tc_stage2.cu), so every d^2 is known inside a rigorous interval
+// [dt - E, dt + E].  Two passes over the representatives (the accumulator
+// row of |R| columns does not fit TMEM):
+//   pass 1: the k smallest upper bounds give U_k >= gamma_k^2; every rep
+//           with lb <= U_k is buffered as a gamma candidate, and
+//           gamma_k^2 lies in [U_k - 2E, U_k];
+//   pass 2: every rep is classified against 3 gamma, gamma + psi_r and
+//           gamma with that gamma interval.  Far reps (almost all) are
+//           only counted, 8 at a time through a max-reduce; certain
+//           survivors are recorded with a flag, undecided reps recorded
+//           plain.
+// No fp64 work happens here.  The fix-up kernel (one warp per query) turns
+// the gamma candidates into the exact gamma_k and nearest rep with the
+// reference arithmetic, decides the undecided reps exactly, computes the
+// 4 gamma cutoffs and emits the surviving segments.  No |Q| x |R| distance
+// matrix is materialised.  Any row that exhausts a buffer raises a flag and
+// the caller recomputes the batch with the exact path (search.cu), so the
+// result is always the reference's.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -39,19 +45,22 @@ namespace rbc {
 namespace {
 
 constexpr int kRows = 128;
-constexpr int kN = 128;       // representatives per chunk (UMMA N)
-constexpr int kStages = 3;
+constexpr int kN = 128;        // representatives per chunk (UMMA N)
+constexpr int kStages = 4;
+constexpr int kVStride = 68;  // floats per row of the slow-path value stage (16-byte aligned, bank-spread)
 constexpr int kThreads = 192;  // producer, MMA, 4 epilogue warps
 constexpr int kP0 = 128, kP1 = 32;
-// per row: hi plane (SW128) | lo plane (SW128) | aug plane (SW32, d > 62 only)
-constexpr int kStageBytes = kN * (2 * kP0 + kP1);
-constexpr int kABytes = kRows * (2 * kP0 + kP1);
+// per chunk: plane 0 (kN rows x 128 B, SW128: 64 f16, aug in columns 62/63 when
+// d <= 62) | plane 1 (kN rows x 32 B, SW32: the aug pair, d > 62 only)
+constexpr int kStageBytes = kN * (kP0 + kP1);
+constexpr int kABytes = kRows * (kP0 + kP1);
 constexpr int kMaxRepsSmem = 6144;  // radii staged in shared memory
 
-// hi/lo split: per-product error 3 * 2^-22, fp32 accumulation of <= 208 terms; factor-2 safety, x2 for d^2
-constexpr float kC1 = 4.0f * (3.0f / 4194304.0f + 208.0f / 8388608.0f);
+// error bound of the centred f16 expanded form (same derivation as tc_stage2.cu:
+// f16 rounding of a and b, fp32 accumulation of <= 80 products, factor-2 safety)
+constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 128.0f / 4194304.0f);
 constexpr float kC2 = 1.0f / 1048576.0f;
-constexpr float kC4 = 1.0f / 1073741824.0f;  // subnormal flush of the lo parts (absolute, scaled)
+constexpr float kC4 = 1.0f / 262144.0f;
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;
 constexpr float kTie = 1.0f + 1.0f / 524288.0f;
 constexpr float kEps = 1.0f / 262144.0f;  // relative slack of the interval classification
@@ -59,13 +68,16 @@ constexpr float kEps = 1.0f / 262144.0f;  // relative slack of the interval clas
 struct Tc1Index {
     int64_t nrpad = 0;
     bool plane1 = false;
-    uint8_t *rb = nullptr;   // [nrpad] rows of (hi 128 B | lo 128 B | aug 32 B), pre-swizzled
+    uint8_t *rb = nullptr;   // [nchunks] x kStageBytes, pre-swizzled f16 rows of (r - c) sG (+ aug)
     float *c64 = nullptr;    // [64] centre (mean of the reps), zero padded
     float *stat = nullptr;   // [2] sG, rmax (max |r - c|, rounded up)
     float *psimax = nullptr; // [nchunks] largest list radius of each rep chunk
     float *lskip = nullptr;  // [nr][32] list_dists at the end of each of 32 equal blocks (cutoff skip table)
+    float *reps64 = nullptr; // [nr][64] representatives, zero padded (16-byte rows for the fix-up)
     float sG = 1.f, rmax = 0.f;
 };
+
+constexpr int kPilots = 64;  // query-ordering pilots (a spread subset of the reps)
 
 // skip table: sample i of list p = list_dists at position min(len, (i+1) * s) - 1, s = ceil(len / 32)
 __global__ void list_skip_kernel(const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, int64_t nr,
@@ -107,37 +119,35 @@ struct S1Params {
     const uint8_t *rb;
     int plane1;
     int64_t nr;
-    int64_t nrpad;
     float sG;
     float rmax;
     const float *c64;
     const float *psimax;
     const float *q64;
-    const float *q;
-    const float *reps;
+    const int32_t *qorder;  // tile slot -> query id (queries sorted by nearest pilot)
     const float *radii;
-    int d;
     int k;
     int64_t nq;
     int ntiles;
-    float *c1_lb;
-    int32_t *c1_p;
+    float *c1_lb;      // [nq][cap1] gamma-candidate lower bounds
+    int32_t *c1_p;     // [nq][cap1] their rep positions
     int cap1;
-    float *gamma;
-    int32_t *nearest;
-    int32_t *pr;
-    int32_t *p3;
-    int32_t *rec_cnt;
-    int32_t *rec;
+    int32_t *c1_cnt;   // [nq] buffered gamma candidates (-1: row failed)
+    float *c1_u;       // [nq] U_k * kTie: a candidate matters iff lb <= c1_u
+    int32_t *pr;       // [nq] reps decided here as pruned by the radius test
+    int32_t *p3;       // [nq] ... by the 3 gamma test
+    int32_t *rec_cnt;  // [nq]
+    int32_t *rec;      // [nq][cap_rec] recorded (not certainly far) reps
+    float *rec_dt;     // [nq][cap_rec] their d^2 estimate (true d^2 within +-rec_e)
+    float *rec_e;      // [nq] the row's error bound E
     int cap_rec;
     int32_t *fail;
     int32_t *tile_counter;
+    unsigned long long *timing;  // diagnostic [12] summed role wait cycles (nullptr = off)
 };
 
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
-__device__ __forceinline__ float max8(const float *v) {
-    return fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
-}
+__device__ __forceinline__ float max8(const float *v) { return sm100::max8(v); }
 __device__ __forceinline__ float pick8(const float *v, int j) {
     const float a0 = (j & 4) ? v[4] : v[0], a1 = (j & 4) ? v[5] : v[1];
     const float a2 = (j & 4) ? v[6] : v[2], a3 = (j & 4) ? v[7] : v[3];
@@ -145,42 +155,25 @@ __device__ __forceinline__ float pick8(const float *v, int j) {
     return (j & 1) ? b1 : b0;
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-// r[j] for a runtime j in [0, 32) without local memory (select tree)
-__device__ __forceinline__ uint32_t pick32u(const uint32_t (&r)[32], int j) {
-    uint32_t t16[16], t8[8], t4[4];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) t16[i] = (j & 16) ? r[i + 16] : r[i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) t8[i] = (j & 8) ? t16[i + 8] : t16[i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[i + 4] : t8[i];
-    const uint32_t a = (j & 2) ? t4[2] : t4[0], b = (j & 2) ? t4[3] : t4[1];
-    return (j & 1) ? b : a;
-}
 
-// f16 hi/lo split of x: hi = f16(x), lo = f16(x - hi)
-__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t &hi, uint32_t &lo) {
-    hi = sm100::pack_f16x2_sat(x0, x1);
-    const __half2 h = *reinterpret_cast<const __half2 *>(&hi);
-    lo = sm100::pack_f16x2_sat(x0 - __low2float(h), x1 - __high2float(h));
-}
-
-// one 128-byte row (64 f16) of hi and lo planes + aug word at column 62/63 when d <= 62
-__device__ __forceinline__ void write_split_row(uint8_t *hi_row, uint8_t *lo_row, int row, const float *v, float s,
-                                                bool aug_in_row, uint32_t aug) {
+// one 128-byte row (64 f16 of v * s), aug word at columns 62/63 when d <= 62
+__device__ __forceinline__ void write_row(uint8_t *dst, int row, const float *v, float s, bool aug_in_row,
+                                          uint32_t aug) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-        uint32_t wh[4], wl[4];
+        uint32_t w[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) split_f16x2(v[c * 8 + 2 * e] * s, v[c * 8 + 2 * e + 1] * s, wh[e], wl[e]);
-        if (aug_in_row && c == 7) {
-            wh[3] = aug;
-            wl[3] = 0;
-        }
-        const uint32_t o = (c ^ (row & 7)) << 4;
-        *reinterpret_cast<uint4 *>(hi_row + o) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
-        *reinterpret_cast<uint4 *>(lo_row + o) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+        for (int e = 0; e < 4; ++e) w[e] = sm100::pack_f16x2_sat(v[c * 8 + 2 * e] * s, v[c * 8 + 2 * e + 1] * s);
+        if (aug_in_row && c == 7) w[3] = aug;
+        *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
+}
+
+// aug pair in its own 32-byte SW32 row (d > 62)
+__device__ __forceinline__ void write_aug_row(uint8_t *dst, int row, uint32_t aug) {
+    const int sw = (row >> 2) & 1;
+    *reinterpret_cast<uint4 *>(dst + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
+    *reinterpret_cast<uint4 *>(dst + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
 }
 
 // ---- index preparation ------------------------------------------------------------
@@ -221,7 +214,7 @@ __global__ void rep_scale_kernel(const unsigned *__restrict__ rmax_bits, float *
     stat[1] = r;
 }
 
-// B operand rows: f16 hi/lo of (r - c) * sG, aug = (|r - c|^2 / 2) sG^2 hi/lo
+// B operand rows: f16 of (r - c) sG, aug = (|r - c|^2 / 2) sG^2 as an f16 hi/lo pair
 __global__ void rep_rows_kernel(const float *__restrict__ reps, int64_t nr, int d, const float *__restrict__ c64,
                                 const float *__restrict__ stat, int plane1, uint8_t *__restrict__ rb) {
     const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -239,19 +232,75 @@ __global__ void rep_rows_kernel(const float *__restrict__ reps, int64_t nr, int 
     const __half glo = __float2half_rn(gp - __half2float(ghi));
     const uint32_t aug =
         static_cast<uint32_t>(__half_as_ushort(ghi)) | (static_cast<uint32_t>(__half_as_ushort(glo)) << 16);
-    uint8_t *row = rb + p * (2 * kP0 + kP1);
-    // rows are grouped in kN-row chunks: chunk base | hi plane (kN x 128) | lo plane | aug plane
     const int64_t ch = p / kN, r = p % kN;
     uint8_t *base = rb + ch * static_cast<int64_t>(kStageBytes);
-    (void)row;
-    write_split_row(base + r * kP0, base + kN * kP0 + r * kP0, static_cast<int>(r), v, s, !plane1, aug);
-    if (plane1) {
-        uint8_t *d1p = base + 2 * kN * kP0 + r * kP1;
-        const int sw = static_cast<int>((r >> 2) & 1);
-        *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
-        *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
-    }
+    write_row(base + r * kP0, static_cast<int>(r), v, s, !plane1, aug);
+    if (plane1) write_aug_row(base + kN * kP0 + r * kP1, static_cast<int>(r), aug);
 }
+
+// Query ordering: key = nearest of kPilots spread reps (fp32, approximate --
+// it only decides which queries share a tile, never a result).  Queries of one
+// region then share their near reps, so the per-tile slow paths run in lockstep.
+__global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
+                                                        const float *__restrict__ reps64, int64_t nr, int npilot,
+                                                        uint32_t *__restrict__ key, int32_t *__restrict__ ids) {
+    __shared__ float4 sp[kPilots * 16];
+    for (int t = threadIdx.x; t < npilot * 16; t += blockDim.x) {
+        const int j = t >> 4, c = t & 15;
+        sp[t] = reinterpret_cast<const float4 *>(reps64 + (static_cast<int64_t>(j) * nr / npilot) * 64)[c];
+    }
+    __syncthreads();
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nq) return;
+    float4 qv[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
+    float best = __int_as_float(0x7f800000);
+    int bj = 0;
+    for (int j = 0; j < npilot; ++j) {
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const float4 r = sp[j * 16 + c];
+            const float t0 = qv[c].x - r.x, t1 = qv[c].y - r.y, t2 = qv[c].z - r.z, t3 = qv[c].w - r.w;
+            a0 = fmaf(t0, t0, fmaf(t1, t1, a0));
+            a1 = fmaf(t2, t2, fmaf(t3, t3, a1));
+        }
+        const float dd = a0 + a1;
+        if (dd < best) {
+            best = dd;
+            bj = j;
+        }
+    }
+    key[i] = static_cast<uint32_t>(bj);
+    ids[i] = static_cast<int32_t>(i);
+}
+
+__global__ void pad_reps64_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= rows * 64) return;
+    const int64_t r = t >> 6;
+    const int c = static_cast<int>(t & 63);
+    dst[t] = c < d ? src[r * d + c] : 0.f;
+}
+
+// Diagnostic role timing (build with -DRBC_S1_TIMING, run with RBC_DEBUG_S1=1)
+#ifdef RBC_S1_TIMING
+__device__ __forceinline__ void s1_wait_t(uint64_t *bar, uint32_t parity, unsigned long long &acc) {
+    const unsigned long long t0 = clock64();
+    sm100::mbar_wait(bar, parity);
+    acc += clock64() - t0;
+}
+#define S1_WAIT(bar, parity, slot) s1_wait_t(bar, parity, tw[slot])
+#else
+#define S1_WAIT(bar, parity, slot) sm100::mbar_wait(bar, parity)
+#endif
+
+#ifdef RBC_S1_NOEPI
+#define S1_LIM(x) 0  // diagnostic: pipeline without epilogue work (results invalid)
+#else
+#define S1_LIM(x) (x)
+#endif
 
 // ---- the fused stage-1 kernel ---------------------------------------------------------
 template <int KT>
@@ -261,14 +310,19 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
     uint8_t *sB = smem;
     uint8_t *sA = sB + kStages * kStageBytes;
     float *s_radii = reinterpret_cast<float *>(sA + 2 * kABytes);  // [nr]
-    float *s_red = s_radii + kMaxRepsSmem;                          // [4] tile max of |q - c|
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_red + 4);
+    float *s_red = s_radii + ((P.nr + 3) & ~int64_t(3));            // [4] tile max of |q - c|
+    float *s_v = s_red + 4;                                          // [128][kVStride] slow-path value stage
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_v + kRows * kVStride);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
     uint64_t *afull = tempty + 2, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef RBC_S1_TIMING
+    unsigned long long tw[12] = {};
+    const unsigned long long t_start = clock64();
+#endif
     for (int64_t p = tid; p < P.nr; p += blockDim.x) s_radii[p] = P.radii[p];
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -298,17 +352,17 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             uint32_t bi = 0;
             for (uint32_t it = 0;; ++it) {
                 const uint32_t slot = it & 1;
-                sm100::mbar_wait(&tile_empty[slot], ((it >> 1) & 1) ^ 1);
+                S1_WAIT(&tile_empty[slot], ((it >> 1) & 1) ^ 1, 0);
                 const int t = atomicAdd(P.tile_counter, 1);
                 const int tile = t < P.ntiles ? t : -1;
                 s_tiles[slot] = tile;
                 sm100::mbar_arrive(&tile_full[slot]);
                 if (tile < 0) break;
-                const uint32_t bytes = P.plane1 ? kStageBytes : 2 * kN * kP0;
+                const uint32_t bytes = P.plane1 ? kStageBytes : kN * kP0;
                 for (int pass = 0; pass < 2; ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
                         const uint32_t s = bi % kStages;
-                        sm100::mbar_wait(&empty[s], ((bi / kStages) & 1) ^ 1);
+                        S1_WAIT(&empty[s], ((bi / kStages) & 1) ^ 1, 1);
                         sm100::mbar_arrive_expect_tx(&full[s], bytes);
                         sm100::bulk_g2s(sB + s * kStageBytes, P.rb + static_cast<int64_t>(ch) * kStageBytes, bytes,
                                         &full[s]);
@@ -317,44 +371,36 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer: hi.hi + hi.lo + lo.hi (+ aug plane) =====
+        // ===== MMA issuer: 4 x K16 over plane 0 (+ the aug plane) =====
         if (lane == 0) {
             uint32_t bi = 0, ti = 0, ai = 0;
             for (uint32_t it = 0;; ++it) {
                 const uint32_t slot = it & 1;
-                sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
+                S1_WAIT(&tile_full[slot], (it >> 1) & 1, 2);
                 const int tile = s_tiles[slot];
                 sm100::mbar_arrive(&tile_empty[slot]);
                 if (tile < 0) break;
                 const uint32_t a = ai & 1;
-                sm100::mbar_wait(&afull[a], (ai >> 1) & 1);
+                S1_WAIT(&afull[a], (ai >> 1) & 1, 3);
                 sm100::tc_fence_after();
-                const uint32_t ah = sm100::smem_u32(sA + a * kABytes), al = ah + kRows * kP0;
+                const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
                 for (int pass = 0; pass < 2; ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
                         const int n = min(kN, roundup16(static_cast<int>(P.nr) - ch * kN));
                         const uint32_t s = bi % kStages, tb = ti & 1;
-                        sm100::mbar_wait(&full[s], (bi / kStages) & 1);
-                        sm100::mbar_wait(&tempty[tb], ((ti >> 1) & 1) ^ 1);
+                        S1_WAIT(&full[s], (bi / kStages) & 1, 4);
+                        S1_WAIT(&tempty[tb], ((ti >> 1) & 1) ^ 1, 5);
                         sm100::tc_fence_after();
                         const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
-                        const uint32_t bh = sm100::smem_u32(sB + s * kStageBytes), bl = bh + kN * kP0;
+                        const uint32_t b0 = sm100::smem_u32(sB + s * kStageBytes);
                         const uint32_t d_tmem = tmem + tb * kN;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(ah + kk * 32), sm100::umma_desc_sw128(bh + kk * 32),
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32), sm100::umma_desc_sw128(b0 + kk * 32),
                                             idesc, kk > 0);
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(ah + kk * 32), sm100::umma_desc_sw128(bl + kk * 32),
-                                            idesc, 1);
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(al + kk * 32), sm100::umma_desc_sw128(bh + kk * 32),
-                                            idesc, 1);
                         if (P.plane1)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(al + kRows * kP0),
-                                            sm100::umma_desc_sw32(bl + kN * kP0), idesc, 1);
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(a0 + kRows * kP0),
+                                            sm100::umma_desc_sw32(b0 + kN * kP0), idesc, 1);
                         sm100::umma_commit(&empty[s]);
                         sm100::umma_commit(&tfull[tb]);
                         ++bi;
@@ -372,13 +418,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
         uint32_t ti = 0, ai = 0;
         for (uint32_t it = 0;; ++it) {
             const uint32_t slot = it & 1;
-            sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
+            S1_WAIT(&tile_full[slot], (it >> 1) & 1, 6);
             const int tile = s_tiles[slot];
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&tile_empty[slot]);
             if (tile < 0) break;
-            const int64_t qi = static_cast<int64_t>(tile) * kRows + row;
-            const bool live = qi < P.nq;
+            const int64_t slot_i = static_cast<int64_t>(tile) * kRows + row;
+            const bool live = slot_i < P.nq;
+            const int64_t qi = live ? P.qorder[slot_i] : 0;
             // (q - c), |q - c|^2 in fp64, tile scale sA
             float qv[64];
             double qn64 = 0.0;
@@ -413,21 +460,15 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             const float cf = sa / P.sG;
             const float acoef = (cf >= 6.103515625e-05f && cf <= 32768.0f) ? -cf : 0.0f;
             bool fail = acoef == 0.0f;
-            // A operand: hi | lo | aug planes
+            // A operand: f16 rows of (q - c) sA, aug = -sA / sG in the aug columns
             {
                 const uint32_t a = ai & 1;
-                sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
+                S1_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 7);
                 const __half ac = __float2half_rn(acoef);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 uint8_t *abuf = sA + a * kABytes;
-                write_split_row(abuf + row * kP0, abuf + kRows * kP0 + row * kP0, row, qv, sa, !P.plane1, aug);
-                if (P.plane1) {
-                    // the aug pairs with the B aug plane through the lo-plane descriptor slot
-                    uint8_t *d1p = abuf + 2 * kRows * kP0 + row * kP1;
-                    const int sw = (row >> 2) & 1;
-                    *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
-                    *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
-                }
+                write_row(abuf + row * kP0, row, qv, sa, !P.plane1, aug);
+                if (P.plane1) write_aug_row(abuf + kRows * kP0 + row * kP1, row, aug);
                 sm100::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(&afull[a]);
@@ -436,7 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             const float rb = P.rmax;
             const float E = kC1 * nqv * rb + kC2 * (qn + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
 
-            // ---------- pass 1: bound and collect the k nearest representatives ----------
+            // ---------- pass 1: bound and collect the gamma candidates ----------
+            // Every rep with lb <= U (U = running k-th smallest upper bound) is buffered;
+            // the bound is tightened from group maxima (each group's best is a distinct rep).
             float ubk[KT];
 #pragma unroll
             for (int j = 0; j < KT; ++j) ubk[j] = __int_as_float(0x7f800000);
@@ -445,62 +488,19 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             float *clb = P.c1_lb + (live ? qi : 0) * P.cap1;
             int32_t *cp = P.c1_p + (live ? qi : 0) * P.cap1;
             auto threshold = [&]() {
-                // V >= T  <=>  lb = qn - E - 2 V / scale <= U * kTie
+                // V >= T  <=>  lb = qn - E - 2 V / scale <= U * kTie   (loosened by 2^-18 relative)
                 const float t = 0.5f * scale * (qn - E - U * kTie);
                 return t - fabsf(t) * (1.0f / 262144.0f) - 1e-30f;
             };
+            const float lb0 = qn - E;  // lb(V) = lb0 - V * inv2s
             float T = live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
-            float vbest = -__int_as_float(0x7f800000);
-            auto slow8 = [&](const float *v, int col0) {
-                unsigned mask = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
-                if (col0 + 8 > P.nr) mask &= P.nr > col0 ? (0xFFu >> (8 - (P.nr - col0))) : 0u;
-                while (mask) {
-                    const int j = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const float lb = qn - E - pick8(v, j) * inv2s;
-                    if (!(lb <= U * kTie)) continue;
-                    const float ub = lb + 2.0f * E;
-                    if (count == P.cap1) {
-                        int c2 = 0;
-                        for (int e = 0; e < count; ++e)
-                            if (clb[e] <= U * kTie) {
-                                clb[c2] = clb[e];
-                                cp[c2] = cp[e];
-                                ++c2;
-                            }
-                        count = c2;
-                        if (count == P.cap1) {
-                            fail = true;
-                            continue;
-                        }
-                    }
-                    clb[count] = lb;
-                    cp[count] = col0 + j;
-                    ++count;
-                    float x = ub;
-#pragma unroll
-                    for (int t = 0; t < KT; ++t) {
-                        const float lo = fminf(ubk[t], x), hi = fmaxf(ubk[t], x);
-                        ubk[t] = lo;
-                        x = hi;
-                    }
-                    float kth = ubk[0];
-#pragma unroll
-                    for (int t = 0; t < KT; ++t)
-                        if (t == P.k - 1) kth = ubk[t];
-                    U = fminf(U, kth);
-                    T = threshold();
-                }
-            };
             for (int ch = 0; ch < nchunks; ++ch) {
                 const int off = ch * kN;
                 const int lim = min(kN, static_cast<int>(P.nr) - off);
                 const uint32_t tb = ti & 1;
-                sm100::mbar_wait(&tfull[tb], (ti >> 1) & 1);
+                S1_WAIT(&tfull[tb], (ti >> 1) & 1, 8);
                 sm100::tc_fence_after();
-                for (int c0 = 0; c0 < lim; c0 += 64) {
+                for (int c0 = 0; c0 < S1_LIM(lim); c0 += 64) {
                     uint32_t ra[32], rbv[32];
                     sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0, ra);
                     sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0 + 32, rbv);
@@ -515,103 +515,148 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     float m8[8];
 #pragma unroll
                     for (int s = 0; s < 8; ++s) m8[s] = max8(v + 8 * s);
-                    if (KT == 1 && live) {
+                    // bound from the valid groups' maxima first (k = 1: the block's best)
+                    if (KT == 1) {
                         float mv = -__int_as_float(0x7f800000);
 #pragma unroll
                         for (int s = 0; s < 8; ++s)
                             if (c0 + 8 * s + 8 <= lim) mv = fmaxf(mv, m8[s]);
-                        if (mv > vbest) {
-                            vbest = mv;
-                            const float ub = qn + E - mv * inv2s;
-                            if (ub < U) {
-                                U = ub;
-                                T = threshold();
-                            }
+                        const float ub = fmaf(-mv, inv2s, lb0) + 2.0f * E;
+                        if (live && ub < U) {
+                            U = ub;
+                            T = threshold();
                         }
                     }
+                    unsigned gm = 0;  // groups that may hold a candidate
 #pragma unroll
-                    for (int s = 0; s < 8; ++s)
-                        if (m8[s] >= T) slow8(v + 8 * s, off + c0 + 8 * s);
+                    for (int s = 0; s < 8; ++s) gm |= (m8[s] >= T ? 1u : 0u) << s;
+                    if (__any_sync(0xffffffffu, gm != 0)) {
+                        // rare path, compact code: stage the block's values, walk the flagged groups
+                        float4 *sv4 = reinterpret_cast<float4 *>(s_v + row * kVStride);
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) sv4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        __syncwarp();
+                        const float *sv = s_v + row * kVStride;
+                        while (gm) {
+                            const int s = __ffs(gm) - 1;
+                            gm &= gm - 1;
+                            const int g0 = off + c0 + 8 * s;
+#pragma unroll 1
+                            for (int j = 0; j < 8; ++j) {
+                                const float x = sv[8 * s + j];
+                                if (!(x >= T) || g0 + j >= P.nr) continue;
+                                const float lb = fmaf(-x, inv2s, lb0);
+                                if (count == P.cap1) {  // compact: drop entries that can no longer qualify
+                                    int c2 = 0;
+                                    for (int e = 0; e < count; ++e)
+                                        if (clb[e] <= U * kTie) {
+                                            clb[c2] = clb[e];
+                                            cp[c2] = cp[e];
+                                            ++c2;
+                                        }
+                                    count = c2;
+                                    if (count == P.cap1) {
+                                        fail = true;
+                                        continue;
+                                    }
+                                }
+                                clb[count] = lb;
+                                cp[count] = g0 + j;
+                                ++count;
+                                if (KT > 1) {
+                                    float y = lb + 2.0f * E;
+#pragma unroll
+                                    for (int t = 0; t < KT; ++t) {
+                                        const float lo = fminf(ubk[t], y), hi = fmaxf(ubk[t], y);
+                                        ubk[t] = lo;
+                                        y = hi;
+                                    }
+                                    float kth = ubk[0];
+#pragma unroll
+                                    for (int t = 0; t < KT; ++t)
+                                        if (t == P.k - 1) kth = ubk[t];
+                                    U = fminf(U, kth);
+                                    T = threshold();
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    }
                 }
                 sm100::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(&tempty[tb]);
                 ++ti;
             }
-            // exact gamma_k and nearest representative from the collected candidates
-            uint64_t best[KT];
-#pragma unroll
-            for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-            if (live && !fail) {
-                const float ufin = U * kTie;
-                const float *qrow = P.q + qi * P.d;
-                for (int e = 0; e < count; ++e) {
-                    if (!(clb[e] <= ufin)) continue;
-                    const int32_t p = cp[e];
-                    const float dist = exact_dist<RBC_L2>(qrow, P.reps + static_cast<int64_t>(p) * P.d, P.d);
-                    const uint64_t key = pack_key(dist, static_cast<uint32_t>(p));
-                    if (key < best[KT - 1]) sorted_insert<KT>(best, key);
-                }
-            }
-            uint64_t kth_key = best[0];
-#pragma unroll
-            for (int t = 0; t < KT; ++t)
-                if (t == P.k - 1) kth_key = best[t];
-            if (live && kth_key == kEmptyKey) fail = true;
-            const float g = live ? key_dist(kth_key) : 0.f;
-            const float g2 = g * g;
-            const float t3 = 9.0f * g2;
+            // U >= gamma_k^2 (U is an achieved k-th smallest upper bound)
+            const float Uk = U;
+            if (live && !(Uk < __int_as_float(0x7f800000))) fail = true;  // fewer than k candidates
+            const float ghi = sqrtf(Uk * kTie) * kUp;
+            const float t9hi = 9.0f * ghi * ghi * (1.0f + kEps);
 
-            // ---------- pass 2: classify every representative ----------
+            // ---------- pass 2: count the far reps, record the rest with their estimate ----------
             int pr = 0, p3 = 0, rc = 0;
             int32_t *rec = P.rec + (live ? qi : 0) * P.cap_rec;
+            float *rdt = P.rec_dt + (live ? qi : 0) * P.cap_rec;
             for (int ch = 0; ch < nchunks; ++ch) {
                 const int off = ch * kN;
                 const int lim = min(kN, static_cast<int>(P.nr) - off);
                 const uint32_t tb = ti & 1;
-                // reps farther than max(3 gamma, gamma + max psi of the chunk) are pruned by both tests
-                const float tpm = g + P.psimax[ch];
-                const float thr_far = fmaxf(t3, tpm * tpm) * (1.0f + kEps) + E;  // on dt = d^2 estimate
-                sm100::mbar_wait(&tfull[tb], (ti >> 1) & 1);
+                // reps with lb > max(9 ghi^2, (ghi + max psi of the chunk)^2) are pruned by both tests
+                const float tpm = ghi + P.psimax[ch];
+                const float thr_far = fmaxf(t9hi, tpm * tpm * (1.0f + kEps));
+                // far  <=>  V < Tf   (Tf lowered by 2^-18 relative: only certain cases count as far)
+                const float tf = 0.5f * scale * (qn - E - thr_far);
+                const float Tf = tf - fabsf(tf) * (1.0f / 262144.0f) - 1e-30f;
+                S1_WAIT(&tfull[tb], (ti >> 1) & 1, 9);
                 sm100::tc_fence_after();
-                for (int c0 = 0; c0 < lim; c0 += 32) {
-                    uint32_t ra[32];
+                for (int c0 = 0; c0 < S1_LIM(lim); c0 += 64) {
+                    uint32_t ra[32], rbv[32];
                     sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0, ra);
+                    sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0 + 32, rbv);
                     sm100::tmem_wait_ld(ra);
+                    sm100::tmem_tie(rbv);
                     if (!live) continue;
-                    const int nvalid = min(32, lim - c0);
-                    const unsigned valid = nvalid == 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
-                    unsigned nearm = 0;
+                    float v[64];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        nearm |= ((qn - __uint_as_float(ra[j]) * inv2s) > thr_far ? 0u : 1u) << j;
-                    nearm &= valid;
-                    const int nfar = nvalid - __popc(nearm);
-                    pr += nfar;
-                    p3 += nfar;
-                    while (nearm) {
-                        const int j = __ffs(nearm) - 1;
-                        nearm &= nearm - 1;
-                        const int p = off + c0 + j;
-                        const float dt = qn - __uint_as_float(pick32u(ra, j)) * inv2s;
-                        const float lb = dt - E, ub = dt + E;
-                        if (lb > t3 * (1.0f + kEps)) {
-                            // certainly d > 3 gamma (and d > gamma); radius test decides pr
-                            const float tp = g + s_radii[p];
-                            const float tp2 = tp * tp;
-                            if (lb > tp2 * (1.0f + kEps)) {
-                                ++p3;
-                                ++pr;
-                            } else if (ub < tp2 * (1.0f - kEps)) {
-                                ++p3;
-                            } else {
-                                if (rc < P.cap_rec) rec[rc] = p;  // undecided radius test
-                                ++rc;
+                    for (int j = 0; j < 32; ++j) {
+                        v[j] = __uint_as_float(ra[j]);
+                        v[32 + j] = __uint_as_float(rbv[j]);
+                    }
+                    const int nvb = min(64, lim - c0);
+                    pr += nvb;  // counted far; the recorded ones are taken back below
+                    p3 += nvb;
+                    float m8[8];
+#pragma unroll
+                    for (int s = 0; s < 8; ++s) m8[s] = max8(v + 8 * s);
+                    unsigned gm = 0;
+#pragma unroll
+                    for (int s = 0; s < 8; ++s) gm |= (m8[s] >= Tf ? 1u : 0u) << s;
+                    if (__any_sync(__activemask(), gm != 0)) {
+                        float4 *sv4 = reinterpret_cast<float4 *>(s_v + row * kVStride);
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) sv4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        __syncwarp(__activemask());
+                        const float *sv = s_v + row * kVStride;
+                        while (gm) {
+                            const int s = __ffs(gm) - 1;
+                            gm &= gm - 1;
+                            const int g0 = c0 + 8 * s;
+#pragma unroll 1
+                            for (int j = 0; j < 8; ++j) {
+                                const float x = sv[8 * s + j];
+                                if (x >= Tf && g0 + j < lim) {
+                                    if (rc < P.cap_rec) {
+                                        rec[rc] = off + g0 + j;
+                                        rdt[rc] = fmaf(-x, inv2s, qn);
+                                    }
+                                    ++rc;
+                                    --pr;
+                                    --p3;
+                                }
                             }
-                        } else {
-                            if (rc < P.cap_rec) rec[rc] = p;  // possible survivor / straddle
-                            ++rc;
                         }
+                        __syncwarp(__activemask());
                     }
                 }
                 sm100::tc_fence_before();
@@ -622,9 +667,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             if (rc > P.cap_rec) fail = true;
             if (live) {
                 // a failed row gets inert, in-range outputs: the batch is re-run on the
-                // exact path, but stage 2 is already queued behind this kernel
-                P.gamma[qi] = fail ? 0.0f : g;
-                P.nearest[qi] = fail ? 0 : static_cast<int32_t>(key_id(best[0]));
+                // exact path, but the fix-up and stage 2 are already queued behind this kernel
+                P.c1_cnt[qi] = fail ? -1 : count;
+                P.c1_u[qi] = Uk * kTie;
+                P.rec_e[qi] = E;
                 P.pr[qi] = pr;
                 P.p3[qi] = p3;
                 P.rec_cnt[qi] = fail ? 0 : rc;
@@ -632,76 +678,183 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             }
         }
     }
+#ifdef RBC_S1_TIMING
+    if (P.timing && lane == 0 && warp <= 2) {
+        tw[10 + (warp == 2 ? 1 : 0)] = clock64() - t_start;  // wall of MMA / epilogue warp
+        for (int j = 0; j < 12; ++j)
+            if (tw[j]) atomicAdd(&P.timing[j], tw[j]);
+    }
+#endif
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 1) sm100::tmem_dealloc<256>(tmem);
 }
 
-// Fix-up, one warp per query: exact decisions for the recorded reps, the
-// 4 gamma cutoffs, the surviving segments (ascending rep position) and stats.
-__global__ void __launch_bounds__(256) stage1_fixup_kernel(
-    const float *__restrict__ q, const float *__restrict__ reps, int d, int64_t nq, const float *__restrict__ radii,
-    const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, const float *__restrict__ lskip,
-    const float *__restrict__ gamma,
-    const int32_t *__restrict__ nearest, const int32_t *__restrict__ rec_cnt, const int32_t *__restrict__ rec,
-    int cap_rec, const int32_t *__restrict__ pr_in, const int32_t *__restrict__ p3_in, int32_t *__restrict__ nseg,
-    int64_t *__restrict__ cand, int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start,
-    int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list, float *__restrict__ seg_d1,
-    uint64_t *__restrict__ order_key, int32_t *__restrict__ pr_out, int32_t *__restrict__ p3_out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (i >= nq) return;
-    const double g = gamma[i], cut = 4.0 * g;
+// Distances of a query row held in registers (16 float4, zero padded to 64) to a
+// zero-padded 64-float row: padding terms are exact zeros, so summing all 64
+// coordinates reproduces the reference's d-term sum bit for bit.
+__device__ __forceinline__ float exact_dist64(const float4 (&qv)[16], const float *__restrict__ row) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    double acc = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        float4 y[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) y[c] = __ldg(r4 + h * 8 + c);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc = exact_acc4<RBC_L2>(acc, qv[h * 8 + c], y[c]);
+    }
+    return __double2float_rn(__dsqrt_rn(acc));
+}
+
+// fp32 |q - r| (relative error <= 66 * 2^-24 on the square; stage 2 bounds it with kD1/kUq)
+__device__ __forceinline__ float approx_dist64(const float4 (&qv)[16], const float *__restrict__ row) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        const float4 y = __ldg(r4 + c);
+        const float t0 = qv[c].x - y.x, t1 = qv[c].y - y.y, t2 = qv[c].z - y.z, t3 = qv[c].w - y.w;
+        a0 = fmaf(t0, t0, fmaf(t1, t1, a0));
+        a1 = fmaf(t2, t2, fmaf(t3, t3, a1));
+    }
+    return sqrtf(a0 + a1);
+}
+
+// Fix-up, one thread per query, threads in pilot order (neighbouring lanes share
+// their reps, so the rep-row loads coalesce): exact gamma_k and nearest rep from
+// the gamma candidates (reference arithmetic), exact decisions for the undecided
+// reps, the 4 gamma cutoffs, the surviving segments (ascending rep position) and
+// stats.  Each thread first compacts its own candidates into a local list, so a
+// warp runs max(list length) exact distances with all lanes busy.
+constexpr int kFixThreads = 128;
+constexpr int kFixList = 64;  // per-thread gamma-candidate list (more: a second sweep)
+
+template <int KT>
+__global__ void __launch_bounds__(kFixThreads) stage1_fixup_kernel(
+    const float *__restrict__ q64, const int32_t *__restrict__ qorder, const float *__restrict__ reps64, int64_t nq,
+    int k, const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
+    const float *__restrict__ lskip, const float *__restrict__ c1_lb, const int32_t *__restrict__ c1_p, int cap1,
+    const int32_t *__restrict__ c1_cnt, const float *__restrict__ c1_u, const int32_t *__restrict__ rec_cnt,
+    const int32_t *__restrict__ rec, const float *__restrict__ rec_dt, const float *__restrict__ rec_e, int cap_rec,
+    const int32_t *__restrict__ pr_in, const int32_t *__restrict__ p3_in, float *__restrict__ gamma_out, int32_t *__restrict__ nseg, int64_t *__restrict__ cand, int64_t *__restrict__ seg_off,
+    int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list,
+    float *__restrict__ seg_d1, uint64_t *__restrict__ order_key, int32_t *__restrict__ pr_out,
+    int32_t *__restrict__ p3_out, int32_t *__restrict__ fail) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= nq) return;
+    const int64_t i = qorder[t];
+    const int n1 = c1_cnt[i];
+    const int64_t base = i * static_cast<int64_t>(cap_rec);
+    if (n1 < 0) {  // failed row (the batch is recomputed): inert outputs
+        gamma_out[i] = 0.f;
+        nseg[i] = 0;
+        cand[i] = 0;
+        seg_off[i] = base;
+        order_key[i] = 0;
+        return;
+    }
+    float4 qv[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
+    // ---- exact gamma_k over the candidates with lb <= U_k
+    const float ufin = c1_u[i];
+    uint64_t best[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+    for (int e0 = 0; e0 < n1; e0 += kFixList) {
+        int32_t list[kFixList];
+        int m = 0;
+        const int e1 = min(n1, e0 + kFixList);
+        for (int e = e0; e < e1; ++e)
+            if (c1_lb[i * cap1 + e] <= ufin) list[m++] = c1_p[i * cap1 + e];
+        for (int u = 0; u < m; ++u) {
+            const int32_t p = list[u];
+            const float dist = exact_dist64(qv, reps64 + static_cast<int64_t>(p) * 64);
+            const uint64_t key = pack_key(dist, static_cast<uint32_t>(p));
+            if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+        }
+    }
+    uint64_t kth = best[0];
+#pragma unroll
+    for (int u = 0; u < KT; ++u)
+        if (u == k - 1) kth = best[u];
+    if (kth == kEmptyKey) {  // cannot happen with a consistent bound; keep the result exact anyway
+        atomicExch(fail, 1);
+        gamma_out[i] = 0.f;
+        nseg[i] = 0;
+        cand[i] = 0;
+        seg_off[i] = base;
+        order_key[i] = 0;
+        return;
+    }
+    const float gf = key_dist(kth);
+    const double g = gf, cutd = 4.0 * g;
+    // ---- recorded reps: classify with the exact gamma on the interval [dt - E, dt + E]
+    // (tri-state tests A: d > 3 gamma, B: d >= gamma + psi, C: d > gamma, search.py:62-74,
+    // 194-195); only an undecided rep costs an exact distance
     const int n = rec_cnt[i];
-    const int32_t *r = rec + i * cap_rec;
-    const float *qrow = q + i * d;
-    const int64_t base = i * cap_rec;
+    const int32_t *r = rec + base;
+    const float *rd = rec_dt + base;
+    const float E = rec_e[i];
+    const float g2 = gf * gf, t9 = 9.0f * g2;
     int pr = 0, p3 = 0, ns = 0;
     long long cs = 0;
     unsigned first = 0xFFFFFFFFu;
-    for (int e0 = 0; e0 < n; e0 += 32) {
-        const int e = e0 + lane;
-        int32_t len = 0, p = 0;
-        float dist = 0.f;
-        if (e < n) {
-            p = r[e];
-            dist = exact_dist<RBC_L2>(qrow, reps + static_cast<int64_t>(p) * d, d);
-            pr += pruned_radius(dist, radii[p], g) ? 1 : 0;
+    for (int e = 0; e < n; ++e) {
+        const int32_t p = r[e];
+        const float dt = rd[e];
+        const float lb = dt - E, ub = dt + E;
+        const float psi = radii[p];
+        const float tp = gf + psi, tp2 = tp * tp;
+        const bool a_t = lb > t9 * (1.0f + kEps), a_f = ub < t9 * (1.0f - kEps);
+        const bool b_t = lb > tp2 * (1.0f + kEps), b_f = ub < tp2 * (1.0f - kEps);
+        const bool c_t = lb > g2 * (1.0f + kEps), c_f = ub < g2 * (1.0f - kEps);
+        const bool bc_t = b_t && c_t, bc_f = b_f || c_f;
+        const float *row = reps64 + static_cast<int64_t>(p) * 64;
+        bool surv;
+        float dist;
+        if ((a_t || a_f) && (bc_t || bc_f)) {
+            p3 += a_t ? 1 : 0;
+            pr += bc_t ? 1 : 0;
+            surv = a_f && bc_f;
+            dist = surv ? approx_dist64(qv, row) : 0.f;
+        } else {
+            dist = exact_dist64(qv, row);
+            pr += pruned_radius(dist, psi, g) ? 1 : 0;
             p3 += pruned_3gamma(dist, g) ? 1 : 0;
-            if (survives(dist, radii[p], g))
-                len = list_cutoff_skip(list_dists + offsets[p], static_cast<int32_t>(offsets[p + 1] - offsets[p]),
-                                       lskip + static_cast<int64_t>(p) * 32, cut);
+            surv = survives(dist, psi, g);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, len > 0);
+        if (!surv) continue;
+        const int32_t full = static_cast<int32_t>(offsets[p + 1] - offsets[p]);
+        // the list's last (largest) distance is psi: the whole list is within 4 gamma iff psi <= 4 gamma
+        const int32_t len = static_cast<double>(psi) <= cutd
+                                ? full
+                                : list_cutoff_skip(list_dists + offsets[p], full, lskip + static_cast<int64_t>(p) * 32, cutd);
         if (len > 0) {
-            const int64_t at = base + ns + __popc(bal & ((1u << lane) - 1u));
-            seg_start[at] = offsets[p];
-            seg_len[at] = len;
-            seg_list[at] = p;
-            seg_d1[at] = dist;
+            seg_start[base + ns] = offsets[p];
+            seg_len[base + ns] = len;
+            seg_list[base + ns] = p;
+            seg_d1[base + ns] = dist;
+            ++ns;
             cs += len;
             if (static_cast<unsigned>(p) < first) first = static_cast<unsigned>(p);
         }
-        ns += __popc(bal);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        pr += __shfl_xor_sync(0xffffffffu, pr, o);
-        p3 += __shfl_xor_sync(0xffffffffu, p3, o);
-        cs += __shfl_xor_sync(0xffffffffu, cs, o);
-        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    }
-    if (lane == 0) {
-        if (pr_out) pr_out[i] = pr_in[i] + pr;
-        if (p3_out) p3_out[i] = p3_in[i] + p3;
-        nseg[i] = ns;
-        cand[i] = cs;
-        seg_off[i] = base;
-        order_key[i] = (static_cast<uint64_t>(first & 0xFFFFFFu) << 24) | (static_cast<uint32_t>(nearest[i]) & 0xFFFFFFu);
-    }
+    gamma_out[i] = gf;
+    if (pr_out) pr_out[i] = pr_in[i] + pr;
+    if (p3_out) p3_out[i] = p3_in[i] + p3;
+    nseg[i] = ns;
+    cand[i] = cs;
+    seg_off[i] = base;
+    order_key[i] = (static_cast<uint64_t>(first & 0xFFFFFFu) << 24) | (key_id(best[0]) & 0xFFFFFFu);
 }
 
-constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + (kMaxRepsSmem + 4) * sizeof(float) + 256;
+// dynamic shared memory: stages, A buffers, radii[nr], reduction slots, barriers
+inline size_t s1_smem_bytes(int64_t nr) {
+    return 1024 + kStages * kStageBytes + 2 * kABytes + (((nr + 3) & ~int64_t(3)) + 4 + kRows * kVStride) * sizeof(float) +
+           256;
+}
 
 }  // namespace
 
@@ -717,6 +870,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
               cudaMalloc(&t->lskip, idx->nr * 32 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->c64, 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->stat, 2 * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&t->reps64, idx->nr * 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&rmax_bits, sizeof(unsigned)) == cudaSuccess;
     auto cleanup = [&](int rc) {
         cudaFree(t->rb);
@@ -724,6 +878,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaFree(t->lskip);
         cudaFree(t->c64);
         cudaFree(t->stat);
+        cudaFree(t->reps64);
         cudaFree(rmax_bits);
         delete t;
         return rc;
@@ -741,7 +896,8 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
                                                           t->plane1 ? 1 : 0, t->rb);
     chunk_psimax_kernel<<<grid_for(nchunks, 64), 64, 0, st>>>(idx->radii, idx->nr, t->psimax);
     list_skip_kernel<<<grid_for(idx->nr * 32, 256), 256, 0, st>>>(idx->offsets, idx->list_dists, idx->nr, t->lskip);
-    note_launch(6);
+    pad_reps64_kernel<<<grid_for(idx->nr * 64, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, t->reps64);
+    note_launch(7);
     float stat[2] = {1.f, 0.f};
     if (cudaMemcpyAsync(stat, t->stat, sizeof(stat), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -750,7 +906,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     rmax_bits = nullptr;
     t->sG = stat[0];
     t->rmax = stat[1];
-    idx->bytes += nchunks * kStageBytes + 66 * sizeof(float);
+    idx->bytes += nchunks * kStageBytes + 66 * sizeof(float) + idx->nr * (64 + 32) * sizeof(float);
     idx->tc1 = t;
     return RBC_OK;
 }
@@ -763,6 +919,7 @@ void tc1_index_release(rbc_index *idx) {
     cudaFree(t->lskip);
     cudaFree(t->c64);
     cudaFree(t->stat);
+    cudaFree(t->reps64);
     delete t;
     idx->tc1 = nullptr;
 }
@@ -771,7 +928,7 @@ bool tc_stage1_supported(const rbc_index *idx, int k) { return idx->tc1 != nullp
 
 static int g_num_sms1 = 0;
 
-// Fused stage 1 + pruning.  Returns RBC_OK with *fallback = true when some
+// Fused stage 1 + pruning, stream-ordered.  *fail_dev becomes nonzero when some
 // row exhausted a buffer (the caller then runs the exact path).
 int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut &out, int32_t *fail_dev,
               cudaStream_t st) {
@@ -779,21 +936,43 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
     const int cap1 = 32 + 16 * k;
     const int cap_rec = static_cast<int>(idx->nr < 512 ? idx->nr : 512);
-    DevBuf<float> q64buf, c1_lb;
-    DevBuf<int32_t> c1_p, nearest, pr0, p30, rec_cnt, rec, flags;
+    DevBuf<float> q64buf, c1_lb, c1_u, rec_dt, rec_e;
+    DevBuf<int32_t> c1_p, c1_cnt, pr0, p30, rec_cnt, rec, flags, qids, qorder;
+    DevBuf<uint32_t> pkey, pkey_sorted;
     const float *q64 = q;
     if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
         RBC_CHECK(q64buf.alloc(nq * 64, st));
         pad_rows64(q, nq, idx->d, q64buf.get(), st);
         q64 = q64buf.get();
     }
+    // query order: sort by nearest pilot (stable, so equal keys keep id order)
+    const int npilot = static_cast<int>(idx->nr < kPilots ? idx->nr : kPilots);
+    RBC_CHECK(qids.alloc(nq, st));
+    RBC_CHECK(qorder.alloc(nq, st));
+    RBC_CHECK(pkey.alloc(nq, st));
+    RBC_CHECK(pkey_sorted.alloc(nq, st));
+    pilot_key_kernel<<<grid_for(nq, 128), 128, 0, st>>>(q64, nq, t->reps64, idx->nr, npilot, pkey.get(), qids.get());
+    RBC_LAUNCHED();
+    {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, pkey.get(), pkey_sorted.get(), qids.get(), qorder.get(), nq, 0, 7,
+                                        st);
+        DevBuf<unsigned char> tmp;
+        RBC_CHECK(tmp.alloc(tb, st));
+        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, pkey.get(), pkey_sorted.get(), qids.get(), qorder.get(),
+                                                 nq, 0, 7, st));
+        note_launch();
+    }
     RBC_CHECK(c1_lb.alloc(nq * cap1, st));
     RBC_CHECK(c1_p.alloc(nq * cap1, st));
-    RBC_CHECK(nearest.alloc(nq, st));
+    RBC_CHECK(c1_cnt.alloc(nq, st));
+    RBC_CHECK(c1_u.alloc(nq, st));
     RBC_CHECK(pr0.alloc(nq, st));
     RBC_CHECK(p30.alloc(nq, st));
     RBC_CHECK(rec_cnt.alloc(nq, st));
     RBC_CHECK(rec.alloc(nq * cap_rec, st));
+    RBC_CHECK(rec_dt.alloc(nq * cap_rec, st));
+    RBC_CHECK(rec_e.alloc(nq, st));
     RBC_CHECK(flags.alloc(2, st));
     RBC_CHECK(out.gamma.alloc(nq, st));
     RBC_CHECK(out.nseg.alloc(nq, st));
@@ -809,28 +988,27 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     P.rb = t->rb;
     P.plane1 = t->plane1 ? 1 : 0;
     P.nr = idx->nr;
-    P.nrpad = t->nrpad;
     P.sG = t->sG;
     P.rmax = t->rmax;
     P.c64 = t->c64;
     P.psimax = t->psimax;
     P.q64 = q64;
-    P.q = q;
-    P.reps = idx->reps;
+    P.qorder = qorder.get();
     P.radii = idx->radii;
-    P.d = idx->d;
     P.k = k;
     P.nq = nq;
     P.ntiles = ntiles;
     P.c1_lb = c1_lb.get();
     P.c1_p = c1_p.get();
     P.cap1 = cap1;
-    P.gamma = out.gamma.get();
-    P.nearest = nearest.get();
+    P.c1_cnt = c1_cnt.get();
+    P.c1_u = c1_u.get();
     P.pr = pr0.get();
     P.p3 = p30.get();
     P.rec_cnt = rec_cnt.get();
     P.rec = rec.get();
+    P.rec_dt = rec_dt.get();
+    P.rec_e = rec_e.get();
     P.cap_rec = cap_rec;
     P.fail = fail_dev;
     P.tile_counter = flags.get() + 1;
@@ -839,21 +1017,53 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms1, cudaDevAttrMultiProcessorCount, dev);
     }
-    const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms1 ? ntiles : g_num_sms1);
+    // persistent CTAs, two per SM when the representatives' radii fit (tiles come from a counter)
+    const size_t smem = s1_smem_bytes(idx->nr);
+    const int per_sm = smem <= 110 * 1024 ? 2 : 1;  // (one CTA per SM at the current stage count)
+    const unsigned grid = static_cast<unsigned>(ntiles < per_sm * g_num_sms1 ? ntiles : per_sm * g_num_sms1);
     auto launch = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-        kern<<<grid, kThreads, kSmemBytes, st>>>(P);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kThreads, smem, st>>>(P);
     };
+    P.timing = nullptr;
+#ifdef RBC_S1_TIMING
+    DevBuf<unsigned long long> timing;
+    if (getenv("RBC_DEBUG_S1")) {
+        RBC_CHECK(timing.alloc(12, st));
+        RBC_CUDA(cudaMemsetAsync(timing.get(), 0, sizeof(unsigned long long) * 12, st));
+        P.timing = timing.get();
+    }
+#endif
     if (k == 1) launch(stage1_tc_kernel<1>);
     else if (k <= 4) launch(stage1_tc_kernel<4>);
     else if (k <= 8) launch(stage1_tc_kernel<8>);
     else launch(stage1_tc_kernel<16>);
     RBC_LAUNCHED();
-    stage1_fixup_kernel<<<grid_for(nq * 32, 256), 256, 0, st>>>(
-        q, idx->reps, idx->d, nq, idx->radii, idx->offsets, idx->list_dists, t->lskip, out.gamma.get(), nearest.get(),
-        rec_cnt.get(), rec.get(), cap_rec, pr0.get(), p30.get(), out.nseg.get(), out.cand.get(), out.seg_off.get(),
-        out.seg_start.get(), out.seg_len.get(), out.seg_list.get(), out.seg_d1.get(), out.order_key.get(), out.pr,
-        out.p3);
+#ifdef RBC_S1_TIMING
+    if (P.timing) {
+        unsigned long long h[12];
+        cudaMemcpy(h, P.timing, sizeof(h), cudaMemcpyDeviceToHost);
+        const char *nm[12] = {"prod:tile_empty", "prod:empty", "mma:tile_full", "mma:afull", "mma:full", "mma:tempty",
+                              "epi:tile_full", "epi:aempty", "epi:tfull1", "epi:tfull2", "wall:mma", "wall:epi"};
+        fprintf(stderr, "[s1] per-CTA cycles (grid %u):", grid);
+        for (int j = 0; j < 12; ++j) fprintf(stderr, " %s=%.0f", nm[j], double(h[j]) / grid);
+        fprintf(stderr, "\n");
+    }
+#endif
+    const unsigned fgrid = grid_for(nq, kFixThreads);
+#define RBC_FIXUP(KT)                                                                                                 \
+    stage1_fixup_kernel<KT><<<fgrid, kFixThreads, 0, st>>>(                                                           \
+        q64, qorder.get(), t->reps64, nq, k, idx->radii, idx->offsets, idx->list_dists, t->lskip, c1_lb.get(),          \
+        c1_p.get(),                                                                                                    \
+        cap1, c1_cnt.get(), c1_u.get(), rec_cnt.get(), rec.get(), rec_dt.get(), rec_e.get(), cap_rec, pr0.get(),        \
+        p30.get(), out.gamma.get(),                                                                                    \
+        out.nseg.get(), out.cand.get(), out.seg_off.get(), out.seg_start.get(), out.seg_len.get(), out.seg_list.get(), \
+        out.seg_d1.get(), out.order_key.get(), out.pr, out.p3, fail_dev)
+    if (k == 1) RBC_FIXUP(1);
+    else if (k <= 4) RBC_FIXUP(4);
+    else if (k <= 8) RBC_FIXUP(8);
+    else RBC_FIXUP(16);
+#undef RBC_FIXUP
     RBC_LAUNCHED();
     return RBC_OK;
 }

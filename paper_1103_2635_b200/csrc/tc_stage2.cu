@@ -39,6 +39,8 @@
 //               its half of K), candidate filter, per-half candidate buffers
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -69,6 +71,8 @@ constexpr float kC2 = 1.0f / 1048576.0f;                              // norms, 
 constexpr float kC4 = 1.0f / 262144.0f;                               // f16 subnormal flush (absolute, scaled)
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                       // rounding-up factor for norms
 constexpr float kTie = 1.0f + 1.0f / 524288.0f;                       // tie slack: 8 fp32 ulps of the distance
+constexpr float kD1 = 1.0f / 32768.0f;                                // approximate stage-1 distance (A2 term)
+constexpr float kUq = 1.0f + 1.0f / 65536.0f;                          // ... and its |a| bound
 
 struct TcIndex {
     int64_t npad = 0;
@@ -118,13 +122,27 @@ struct S2Params {
     int32_t *overflow_count;
     int32_t *tile_counter;
     int64_t cap_work;
+    unsigned long long *timing;  // diagnostic [grid][8] role wait/busy cycles (nullptr = off)
 };
 
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
 
-__device__ __forceinline__ float max8(const float *v) {
-    return fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+// Diagnostic role timing (build with -DRBC_S2_TIMING and run with RBC_DEBUG_S2=1):
+// cycles each role spends waiting on its mbarriers, per CTA.
+#ifdef RBC_S2_TIMING
+__device__ __forceinline__ void mbar_wait_t(uint64_t *bar, uint32_t parity, unsigned long long &acc) {
+    const unsigned long long t0 = clock64();
+    sm100::mbar_wait(bar, parity);
+    acc += clock64() - t0;
 }
+#define S2_WAIT(bar, parity, slot) mbar_wait_t(bar, parity, tw[slot])
+#define S2_TIME(stmt) stmt
+#else
+#define S2_WAIT(bar, parity, slot) sm100::mbar_wait(bar, parity)
+#define S2_TIME(stmt)
+#endif
+
+__device__ __forceinline__ float max8(const float *v) { return sm100::max8(v); }
 
 // ---- index preparation ----------------------------------------------------------
 __global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, float *__restrict__ sB) {
@@ -354,6 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);  // 2-slot ring of tile ids
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    S2_TIME(unsigned long long tw[12] = {});
+    S2_TIME(const unsigned long long t_start = clock64());
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             sm100::mbar_init(&full[s], 1);
@@ -392,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     for (int off = 0; off < wi.ext; off += kNmax) {
                         const int n = min(kNmax, roundup16(wi.ext - off));
                         const uint32_t s = bi % kStages;
-                        sm100::mbar_wait(&empty[s], ((bi / kStages) & 1) ^ 1);
+                        S2_WAIT(&empty[s], ((bi / kStages) & 1) ^ 1, 0);
                         uint8_t *dst = sB + s * kStageBytes;
                         const uint32_t b0 = static_cast<uint32_t>(n) * kP0;
                         const uint32_t b1 = P.plane1 ? static_cast<uint32_t>(n) * kP1 : 0u;
@@ -419,14 +439,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
                     const int ext = P.work[w].ext;
                     const uint32_t a = ai & 1;
-                    sm100::mbar_wait(&afull[a], (ai >> 1) & 1);
+                    S2_WAIT(&afull[a], (ai >> 1) & 1, 1);
                     sm100::tc_fence_after();
                     const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
                     for (int off = 0; off < ext; off += kNmax) {
                         const int n = min(kNmax, roundup16(ext - off));
                         const uint32_t s = bi % kStages, tb = ti & 1;
-                        sm100::mbar_wait(&full[s], (bi / kStages) & 1);
-                        sm100::mbar_wait(&tempty[tb], ((ti >> 1) & 1) ^ 1);
+                        S2_WAIT(&full[s], (bi / kStages) & 1, 2);
+                        S2_WAIT(&tempty[tb], ((ti >> 1) & 1) ^ 1, 3);
                         sm100::tc_fence_after();
                         const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
                         const uint32_t b0 = sm100::smem_u32(sB + s * kStageBytes);
@@ -483,6 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
             // A operand of list w: this thread's 64 bytes of row `row` (+ the aug columns on half 1)
             auto prep_a = [&](int64_t w) {
+                S2_TIME(const unsigned long long tp0 = clock64());
+                S2_TIME(++tw[11]);
                 const WorkItem wi = P.work[w];
                 const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64 + half * 32);
                 float4 rr4[8];
@@ -492,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 const float sa = wi.sA;
                 const uint32_t a = ai & 1;
-                sm100::mbar_wait(&aempty[a], ((ai >> 1) & 1) ^ 1);
+                S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -520,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(&afull[a]);
                 ++ai;
+                S2_TIME(tw[8] += clock64() - tp0);
             };
             if (w0 < w1) prep_a(w0);
 
@@ -529,10 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             const float gk = live ? P.gamma[qi] : 0.f;
             const float u_init = gk * gk * kUp * kUp;
             float U = u_init;  // running upper bound of the k-th smallest candidate d^2
-            int count = 0;
+            int count = 0;     // buffered 8-column groups
             bool overflow = false;
             const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * 2 + half);
-            float *clb = P.cand_lb + slot_id * P.cap;
+            float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 2;
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
             int cut_n = 0;
@@ -555,10 +578,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const float scale = sa * wi.sB, inv2s = 2.0f / scale;
                 float A2 = 0.f, E = 0.f;
                 if (cutv > 0) {
-                    const float na = dq * kUp, rb = wi.radius * kUp;
+                    // dq = |q - r_p| from stage 1's fix-up: exact, or fp32 with relative error
+                    // <= (d + 2) 2^-24 on dq^2 -- covered by kD1 (on A2) and kUq (on |a|)
+                    const float na = dq * kUq, rb = wi.radius * kUp;
                     A2 = dq * dq;
-                    E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
+                    E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 + kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
+                const float lb0 = A2 - E;  // lb(V) = lb0 - V * inv2s
                 // V >= T  <=>  lb = A2 - E - 2 V / scale <= U * kTie   (loosened by 2^-18 relative)
                 auto threshold = [&]() {
                     const float t = 0.5f * scale * (A2 - E - U * kTie);
@@ -567,38 +593,39 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const bool maxonly = wi.csr < 0;  // warm-up copy: bound only, no candidates
                 float T = (cutv > 0 && !maxonly) ? threshold() : __int_as_float(0x7f800000);
                 float vbest = -__int_as_float(0x7f800000);
-                // push every element of an 8-column group that passes the exact-bound test
-                auto slow8 = [&](const float *v, int col0, int lim) {
-                    unsigned mask = 0;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) mask |= (v[j] >= T ? 1u : 0u) << j;
-                    if (col0 + 8 > lim) mask &= lim > col0 ? (0xFFu >> (8 - (lim - col0))) : 0u;
-                    while (mask) {
-                        const int j = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        const float vj = pick8(v, j);
-                        const float lb = A2 - E - vj * inv2s;
-                        if (!(lb <= U * kTie)) continue;
-                        const float ub = lb + 2.0f * E;
-                        if (count == P.cap && !overflow) {
-                            // compact: drop entries that can no longer qualify
-                            int c2 = 0;
-                            for (int e = 0; e < count; ++e) {
-                                const float l2 = clb[e];
-                                if (l2 <= U * kTie) {
-                                    clb[c2] = l2;
-                                    cpos[c2] = cpos[e];
-                                    ++c2;
-                                }
+                // buffer a whole 8-column group (lower bounds; +inf beyond the row's cutoff) and
+                // tighten the bound with the group's best element; the exact re-rank filters
+                auto push8 = [&](const float *v, float m, int col0, int lim) {
+                    if (count == P.cap && !overflow) {
+                        // compact: drop groups none of whose elements can still qualify
+                        const float ut = U * kTie;
+                        int c2 = 0;
+                        for (int e = 0; e < count; ++e) {
+                            const float4 a = clb[2 * e], b = clb[2 * e + 1];
+                            const float lo = fminf(fminf(fminf(a.x, a.y), fminf(a.z, a.w)), fminf(fminf(b.x, b.y), fminf(b.z, b.w)));
+                            if (lo <= ut) {
+                                clb[2 * c2] = a;
+                                clb[2 * c2 + 1] = b;
+                                cpos[c2] = cpos[e];
+                                ++c2;
                             }
-                            count = c2;
-                            if (count == P.cap) overflow = true;
                         }
-                        if (!overflow) {
-                            clb[count] = lb;
-                            cpos[count] = wi.csr + col0 + j;
-                            ++count;
-                        }
+                        count = c2;
+                    }
+                    if (count < P.cap) {
+                        float l[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            l[j] = col0 + j < lim ? fmaf(-v[j], inv2s, lb0) : __int_as_float(0x7f800000);
+                        clb[2 * count] = make_float4(l[0], l[1], l[2], l[3]);
+                        clb[2 * count + 1] = make_float4(l[4], l[5], l[6], l[7]);
+                        cpos[count] = wi.csr + col0;
+                        ++count;
+                    } else {
+                        overflow = true;
+                    }
+                    if (col0 + 8 <= lim) {  // the group's best is a valid element: its ub bounds the k-th best
+                        const float ub = fmaf(-m, inv2s, lb0) + 2.0f * E;
                         if (KT == 1) {
                             U = fminf(U, ub);
                         } else {
@@ -629,12 +656,16 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         reinterpret_cast<float4 *>(g)[lane] = g0;
                     }
                     const uint32_t tb = ti & 1;
-                    sm100::mbar_wait(&tfull[tb], (ti >> 1) & 1);
+                    S2_WAIT(&tfull[tb], (ti >> 1) & 1, 5);
                     sm100::tc_fence_after();
                     __syncwarp();
                     // valid columns of this row, relative to this warp's half of the chunk
                     const int lim = min(min(cutv - off, n) - hb, kNmax / 2);
+#ifdef RBC_S2_NOEPI
+                    const int wlim = 0;  // diagnostic: pipeline without epilogue work (results invalid)
+#else
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
+#endif
                     const uint32_t tbase = tmem + tb * kNmax + hb + (static_cast<uint32_t>(quad * 32) << 16);
                     for (int c0 = 0; c0 < wlim; c0 += 64) {
                         uint32_t ra[32], rb[32];
@@ -661,14 +692,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                             m8[s] = max8(va + 8 * s);
                             m8[4 + s] = max8(vb + 8 * s);
                         }
-                        const float ma = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3]));
-                        const float mb = fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                        const float ma = sm100::fmax3(m8[0], m8[1], fmaxf(m8[2], m8[3]));
+                        const float mb = sm100::fmax3(m8[4], m8[5], fmaxf(m8[6], m8[7]));
                         if (KT == 1) {
                             // k = 1: a fully valid group's best element bounds the nearest candidate
                             const float mv = c0 + 64 <= lim ? fmaxf(ma, mb) : (c0 + 32 <= lim ? ma : -__int_as_float(0x7f800000));
                             if (mv > vbest) {
                                 vbest = mv;
-                                const float ub = A2 + E - mv * inv2s;
+                                const float ub = fmaf(-mv, inv2s, lb0) + 2.0f * E;
                                 if (ub < U) {
                                     U = ub;
                                     if (!maxonly) T = threshold();
@@ -679,8 +710,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                             const int base = off + hb + c0, llim = off + hb + lim;
 #pragma unroll
                             for (int s = 0; s < 4; ++s) {
-                                if (m8[s] >= T) slow8(va + 8 * s, base + 8 * s, llim);
-                                if (m8[4 + s] >= T) slow8(vb + 8 * s, base + 32 + 8 * s, llim);
+                                if (m8[s] >= T) push8(va + 8 * s, m8[s], base + 8 * s, llim);
+                                if (m8[4 + s] >= T) push8(vb + 8 * s, m8[4 + s], base + 32 + 8 * s, llim);
                             }
                         }
                     }
@@ -698,24 +729,35 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             }
         }
     }
+#ifdef RBC_S2_TIMING
+    if (P.timing && lane == 0 && (warp <= 1 || warp == 2)) {
+        // warp 0: producer, warp 1: MMA, warp 2: one epilogue warp (wait slots 0..5, 6 = role busy-until-exit)
+        tw[6] = clock64() - t_start;
+        for (int j = 0; j < 12; ++j)
+            if (tw[j]) atomicAdd(&P.timing[blockIdx.x * 12 + j], tw[j]);
+    }
+#endif
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 1) sm100::tmem_dealloc<512>(tmem);
 }
 
-// Exact re-rank (reference arithmetic) of the buffered candidates of both column
-// halves: one warp per query, one candidate per lane, warp merge of the lanes'
-// sorted key64 lists.
+// Exact re-rank (reference arithmetic) of the buffered candidate groups of both
+// column halves, one thread per query: the elements that can still qualify
+// (lb <= final bound) are compacted into a per-thread list first, so a warp
+// runs max(list length) exact distances with all 32 lanes busy.
+constexpr int kRerankThreads = 128;
+constexpr int kRerankGroups = 4;  // groups per sweep (list of up to 32 elements)
+
 template <int KT>
-__global__ void __launch_bounds__(256) rerank_kernel(const float *__restrict__ cand_lb,
+__global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__restrict__ cand_lb,
                                                      const int32_t *__restrict__ cand_pos,
                                                      const int32_t *__restrict__ cand_count,
                                                      const float *__restrict__ cand_ufin, int cap, int64_t nq,
                                                      const float *__restrict__ q, const float *__restrict__ xp,
                                                      const int32_t *__restrict__ perm, int d, int k,
                                                      uint64_t *__restrict__ out_keys) {
-    const int lane = threadIdx.x & 31;
-    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= nq) return;
     const int c0 = cand_count[2 * i], c1 = cand_count[2 * i + 1];
     if (c0 < 0 || c1 < 0) return;  // overflowed: recomputed by the exact scan
@@ -724,15 +766,28 @@ __global__ void __launch_bounds__(256) rerank_kernel(const float *__restrict__ c
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-    for (int e = lane; e < c0 + c1; e += 32) {
-        const int64_t at = e < c0 ? (2 * i) * cap + e : (2 * i + 1) * cap + (e - c0);
-        if (!(cand_lb[at] <= ufin)) continue;
-        const int32_t pos = cand_pos[at];
-        const float dist = exact_dist<RBC_L2>(qrow, xp + static_cast<int64_t>(pos) * d, d);
-        const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos]));
-        if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+    const int n = c0 + c1;
+    for (int g0 = 0; g0 < n; g0 += kRerankGroups) {
+        int32_t list[8 * kRerankGroups];
+        int m = 0;
+        const int g1 = min(n, g0 + kRerankGroups);
+        for (int g = g0; g < g1; ++g) {
+            const int64_t at = g < c0 ? (2 * i) * cap + g : (2 * i + 1) * cap + (g - c0);
+            const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
+            const int32_t pos = cand_pos[at];
+            const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (l[j] <= ufin) list[m++] = pos + j;
+        }
+        for (int t = 0; t < m; ++t) {
+            const int32_t pos = list[t];
+            const float dist = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pos) * d, d);
+            const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos]));
+            if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+        }
     }
-    warp_merge_sorted<KT>(best, k, out_keys + i * k);
+    for (int j = 0; j < k && j < KT; ++j) out_keys[i * k + j] = best[j];
 }
 __global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
                                          float *__restrict__ out) {
@@ -940,10 +995,10 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                              tile_order.get(), ntiles, 0, 40, st));
     note_launch();
     // 3. the tensor-core scan
-    const int cap = 48 + 16 * k;  // per query and column half
+    const int cap = 16 + 8 * k;  // 8-column groups per query and column half
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, cand_count, ovf_list, counters;
-    RBC_CHECK(cand_lb.alloc(nq * 2 * cap, st));
+    RBC_CHECK(cand_lb.alloc(nq * 2 * cap * 8, st));
     RBC_CHECK(cand_pos.alloc(nq * 2 * cap, st));
     RBC_CHECK(cand_count.alloc(nq * 2, st));
     RBC_CHECK(cand_ufin.alloc(nq * 2, st));
@@ -983,6 +1038,15 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.overflow_count = counters.get();
     P.tile_counter = counters.get() + 1;
     P.cap_work = cap_work;
+    DevBuf<unsigned long long> timing;
+    P.timing = nullptr;
+#ifdef RBC_S2_TIMING
+    if (getenv("RBC_DEBUG_S2")) {
+        RBC_CHECK(timing.alloc(148 * 12, st));
+        RBC_CUDA(cudaMemsetAsync(timing.get(), 0, sizeof(unsigned long long) * 148 * 12, st));
+        P.timing = timing.get();
+    }
+#endif
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1003,10 +1067,12 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_LAUNCHED();
     // 4. exact re-rank of the buffered candidates
     {
-        const unsigned rgrid = grid_for(nq * 32, 256);
+        const unsigned rgrid = grid_for(nq, kRerankThreads);
 #define RBC_RERANK(KT)                                                                                              \
-    rerank_kernel<KT><<<rgrid, 256, 0, st>>>(cand_lb.get(), cand_pos.get(), cand_count.get(), cand_ufin.get(), cap, \
-                                             nq, q, idx->xp, idx->perm, idx->d, k, keys)
+    rerank_kernel<KT><<<rgrid, kRerankThreads, 0, st>>>(reinterpret_cast<const float4 *>(cand_lb.get()),           \
+                                                        cand_pos.get(), cand_count.get(),                           \
+                                                        cand_ufin.get(), cap, nq, q, idx->xp, idx->perm, idx->d, k, \
+                                                        keys)
         if (k == 1) RBC_RERANK(1);
         else if (k <= 4) RBC_RERANK(4);
         else if (k <= 8) RBC_RERANK(8);
@@ -1028,6 +1094,40 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     }
     stage2_status_kernel<<<1, 1, 0, st>>>(work_off.get(), ntiles, counters.get(), status_dev);
     RBC_LAUNCHED();
+    if (getenv("RBC_DEBUG_S2")) {  // diagnostic: buffered-candidate statistics (synchronises)
+        std::vector<int32_t> cc(nq * 2);
+        std::vector<float> lb(nq * 2 * cap * 8), uf(nq * 2);
+        cudaMemcpyAsync(cc.data(), cand_count.get(), sizeof(int32_t) * nq * 2, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(lb.data(), cand_lb.get(), sizeof(float) * nq * 2 * cap * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(uf.data(), cand_ufin.get(), sizeof(float) * nq * 2, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        double tot = 0, pass = 0;
+        int mx = 0, ovf = 0;
+        for (int64_t i = 0; i < nq; ++i) {
+            const float u = fminf(uf[2 * i], uf[2 * i + 1]);
+            for (int h = 0; h < 2; ++h) {
+                const int c = cc[2 * i + h];
+                if (c < 0) { ++ovf; continue; }
+                tot += c;
+                mx = c > mx ? c : mx;
+                for (int e = 0; e < c * 8; ++e) pass += lb[(2 * i + h) * cap * 8 + e] <= u;
+            }
+        }
+#ifdef RBC_S2_TIMING
+        std::vector<unsigned long long> tm(148 * 12);
+        cudaMemcpy(tm.data(), timing.get(), sizeof(unsigned long long) * 148 * 12, cudaMemcpyDeviceToHost);
+        double sum[12] = {0};
+        for (int b = 0; b < (int)grid; ++b)
+            for (int j = 0; j < 12; ++j) sum[j] += tm[b * 12 + j];
+        const char *nm[12] = {"prod:empty", "mma:afull", "mma:full", "mma:tempty", "epi:aempty", "epi:tfull",
+                              "wall(3 roles)", "-", "epi:prep", "-", "-", "epi:lists#"};
+        fprintf(stderr, "[s2] per-CTA cycles:");
+        for (int j = 0; j < 12; ++j) fprintf(stderr, " %s=%.0f", nm[j], sum[j] / grid / (j == 6 ? 3.0 : 1.0));
+        fprintf(stderr, "\n");
+#endif
+        fprintf(stderr, "[s2] nq=%lld buffered groups/query %.2f (max per half %d, cap %d), passing/query %.2f, overflow halves %d\n",
+                (long long)nq, tot / nq, mx, cap, pass / nq, ovf);
+    }
     return RBC_OK;
 }
 

@@ -399,7 +399,7 @@ def test_tc_engine_wide_tile_unions(rbc, oracle, k):
 def test_tc_engine_overflow_fallback(rbc):
     from paper_1103_2635_b200 import _lib
 
-    base = np.repeat(uniform(40, 8, 3), 300, axis=0)  # 300 exact copies of each point
+    base = np.repeat(uniform(20, 8, 3), 2000, axis=0)  # 2000 exact copies of each point: ties overflow the buffer
     idx = rbc.build_exact(rbc.DataMatrix(base), 30, rbc.MetricSpec("l2", 8), seed=0)
     q = base[::997][:12]
     fast, exact = _both_engines(rbc, idx, q, 1)
