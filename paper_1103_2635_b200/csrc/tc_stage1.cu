@@ -46,7 +46,7 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kN = 128;        // representatives per chunk (UMMA N)
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kVStride = 68;  // floats per row of the slow-path value stage (16-byte aligned, bank-spread)
 constexpr int kThreads = 192;  // producer, MMA, 4 epilogue warps
 constexpr int kP0 = 128, kP1 = 32;
@@ -64,6 +64,7 @@ constexpr float kC4 = 1.0f / 262144.0f;
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;
 constexpr float kTie = 1.0f + 1.0f / 524288.0f;
 constexpr float kEps = 1.0f / 262144.0f;  // relative slack of the interval classification
+constexpr float kCq = 1.0f / 65536.0f;    // fp32 |q - c|^2 (<= 66 ulps) and its square root
 
 struct Tc1Index {
     int64_t nrpad = 0;
@@ -312,15 +313,17 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
     float *s_radii = reinterpret_cast<float *>(sA + 2 * kABytes);  // [nr]
     float *s_red = s_radii + ((P.nr + 3) & ~int64_t(3));            // [4] tile max of |q - c|
     float *s_v = s_red + 4;                                          // [128][kVStride] slow-path value stage
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_v + kRows * kVStride);
+    float *s_q = s_v + kRows * kVStride;                             // [128][kVStride] the tile's query rows
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_q + kRows * kVStride);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
     uint64_t *afull = tempty + 2, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
+    uint64_t *qfull = tile_empty + 2, *qempty = qfull + 1;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(qempty + 1);
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #ifdef RBC_S1_TIMING
-    unsigned long long tw[12] = {};
+    unsigned long long tw[14] = {};
     const unsigned long long t_start = clock64();
 #endif
     for (int64_t p = tid; p < P.nr; p += blockDim.x) s_radii[p] = P.radii[p];
@@ -337,6 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             sm100::mbar_init(&tile_full[b], 1);
             sm100::mbar_init(&tile_empty[b], 5);
         }
+        sm100::mbar_init(qfull, 1);
+        sm100::mbar_init(qempty, 4);
         sm100::fence_barrier_init();
     }
     if (warp == 1) sm100::tmem_alloc<256>(s_tmem);
@@ -347,17 +352,32 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
     const int nchunks = static_cast<int>((P.nr + kN - 1) / kN);
 
     if (warp == 0) {
-        // ===== scheduler + producer: both passes stream all representatives =====
-        if (lane == 0) {
-            uint32_t bi = 0;
-            for (uint32_t it = 0;; ++it) {
-                const uint32_t slot = it & 1;
+        // ===== scheduler + producer: the tile's query rows (gathered through qorder, one
+        // 256-byte bulk copy per row, all lanes), then both passes of the representatives =====
+        uint32_t bi = 0;
+        for (uint32_t it = 0;; ++it) {
+            const uint32_t slot = it & 1;
+            int tile = 0;
+            if (lane == 0) {
                 S1_WAIT(&tile_empty[slot], ((it >> 1) & 1) ^ 1, 0);
                 const int t = atomicAdd(P.tile_counter, 1);
-                const int tile = t < P.ntiles ? t : -1;
+                tile = t < P.ntiles ? t : -1;
                 s_tiles[slot] = tile;
                 sm100::mbar_arrive(&tile_full[slot]);
-                if (tile < 0) break;
+            }
+            tile = __shfl_sync(0xffffffffu, tile, 0);
+            if (tile < 0) break;
+            if (lane == 0) {
+                sm100::mbar_wait(qempty, (it & 1) ^ 1);
+                sm100::mbar_arrive_expect_tx(qfull, kRows * 256);
+            }
+            __syncwarp();
+            for (int r = lane; r < kRows; r += 32) {
+                const int64_t slot_i = static_cast<int64_t>(tile) * kRows + r;
+                const int64_t qi = P.qorder[slot_i < P.nq ? slot_i : P.nq - 1];
+                sm100::bulk_g2s(s_q + r * kVStride, P.q64 + qi * 64, 256, qfull);
+            }
+            if (lane == 0) {
                 const uint32_t bytes = P.plane1 ? kStageBytes : kN * kP0;
                 for (int pass = 0; pass < 2; ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
@@ -369,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                         ++bi;
                     }
             }
+            __syncwarp();
         }
     } else if (warp == 1) {
         // ===== MMA issuer: 4 x K16 over plane 0 (+ the aug plane) =====
@@ -426,26 +447,30 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             const int64_t slot_i = static_cast<int64_t>(tile) * kRows + row;
             const bool live = slot_i < P.nq;
             const int64_t qi = live ? P.qorder[slot_i] : 0;
-            // (q - c), |q - c|^2 in fp64, tile scale sA
+            // (q - c) from the staged row, |q - c|^2 (fp32: relative error <= 66 * 2^-24, covered by kCq)
             float qv[64];
-            double qn64 = 0.0;
+            float qn;
             {
-                const float4 *src = reinterpret_cast<const float4 *>(P.q64 + (live ? qi : 0) * 64);
+                S1_WAIT(qfull, it & 1, 10);
+                const float4 *src = reinterpret_cast<const float4 *>(s_q + row * kVStride);
                 const float4 *cc = reinterpret_cast<const float4 *>(P.c64);
+                float n0 = 0.f, n1 = 0.f;
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
                     const float4 m = __ldg(cc + c);
-                    const float4 t = live ? __ldg(src + c) : m;
+                    const float4 t = live ? src[c] : m;
                     qv[4 * c] = __fsub_rn(t.x, m.x);
                     qv[4 * c + 1] = __fsub_rn(t.y, m.y);
                     qv[4 * c + 2] = __fsub_rn(t.z, m.z);
                     qv[4 * c + 3] = __fsub_rn(t.w, m.w);
+                    n0 = fmaf(qv[4 * c], qv[4 * c], fmaf(qv[4 * c + 1], qv[4 * c + 1], n0));
+                    n1 = fmaf(qv[4 * c + 2], qv[4 * c + 2], fmaf(qv[4 * c + 3], qv[4 * c + 3], n1));
                 }
-#pragma unroll
-                for (int c = 0; c < 64; ++c) qn64 += static_cast<double>(qv[c]) * qv[c];
+                qn = n0 + n1;
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(qempty);
             }
-            const float qn = static_cast<float>(qn64);
-            const float nqv = sqrtf(qn) * kUp;
+            const float nqv = sqrtf(qn) * (1.0f + kCq);
             float tmax = nqv;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
@@ -475,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                 ++ai;
             }
             const float rb = P.rmax;
-            const float E = kC1 * nqv * rb + kC2 * (qn + rb * rb) + kC4 * rb * (2.0f / sa) + 1e-30f;
+            const float E = kC1 * nqv * rb + kC2 * (qn + rb * rb) + kCq * qn + kC4 * rb * (2.0f / sa) + 1e-30f;
 
             // ---------- pass 1: bound and collect the gamma candidates ----------
             // Every rep with lb <= U (U = running k-th smallest upper bound) is buffered;
@@ -541,43 +566,48 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                             const int s = __ffs(gm) - 1;
                             gm &= gm - 1;
                             const int g0 = off + c0 + 8 * s;
-#pragma unroll 1
+                            const float4 xa = reinterpret_cast<const float4 *>(sv)[2 * s];
+                            const float4 xb = reinterpret_cast<const float4 *>(sv)[2 * s + 1];
+                            const float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                            if (count + 8 > P.cap1) {  // compact: drop entries that can no longer qualify
+                                int c2 = 0;
+                                for (int e = 0; e < count; ++e)
+                                    if (clb[e] <= U * kTie) {
+                                        clb[c2] = clb[e];
+                                        cp[c2] = cp[e];
+                                        ++c2;
+                                    }
+                                count = c2;
+                                if (count + 8 > P.cap1) {
+                                    fail = true;
+                                    continue;
+                                }
+                            }
+#pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const float x = sv[8 * s + j];
-                                if (!(x >= T) || g0 + j >= P.nr) continue;
-                                const float lb = fmaf(-x, inv2s, lb0);
-                                if (count == P.cap1) {  // compact: drop entries that can no longer qualify
-                                    int c2 = 0;
-                                    for (int e = 0; e < count; ++e)
-                                        if (clb[e] <= U * kTie) {
-                                            clb[c2] = clb[e];
-                                            cp[c2] = cp[e];
-                                            ++c2;
+                                if (x[j] >= T && g0 + j < P.nr) {
+                                    const float lb = fmaf(-x[j], inv2s, lb0);
+                                    clb[count] = lb;
+                                    cp[count] = g0 + j;
+                                    ++count;
+                                    if (KT > 1) {
+                                        float y = lb + 2.0f * E;
+#pragma unroll
+                                        for (int t = 0; t < KT; ++t) {
+                                            const float lo = fminf(ubk[t], y), hi = fmaxf(ubk[t], y);
+                                            ubk[t] = lo;
+                                            y = hi;
                                         }
-                                    count = c2;
-                                    if (count == P.cap1) {
-                                        fail = true;
-                                        continue;
                                     }
                                 }
-                                clb[count] = lb;
-                                cp[count] = g0 + j;
-                                ++count;
-                                if (KT > 1) {
-                                    float y = lb + 2.0f * E;
+                            }
+                            if (KT > 1) {
+                                float kth = ubk[0];
 #pragma unroll
-                                    for (int t = 0; t < KT; ++t) {
-                                        const float lo = fminf(ubk[t], y), hi = fmaxf(ubk[t], y);
-                                        ubk[t] = lo;
-                                        y = hi;
-                                    }
-                                    float kth = ubk[0];
-#pragma unroll
-                                    for (int t = 0; t < KT; ++t)
-                                        if (t == P.k - 1) kth = ubk[t];
-                                    U = fminf(U, kth);
-                                    T = threshold();
-                                }
+                                for (int t = 0; t < KT; ++t)
+                                    if (t == P.k - 1) kth = ubk[t];
+                                U = fminf(U, kth);
+                                T = threshold();
                             }
                         }
                         __syncwarp();
@@ -642,13 +672,15 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                             const int s = __ffs(gm) - 1;
                             gm &= gm - 1;
                             const int g0 = c0 + 8 * s;
-#pragma unroll 1
+                            const float4 xa = reinterpret_cast<const float4 *>(sv)[2 * s];
+                            const float4 xb = reinterpret_cast<const float4 *>(sv)[2 * s + 1];
+                            const float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const float x = sv[8 * s + j];
-                                if (x >= Tf && g0 + j < lim) {
+                                if (x[j] >= Tf && g0 + j < lim) {
                                     if (rc < P.cap_rec) {
                                         rec[rc] = off + g0 + j;
-                                        rdt[rc] = fmaf(-x, inv2s, qn);
+                                        rdt[rc] = fmaf(-x[j], inv2s, qn);
                                     }
                                     ++rc;
                                     --pr;
@@ -680,8 +712,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
     }
 #ifdef RBC_S1_TIMING
     if (P.timing && lane == 0 && warp <= 2) {
-        tw[10 + (warp == 2 ? 1 : 0)] = clock64() - t_start;  // wall of MMA / epilogue warp
-        for (int j = 0; j < 12; ++j)
+        tw[12 + (warp == 2 ? 1 : 0)] = clock64() - t_start;  // wall of MMA / epilogue warp
+        for (int j = 0; j < 14; ++j)
             if (tw[j]) atomicAdd(&P.timing[j], tw[j]);
     }
 #endif
@@ -852,8 +884,8 @@ __global__ void __launch_bounds__(kFixThreads) stage1_fixup_kernel(
 
 // dynamic shared memory: stages, A buffers, radii[nr], reduction slots, barriers
 inline size_t s1_smem_bytes(int64_t nr) {
-    return 1024 + kStages * kStageBytes + 2 * kABytes + (((nr + 3) & ~int64_t(3)) + 4 + kRows * kVStride) * sizeof(float) +
-           256;
+    return 1024 + kStages * kStageBytes + 2 * kABytes +
+           (((nr + 3) & ~int64_t(3)) + 4 + 2 * kRows * kVStride) * sizeof(float) + 256;
 }
 
 }  // namespace
@@ -1029,8 +1061,8 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
 #ifdef RBC_S1_TIMING
     DevBuf<unsigned long long> timing;
     if (getenv("RBC_DEBUG_S1")) {
-        RBC_CHECK(timing.alloc(12, st));
-        RBC_CUDA(cudaMemsetAsync(timing.get(), 0, sizeof(unsigned long long) * 12, st));
+        RBC_CHECK(timing.alloc(14, st));
+        RBC_CUDA(cudaMemsetAsync(timing.get(), 0, sizeof(unsigned long long) * 14, st));
         P.timing = timing.get();
     }
 #endif
@@ -1041,12 +1073,13 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_LAUNCHED();
 #ifdef RBC_S1_TIMING
     if (P.timing) {
-        unsigned long long h[12];
+        unsigned long long h[14];
         cudaMemcpy(h, P.timing, sizeof(h), cudaMemcpyDeviceToHost);
-        const char *nm[12] = {"prod:tile_empty", "prod:empty", "mma:tile_full", "mma:afull", "mma:full", "mma:tempty",
-                              "epi:tile_full", "epi:aempty", "epi:tfull1", "epi:tfull2", "wall:mma", "wall:epi"};
+        const char *nm[14] = {"prod:tile_empty", "prod:empty", "mma:tile_full", "mma:afull", "mma:full", "mma:tempty",
+                              "epi:tile_full", "epi:aempty", "epi:tfull1", "epi:tfull2", "epi:qfull", "-",
+                              "wall:prod+mma", "wall:epi"};
         fprintf(stderr, "[s1] per-CTA cycles (grid %u):", grid);
-        for (int j = 0; j < 12; ++j) fprintf(stderr, " %s=%.0f", nm[j], double(h[j]) / grid);
+        for (int j = 0; j < 14; ++j) fprintf(stderr, " %s=%.0f", nm[j], double(h[j]) / grid);
         fprintf(stderr, "\n");
     }
 #endif

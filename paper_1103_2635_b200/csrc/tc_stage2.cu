@@ -595,23 +595,23 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 float vbest = -__int_as_float(0x7f800000);
                 // buffer a whole 8-column group (lower bounds; +inf beyond the row's cutoff) and
                 // tighten the bound with the group's best element; the exact re-rank filters
-                auto push8 = [&](const float *v, float m, int col0, int lim) {
-                    if (count == P.cap && !overflow) {
-                        // compact: drop groups none of whose elements can still qualify
-                        const float ut = U * kTie;
-                        int c2 = 0;
-                        for (int e = 0; e < count; ++e) {
-                            const float4 a = clb[2 * e], b = clb[2 * e + 1];
-                            const float lo = fminf(fminf(fminf(a.x, a.y), fminf(a.z, a.w)), fminf(fminf(b.x, b.y), fminf(b.z, b.w)));
-                            if (lo <= ut) {
-                                clb[2 * c2] = a;
-                                clb[2 * c2 + 1] = b;
-                                cpos[c2] = cpos[e];
-                                ++c2;
-                            }
+                // compact the buffer once per 64-column block when it could fill up
+                auto compact = [&]() {
+                    const float ut = U * kTie;
+                    int c2 = 0;
+                    for (int e = 0; e < count; ++e) {
+                        const float4 a = clb[2 * e], b = clb[2 * e + 1];
+                        const float lo = fminf(fminf(fminf(a.x, a.y), fminf(a.z, a.w)), fminf(fminf(b.x, b.y), fminf(b.z, b.w)));
+                        if (lo <= ut) {
+                            clb[2 * c2] = a;
+                            clb[2 * c2 + 1] = b;
+                            cpos[c2] = cpos[e];
+                            ++c2;
                         }
-                        count = c2;
                     }
+                    count = c2;
+                };
+                auto push8 = [&](const float *v, float m, int col0, int lim) {
                     if (count < P.cap) {
                         float l[8];
 #pragma unroll
@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                             }
                         }
                         if (fmaxf(ma, mb) >= T) {
+                            if (count + 8 > P.cap && !overflow) compact();
                             const int base = off + hb + c0, llim = off + hb + lim;
 #pragma unroll
                             for (int s = 0; s < 4; ++s) {
