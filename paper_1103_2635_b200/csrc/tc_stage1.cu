@@ -258,19 +258,26 @@ __global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict_
     for (int c = 0; c < 16; ++c) qv[c] = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
     float best = __int_as_float(0x7f800000);
     int bj = 0;
-    for (int j = 0; j < npilot; ++j) {
-        float a0 = 0.f, a1 = 0.f;
+    // four pilots per sweep: eight independent accumulation chains
+    for (int j0 = 0; j0 < npilot; j0 += 4) {
+        float a[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-            const float4 r = sp[j * 16 + c];
-            const float t0 = qv[c].x - r.x, t1 = qv[c].y - r.y, t2 = qv[c].z - r.z, t3 = qv[c].w - r.w;
-            a0 = fmaf(t0, t0, fmaf(t1, t1, a0));
-            a1 = fmaf(t2, t2, fmaf(t3, t3, a1));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float4 r = sp[((j0 + u) & (kPilots - 1)) * 16 + c];
+                const float t0 = qv[c].x - r.x, t1 = qv[c].y - r.y, t2 = qv[c].z - r.z, t3 = qv[c].w - r.w;
+                a[u][0] = fmaf(t0, t0, fmaf(t1, t1, a[u][0]));
+                a[u][1] = fmaf(t2, t2, fmaf(t3, t3, a[u][1]));
+            }
         }
-        const float dd = a0 + a1;
-        if (dd < best) {
-            best = dd;
-            bj = j;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float dd = a[u][0] + a[u][1];
+            if (j0 + u < npilot && dd < best) {
+                best = dd;
+                bj = j0 + u;
+            }
         }
     }
     key[i] = static_cast<uint32_t>(bj);
@@ -760,10 +767,10 @@ __device__ __forceinline__ float approx_dist64(const float4 (&qv)[16], const flo
 // stats.  Each thread first compacts its own candidates into a local list, so a
 // warp runs max(list length) exact distances with all lanes busy.
 constexpr int kFixThreads = 128;
-constexpr int kFixList = 64;  // per-thread gamma-candidate list (more: a second sweep)
+constexpr int kFixList = 16;  // per-thread gamma-candidate list (more: further sweeps)
 
 template <int KT>
-__global__ void __launch_bounds__(kFixThreads) stage1_fixup_kernel(
+__global__ void __launch_bounds__(kFixThreads, 4) stage1_fixup_kernel(
     const float *__restrict__ q64, const int32_t *__restrict__ qorder, const float *__restrict__ reps64, int64_t nq,
     int k, const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
     const float *__restrict__ lskip, const float *__restrict__ c1_lb, const int32_t *__restrict__ c1_p, int cap1,

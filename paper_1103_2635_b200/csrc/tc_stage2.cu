@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
-    if (qi >= 0)
+    if (qi >= 0)  // benign races: every writer stores 1
         for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) present[seg_list[s]] = 1;
     __syncthreads();
     int c = 0;
@@ -269,13 +269,28 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
-    if (qi >= 0) {
-        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) {
-            const int32_t p = seg_list[s];
-            atomicMax(&maxlen[p], seg_len[s]);
-            atomicMax(&maxd1[p], __float_as_int(seg_d1[s]));
+    {
+        // warp-aggregated shared-memory atomics: the rows of a tile mostly share their
+        // lists (segments ascend by list), so lanes holding the same list combine first
+        const int lane = threadIdx.x & 31;
+        const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
+        const int cnt = qi >= 0 ? seg_cnt[qi] : 0;
+        const int wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
+        for (int it = 0; it < wmax; ++it) {
+            const bool has = it < cnt;
+            const int32_t p = has ? seg_list[s0 + it] : -1;
+            const unsigned len = has ? static_cast<unsigned>(seg_len[s0 + it]) : 0u;
+            const unsigned d1b = has ? __float_as_uint(seg_d1[s0 + it]) : 0u;
+            const unsigned grp = __match_any_sync(0xffffffffu, p);
+            const unsigned mlen = __reduce_max_sync(grp, len), md1 = __reduce_max_sync(grp, d1b);
+            if (has && lane == __ffs(grp) - 1) {
+                atomicMax(&maxlen[p], static_cast<int>(mlen));
+                atomicMax(&maxd1[p], static_cast<int>(md1));
+            }
         }
-        atomicAdd(&nearcnt[order_key[qi] & 0xFFFFFF], 1);
+        const int32_t nr_near = qi >= 0 ? static_cast<int32_t>(order_key[qi] & 0xFFFFFF) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, nr_near);
+        if (qi >= 0 && lane == __ffs(grp) - 1) atomicAdd(&nearcnt[nr_near], __popc(grp));
     }
     __syncthreads();
     // front list = the most common nearest rep of the tile (ties: lowest position)
