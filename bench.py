@@ -86,12 +86,16 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return
-        # NVML start-up takes driver locks that stall CUDA calls: keep it out of the
-        # timed region by waiting for the first sample
+        # NVML start-up takes driver locks that stall CUDA calls (a ~1 s hiccup was
+        # seen inside a timed step): keep it out of the timed region by waiting for
+        # several samples before returning
         t0 = time.time()
-        while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
-            time.sleep(0.02)
-        time.sleep(0.05)
+        while time.time() - t0 < 8.0:
+            with open(self.path) as f:
+                if sum(1 for _ in f) >= 3:
+                    break
+            time.sleep(0.05)
+        time.sleep(0.2)
 
     def stop(self):
         if self.proc is None:

@@ -55,10 +55,14 @@ namespace rbc {
 namespace {
 
 constexpr int kRows = 128;       // queries per tile = UMMA M = TMEM lanes
-constexpr int kNmax = 256;       // max UMMA N per chunk
+constexpr int kNmax = 256;       // max UMMA N per chunk (N = 256 keeps the single MMA thread compute-bound)
+constexpr int kAcc = 2;          // TMEM accumulator stages (2 x 256 columns)
 constexpr int kStages = 4;       // B ring depth
-constexpr int kThreads = 320;    // 10 warps: producer, MMA, 8 epilogue
-constexpr int kEpiWarps = 8;
+constexpr int kParts = 2;        // epilogue warps per TMEM lane quadrant (column halves / K halves)
+constexpr int kEpiWarps = 4 * kParts;
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 16 epilogue warps
+constexpr int kCols = kNmax / kParts;          // columns of each chunk per epilogue warp
+constexpr int kKd = 64 / kParts;               // A-operand dims per epilogue warp
 constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
 constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
 constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
@@ -380,9 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     uint8_t *sB = smem;                                   // kStages x (plane 0 | plane 1)
     uint8_t *sA = sB + kStages * kStageBytes;             // 2 x (plane 0 | plane 1)
     float *gbuf = reinterpret_cast<float *>(sA + 2 * kABytes);  // 8 epilogue warps x 128 (fallback column)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + kEpiWarps * (kNmax / 2));
-    uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
-    uint64_t *afull = tempty + 2, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + kEpiWarps * kCols);
+    uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + kAcc;
+    uint64_t *afull = tempty + kAcc, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);  // 2-slot ring of tile ids
 
@@ -459,9 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
                     for (int off = 0; off < ext; off += kNmax) {
                         const int n = min(kNmax, roundup16(ext - off));
-                        const uint32_t s = bi % kStages, tb = ti & 1;
+                        const uint32_t s = bi % kStages, tb = ti % kAcc;
                         S2_WAIT(&full[s], (bi / kStages) & 1, 2);
-                        S2_WAIT(&tempty[tb], ((ti >> 1) & 1) ^ 1, 3);
+                        S2_WAIT(&tempty[tb], ((ti / kAcc) & 1) ^ 1, 3);
                         sm100::tc_fence_after();
                         const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
                         const uint32_t b0 = sm100::smem_u32(sB + s * kStageBytes);
@@ -484,13 +488,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             }
         }
     } else {
-        // ===== epilogue warps (2 per TMEM lane quadrant): A prep + filter + candidate buffer =====
-        // warp pair (quad, half): rows quad*32 .. +31, columns [half*128, half*128+128) of every
-        // 256-column chunk, K range [half*32, half*32+32) of the A operand.
+        // ===== epilogue warps (kParts per TMEM lane quadrant): A prep + filter + candidate buffer =====
+        // warp (quad, part): rows quad*32 .. +31, columns [part*kCols, +kCols) of every 256-column
+        // chunk (two 32-column halves), K range [part*kKd, +kKd) of the A operand.
         const int quad = warp & 3;
-        const int half = (warp - 2) >> 2;
+        const int part = (warp - 2) >> 2;
         const int row = quad * 32 + lane;
-        float *g = gbuf + (warp - 2) * (kNmax / 2);
+        float *g = gbuf + (warp - 2) * kCols;
         uint32_t ti = 0, ai = 0;
         for (uint32_t it = 0;; ++it) {
             const uint32_t slot = it & 1;
@@ -501,13 +505,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             if (tile < 0) break;
             const int32_t qi = P.tile_rows[tile * kRows + row];
             const bool live = qi >= 0;
-            // this thread's half of the query row (rows padded to 64 floats with zeros)
-            float qv[32];
+            // this thread's quarter of the query row (rows padded to 64 floats with zeros)
+            float qv[kKd];
             {
                 const float4 *src =
-                    reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(live ? qi : 0) * 64 + half * 32);
+                    reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(live ? qi : 0) * 64 + part * kKd);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < kKd / 4; ++c) {
                     const float4 t = live ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                     qv[4 * c] = t.x;
                     qv[4 * c + 1] = t.y;
@@ -516,15 +520,15 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 }
             }
             const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
-            // A operand of list w: this thread's 64 bytes of row `row` (+ the aug columns on half 1)
+            // A operand of list w: this thread's kKd * 2 bytes of row `row` (+ the aug columns, last part)
             auto prep_a = [&](int64_t w) {
                 S2_TIME(const unsigned long long tp0 = clock64());
                 S2_TIME(++tw[11]);
                 const WorkItem wi = P.work[w];
-                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64 + half * 32);
-                float4 rr4[8];
+                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64 + part * kKd);
+                float4 rr4[kKd / 4];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) rr4[c] = __ldg(rep4 + c);
+                for (int c = 0; c < kKd / 4; ++c) rr4[c] = __ldg(rep4 + c);
                 const __half ac = __float2half_rn(wi.aug);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 const float sa = wi.sA;
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < kKd / 8; ++c) {
                     const float rr[8] = {rr4[2 * c].x, rr4[2 * c].y, rr4[2 * c].z, rr4[2 * c].w,
                                          rr4[2 * c + 1].x, rr4[2 * c + 1].y, rr4[2 * c + 1].z, rr4[2 * c + 1].w};
                     uint32_t wv[4];
@@ -543,11 +547,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         const float v1 = fmaf(qv[k0 + 1], sa, -(rr[2 * e + 1] * sa));
                         wv[e] = sm100::pack_f16x2_sat(v0, v1);
                     }
-                    const int cc = half * 4 + c;
+                    const int cc = part * (kKd / 8) + c;
                     if (!P.plane1 && cc == 7) wv[3] = aug;
                     *reinterpret_cast<uint4 *>(dst + ((cc ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                 }
-                if (P.plane1 && half == 1) {
+                if (P.plane1 && part == kParts - 1) {
                     uint8_t *d1p = sA + a * kABytes + kRows * kP0 + row * kP1;
                     const int sw = (row >> 2) & 1;
                     *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             float U = u_init;  // running upper bound of the k-th smallest candidate d^2
             int count = 0;     // buffered 8-column groups
             bool overflow = false;
-            const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * 2 + half);
+            const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * kParts + part);
             float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 2;
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
@@ -608,9 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const bool maxonly = wi.csr < 0;  // warm-up copy: bound only, no candidates
                 float T = (cutv > 0 && !maxonly) ? threshold() : __int_as_float(0x7f800000);
                 float vbest = -__int_as_float(0x7f800000);
-                // buffer a whole 8-column group (lower bounds; +inf beyond the row's cutoff) and
-                // tighten the bound with the group's best element; the exact re-rank filters
-                // compact the buffer once per 64-column block when it could fill up
+                // compact the buffer (once per 32-column half) when it could fill up
                 auto compact = [&]() {
                     const float ut = U * kTie;
                     int c2 = 0;
@@ -626,6 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     }
                     count = c2;
                 };
+                // buffer a whole 8-column group (lower bounds; +inf beyond the row's cutoff) and
+                // tighten the bound with the group's best element; the exact re-rank filters
                 auto push8 = [&](const float *v, float m, int col0, int lim) {
                     if (count < P.cap) {
                         float l[8];
@@ -662,73 +666,69 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 };
                 for (int off = 0; off < wi.ext; off += kNmax) {
                     const int n = min(kNmax, roundup16(wi.ext - off));
-                    const int hb = half * (kNmax / 2);  // this warp's first column in the chunk
+                    const int hb = part * kCols;  // this warp's first column in the chunk
                     if (noaug) {
                         // rare: per-column norm term subtracted here instead of in the MMA
                         const float *src = P.gcol + wi.poff + off + hb;
-                        float4 g0 = make_float4(0, 0, 0, 0);
-                        if (hb + lane * 4 < n) g0 = *reinterpret_cast<const float4 *>(src + lane * 4);
-                        reinterpret_cast<float4 *>(g)[lane] = g0;
+                        for (int c = lane; c < kCols; c += 32) g[c] = hb + c < n ? src[c] : 0.f;
                     }
-                    const uint32_t tb = ti & 1;
-                    S2_WAIT(&tfull[tb], (ti >> 1) & 1, 5);
+                    const uint32_t tb = ti % kAcc;
+                    S2_WAIT(&tfull[tb], (ti / kAcc) & 1, 5);
                     sm100::tc_fence_after();
                     __syncwarp();
-                    // valid columns of this row, relative to this warp's half of the chunk
-                    const int lim = min(min(cutv - off, n) - hb, kNmax / 2);
+                    // valid columns of this row, relative to this warp's part of the chunk
+                    const int lim = min(min(cutv - off, n) - hb, kCols);
 #ifdef RBC_S2_NOEPI
                     const int wlim = 0;  // diagnostic: pipeline without epilogue work (results invalid)
 #else
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
 #endif
                     const uint32_t tbase = tmem + tb * kNmax + hb + (static_cast<uint32_t>(quad * 32) << 16);
-                    for (int c0 = 0; c0 < wlim; c0 += 64) {
-                        uint32_t ra[32], rb[32];
+                    for (int c0 = 0; c0 < wlim; c0 += 32) {
+                        uint32_t ra[32];
                         sm100::tmem_ld32_async(tbase + c0, ra);
-                        sm100::tmem_ld32_async(tbase + c0 + 32, rb);
                         sm100::tmem_wait_ld(ra);
-                        sm100::tmem_tie(rb);
-                        float va[32], vb[32];
+#if defined(RBC_S2_LEVEL) && RBC_S2_LEVEL == 1
+                        {  // diagnostic: TMEM loads only
+                            uint32_t x = 0;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            va[j] = __uint_as_float(ra[j]);
-                            vb[j] = __uint_as_float(rb[j]);
+                            for (int j = 0; j < 32; ++j) x ^= ra[j];
+                            if (x == 0x12345u) count += 1;
+                            continue;
                         }
+#endif
+                        float va[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) va[j] = __uint_as_float(ra[j]);
                         if (noaug) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                va[j] = fmaf(-sa, g[c0 + j], va[j]);
-                                vb[j] = fmaf(-sa, g[c0 + 32 + j], vb[j]);
-                            }
+                            for (int j = 0; j < 32; ++j) va[j] = fmaf(-sa, g[c0 + j], va[j]);
                         }
-                        float m8[8];
+                        float m8[4];
 #pragma unroll
-                        for (int s = 0; s < 4; ++s) {
-                            m8[s] = max8(va + 8 * s);
-                            m8[4 + s] = max8(vb + 8 * s);
-                        }
+                        for (int s = 0; s < 4; ++s) m8[s] = max8(va + 8 * s);
                         const float ma = sm100::fmax3(m8[0], m8[1], fmaxf(m8[2], m8[3]));
-                        const float mb = sm100::fmax3(m8[4], m8[5], fmaxf(m8[6], m8[7]));
                         if (KT == 1) {
-                            // k = 1: a fully valid group's best element bounds the nearest candidate
-                            const float mv = c0 + 64 <= lim ? fmaxf(ma, mb) : (c0 + 32 <= lim ? ma : -__int_as_float(0x7f800000));
-                            if (mv > vbest) {
-                                vbest = mv;
-                                const float ub = fmaf(-mv, inv2s, lb0) + 2.0f * E;
+                            // k = 1: a fully valid half's best element bounds the nearest candidate
+                            if (c0 + 32 <= lim && ma > vbest) {
+                                vbest = ma;
+                                const float ub = fmaf(-ma, inv2s, lb0) + 2.0f * E;
                                 if (ub < U) {
                                     U = ub;
                                     if (!maxonly) T = threshold();
                                 }
                             }
                         }
-                        if (fmaxf(ma, mb) >= T) {
-                            if (count + 8 > P.cap && !overflow) compact();
+#if defined(RBC_S2_LEVEL) && RBC_S2_LEVEL == 2
+                        if (ma == 1234.5f) count += 1;  // diagnostic: loads + reductions, no candidates
+                        continue;
+#endif
+                        if (ma >= T) {
+                            if (count + 4 > P.cap && !overflow) compact();
                             const int base = off + hb + c0, llim = off + hb + lim;
 #pragma unroll
-                            for (int s = 0; s < 4; ++s) {
+                            for (int s = 0; s < 4; ++s)
                                 if (m8[s] >= T) push8(va + 8 * s, m8[s], base + 8 * s, llim);
-                                if (m8[4 + s] >= T) push8(vb + 8 * s, m8[4 + s], base + 32 + 8 * s, llim);
-                            }
                         }
                     }
                     sm100::tc_fence_before();
@@ -775,20 +775,34 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
                                                      uint64_t *__restrict__ out_keys) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= nq) return;
-    const int c0 = cand_count[2 * i], c1 = cand_count[2 * i + 1];
-    if (c0 < 0 || c1 < 0) return;  // overflowed: recomputed by the exact scan
-    const float ufin = fminf(cand_ufin[2 * i], cand_ufin[2 * i + 1]);
+    int cnt[kParts];
+    float ufin = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int h = 0; h < kParts; ++h) {
+        cnt[h] = cand_count[kParts * i + h];
+        if (cnt[h] < 0) return;  // overflowed: recomputed by the exact scan
+        ufin = fminf(ufin, cand_ufin[kParts * i + h]);
+    }
     const float *qrow = q + i * d;
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-    const int n = c0 + c1;
+    int n = 0;
+#pragma unroll
+    for (int h = 0; h < kParts; ++h) n += cnt[h];
     for (int g0 = 0; g0 < n; g0 += kRerankGroups) {
         int32_t list[8 * kRerankGroups];
         int m = 0;
         const int g1 = min(n, g0 + kRerankGroups);
         for (int g = g0; g < g1; ++g) {
-            const int64_t at = g < c0 ? (2 * i) * cap + g : (2 * i + 1) * cap + (g - c0);
+            int h = 0, gg = g;
+#pragma unroll
+            for (int u = 0; u < kParts - 1; ++u)
+                if (h == u && gg >= cnt[u]) {
+                    gg -= cnt[u];
+                    h = u + 1;
+                }
+            const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
             const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
             const int32_t pos = cand_pos[at];
             const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
@@ -818,7 +832,7 @@ __global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int3
     if (t < m * k) dst[static_cast<int64_t>(ids[t / k]) * k + t % k] = src[t];
 }
 
-constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kEpiWarps * (kNmax / 2) * sizeof(float) + 256;
+constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kEpiWarps * kCols * sizeof(float) + 512;
 
 // Exact SIMT scan for the queries whose candidate buffer overflowed; the count
 // lives on the device (no host round trip).  One warp per entry, grid-stride.
@@ -1011,15 +1025,15 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                              tile_order.get(), ntiles, 0, 40, st));
     note_launch();
     // 3. the tensor-core scan
-    const int cap = 16 + 8 * k;  // 8-column groups per query and column half
+    const int cap = 12 + 6 * k;  // 8-column groups per query and column part
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, cand_count, ovf_list, counters;
-    RBC_CHECK(cand_lb.alloc(nq * 2 * cap * 8, st));
-    RBC_CHECK(cand_pos.alloc(nq * 2 * cap, st));
-    RBC_CHECK(cand_count.alloc(nq * 2, st));
-    RBC_CHECK(cand_ufin.alloc(nq * 2, st));
-    RBC_CUDA(cudaMemsetAsync(cand_count.get(), 0, sizeof(int32_t) * nq * 2, st));
-    RBC_CHECK(ovf_list.alloc(nq * 2, st));
+    RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 8, st));
+    RBC_CHECK(cand_pos.alloc(nq * kParts * cap, st));
+    RBC_CHECK(cand_count.alloc(nq * kParts, st));
+    RBC_CHECK(cand_ufin.alloc(nq * kParts, st));
+    RBC_CUDA(cudaMemsetAsync(cand_count.get(), 0, sizeof(int32_t) * nq * kParts, st));
+    RBC_CHECK(ovf_list.alloc(nq * kParts, st));
     RBC_CHECK(counters.alloc(2, st));
     RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
     const float *q64 = q;
@@ -1111,22 +1125,23 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     stage2_status_kernel<<<1, 1, 0, st>>>(work_off.get(), ntiles, counters.get(), status_dev);
     RBC_LAUNCHED();
     if (getenv("RBC_DEBUG_S2")) {  // diagnostic: buffered-candidate statistics (synchronises)
-        std::vector<int32_t> cc(nq * 2);
-        std::vector<float> lb(nq * 2 * cap * 8), uf(nq * 2);
-        cudaMemcpyAsync(cc.data(), cand_count.get(), sizeof(int32_t) * nq * 2, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(lb.data(), cand_lb.get(), sizeof(float) * nq * 2 * cap * 8, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(uf.data(), cand_ufin.get(), sizeof(float) * nq * 2, cudaMemcpyDeviceToHost, st);
+        std::vector<int32_t> cc(nq * kParts);
+        std::vector<float> lb(nq * kParts * cap * 8), uf(nq * kParts);
+        cudaMemcpyAsync(cc.data(), cand_count.get(), sizeof(int32_t) * nq * kParts, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(lb.data(), cand_lb.get(), sizeof(float) * nq * kParts * cap * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(uf.data(), cand_ufin.get(), sizeof(float) * nq * kParts, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         double tot = 0, pass = 0;
         int mx = 0, ovf = 0;
         for (int64_t i = 0; i < nq; ++i) {
-            const float u = fminf(uf[2 * i], uf[2 * i + 1]);
-            for (int h = 0; h < 2; ++h) {
-                const int c = cc[2 * i + h];
+            float u = uf[kParts * i];
+            for (int h = 1; h < kParts; ++h) u = fminf(u, uf[kParts * i + h]);
+            for (int h = 0; h < kParts; ++h) {
+                const int c = cc[kParts * i + h];
                 if (c < 0) { ++ovf; continue; }
                 tot += c;
                 mx = c > mx ? c : mx;
-                for (int e = 0; e < c * 8; ++e) pass += lb[(2 * i + h) * cap * 8 + e] <= u;
+                for (int e = 0; e < c * 8; ++e) pass += lb[(kParts * i + h) * cap * 8 + e] <= u;
             }
         }
 #ifdef RBC_S2_TIMING
@@ -1141,7 +1156,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         for (int j = 0; j < 12; ++j) fprintf(stderr, " %s=%.0f", nm[j], sum[j] / grid / (j == 6 ? 3.0 : 1.0));
         fprintf(stderr, "\n");
 #endif
-        fprintf(stderr, "[s2] nq=%lld buffered groups/query %.2f (max per half %d, cap %d), passing/query %.2f, overflow halves %d\n",
+        fprintf(stderr, "[s2] nq=%lld buffered groups/query %.2f (max per part %d, cap %d), passing/query %.2f, overflow parts %d\n",
                 (long long)nq, tot / nq, mx, cap, pass / nq, ovf);
     }
     return RBC_OK;
