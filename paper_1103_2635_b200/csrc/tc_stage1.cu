@@ -239,45 +239,65 @@ __global__ void rep_rows_kernel(const float *__restrict__ reps, int64_t nr, int 
     if (plane1) write_aug_row(base + kN * kP0 + r * kP1, static_cast<int>(r), aug);
 }
 
-// Query ordering: key = nearest of kPilots spread reps (fp32, approximate --
-// it only decides which queries share a tile, never a result).  Queries of one
-// region then share their near reps, so the per-tile slow paths run in lockstep.
+// Query ordering: key = nearest of kPilots spread reps.  Approximate on purpose
+// (f16 products, max of q.r - |r|^2/2): it only decides which queries share a
+// tile, never a result.  Queries of one region then share their near reps, so
+// the per-tile slow paths run in lockstep.
 __global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
                                                         const float *__restrict__ reps64, int64_t nr, int npilot,
                                                         uint32_t *__restrict__ key, int32_t *__restrict__ ids) {
-    __shared__ float4 sp[kPilots * 16];
-    for (int t = threadIdx.x; t < npilot * 16; t += blockDim.x) {
-        const int j = t >> 4, c = t & 15;
-        sp[t] = reinterpret_cast<const float4 *>(reps64 + (static_cast<int64_t>(j) * nr / npilot) * 64)[c];
+    __shared__ uint4 sp[kPilots * 8];  // pilot rows, 64 f16 each
+    __shared__ float sn[kPilots];      // |r|^2 / 2
+    for (int t = threadIdx.x; t < npilot * 8; t += blockDim.x) {
+        const int j = t >> 3, c = t & 7;
+        const float4 *row = reinterpret_cast<const float4 *>(reps64 + (static_cast<int64_t>(j) * nr / npilot) * 64) + 2 * c;
+        const float4 a = __ldg(row), b = __ldg(row + 1);
+        sp[t] = make_uint4(sm100::pack_f16x2_sat(a.x, a.y), sm100::pack_f16x2_sat(a.z, a.w),
+                           sm100::pack_f16x2_sat(b.x, b.y), sm100::pack_f16x2_sat(b.z, b.w));
+    }
+    for (int j = threadIdx.x; j < npilot; j += blockDim.x) {
+        const float4 *row = reinterpret_cast<const float4 *>(reps64 + (static_cast<int64_t>(j) * nr / npilot) * 64);
+        float n = 0.f;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const float4 v = __ldg(row + c);
+            n = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, n))));
+        }
+        sn[j] = 0.5f * n;
     }
     __syncthreads();
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= nq) return;
-    float4 qv[16];
+    __half2 qh[32];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) qv[c] = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
-    float best = __int_as_float(0x7f800000);
+    for (int c = 0; c < 16; ++c) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
+        qh[2 * c] = __floats2half2_rn(v.x, v.y);
+        qh[2 * c + 1] = __floats2half2_rn(v.z, v.w);
+    }
+    float best = -__int_as_float(0x7f800000);
     int bj = 0;
-    // four pilots per sweep: eight independent accumulation chains
-    for (int j0 = 0; j0 < npilot; j0 += 4) {
-        float a[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    for (int j = 0; j < npilot; ++j) {
+        const uint4 *row = sp + j * 8;
+        __half2 acc[4];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int u = 0; u < 4; ++u) acc[u] = __float2half2_rn(0.f);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float4 r = sp[((j0 + u) & (kPilots - 1)) * 16 + c];
-                const float t0 = qv[c].x - r.x, t1 = qv[c].y - r.y, t2 = qv[c].z - r.z, t3 = qv[c].w - r.w;
-                a[u][0] = fmaf(t0, t0, fmaf(t1, t1, a[u][0]));
-                a[u][1] = fmaf(t2, t2, fmaf(t3, t3, a[u][1]));
+        for (int c = 0; c < 8; ++c) {
+            const uint4 v = row[c];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                __half2 r;
+                *reinterpret_cast<uint32_t *>(&r) = w[e];
+                acc[c & 3] = __hfma2(qh[4 * c + e], r, acc[c & 3]);
             }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float dd = a[u][0] + a[u][1];
-            if (j0 + u < npilot && dd < best) {
-                best = dd;
-                bj = j0 + u;
-            }
+        const float2 s0 = __half22float2(__hadd2(acc[0], acc[1])), s1 = __half22float2(__hadd2(acc[2], acc[3]));
+        const float score = (s0.x + s0.y) + (s1.x + s1.y) - sn[j];
+        if (score > best) {
+            best = score;
+            bj = j;
         }
     }
     key[i] = static_cast<uint32_t>(bj);
@@ -729,10 +749,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
     if (warp == 1) sm100::tmem_dealloc<256>(tmem);
 }
 
-// Distances of a query row held in registers (16 float4, zero padded to 64) to a
-// zero-padded 64-float row: padding terms are exact zeros, so summing all 64
-// coordinates reproduces the reference's d-term sum bit for bit.
-__device__ __forceinline__ float exact_dist64(const float4 (&qv)[16], const float *__restrict__ row) {
+// Distances of a query row (16 float4, zero padded to 64; shared memory,
+// read as warp-wide broadcasts) to a zero-padded 64-float row: padding terms
+// are exact zeros, so summing all 64 coordinates reproduces the reference's
+// d-term sum bit for bit.
+__device__ __forceinline__ float exact_dist64(const float4 *__restrict__ qv, const float *__restrict__ row) {
     const float4 *r4 = reinterpret_cast<const float4 *>(row);
     double acc = 0.0;
 #pragma unroll
@@ -747,30 +768,41 @@ __device__ __forceinline__ float exact_dist64(const float4 (&qv)[16], const floa
 }
 
 // fp32 |q - r| (relative error <= 66 * 2^-24 on the square; stage 2 bounds it with kD1/kUq)
-__device__ __forceinline__ float approx_dist64(const float4 (&qv)[16], const float *__restrict__ row) {
+__device__ __forceinline__ float approx_dist64(const float4 *__restrict__ qv, const float *__restrict__ row) {
     const float4 *r4 = reinterpret_cast<const float4 *>(row);
     float a0 = 0.f, a1 = 0.f;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
         const float4 y = __ldg(r4 + c);
-        const float t0 = qv[c].x - y.x, t1 = qv[c].y - y.y, t2 = qv[c].z - y.z, t3 = qv[c].w - y.w;
+        const float4 x = qv[c];
+        const float t0 = x.x - y.x, t1 = x.y - y.y, t2 = x.z - y.z, t3 = x.w - y.w;
         a0 = fmaf(t0, t0, fmaf(t1, t1, a0));
         a1 = fmaf(t2, t2, fmaf(t3, t3, a1));
     }
     return sqrtf(a0 + a1);
 }
 
-// Fix-up, one thread per query, threads in pilot order (neighbouring lanes share
-// their reps, so the rep-row loads coalesce): exact gamma_k and nearest rep from
-// the gamma candidates (reference arithmetic), exact decisions for the undecided
-// reps, the 4 gamma cutoffs, the surviving segments (ascending rep position) and
-// stats.  Each thread first compacts its own candidates into a local list, so a
-// warp runs max(list length) exact distances with all lanes busy.
-constexpr int kFixThreads = 128;
-constexpr int kFixList = 16;  // per-thread gamma-candidate list (more: further sweeps)
+// Fix-up, one 8-lane group per query (4 queries per warp; queries in pilot
+// order, so neighbouring groups share their reps in L1/L2), lanes over the
+// query's entries: exact gamma_k and nearest rep from the gamma candidates
+// (reference arithmetic, group top-k merge), exact decisions for the undecided
+// reps, the 4 gamma cutoffs, the surviving segments (ascending rep position,
+// ballot-compacted) and stats.  Eight lanes match the typical entry counts
+// (a few gamma candidates, ~20 recorded reps), so few lanes idle.
+constexpr int kFixLanes = 8;
+constexpr int kFixQueries = 32;  // queries per block (256 threads)
+
+__device__ __forceinline__ uint64_t group_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = kFixLanes / 2; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
 
 template <int KT>
-__global__ void __launch_bounds__(kFixThreads, 4) stage1_fixup_kernel(
+__global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
     const float *__restrict__ q64, const int32_t *__restrict__ qorder, const float *__restrict__ reps64, int64_t nq,
     int k, const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
     const float *__restrict__ lskip, const float *__restrict__ c1_lb, const int32_t *__restrict__ c1_p, int cap1,
@@ -780,113 +812,137 @@ __global__ void __launch_bounds__(kFixThreads, 4) stage1_fixup_kernel(
     int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list,
     float *__restrict__ seg_d1, uint64_t *__restrict__ order_key, int32_t *__restrict__ pr_out,
     int32_t *__restrict__ p3_out, int32_t *__restrict__ fail) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t >= nq) return;
-    const int64_t i = qorder[t];
-    const int n1 = c1_cnt[i];
+    __shared__ float4 s_q[kFixQueries][16];
+    const int lane = threadIdx.x & 31, sub = lane & (kFixLanes - 1);
+    const int gq = threadIdx.x / kFixLanes;  // query slot in the block
+    const int gshift = (lane / kFixLanes) * kFixLanes;
+    const int64_t t = blockIdx.x * static_cast<int64_t>(kFixQueries) + gq;
+    if (blockIdx.x * static_cast<int64_t>(kFixQueries) + (threadIdx.x & ~31) / kFixLanes >= nq) return;  // whole warp idle
+    const bool live = t < nq;
+    const int64_t i = live ? qorder[t] : 0;
+    const int n1 = live ? c1_cnt[i] : -1;
     const int64_t base = i * static_cast<int64_t>(cap_rec);
-    if (n1 < 0) {  // failed row (the batch is recomputed): inert outputs
-        gamma_out[i] = 0.f;
-        nseg[i] = 0;
-        cand[i] = 0;
-        seg_off[i] = base;
-        order_key[i] = 0;
-        return;
+    bool ok = n1 >= 0;  // a failed row (the batch is recomputed) gets inert outputs
+    if (ok) {
+        for (int c = sub; c < 16; c += kFixLanes) s_q[gq][c] = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
     }
-    float4 qv[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) qv[c] = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
-    // ---- exact gamma_k over the candidates with lb <= U_k
-    const float ufin = c1_u[i];
+    __syncwarp();
+    const float4 *qv = s_q[gq];
+    // ---- exact gamma_k over the candidates with lb <= U_k (lanes over candidates)
+    const float ufin = ok ? c1_u[i] : 0.f;
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-    for (int e0 = 0; e0 < n1; e0 += kFixList) {
-        int32_t list[kFixList];
-        int m = 0;
-        const int e1 = min(n1, e0 + kFixList);
-        for (int e = e0; e < e1; ++e)
-            if (c1_lb[i * cap1 + e] <= ufin) list[m++] = c1_p[i * cap1 + e];
-        for (int u = 0; u < m; ++u) {
-            const int32_t p = list[u];
-            const float dist = exact_dist64(qv, reps64 + static_cast<int64_t>(p) * 64);
-            const uint64_t key = pack_key(dist, static_cast<uint32_t>(p));
+    const int m1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(ok ? n1 : 0));
+    for (int e0 = 0; e0 < m1; e0 += kFixLanes) {
+        const int e = e0 + sub;
+        if (ok && e < n1 && c1_lb[i * cap1 + e] <= ufin) {
+            const int32_t p = c1_p[i * cap1 + e];
+            const uint64_t key = pack_key(exact_dist64(qv, reps64 + static_cast<int64_t>(p) * 64), static_cast<uint32_t>(p));
             if (key < best[KT - 1]) sorted_insert<KT>(best, key);
         }
     }
-    uint64_t kth = best[0];
+    // group merge: the smallest key (nearest rep) and the k-th smallest (gamma_k)
+    uint64_t first_key = kEmptyKey, kth = kEmptyKey;
+    for (int r = 0; r < k; ++r) {
+        const uint64_t m = group_min_u64(best[0]);
+        if (r == 0) first_key = m;
+        kth = m;
+        if (best[0] == m && m != kEmptyKey) {  // keys are unique (distinct rep positions)
 #pragma unroll
-    for (int u = 0; u < KT; ++u)
-        if (u == k - 1) kth = best[u];
-    if (kth == kEmptyKey) {  // cannot happen with a consistent bound; keep the result exact anyway
-        atomicExch(fail, 1);
-        gamma_out[i] = 0.f;
-        nseg[i] = 0;
-        cand[i] = 0;
-        seg_off[i] = base;
-        order_key[i] = 0;
-        return;
+            for (int j = 0; j < KT - 1; ++j) best[j] = best[j + 1];
+            best[KT - 1] = kEmptyKey;
+        }
     }
-    const float gf = key_dist(kth);
+    if (ok && kth == kEmptyKey) {  // cannot happen with a consistent bound; keep the result exact anyway
+        if (sub == 0) atomicExch(fail, 1);
+        ok = false;
+    }
+    const float gf = ok ? key_dist(kth) : 0.f;
     const double g = gf, cutd = 4.0 * g;
     // ---- recorded reps: classify with the exact gamma on the interval [dt - E, dt + E]
     // (tri-state tests A: d > 3 gamma, B: d >= gamma + psi, C: d > gamma, search.py:62-74,
     // 194-195); only an undecided rep costs an exact distance
-    const int n = rec_cnt[i];
+    const int n = ok ? rec_cnt[i] : 0;
     const int32_t *r = rec + base;
     const float *rd = rec_dt + base;
-    const float E = rec_e[i];
+    const float E = ok ? rec_e[i] : 0.f;
     const float g2 = gf * gf, t9 = 9.0f * g2;
     int pr = 0, p3 = 0, ns = 0;
     long long cs = 0;
     unsigned first = 0xFFFFFFFFu;
-    for (int e = 0; e < n; ++e) {
-        const int32_t p = r[e];
-        const float dt = rd[e];
-        const float lb = dt - E, ub = dt + E;
-        const float psi = radii[p];
-        const float tp = gf + psi, tp2 = tp * tp;
-        const bool a_t = lb > t9 * (1.0f + kEps), a_f = ub < t9 * (1.0f - kEps);
-        const bool b_t = lb > tp2 * (1.0f + kEps), b_f = ub < tp2 * (1.0f - kEps);
-        const bool c_t = lb > g2 * (1.0f + kEps), c_f = ub < g2 * (1.0f - kEps);
-        const bool bc_t = b_t && c_t, bc_f = b_f || c_f;
-        const float *row = reps64 + static_cast<int64_t>(p) * 64;
-        bool surv;
-        float dist;
-        if ((a_t || a_f) && (bc_t || bc_f)) {
-            p3 += a_t ? 1 : 0;
-            pr += bc_t ? 1 : 0;
-            surv = a_f && bc_f;
-            dist = surv ? approx_dist64(qv, row) : 0.f;
-        } else {
-            dist = exact_dist64(qv, row);
-            pr += pruned_radius(dist, psi, g) ? 1 : 0;
-            p3 += pruned_3gamma(dist, g) ? 1 : 0;
-            surv = survives(dist, psi, g);
+    const int mn = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(n));
+    for (int e0 = 0; e0 < mn; e0 += kFixLanes) {
+        const int e = e0 + sub;
+        bool emit = false;
+        int32_t p = 0, len = 0;
+        float dist = 0.f;
+        if (e < n) {
+            p = r[e];
+            const float dt = rd[e];
+            const float lb = dt - E, ub = dt + E;
+            const float psi = radii[p];
+            const float tp = gf + psi, tp2 = tp * tp;
+            const bool a_t = lb > t9 * (1.0f + kEps), a_f = ub < t9 * (1.0f - kEps);
+            const bool b_t = lb > tp2 * (1.0f + kEps), b_f = ub < tp2 * (1.0f - kEps);
+            const bool c_t = lb > g2 * (1.0f + kEps), c_f = ub < g2 * (1.0f - kEps);
+            const bool bc_t = b_t && c_t, bc_f = b_f || c_f;
+            const float *row = reps64 + static_cast<int64_t>(p) * 64;
+            bool surv;
+            if ((a_t || a_f) && (bc_t || bc_f)) {
+                p3 += a_t ? 1 : 0;
+                pr += bc_t ? 1 : 0;
+                surv = a_f && bc_f;
+                dist = surv ? approx_dist64(qv, row) : 0.f;
+            } else {
+                dist = exact_dist64(qv, row);
+                pr += pruned_radius(dist, psi, g) ? 1 : 0;
+                p3 += pruned_3gamma(dist, g) ? 1 : 0;
+                surv = survives(dist, psi, g);
+            }
+            if (surv) {
+                const int32_t full = static_cast<int32_t>(offsets[p + 1] - offsets[p]);
+                // the list's last (largest) distance is psi: the whole list is within 4 gamma iff psi <= 4 gamma
+                len = static_cast<double>(psi) <= cutd
+                          ? full
+                          : list_cutoff_skip(list_dists + offsets[p], full, lskip + static_cast<int64_t>(p) * 32, cutd);
+                emit = len > 0;
+            }
         }
-        if (!surv) continue;
-        const int32_t full = static_cast<int32_t>(offsets[p + 1] - offsets[p]);
-        // the list's last (largest) distance is psi: the whole list is within 4 gamma iff psi <= 4 gamma
-        const int32_t len = static_cast<double>(psi) <= cutd
-                                ? full
-                                : list_cutoff_skip(list_dists + offsets[p], full, lskip + static_cast<int64_t>(p) * 32, cutd);
-        if (len > 0) {
-            seg_start[base + ns] = offsets[p];
-            seg_len[base + ns] = len;
-            seg_list[base + ns] = p;
-            seg_d1[base + ns] = dist;
-            ++ns;
+        const unsigned m = (__ballot_sync(0xffffffffu, emit) >> gshift) & ((1u << kFixLanes) - 1u);
+        if (emit) {
+            const int64_t at = base + ns + __popc(m & ((1u << sub) - 1u));
+            seg_start[at] = offsets[p];
+            seg_len[at] = len;
+            seg_list[at] = p;
+            seg_d1[at] = dist;
             cs += len;
-            if (static_cast<unsigned>(p) < first) first = static_cast<unsigned>(p);
+            first = min(first, static_cast<unsigned>(p));
+        }
+        ns += __popc(m);
+    }
+#pragma unroll
+    for (int o = kFixLanes / 2; o > 0; o >>= 1) {
+        pr += __shfl_xor_sync(0xffffffffu, pr, o);
+        p3 += __shfl_xor_sync(0xffffffffu, p3, o);
+        cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    }
+    if (live && sub == 0) {
+        gamma_out[i] = gf;
+        seg_off[i] = base;
+        if (!ok) {
+            nseg[i] = 0;
+            cand[i] = 0;
+            order_key[i] = 0;
+        } else {
+            if (pr_out) pr_out[i] = pr_in[i] + pr;
+            if (p3_out) p3_out[i] = p3_in[i] + p3;
+            nseg[i] = ns;
+            cand[i] = cs;
+            order_key[i] = (static_cast<uint64_t>(first & 0xFFFFFFu) << 24) | (key_id(first_key) & 0xFFFFFFu);
         }
     }
-    gamma_out[i] = gf;
-    if (pr_out) pr_out[i] = pr_in[i] + pr;
-    if (p3_out) p3_out[i] = p3_in[i] + p3;
-    nseg[i] = ns;
-    cand[i] = cs;
-    seg_off[i] = base;
-    order_key[i] = (static_cast<uint64_t>(first & 0xFFFFFFu) << 24) | (key_id(best[0]) & 0xFFFFFFu);
 }
 
 // dynamic shared memory: stages, A buffers, radii[nr], reduction slots, barriers
@@ -1090,9 +1146,9 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
         fprintf(stderr, "\n");
     }
 #endif
-    const unsigned fgrid = grid_for(nq, kFixThreads);
+    const unsigned fgrid = grid_for(nq, kFixQueries);
 #define RBC_FIXUP(KT)                                                                                                 \
-    stage1_fixup_kernel<KT><<<fgrid, kFixThreads, 0, st>>>(                                                           \
+    stage1_fixup_kernel<KT><<<fgrid, kFixQueries * kFixLanes, 0, st>>>(                                                           \
         q64, qorder.get(), t->reps64, nq, k, idx->radii, idx->offsets, idx->list_dists, t->lskip, c1_lb.get(),          \
         c1_p.get(),                                                                                                    \
         cap1, c1_cnt.get(), c1_u.get(), rec_cnt.get(), rec.get(), rec_dt.get(), rec_e.get(), cap_rec, pr0.get(),        \

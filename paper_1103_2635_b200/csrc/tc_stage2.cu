@@ -120,8 +120,8 @@ struct S2Params {
     float *cand_lb;
     int32_t *cand_pos;
     int cap;
-    int32_t *cand_count;        // [nq] buffered candidates, -1 = overflow
-    float *cand_ufin;           // [nq] final k-th best upper bound (with tie slack)
+    int32_t *cand_count;        // [nq][kParts] buffered groups, -1 = overflow
+    float *cand_ufin;           // [nq][kParts] final k-th best upper bound (with tie slack)
     int32_t *overflow_list;
     int32_t *overflow_count;
     int32_t *tile_counter;
@@ -130,6 +130,8 @@ struct S2Params {
 };
 
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
+
+constexpr int kSegBatch = 8;  // per-row segment entries loaded together in the tile kernels
 
 // Diagnostic role timing (build with -DRBC_S2_TIMING and run with RBC_DEBUG_S2=1):
 // cycles each role spends waiting on its mbarriers, per CTA.
@@ -235,8 +237,18 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
-    if (qi >= 0)  // benign races: every writer stores 1
-        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) present[seg_list[s]] = 1;
+    if (qi >= 0) {  // benign races: every writer stores 1
+        const int64_t s0 = seg_off[qi];
+        const int cnt = seg_cnt[qi];
+        for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
+            int32_t pb[kSegBatch];
+#pragma unroll
+            for (int j = 0; j < kSegBatch; ++j) pb[j] = it0 + j < cnt ? seg_list[s0 + it0 + j] : -1;
+#pragma unroll
+            for (int j = 0; j < kSegBatch; ++j)
+                if (pb[j] >= 0) present[pb[j]] = 1;
+        }
+    }
     __syncthreads();
     int c = 0;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) c += present[p];
@@ -263,33 +275,42 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     int32_t *nearcnt = sm + 2 * nr; // [nr]
     typedef cub::BlockScan<int, kRows> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ int s_base;
     __shared__ unsigned long long s_front, s_work;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) maxlen[p] = maxd1[p] = nearcnt[p] = 0;
     if (threadIdx.x == 0) {
-        s_base = 0;
         s_front = ~0ull;
         s_work = 0;
     }
     __syncthreads();
     const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
+    const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
+    const int cnt = qi >= 0 ? seg_cnt[qi] : 0;
     {
         // warp-aggregated shared-memory atomics: the rows of a tile mostly share their
-        // lists (segments ascend by list), so lanes holding the same list combine first
+        // lists (segments ascend by list), so lanes holding the same list combine first.
+        // Each row's segments are read kSegBatch at a time (independent loads in flight).
         const int lane = threadIdx.x & 31;
-        const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
-        const int cnt = qi >= 0 ? seg_cnt[qi] : 0;
         const int wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
-        for (int it = 0; it < wmax; ++it) {
-            const bool has = it < cnt;
-            const int32_t p = has ? seg_list[s0 + it] : -1;
-            const unsigned len = has ? static_cast<unsigned>(seg_len[s0 + it]) : 0u;
-            const unsigned d1b = has ? __float_as_uint(seg_d1[s0 + it]) : 0u;
-            const unsigned grp = __match_any_sync(0xffffffffu, p);
-            const unsigned mlen = __reduce_max_sync(grp, len), md1 = __reduce_max_sync(grp, d1b);
-            if (has && lane == __ffs(grp) - 1) {
-                atomicMax(&maxlen[p], static_cast<int>(mlen));
-                atomicMax(&maxd1[p], static_cast<int>(md1));
+        for (int it0 = 0; it0 < wmax; it0 += kSegBatch) {
+            int32_t pb[kSegBatch];
+            unsigned lb[kSegBatch], db[kSegBatch];
+#pragma unroll
+            for (int j = 0; j < kSegBatch; ++j) {
+                const bool has = it0 + j < cnt;
+                pb[j] = has ? seg_list[s0 + it0 + j] : -1;
+                lb[j] = has ? static_cast<unsigned>(seg_len[s0 + it0 + j]) : 0u;
+                db[j] = has ? __float_as_uint(seg_d1[s0 + it0 + j]) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < kSegBatch; ++j) {
+                if (it0 + j >= wmax) break;  // warp-uniform
+                const int32_t p = pb[j];
+                const unsigned grp = __match_any_sync(0xffffffffu, p);
+                const unsigned mlen = __reduce_max_sync(grp, lb[j]), md1 = __reduce_max_sync(grp, db[j]);
+                if (p >= 0 && lane == __ffs(grp) - 1) {
+                    atomicMax(&maxlen[p], static_cast<int>(mlen));
+                    atomicMax(&maxd1[p], static_cast<int>(md1));
+                }
             }
         }
         const int32_t nr_near = qi >= 0 ? static_cast<int32_t>(order_key[qi] & 0xFFFFFF) : -1;
@@ -311,16 +332,19 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     // tightens the running bound before any candidate is buffered)
     const int64_t wbase = work_off[blockIdx.x];
     const int64_t w0 = wbase + ((warm && work_off[blockIdx.x + 1] > wbase) ? 1 : 0);
-    // ordered compaction: front first, then the others ascending
-    for (int64_t p0 = 0; p0 < nr; p0 += kRows) {
-        const int64_t p = p0 + threadIdx.x;
-        const int flag = (p < nr && maxlen[p] > 0 && p != front) ? 1 : 0;
+    // ordered compaction: front first, then the others ascending (each thread a
+    // contiguous range of lists, one block scan)
+    {
+        const int64_t per = (nr + kRows - 1) / kRows;
+        const int64_t pa = threadIdx.x * per, pe = min(nr, pa + per);
+        int c = 0;
+        for (int64_t p = pa; p < pe; ++p) c += (maxlen[p] > 0 && p != front) ? 1 : 0;
         int pos, total;
-        Scan(scan_tmp).ExclusiveSum(flag, pos, total);
-        if (flag) nearcnt[p] = s_base + pos + (front >= 0 ? 1 : 0);  // reuse as list -> work index
-        __syncthreads();
-        if (threadIdx.x == 0) s_base += total;
-        __syncthreads();
+        Scan(scan_tmp).ExclusiveSum(c, pos, total);
+        __syncthreads();  // every count read before nearcnt is overwritten
+        pos += front >= 0 ? 1 : 0;
+        for (int64_t p = pa; p < pe; ++p)
+            if (maxlen[p] > 0 && p != front) nearcnt[p] = pos++;  // reuse as list -> work index
     }
     if (front >= 0 && threadIdx.x == 0) nearcnt[front] = 0;
     __syncthreads();
@@ -343,13 +367,24 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         }
     }
     __syncthreads();
-    if (qi >= 0)
-        for (int64_t s = seg_off[qi]; s < seg_off[qi] + seg_cnt[qi]; ++s) {
-            const int32_t p = seg_list[s];
-            const int64_t at = (w0 + nearcnt[p]) * kRows + threadIdx.x;
-            cut[at] = seg_len[s];
-            rowd1[at] = seg_d1[s];
+    for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
+        int32_t pb[kSegBatch], lb[kSegBatch];
+        float db[kSegBatch];
+#pragma unroll
+        for (int j = 0; j < kSegBatch; ++j) {
+            const bool has = it0 + j < cnt;
+            pb[j] = has ? seg_list[s0 + it0 + j] : 0;
+            lb[j] = has ? seg_len[s0 + it0 + j] : 0;
+            db[j] = has ? seg_d1[s0 + it0 + j] : 0.f;
         }
+#pragma unroll
+        for (int j = 0; j < kSegBatch; ++j)
+            if (it0 + j < cnt) {
+                const int64_t at = (w0 + nearcnt[pb[j]]) * kRows + threadIdx.x;
+                cut[at] = lb[j];
+                rowd1[at] = db[j];
+            }
+    }
     if (w0 > wbase) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -759,11 +794,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
 }
 
 // Exact re-rank (reference arithmetic) of the buffered candidate groups of both
-// column halves, one thread per query: the elements that can still qualify
-// (lb <= final bound) are compacted into a per-thread list first, so a warp
-// runs max(list length) exact distances with all 32 lanes busy.
-constexpr int kRerankThreads = 128;
-constexpr int kRerankGroups = 4;  // groups per sweep (list of up to 32 elements)
+// column parts: one 8-lane group per query (4 queries per warp), lanes over the
+// query's buffered 8-column groups (all groups in flight at once; ~7 per query
+// at cfg2), each lane re-ranking its group's elements that can still qualify
+// (lb <= final bound, ~1.4 per query); a lane top-k merge emits the keys.
+constexpr int kRerankLanes = 8;
+constexpr int kRerankThreads = 256;
 
 template <int KT>
 __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__restrict__ cand_lb,
@@ -773,52 +809,64 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
                                                      const float *__restrict__ q, const float *__restrict__ xp,
                                                      const int32_t *__restrict__ perm, int d, int k,
                                                      uint64_t *__restrict__ out_keys) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= nq) return;
+    const int sub = threadIdx.x & (kRerankLanes - 1);
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(kRerankThreads) + threadIdx.x) / kRerankLanes;
+    if ((blockIdx.x * static_cast<int64_t>(kRerankThreads) + (threadIdx.x & ~31)) / kRerankLanes >= nq) return;
+    bool live = i < nq;
     int cnt[kParts];
     float ufin = __int_as_float(0x7f800000);
 #pragma unroll
     for (int h = 0; h < kParts; ++h) {
-        cnt[h] = cand_count[kParts * i + h];
-        if (cnt[h] < 0) return;  // overflowed: recomputed by the exact scan
-        ufin = fminf(ufin, cand_ufin[kParts * i + h]);
+        cnt[h] = live ? cand_count[kParts * i + h] : 0;
+        if (cnt[h] < 0) live = false;  // overflowed: recomputed by the exact scan
+        if (live) ufin = fminf(ufin, cand_ufin[kParts * i + h]);
     }
-    const float *qrow = q + i * d;
+    int n = 0;
+#pragma unroll
+    for (int h = 0; h < kParts; ++h) n += live ? cnt[h] : 0;
+    const float *qrow = q + (live ? i : 0) * d;
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-    int n = 0;
+    for (int g = sub; g < n; g += kRerankLanes) {
+        int h = 0, gg = g;
 #pragma unroll
-    for (int h = 0; h < kParts; ++h) n += cnt[h];
-    for (int g0 = 0; g0 < n; g0 += kRerankGroups) {
-        int32_t list[8 * kRerankGroups];
-        int m = 0;
-        const int g1 = min(n, g0 + kRerankGroups);
-        for (int g = g0; g < g1; ++g) {
-            int h = 0, gg = g;
+        for (int u = 0; u < kParts - 1; ++u)
+            if (h == u && gg >= cnt[u]) {
+                gg -= cnt[u];
+                h = u + 1;
+            }
+        const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
+        const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
+        const int32_t pos = cand_pos[at];
+        const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        unsigned pass = 0;
 #pragma unroll
-            for (int u = 0; u < kParts - 1; ++u)
-                if (h == u && gg >= cnt[u]) {
-                    gg -= cnt[u];
-                    h = u + 1;
-                }
-            const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
-            const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
-            const int32_t pos = cand_pos[at];
-            const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (l[j] <= ufin) list[m++] = pos + j;
-        }
-        for (int t = 0; t < m; ++t) {
-            const int32_t pos = list[t];
-            const float dist = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pos) * d, d);
-            const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos]));
+        for (int j = 0; j < 8; ++j) pass |= (l[j] <= ufin ? 1u : 0u) << j;
+        while (pass) {
+            const int j = __ffs(pass) - 1;
+            pass &= pass - 1;
+            const float dist = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pos + j) * d, d);
+            const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos + j]));
             if (key < best[KT - 1]) sorted_insert<KT>(best, key);
         }
     }
-    for (int j = 0; j < k && j < KT; ++j) out_keys[i * k + j] = best[j];
+    for (int r = 0; r < k; ++r) {
+        uint64_t m = best[0];
+#pragma unroll
+        for (int o = kRerankLanes / 2; o > 0; o >>= 1) {
+            const uint64_t w = __shfl_xor_sync(0xffffffffu, m, o);
+            m = w < m ? w : m;
+        }
+        if (live && sub == 0) out_keys[i * k + r] = m;
+        if (best[0] == m && m != kEmptyKey) {  // keys are unique (distinct ids) unless empty
+#pragma unroll
+            for (int j = 0; j < KT - 1; ++j) best[j] = best[j + 1];
+            best[KT - 1] = kEmptyKey;
+        }
+    }
 }
+
 __global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
                                          float *__restrict__ out) {
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < m * d;
@@ -1097,7 +1145,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_LAUNCHED();
     // 4. exact re-rank of the buffered candidates
     {
-        const unsigned rgrid = grid_for(nq, kRerankThreads);
+        const unsigned rgrid = grid_for(nq * kRerankLanes, kRerankThreads);
 #define RBC_RERANK(KT)                                                                                              \
     rerank_kernel<KT><<<rgrid, kRerankThreads, 0, st>>>(reinterpret_cast<const float4 *>(cand_lb.get()),           \
                                                         cand_pos.get(), cand_count.get(),                           \
@@ -1124,27 +1172,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     }
     stage2_status_kernel<<<1, 1, 0, st>>>(work_off.get(), ntiles, counters.get(), status_dev);
     RBC_LAUNCHED();
-    if (getenv("RBC_DEBUG_S2")) {  // diagnostic: buffered-candidate statistics (synchronises)
-        std::vector<int32_t> cc(nq * kParts);
-        std::vector<float> lb(nq * kParts * cap * 8), uf(nq * kParts);
-        cudaMemcpyAsync(cc.data(), cand_count.get(), sizeof(int32_t) * nq * kParts, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(lb.data(), cand_lb.get(), sizeof(float) * nq * kParts * cap * 8, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(uf.data(), cand_ufin.get(), sizeof(float) * nq * kParts, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        double tot = 0, pass = 0;
-        int mx = 0, ovf = 0;
-        for (int64_t i = 0; i < nq; ++i) {
-            float u = uf[kParts * i];
-            for (int h = 1; h < kParts; ++h) u = fminf(u, uf[kParts * i + h]);
-            for (int h = 0; h < kParts; ++h) {
-                const int c = cc[kParts * i + h];
-                if (c < 0) { ++ovf; continue; }
-                tot += c;
-                mx = c > mx ? c : mx;
-                for (int e = 0; e < c * 8; ++e) pass += lb[(kParts * i + h) * cap * 8 + e] <= u;
-            }
-        }
 #ifdef RBC_S2_TIMING
+    if (getenv("RBC_DEBUG_S2")) {  // diagnostic: role timing (synchronises)
         std::vector<unsigned long long> tm(148 * 12);
         cudaMemcpy(tm.data(), timing.get(), sizeof(unsigned long long) * 148 * 12, cudaMemcpyDeviceToHost);
         double sum[12] = {0};
@@ -1155,10 +1184,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         fprintf(stderr, "[s2] per-CTA cycles:");
         for (int j = 0; j < 12; ++j) fprintf(stderr, " %s=%.0f", nm[j], sum[j] / grid / (j == 6 ? 3.0 : 1.0));
         fprintf(stderr, "\n");
-#endif
-        fprintf(stderr, "[s2] nq=%lld buffered groups/query %.2f (max per part %d, cap %d), passing/query %.2f, overflow parts %d\n",
-                (long long)nq, tot / nq, mx, cap, pass / nq, ovf);
     }
+#endif
     return RBC_OK;
 }
 
