@@ -11,6 +11,9 @@
 // set -- and therefore every result and every SearchStats field -- matches.
 #include <cub/cub.cuh>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 
 #include "common.cuh"
@@ -287,6 +290,17 @@ int prune(const rbc_index *idx, const float *d1, int64_t nq, int k, PruneOut &ou
 }
 
 // ---- exact search (search.py:150-208) --------------------------------------
+// host-side enqueue timing (diagnostic, RBC_DEBUG_HOST=1)
+struct HostClock {
+    bool on = getenv("RBC_DEBUG_HOST") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        const double us =
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[host] %-14s %8.1f us\n", what, us);
+    }
+};
 int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
                       const rbc_search_stats &stats, cudaStream_t st) {
     if (nq == 0) return RBC_OK;
@@ -311,21 +325,25 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
             RBC_CHECK(s1fail.alloc(1, st));
             RBC_CHECK(s2status.alloc(2, st));
             RBC_CUDA(cudaMemsetAsync(s1fail.get(), 0, sizeof(int32_t), st));
+            HostClock hc;
             {
                 ProfScope ps(kPhaseStage1, st);
                 RBC_CHECK(tc_stage1(idx, qc, m, k, *po, s1fail.get(), st));
             }
+            hc.mark("stage1 queued");
             const bool tc2 = tc_stage2_supported(idx, k);
             const int64_t cap = stage2_work_capacity(idx, m);
             if (tc2) {
                 ProfScope ps(kPhaseStage2, st);
                 RBC_CHECK(tc_stage2(idx, qc, m, k, *po, keys + q0 * k, cap, s2status.get(), st));
             }
+            hc.mark("stage2 queued");
             int32_t f = 0;
             int64_t s2[2] = {0, 0};
             RBC_CUDA(cudaMemcpyAsync(&f, s1fail.get(), sizeof(f), cudaMemcpyDeviceToHost, st));
             if (tc2) RBC_CUDA(cudaMemcpyAsync(s2, s2status.get(), sizeof(s2), cudaMemcpyDeviceToHost, st));
             RBC_CUDA(cudaStreamSynchronize(st));
+            hc.mark("synced");
             if (!f) {
                 if (!tc2 || s2[0] > cap) {
                     if (tc2) stage2_note_work(idx, m, s2[0]);

@@ -220,6 +220,18 @@ __global__ void tile_rows_kernel(const int32_t *__restrict__ order, int64_t nq, 
     if (t < total) rows[t] = t < nq ? order[t] : -1;
 }
 
+// query grouping key (first surviving list, nearest rep) packed into 2 * kb bits, so the
+// sort runs ceil(2 kb / 8) radix passes instead of six, plus the identity payload
+__global__ void group_key_kernel(const uint64_t *__restrict__ order_key, int64_t nq, int kb, uint32_t *__restrict__ key,
+                                 int32_t *__restrict__ ids) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= nq) return;
+    const uint64_t o = order_key[t];
+    const uint32_t mask = (1u << kb) - 1u;
+    key[t] = ((static_cast<uint32_t>(o >> 24) & mask) << kb) | (static_cast<uint32_t>(o) & mask);
+    ids[t] = static_cast<int32_t>(t);
+}
+
 __global__ void iota_kernel(int32_t *v, int64_t n) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (t < n) v[t] = static_cast<int32_t>(t);
@@ -1007,7 +1019,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     const int64_t nr = idx->nr;
     const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
     // 1. group queries: sort by (first surviving list, nearest rep)
-    DevBuf<uint64_t> skey, tkey, tkey_sorted;
+    DevBuf<uint64_t> tkey, tkey_sorted;
+    DevBuf<uint32_t> gkey, skey;
     DevBuf<int32_t> ids, order, rows, tids, tile_order;
     RBC_CHECK(skey.alloc(nq, st));
     RBC_CHECK(ids.alloc(nq, st));
@@ -1017,18 +1030,22 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(tkey_sorted.alloc(ntiles, st));
     RBC_CHECK(tids.alloc(ntiles, st));
     RBC_CHECK(tile_order.alloc(ntiles, st));
-    iota_kernel<<<grid_for(nq, 256), 256, 0, st>>>(ids.get(), nq);
+    int kb = 1;
+    while ((int64_t(1) << kb) < nr) ++kb;  // nr < 2^24 (tc_stage2_supported)
+    RBC_CHECK(gkey.alloc(nq, st));
+    group_key_kernel<<<grid_for(nq, 256), 256, 0, st>>>(po.order_key.get(), nq, kb, gkey.get(), ids.get());
     RBC_LAUNCHED();
     iota_kernel<<<grid_for(ntiles, 256), 256, 0, st>>>(tids.get(), ntiles);
     RBC_LAUNCHED();
     size_t tb = 0, tb2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq, 0, 48, st);
+    const int kbits = kb > 16 ? 32 : 2 * kb;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, gkey.get(), skey.get(), ids.get(), order.get(), nq, 0, kbits, st);
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles, 0,
                                     40, st);
     DevBuf<unsigned char> tmp;
     RBC_CHECK(tmp.alloc(tb > tb2 ? tb : tb2, st));
-    RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, po.order_key.get(), skey.get(), ids.get(), order.get(), nq,
-                                             0, 48, st));
+    RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, gkey.get(), skey.get(), ids.get(), order.get(), nq, 0,
+                                             kbits, st));
     note_launch();
     tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
         order.get(), nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
