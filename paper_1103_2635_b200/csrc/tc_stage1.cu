@@ -47,7 +47,6 @@ namespace {
 constexpr int kRows = 128;
 constexpr int kN = 128;        // representatives per chunk (UMMA N)
 constexpr int kStages = 3;
-constexpr int kVStride = 68;  // floats per row of the slow-path value stage (16-byte aligned, bank-spread)
 constexpr int kThreads = 192;  // producer, MMA, 4 epilogue warps
 constexpr int kP0 = 128, kP1 = 32;
 // per chunk: plane 0 (kN rows x 128 B, SW128: 64 f16, aug in columns 62/63 when
@@ -332,20 +331,17 @@ __device__ __forceinline__ void s1_wait_t(uint64_t *bar, uint32_t parity, unsign
 
 // ---- the fused stage-1 kernel ---------------------------------------------------------
 template <int KT>
-__global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P) {
+__global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *sB = smem;
     uint8_t *sA = sB + kStages * kStageBytes;
     float *s_radii = reinterpret_cast<float *>(sA + 2 * kABytes);  // [nr]
     float *s_red = s_radii + ((P.nr + 3) & ~int64_t(3));            // [4] tile max of |q - c|
-    float *s_v = s_red + 4;                                          // [128][kVStride] slow-path value stage
-    float *s_q = s_v + kRows * kVStride;                             // [128][kVStride] the tile's query rows
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_q + kRows * kVStride);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_red + 4);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2;
     uint64_t *afull = tempty + 2, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
-    uint64_t *qfull = tile_empty + 2, *qempty = qfull + 1;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(qempty + 1);
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -367,8 +363,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             sm100::mbar_init(&tile_full[b], 1);
             sm100::mbar_init(&tile_empty[b], 5);
         }
-        sm100::mbar_init(qfull, 1);
-        sm100::mbar_init(qempty, 4);
         sm100::fence_barrier_init();
     }
     if (warp == 1) sm100::tmem_alloc<256>(s_tmem);
@@ -394,16 +388,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             }
             tile = __shfl_sync(0xffffffffu, tile, 0);
             if (tile < 0) break;
-            if (lane == 0) {
-                sm100::mbar_wait(qempty, (it & 1) ^ 1);
-                sm100::mbar_arrive_expect_tx(qfull, kRows * 256);
-            }
-            __syncwarp();
-            for (int r = lane; r < kRows; r += 32) {
-                const int64_t slot_i = static_cast<int64_t>(tile) * kRows + r;
-                const int64_t qi = P.qorder[slot_i < P.nq ? slot_i : P.nq - 1];
-                sm100::bulk_g2s(s_q + r * kVStride, P.q64 + qi * 64, 256, qfull);
-            }
             if (lane == 0) {
                 const uint32_t bytes = P.plane1 ? kStageBytes : kN * kP0;
                 for (int pass = 0; pass < 2; ++pass)
@@ -478,14 +462,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
             float qv[64];
             float qn;
             {
-                S1_WAIT(qfull, it & 1, 10);
-                const float4 *src = reinterpret_cast<const float4 *>(s_q + row * kVStride);
+                const float4 *src = reinterpret_cast<const float4 *>(P.q64 + qi * 64);
                 const float4 *cc = reinterpret_cast<const float4 *>(P.c64);
                 float n0 = 0.f, n1 = 0.f;
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
                     const float4 m = __ldg(cc + c);
-                    const float4 t = live ? src[c] : m;
+                    const float4 t = live ? __ldg(src + c) : m;
                     qv[4 * c] = __fsub_rn(t.x, m.x);
                     qv[4 * c + 1] = __fsub_rn(t.y, m.y);
                     qv[4 * c + 2] = __fsub_rn(t.z, m.z);
@@ -494,8 +477,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     n1 = fmaf(qv[4 * c + 2], qv[4 * c + 2], fmaf(qv[4 * c + 3], qv[4 * c + 3], n1));
                 }
                 qn = n0 + n1;
-                __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(qempty);
             }
             const float nqv = sqrtf(qn) * (1.0f + kCq);
             float tmax = nqv;
@@ -582,60 +563,55 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     unsigned gm = 0;  // groups that may hold a candidate
 #pragma unroll
                     for (int s = 0; s < 8; ++s) gm |= (m8[s] >= T ? 1u : 0u) << s;
-                    if (__any_sync(0xffffffffu, gm != 0)) {
-                        // rare path, compact code: stage the block's values, walk the flagged groups
-                        float4 *sv4 = reinterpret_cast<float4 *>(s_v + row * kVStride);
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) sv4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-                        __syncwarp();
-                        const float *sv = s_v + row * kVStride;
-                        while (gm) {
-                            const int s = __ffs(gm) - 1;
-                            gm &= gm - 1;
-                            const int g0 = off + c0 + 8 * s;
-                            const float4 xa = reinterpret_cast<const float4 *>(sv)[2 * s];
-                            const float4 xb = reinterpret_cast<const float4 *>(sv)[2 * s + 1];
-                            const float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-                            if (count + 8 > P.cap1) {  // compact: drop entries that can no longer qualify
-                                int c2 = 0;
-                                for (int e = 0; e < count; ++e)
-                                    if (clb[e] <= U * kTie) {
-                                        clb[c2] = clb[e];
-                                        cp[c2] = cp[e];
-                                        ++c2;
-                                    }
-                                count = c2;
-                                if (count + 8 > P.cap1) {
-                                    fail = true;
-                                    continue;
+                    // rare path, compact code: walk the groups flagged by any lane (warp-uniform),
+                    // re-reading each group's 8 columns from TMEM
+                    unsigned gu = __reduce_or_sync(0xffffffffu, gm);
+                    while (gu) {
+                        const int s = __ffs(gu) - 1;
+                        gu &= gu - 1;
+                        float x[8];
+                        sm100::tmem_ld8(tmem + tb * kN + lane_base + c0 + 8 * s, x);
+                        bool take = (gm & (1u << s)) != 0;
+                        const int g0 = off + c0 + 8 * s;
+                        if (take && count + 8 > P.cap1) {  // compact: drop entries that can no longer qualify
+                            int c2 = 0;
+                            for (int e = 0; e < count; ++e)
+                                if (clb[e] <= U * kTie) {
+                                    clb[c2] = clb[e];
+                                    cp[c2] = cp[e];
+                                    ++c2;
                                 }
+                            count = c2;
+                            if (count + 8 > P.cap1) {
+                                fail = true;
+                                take = false;
                             }
+                        }
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                if (x[j] >= T && g0 + j < P.nr) {
-                                    const float lb = fmaf(-x[j], inv2s, lb0);
-                                    clb[count] = lb;
-                                    cp[count] = g0 + j;
-                                    ++count;
-                                    if (KT > 1) {
-                                        float y = lb + 2.0f * E;
+                        for (int j = 0; j < 8; ++j) {
+                            if (take && x[j] >= T && g0 + j < P.nr) {
+                                const float lb = fmaf(-x[j], inv2s, lb0);
+                                clb[count] = lb;
+                                cp[count] = g0 + j;
+                                ++count;
+                                if (KT > 1) {
+                                    float y = lb + 2.0f * E;
 #pragma unroll
-                                        for (int t = 0; t < KT; ++t) {
-                                            const float lo = fminf(ubk[t], y), hi = fmaxf(ubk[t], y);
-                                            ubk[t] = lo;
-                                            y = hi;
-                                        }
+                                    for (int t = 0; t < KT; ++t) {
+                                        const float lo = fminf(ubk[t], y), hi = fmaxf(ubk[t], y);
+                                        ubk[t] = lo;
+                                        y = hi;
                                     }
                                 }
                             }
-                            if (KT > 1) {
-                                float kth = ubk[0];
+                        }
+                        if (KT > 1 && take) {
+                            float kth = ubk[0];
 #pragma unroll
-                                for (int t = 0; t < KT; ++t)
-                                    if (t == P.k - 1) kth = ubk[t];
-                                U = fminf(U, kth);
-                                T = threshold();
-                            }
+                            for (int t = 0; t < KT; ++t)
+                                if (t == P.k - 1) kth = ubk[t];
+                            U = fminf(U, kth);
+                            T = threshold();
                         }
                         __syncwarp();
                     }
@@ -673,7 +649,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                     sm100::tmem_ld32_async(tmem + tb * kN + lane_base + c0 + 32, rbv);
                     sm100::tmem_wait_ld(ra);
                     sm100::tmem_tie(rbv);
-                    if (!live) continue;
                     float v[64];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -681,41 +656,37 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
                         v[32 + j] = __uint_as_float(rbv[j]);
                     }
                     const int nvb = min(64, lim - c0);
-                    pr += nvb;  // counted far; the recorded ones are taken back below
-                    p3 += nvb;
+                    if (live) {
+                        pr += nvb;  // counted far; the recorded ones are taken back below
+                        p3 += nvb;
+                    }
                     float m8[8];
 #pragma unroll
                     for (int s = 0; s < 8; ++s) m8[s] = max8(v + 8 * s);
                     unsigned gm = 0;
 #pragma unroll
-                    for (int s = 0; s < 8; ++s) gm |= (m8[s] >= Tf ? 1u : 0u) << s;
-                    if (__any_sync(__activemask(), gm != 0)) {
-                        float4 *sv4 = reinterpret_cast<float4 *>(s_v + row * kVStride);
+                    for (int s = 0; s < 8; ++s) gm |= (live && m8[s] >= Tf ? 1u : 0u) << s;
+                    unsigned gu = __reduce_or_sync(0xffffffffu, gm);
+                    while (gu) {
+                        const int s = __ffs(gu) - 1;
+                        gu &= gu - 1;
+                        float x[8];
+                        sm100::tmem_ld8(tmem + tb * kN + lane_base + c0 + 8 * s, x);
+                        const bool take = (gm & (1u << s)) != 0;
+                        const int g0 = c0 + 8 * s;
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) sv4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-                        __syncwarp(__activemask());
-                        const float *sv = s_v + row * kVStride;
-                        while (gm) {
-                            const int s = __ffs(gm) - 1;
-                            gm &= gm - 1;
-                            const int g0 = c0 + 8 * s;
-                            const float4 xa = reinterpret_cast<const float4 *>(sv)[2 * s];
-                            const float4 xb = reinterpret_cast<const float4 *>(sv)[2 * s + 1];
-                            const float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                if (x[j] >= Tf && g0 + j < lim) {
-                                    if (rc < P.cap_rec) {
-                                        rec[rc] = off + g0 + j;
-                                        rdt[rc] = fmaf(-x[j], inv2s, qn);
-                                    }
-                                    ++rc;
-                                    --pr;
-                                    --p3;
+                        for (int j = 0; j < 8; ++j) {
+                            if (take && x[j] >= Tf && g0 + j < lim) {
+                                if (rc < P.cap_rec) {
+                                    rec[rc] = off + g0 + j;
+                                    rdt[rc] = fmaf(-x[j], inv2s, qn);
                                 }
+                                ++rc;
+                                --pr;
+                                --p3;
                             }
                         }
-                        __syncwarp(__activemask());
+                        __syncwarp();
                     }
                 }
                 sm100::tc_fence_before();
@@ -750,9 +721,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage1_tc_kernel(const S1Params P
 }
 
 // Distances of a query row (16 float4, zero padded to 64; shared memory,
-// read as warp-wide broadcasts) to a zero-padded 64-float row: padding terms
-// are exact zeros, so summing all 64 coordinates reproduces the reference's
-// d-term sum bit for bit.
+// read as broadcasts) to a zero-padded 64-float row: padding terms are exact
+// zeros, so summing all 64 coordinates reproduces the reference's d-term sum
+// bit for bit.
 __device__ __forceinline__ float exact_dist64(const float4 *__restrict__ qv, const float *__restrict__ row) {
     const float4 *r4 = reinterpret_cast<const float4 *>(row);
     double acc = 0.0;
@@ -947,8 +918,7 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
 
 // dynamic shared memory: stages, A buffers, radii[nr], reduction slots, barriers
 inline size_t s1_smem_bytes(int64_t nr) {
-    return 1024 + kStages * kStageBytes + 2 * kABytes +
-           (((nr + 3) & ~int64_t(3)) + 4 + 2 * kRows * kVStride) * sizeof(float) + 256;
+    return 1024 + kStages * kStageBytes + 2 * kABytes + (((nr + 3) & ~int64_t(3)) + 4) * sizeof(float) + 256;
 }
 
 }  // namespace
@@ -1114,7 +1084,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     }
     // persistent CTAs, two per SM when the representatives' radii fit (tiles come from a counter)
     const size_t smem = s1_smem_bytes(idx->nr);
-    const int per_sm = smem <= 110 * 1024 ? 2 : 1;  // (one CTA per SM at the current stage count)
+    const int per_sm = smem <= 112 * 1024 ? 2 : 1;  // two CTAs (2 x 256 TMEM columns) when shared memory allows
     const unsigned grid = static_cast<unsigned>(ntiles < per_sm * g_num_sms1 ? ntiles : per_sm * g_num_sms1);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
