@@ -293,7 +293,10 @@ def main():
                                                   _lib.SearchStatsC(None, None, None, None), sptr), "e2e")
         if i >= args.warmup:
             e2e_times.append(time.perf_counter() - t0)
-    e2e_s = sum(e2e_times) / len(e2e_times)
+    # median: the host call's wall time carries OS scheduling noise; min/median/max go to stderr
+    e2e_s = statistics.median(e2e_times)
+    log(f"e2e ms: min {1e3 * min(e2e_times):.3f} median {1e3 * e2e_s:.3f} max {1e3 * max(e2e_times):.3f} "
+        f"(n={len(e2e_times)})")
     if dist:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -738,21 +738,6 @@ __device__ __forceinline__ float exact_dist64(const float4 *__restrict__ qv, con
     return __double2float_rn(__dsqrt_rn(acc));
 }
 
-// fp32 |q - r| (relative error <= 66 * 2^-24 on the square; stage 2 bounds it with kD1/kUq)
-__device__ __forceinline__ float approx_dist64(const float4 *__restrict__ qv, const float *__restrict__ row) {
-    const float4 *r4 = reinterpret_cast<const float4 *>(row);
-    float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        const float4 y = __ldg(r4 + c);
-        const float4 x = qv[c];
-        const float t0 = x.x - y.x, t1 = x.y - y.y, t2 = x.z - y.z, t3 = x.w - y.w;
-        a0 = fmaf(t0, t0, fmaf(t1, t1, a0));
-        a1 = fmaf(t2, t2, fmaf(t3, t3, a1));
-    }
-    return sqrtf(a0 + a1);
-}
-
 // Fix-up, one 8-lane group per query (4 queries per warp; queries in pilot
 // order, so neighbouring groups share their reps in L1/L2), lanes over the
 // query's entries: exact gamma_k and nearest rep from the gamma candidates
@@ -845,7 +830,7 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
     const int mn = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(n));
     for (int e0 = 0; e0 < mn; e0 += kFixLanes) {
         const int e = e0 + sub;
-        bool emit = false;
+        bool emit = false, need = false;
         int32_t p = 0, len = 0;
         float dist = 0.f;
         if (e < n) {
@@ -864,7 +849,7 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
                 p3 += a_t ? 1 : 0;
                 pr += bc_t ? 1 : 0;
                 surv = a_f && bc_f;
-                dist = surv ? approx_dist64(qv, row) : 0.f;
+                need = surv;  // fp32 distance computed cooperatively below
             } else {
                 dist = exact_dist64(qv, row);
                 pr += pruned_radius(dist, psi, g) ? 1 : 0;
@@ -878,6 +863,32 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
                           ? full
                           : list_cutoff_skip(list_dists + offsets[p], full, lskip + static_cast<int64_t>(p) * 32, cutd);
                 emit = len > 0;
+            }
+        }
+        // fp32 |q - r| of the decided survivors, one rep row at a time per group: the
+        // group's 8 lanes read the row's 256 bytes together (coalesced) and reduce by
+        // shuffles -- per-lane row reads cost one L1 wavefront per lane and dominated
+        {
+            unsigned gm = (__ballot_sync(0xffffffffu, need) >> gshift) & ((1u << kFixLanes) - 1u);
+            const int cnt = __popc(gm);
+            const int mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
+            const float4 qa = qv[sub], qb = qv[sub + kFixLanes];
+            for (int t = 0; t < mx; ++t) {
+                const int src = gm ? __ffs(gm) - 1 : 0;
+                gm &= gm - 1;
+                const int32_t pp = __shfl_sync(0xffffffffu, p, gshift + src);
+                float part = 0.f;
+                if (t < cnt) {
+                    const float4 *r4 = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pp) * 64);
+                    const float4 ya = __ldg(r4 + sub), yb = __ldg(r4 + sub + kFixLanes);
+                    const float t0 = qa.x - ya.x, t1 = qa.y - ya.y, t2 = qa.z - ya.z, t3 = qa.w - ya.w;
+                    const float t4 = qb.x - yb.x, t5 = qb.y - yb.y, t6 = qb.z - yb.z, t7 = qb.w - yb.w;
+                    part = fmaf(t0, t0, fmaf(t1, t1, fmaf(t2, t2, fmaf(t3, t3, 0.f))));
+                    part = fmaf(t4, t4, fmaf(t5, t5, fmaf(t6, t6, fmaf(t7, t7, part))));
+                }
+#pragma unroll
+                for (int o = kFixLanes / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                if (t < cnt && sub == src) dist = sqrtf(part);
             }
         }
         const unsigned m = (__ballot_sync(0xffffffffu, emit) >> gshift) & ((1u << kFixLanes) - 1u);
