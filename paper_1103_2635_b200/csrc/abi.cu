@@ -68,6 +68,39 @@ int build_one_shot(const float *x, int64_t n, int d, int metric, const int64_t *
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Host -> device copy of a large host buffer split over kCopyLanes concurrent
+// copies (side streams ordered after `st`, joined back into `st`): several
+// copies in flight keep the PCIe link busier than one.
+static constexpr int kCopyLanes = 4;
+static int copy_h2d_split(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    static cudaStream_t side[kCopyLanes] = {};
+    static cudaEvent_t ev_start = nullptr, ev_done[kCopyLanes] = {};
+    if (!ev_start) {
+        RBC_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+        for (int i = 0; i < kCopyLanes; ++i) {
+            RBC_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+            RBC_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+        }
+    }
+    if (bytes < (size_t(8) << 20)) {
+        RBC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return RBC_OK;
+    }
+    RBC_CUDA(cudaEventRecord(ev_start, st));
+    const size_t part = ((bytes + kCopyLanes - 1) / kCopyLanes + 255) & ~size_t(255);
+    for (int i = 0; i < kCopyLanes; ++i) {
+        const size_t off = part * i;
+        if (off >= bytes) break;
+        const size_t len = bytes - off < part ? bytes - off : part;
+        RBC_CUDA(cudaStreamWaitEvent(side[i], ev_start, 0));
+        RBC_CUDA(cudaMemcpyAsync(static_cast<char *>(dst) + off, static_cast<const char *>(src) + off, len,
+                                 cudaMemcpyHostToDevice, side[i]));
+        RBC_CUDA(cudaEventRecord(ev_done[i], side[i]));
+        RBC_CUDA(cudaStreamWaitEvent(st, ev_done[i], 0));
+    }
+    return RBC_OK;
+}
+
 static int check_common(int64_t n, int d, int metric) {
     if (metric != RBC_L2 && metric != RBC_L1) return fail(RBC_EINVAL, "metric must be 0 (l2) or 1 (l1)");
     if (d < 1) return fail(RBC_EINVAL, "dim must be >= 1");
@@ -398,7 +431,7 @@ int rbc_exact_search_host(const rbc_index *idx, const float *q, int64_t nq, int3
     if (stats.candidates) { RBC_CHECK(dcand.alloc(nq, st)); ds.candidates = dcand.get(); }
     if (stats.reps_pruned_radius) { RBC_CHECK(dpr.alloc(nq, st)); ds.reps_pruned_radius = dpr.get(); }
     if (stats.reps_pruned_3gamma) { RBC_CHECK(dp3.alloc(nq, st)); ds.reps_pruned_3gamma = dp3.get(); }
-    RBC_CUDA(cudaMemcpyAsync(dq.get(), q, sizeof(float) * nq * idx->d, cudaMemcpyHostToDevice, st));
+    RBC_CHECK(copy_h2d_split(dq.get(), q, sizeof(float) * nq * idx->d, st));
     RBC_CHECK(rbc_exact_search(idx, dq.get(), nq, k, dids.get(), ddist.get(), ds, stream));
     RBC_CUDA(cudaMemcpyAsync(ids, dids.get(), sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaMemcpyAsync(dists, ddist.get(), sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
