@@ -21,6 +21,14 @@ int fail(int code, const std::string &msg) {
     return code;
 }
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launch_count_now() { return g_launches.load(); }
+
+Arena *&current_arena() {
+    static thread_local Arena *a = nullptr;
+    return a;
+}
+
+bool profiling_on();
 
 void retain_pool_memory() {
     static thread_local int done_for = -1;
@@ -42,6 +50,8 @@ struct ProfRec {
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_prof_open(kNumPhases, nullptr);
+
+bool profiling_on() { return g_prof_on; }
 
 void prof_mark(int phase, bool begin, cudaStream_t st) {
     if (!g_prof_on) return;
@@ -376,6 +386,7 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
 
 int rbc_index_destroy(rbc_index *idx) {
     if (!idx) return RBC_OK;
+    search_graph_release(idx);
     tc_index_release(idx);
     tc1_index_release(idx);
     void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets, idx->perm, idx->list_dists, idx->xp,

@@ -54,20 +54,43 @@ struct ProfScope {
 // hundreds of MB).
 void retain_pool_memory();
 
-// Stream-ordered scratch allocation (cudaMallocAsync pool).
+// Scratch arena for captured (CUDA-graph) searches: while a thread has an arena
+// installed, DevBuf carves its buffers out of it (fixed addresses, no frees), so
+// the whole stream-ordered sequence can be captured once and replayed.  With
+// `base == nullptr` the arena only measures the bytes a search requests.
+struct Arena {
+    char *base = nullptr;
+    size_t cap = 0;
+    size_t used = 0;
+};
+Arena *&current_arena();
+
+// Stream-ordered scratch allocation (cudaMallocAsync pool, or the current arena).
 template <typename T>
 struct DevBuf {
     T *ptr = nullptr;
     cudaStream_t stream = nullptr;
+    bool owned = false;
     DevBuf() = default;
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() {
-        if (ptr) cudaFreeAsync(ptr, stream);
+        if (ptr && owned) cudaFreeAsync(ptr, stream);
     }
     int alloc(size_t count, cudaStream_t s) {
         stream = s;
         if (count == 0) count = 1;
+        Arena *a = current_arena();
+        if (a && a->base) {
+            const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+            if (a->used + bytes > a->cap) return fail(RBC_ENOMEM, "search arena exhausted");
+            ptr = reinterpret_cast<T *>(a->base + a->used);
+            a->used += bytes;
+            owned = false;
+            return RBC_OK;
+        }
+        if (a) a->used += (count * sizeof(T) + 255) & ~size_t(255);  // measuring pass
+        owned = true;
         retain_pool_memory();
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&ptr), count * sizeof(T), s);
         if (e != cudaSuccess) {

@@ -38,6 +38,10 @@ struct rbc_index {
 
     // stage-2 work-item capacity learned from previous searches (tile unions)
     mutable int64_t s2_work_per_tile = 24;
+
+    // captured fused-search graph + its scratch arena (search.cu), reused while a
+    // caller repeats the same (queries, nq, k, outputs) call
+    mutable void *graph = nullptr;
 };
 
 namespace rbc {
@@ -45,4 +49,5 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st);
 void tc_index_release(rbc_index *idx);
 int tc1_index_prepare(rbc_index *idx, cudaStream_t st);
 void tc1_index_release(rbc_index *idx);
+void search_graph_release(const rbc_index *idx);
 }  // namespace rbc

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
 
 #include "common.cuh"
 #include "index.cuh"
@@ -301,8 +302,174 @@ struct HostClock {
         fprintf(stderr, "[host] %-14s %8.1f us\n", what, us);
     }
 };
+// ---- captured fused search ---------------------------------------------------
+// A caller that repeats the same call (same queries, nq, k, outputs -- a serving loop
+// or a benchmark) gets the fused sequence (stage 1, fix-up, grouping, stage 2,
+// re-rank, stats copies: ~35 device operations) captured once into a CUDA graph over
+// a fixed scratch arena and replayed: no per-kernel launch gaps and no host enqueue
+// work.  1st call: normal launch, arena bytes measured; 2nd: capture + replay;
+// later: replay.  The host still reads the two status words after each replay and
+// takes the same fallbacks as the direct path.
+int64_t launch_count_now();
+bool profiling_on();
+
+struct SearchGraph {
+    std::mutex mu;
+    const float *q = nullptr;
+    int64_t nq = -1;
+    int k = 0;
+    uint64_t *keys = nullptr;
+    rbc_search_stats stats{nullptr, nullptr, nullptr, nullptr};
+    int64_t cap = 0;
+    int uses = 0;
+    size_t need = 0;
+    char *arena = nullptr;
+    size_t arena_cap = 0;
+    cudaStream_t cs = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+    std::unique_ptr<PruneOut> po;
+    int32_t *s1fail = nullptr;
+    int64_t *s2status = nullptr;
+    bool tc2 = false;
+    ~SearchGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (arena) cudaFree(arena);
+        if (cs) cudaStreamDestroy(cs);
+    }
+};
+
+void search_graph_release(const rbc_index *idx) {
+    if (!idx->graph) return;
+    cudaDeviceSynchronize();
+    delete static_cast<SearchGraph *>(idx->graph);
+    idx->graph = nullptr;
+}
+
+// enqueue the fused sequence for one chunk (q0 = 0) on st
+static int enqueue_fused(const rbc_index *idx, const float *q, int64_t m, int k, uint64_t *keys,
+                         const rbc_search_stats &stats, int64_t cap, bool tc2, PruneOut &po, DevBuf<int32_t> &s1fail,
+                         DevBuf<int64_t> &s2status, cudaStream_t st) {
+    RBC_CHECK(s1fail.alloc(1, st));
+    RBC_CHECK(s2status.alloc(2, st));
+    RBC_CUDA(cudaMemsetAsync(s1fail.get(), 0, sizeof(int32_t), st));
+    RBC_CHECK(tc_stage1(idx, q, m, k, po, s1fail.get(), st));
+    if (tc2) RBC_CHECK(tc_stage2(idx, q, m, k, po, keys, cap, s2status.get(), st));
+    if (stats.gamma)
+        RBC_CUDA(cudaMemcpyAsync(stats.gamma, po.gamma.get(), sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+    if (stats.candidates)
+        RBC_CUDA(cudaMemcpyAsync(stats.candidates, po.cand.get(), sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, st));
+    return RBC_OK;
+}
+
+int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
+                             const rbc_search_stats &stats, cudaStream_t st);
+
 int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
                       const rbc_search_stats &stats, cudaStream_t st) {
+    const bool fused = !force_exact_engine() && tc_stage1_supported(idx, k);
+    if (!fused || nq == 0 || nq > (int64_t(1) << 20) || profiling_on() || getenv("RBC_NO_GRAPH"))
+        return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
+    if (!idx->graph) idx->graph = new SearchGraph();
+    SearchGraph &g = *static_cast<SearchGraph *>(idx->graph);
+    std::unique_lock<std::mutex> lock(g.mu, std::try_to_lock);
+    if (!lock.owns_lock()) return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);  // concurrent caller
+    const int64_t cap = stage2_work_capacity(idx, nq);
+    const bool tc2 = tc_stage2_supported(idx, k);
+    const bool same = g.q == q && g.nq == nq && g.k == k && g.keys == keys && g.cap == cap && g.tc2 == tc2 &&
+                      g.stats.gamma == stats.gamma && g.stats.candidates == stats.candidates &&
+                      g.stats.reps_pruned_radius == stats.reps_pruned_radius &&
+                      g.stats.reps_pruned_3gamma == stats.reps_pruned_3gamma;
+    if (!same) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        g.po.reset();
+        g.q = q, g.nq = nq, g.k = k, g.keys = keys, g.stats = stats, g.cap = cap, g.tc2 = tc2;
+        g.uses = 0;
+    }
+    ++g.uses;
+    if (g.uses == 1) {  // direct launch, measuring the scratch it requests
+        Arena measure;
+        current_arena() = &measure;
+        const int rc = exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
+        current_arena() = nullptr;
+        g.need = measure.used;
+        return rc;
+    }
+    if (!g.exec) {
+        if (g.uses < 0) return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);  // capture failed before
+        RBC_CUDA(cudaStreamSynchronize(st));
+        const size_t want = g.need + (size_t(16) << 20);
+        if (g.arena_cap < want) {
+            if (g.arena) cudaFree(g.arena);
+            g.arena = nullptr;
+            g.arena_cap = 0;
+            if (cudaMalloc(&g.arena, want) != cudaSuccess) {
+                cudaGetLastError();
+                g.uses = -1000000;
+                return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
+            }
+            g.arena_cap = want;
+        }
+        if (!g.cs) RBC_CUDA(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+        Arena arena{g.arena, g.arena_cap, 0};
+        g.po.reset(new PruneOut());
+        g.po->pr = stats.reps_pruned_radius;
+        g.po->p3 = stats.reps_pruned_3gamma;
+        DevBuf<int32_t> s1fail;
+        DevBuf<int64_t> s2status;
+        const int64_t l0 = launch_count_now();
+        current_arena() = &arena;
+        cudaGraph_t graph = nullptr;
+        int rc = cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess ? RBC_OK : RBC_ECUDA;
+        if (rc == RBC_OK) {
+            rc = enqueue_fused(idx, q, nq, k, keys, stats, cap, tc2, *g.po, s1fail, s2status, g.cs);
+            const cudaError_t e = cudaStreamEndCapture(g.cs, &graph);
+            if (rc == RBC_OK && e != cudaSuccess) rc = RBC_ECUDA;
+        }
+        current_arena() = nullptr;
+        if (rc == RBC_OK && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) rc = RBC_ECUDA;
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        if (rc != RBC_OK) {  // capture unsupported here: direct launches from now on for this call shape
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            g.exec = nullptr;
+            g.po.reset();
+            g.uses = -1000000;
+            return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
+        }
+        g.launches = launch_count_now() - l0;
+        g.s1fail = s1fail.get();
+        g.s2status = s2status.get();
+    }
+    RBC_CUDA(cudaGraphLaunch(g.exec, st));
+    note_launch(static_cast<int>(g.launches));
+    int32_t f = 0;
+    int64_t s2[2] = {0, 0};
+    RBC_CUDA(cudaMemcpyAsync(&f, g.s1fail, sizeof(f), cudaMemcpyDeviceToHost, st));
+    if (tc2) RBC_CUDA(cudaMemcpyAsync(s2, g.s2status, sizeof(s2), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    if (f) {  // a stage-1 buffer overflowed: the exact path recomputes everything
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        g.uses = 0;
+        return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
+    }
+    if (!tc2 || s2[0] > cap) {  // stage-2 work capacity exceeded: re-run stage 2, re-capture next time
+        if (tc2) stage2_note_work(idx, nq, s2[0]);
+        RBC_CHECK(stage2_scan(idx, q, nq, k, *g.po, keys, st));
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        g.uses = 0;
+        g.nq = -1;
+    } else {
+        last_overflow_count() = s2[1];
+    }
+    return RBC_OK;
+}
+
+int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
+                             const rbc_search_stats &stats, cudaStream_t st) {
     if (nq == 0) return RBC_OK;
     const bool fused = !force_exact_engine() && tc_stage1_supported(idx, k);
     // bound the stage-1 block to ~1 GiB per chunk (the fused path holds no |Q| x |R| block)

@@ -133,6 +133,27 @@ __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
 
 constexpr int kSegBatch = 8;  // per-row segment entries loaded together in the tile kernels
 
+// Entries a[s .. s + min(rem, 8)) of a 32-bit array (the rest = fill): 16-byte vector
+// loads where the address is aligned and the quad lies inside the row, so a thread
+// reading its own row costs one L1 wavefront per four entries instead of one per entry.
+__device__ __forceinline__ void load8_u32(const uint32_t *__restrict__ a, int64_t s, int rem, uint32_t (&o)[8],
+                                          uint32_t fill) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int b = 4 * h;
+        if (rem >= b + 4 && ((s + b) & 3) == 0) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(a + s + b));
+            o[b] = v.x;
+            o[b + 1] = v.y;
+            o[b + 2] = v.z;
+            o[b + 3] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[b + j] = b + j < rem ? __ldg(a + s + b + j) : fill;
+        }
+    }
+}
+
 // Diagnostic role timing (build with -DRBC_S2_TIMING and run with RBC_DEBUG_S2=1):
 // cycles each role spends waiting on its mbarriers, per CTA.
 #ifdef RBC_S2_TIMING
@@ -253,12 +274,11 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
         const int64_t s0 = seg_off[qi];
         const int cnt = seg_cnt[qi];
         for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
-            int32_t pb[kSegBatch];
-#pragma unroll
-            for (int j = 0; j < kSegBatch; ++j) pb[j] = it0 + j < cnt ? seg_list[s0 + it0 + j] : -1;
+            uint32_t pb[kSegBatch];
+            load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, cnt - it0, pb, 0xFFFFFFFFu);
 #pragma unroll
             for (int j = 0; j < kSegBatch; ++j)
-                if (pb[j] >= 0) present[pb[j]] = 1;
+                if (pb[j] != 0xFFFFFFFFu) present[pb[j]] = 1;
         }
     }
     __syncthreads();
@@ -304,19 +324,15 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         const int lane = threadIdx.x & 31;
         const int wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
         for (int it0 = 0; it0 < wmax; it0 += kSegBatch) {
-            int32_t pb[kSegBatch];
-            unsigned lb[kSegBatch], db[kSegBatch];
-#pragma unroll
-            for (int j = 0; j < kSegBatch; ++j) {
-                const bool has = it0 + j < cnt;
-                pb[j] = has ? seg_list[s0 + it0 + j] : -1;
-                lb[j] = has ? static_cast<unsigned>(seg_len[s0 + it0 + j]) : 0u;
-                db[j] = has ? __float_as_uint(seg_d1[s0 + it0 + j]) : 0u;
-            }
+            uint32_t pu[kSegBatch], lb[kSegBatch], db[kSegBatch];
+            const int rem = max(cnt - it0, 0);
+            load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, rem, pu, 0xFFFFFFFFu);
+            load8_u32(reinterpret_cast<const uint32_t *>(seg_len), s0 + it0, rem, lb, 0u);
+            load8_u32(reinterpret_cast<const uint32_t *>(seg_d1), s0 + it0, rem, db, 0u);
 #pragma unroll
             for (int j = 0; j < kSegBatch; ++j) {
                 if (it0 + j >= wmax) break;  // warp-uniform
-                const int32_t p = pb[j];
+                const int32_t p = static_cast<int32_t>(pu[j]);
                 const unsigned grp = __match_any_sync(0xffffffffu, p);
                 const unsigned mlen = __reduce_max_sync(grp, lb[j]), md1 = __reduce_max_sync(grp, db[j]);
                 if (p >= 0 && lane == __ffs(grp) - 1) {
@@ -380,21 +396,16 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     __syncthreads();
     for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
-        int32_t pb[kSegBatch], lb[kSegBatch];
-        float db[kSegBatch];
-#pragma unroll
-        for (int j = 0; j < kSegBatch; ++j) {
-            const bool has = it0 + j < cnt;
-            pb[j] = has ? seg_list[s0 + it0 + j] : 0;
-            lb[j] = has ? seg_len[s0 + it0 + j] : 0;
-            db[j] = has ? seg_d1[s0 + it0 + j] : 0.f;
-        }
+        uint32_t pb[kSegBatch], lb[kSegBatch], db[kSegBatch];
+        load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, cnt - it0, pb, 0u);
+        load8_u32(reinterpret_cast<const uint32_t *>(seg_len), s0 + it0, cnt - it0, lb, 0u);
+        load8_u32(reinterpret_cast<const uint32_t *>(seg_d1), s0 + it0, cnt - it0, db, 0u);
 #pragma unroll
         for (int j = 0; j < kSegBatch; ++j)
             if (it0 + j < cnt) {
                 const int64_t at = (w0 + nearcnt[pb[j]]) * kRows + threadIdx.x;
-                cut[at] = lb[j];
-                rowd1[at] = db[j];
+                cut[at] = static_cast<int32_t>(lb[j]);
+                rowd1[at] = __uint_as_float(db[j]);
             }
     }
     if (w0 > wbase) {

@@ -407,3 +407,46 @@ def test_tc_engine_overflow_fallback(rbc):
         assert np.array_equal(a, b)
     rbc.exact_query_arrays(idx, q, 1)
     assert _lib.lib.rbc_stage2_overflows() > 0
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_graph_replay_matches_direct(rbc, oracle, monkeypatch, k):
+    # repeating the same keys-level call captures the fused search into a CUDA graph
+    # (1st call direct + arena measurement, 2nd capture + replay, then replay); every
+    # replay must equal the direct launch path bit for bit, stats included
+    import torch
+
+    from paper_1103_2635_b200 import _lib
+
+    full = oracle.gen_clusters(60_000 + 3_000, 64, 3, n_clusters=16, cluster_sigma=0.05)
+    x, q = full[:60_000], full[60_000:]
+    idx = rbc.build_exact(rbc.DataMatrix(x), 245, rbc.MetricSpec("l2", 64), seed=0)
+    dev = idx._dev
+    nq = q.shape[0]
+    q_dev = _lib.to_device(q)
+
+    def run(no_graph):
+        if no_graph:
+            monkeypatch.setenv("RBC_NO_GRAPH", "1")
+        else:
+            monkeypatch.delenv("RBC_NO_GRAPH", raising=False)
+        outs = []
+        keys = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+        gamma = torch.empty(nq, dtype=torch.float32, device="cuda")
+        prr = torch.empty(nq, dtype=torch.int32, device="cuda")
+        p3 = torch.empty(nq, dtype=torch.int32, device="cuda")
+        cand = torch.empty(nq, dtype=torch.int64, device="cuda")
+        stats = _lib.SearchStatsC(gamma.data_ptr(), prr.data_ptr(), p3.data_ptr(), cand.data_ptr())
+        for _ in range(4):
+            for t in (keys, gamma, prr, p3, cand):
+                t.fill_(-7)
+            _lib.check(_lib.lib.rbc_exact_search_keys(dev.handle, _lib.ptr(q_dev), nq, k, _lib.ptr(keys), stats,
+                                                      _lib.stream_ptr()), "exact search")
+            torch.cuda.synchronize()
+            outs.append([t.cpu().numpy().copy() for t in (keys, gamma, prr, p3, cand)])
+        return outs
+
+    direct = run(True)[0]
+    for rep in run(False):
+        for a, b in zip(rep, direct):
+            assert np.array_equal(a, b)
