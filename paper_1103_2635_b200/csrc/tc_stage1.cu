@@ -745,6 +745,9 @@ __device__ __forceinline__ float exact_dist64(const float4 *__restrict__ qv, con
 // reps, the 4 gamma cutoffs, the surviving segments (ascending rep position,
 // ballot-compacted) and stats.  Eight lanes match the typical entry counts
 // (a few gamma candidates, ~20 recorded reps), so few lanes idle.
+#ifdef RBC_FIX_STATS
+__device__ unsigned long long g_fix_stats[4];  // gamma exact, undecided exact, records, survivors
+#endif
 constexpr int kFixLanes = 8;
 constexpr int kFixQueries = 32;  // queries per block (256 threads)
 
@@ -796,6 +799,9 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
             const int32_t p = c1_p[i * cap1 + e];
             const uint64_t key = pack_key(exact_dist64(qv, reps64 + static_cast<int64_t>(p) * 64), static_cast<uint32_t>(p));
             if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+#ifdef RBC_FIX_STATS
+            atomicAdd(&g_fix_stats[0], 1ull);
+#endif
         }
     }
     // group merge: the smallest key (nearest rep) and the k-th smallest (gamma_k)
@@ -852,10 +858,17 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
                 need = surv;  // fp32 distance computed cooperatively below
             } else {
                 dist = exact_dist64(qv, row);
+#ifdef RBC_FIX_STATS
+                atomicAdd(&g_fix_stats[1], 1ull);
+#endif
                 pr += pruned_radius(dist, psi, g) ? 1 : 0;
                 p3 += pruned_3gamma(dist, g) ? 1 : 0;
                 surv = survives(dist, psi, g);
             }
+#ifdef RBC_FIX_STATS
+            atomicAdd(&g_fix_stats[2], 1ull);
+            if (surv) atomicAdd(&g_fix_stats[3], 1ull);
+#endif
             if (surv) {
                 const int32_t full = static_cast<int32_t>(offsets[p + 1] - offsets[p]);
                 // the list's last (largest) distance is psi: the whole list is within 4 gamma iff psi <= 4 gamma
@@ -1143,6 +1156,16 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     else RBC_FIXUP(16);
 #undef RBC_FIXUP
     RBC_LAUNCHED();
+#ifdef RBC_FIX_STATS
+    if (getenv("RBC_DEBUG_S1")) {
+        unsigned long long h[4];
+        cudaMemcpyFromSymbol(h, g_fix_stats, sizeof(h));
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_fix_stats, z, sizeof(z));
+        fprintf(stderr, "[fixup] per query: gamma exact %.2f, undecided exact %.2f, records %.2f, survivors %.2f\n",
+                double(h[0]) / nq, double(h[1]) / nq, double(h[2]) / nq, double(h[3]) / nq);
+    }
+#endif
     return RBC_OK;
 }
 
