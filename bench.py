@@ -55,6 +55,27 @@ def gen_inputs(rank: int):
     return x, q
 
 
+def ncu_traffic(kernel="stage2_tc_kernel"):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the newest committed
+    ncu --set full summary under profiles/ (bytes), or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_v*_kernels.txt")),
+                   key=lambda f: int(re.search(r"_v(\d+)_", f).group(1)))
+    for path in reversed(files):
+        block, total = None, 0.0
+        for line in open(path):
+            if line.startswith("== "):
+                block = kernel in line
+            elif block and "dram__bytes_" in line:
+                m = re.search(r"= ([\d.]+) (\w+)", line)
+                if m:
+                    total += float(m.group(1)) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), 1)
+        if total > 0:
+            return {"bytes_per_launch": total, "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 def peaks():
     try:
         with open(PEAKS) as f:
@@ -286,9 +307,12 @@ def main():
     stage2_ms, stage2_n = phases["stage2"]
     stage2_flops = 2.0 * D * float(cand_h.sum())
     pk = peaks()
+    traffic = ncu_traffic()
     achieved_tf = stage2_flops * stage2_n / (stage2_ms / 1e3) / 1e12 if stage2_ms > 0 else None
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": pk["tensor"], "unit": "TFLOP/s",
-                "frac": (achieved_tf / pk["tensor"]) if achieved_tf else None, "traffic": None,
+                "frac": (achieved_tf / pk["tensor"]) if achieved_tf else None,
+                "traffic": (traffic or {}).get("bytes_per_launch"), "traffic_unit": "bytes/launch",
+                "traffic_src": (traffic or {}).get("source"),
                 "kernel": "stage-2 scan (exact search)", "peak_src": pk["src"],
                 "phase_ms_per_step": {k2: (v[0] / v[1] if v[1] else None) for k2, v in phases.items()},
                 "step_share": (stage2_ms / stage2_n) / ms_per_step if stage2_n else None}
