@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
     const int mn = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(n));
     for (int e0 = 0; e0 < mn; e0 += kFixLanes) {
         const int e = e0 + sub;
-        bool emit = false, need = false;
+        bool emit = false;
         int32_t p = 0, len = 0;
         float dist = 0.f;
         if (e < n) {
@@ -920,7 +920,9 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
                 p3 += a_t ? 1 : 0;
                 pr += bc_t ? 1 : 0;
                 surv = a_f && bc_f;
-                need = surv;  // fp32 distance computed cooperatively below
+                // an upper bound of |q - r| (stage 2 only takes its operand scale from it and
+                // computes |q - r|^2 itself in the A-operand prep)
+                dist = surv ? sqrtf(fmaxf(ub, 0.f)) : 0.f;
             } else {
                 dist = exact_dist64(qv, row);
 #ifdef RBC_FIX_STATS
@@ -942,11 +944,6 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
                           : list_cutoff_skip(list_dists + offsets[p], full, lskip + static_cast<int64_t>(p) * 32, cutd);
                 emit = len > 0;
             }
-        }
-        // fp32 |q - r| of the decided survivors (group-cooperative, coalesced rep rows)
-        {
-            const float a = coop_sq(need, p);
-            if (need) dist = sqrtf(a);
         }
         const unsigned m = (__ballot_sync(0xffffffffu, emit) >> gshift) & ((1u << kFixLanes) - 1u);
         if (emit) {

@@ -116,7 +116,6 @@ struct S2Params {
     const int64_t *work_off;    // [ntiles + 1]
     const WorkItem *work;       // [total work]
     const int32_t *cut;         // [total work][128] per-row cutoff (0 = list not a survivor for the row)
-    const float *rowd1;         // [total work][128] per-row exact dist(q, r_p)
     float *cand_lb;
     int32_t *cand_pos;
     int cap;
@@ -298,7 +297,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const uint64_t *__restrict__ order_key,
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
     const int64_t *__restrict__ offsets, const int64_t *__restrict__ work_off, WorkItem *__restrict__ work,
-    int32_t *__restrict__ cut, float *__restrict__ rowd1, uint64_t *__restrict__ tile_key, int warm,
+    int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key, int warm,
     int64_t cap_work) {
     if (work_off[gridDim.x] > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
     extern __shared__ int32_t sm[];
@@ -396,17 +395,12 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     __syncthreads();
     for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
-        uint32_t pb[kSegBatch], lb[kSegBatch], db[kSegBatch];
+        uint32_t pb[kSegBatch], lb[kSegBatch];
         load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, cnt - it0, pb, 0u);
         load8_u32(reinterpret_cast<const uint32_t *>(seg_len), s0 + it0, cnt - it0, lb, 0u);
-        load8_u32(reinterpret_cast<const uint32_t *>(seg_d1), s0 + it0, cnt - it0, db, 0u);
 #pragma unroll
         for (int j = 0; j < kSegBatch; ++j)
-            if (it0 + j < cnt) {
-                const int64_t at = (w0 + nearcnt[pb[j]]) * kRows + threadIdx.x;
-                cut[at] = static_cast<int32_t>(lb[j]);
-                rowd1[at] = __uint_as_float(db[j]);
-            }
+            if (it0 + j < cnt) cut[(w0 + nearcnt[pb[j]]) * kRows + threadIdx.x] = static_cast<int32_t>(lb[j]);
     }
     if (w0 > wbase) {
         __syncthreads();
@@ -416,7 +410,6 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
             work[wbase] = it;
         }
         cut[wbase * kRows + threadIdx.x] = cut[w0 * kRows + threadIdx.x];
-        rowd1[wbase * kRows + threadIdx.x] = rowd1[w0 * kRows + threadIdx.x];
     }
     // LPT: heavier tiles first
     if (threadIdx.x == 0) {
@@ -442,7 +435,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     uint8_t *sB = smem;                                   // kStages x (plane 0 | plane 1)
     uint8_t *sA = sB + kStages * kStageBytes;             // 2 x (plane 0 | plane 1)
     float *gbuf = reinterpret_cast<float *>(sA + 2 * kABytes);  // 8 epilogue warps x 128 (fallback column)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + kEpiWarps * kCols);
+    float *s_dq = gbuf + kEpiWarps * kCols;  // [4 list slots][kParts][128] partial |q - r_p|^2
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_dq + 4 * kParts * kRows);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + kAcc;
     uint64_t *afull = tempty + kAcc, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
@@ -590,6 +584,19 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const __half ac = __float2half_rn(wi.aug);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 const float sa = wi.sA;
+                // this part's share of |q - r_p|^2 (fp32; with the other part's, the A2 term of
+                // the error bound -- same (d + 2) 2^-24 relative error budget as kD1 / kUq)
+                {
+                    float n0 = 0.f, n1 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < kKd / 4; ++c) {
+                        const float t0 = qv[4 * c] - rr4[c].x, t1 = qv[4 * c + 1] - rr4[c].y;
+                        const float t2 = qv[4 * c + 2] - rr4[c].z, t3 = qv[4 * c + 3] - rr4[c].w;
+                        n0 = fmaf(t0, t0, fmaf(t1, t1, n0));
+                        n1 = fmaf(t2, t2, fmaf(t3, t3, n1));
+                    }
+                    s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + part * kRows + row] = n0 + n1;
+                }
                 const uint32_t a = ai & 1;
                 S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
@@ -636,29 +643,29 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
             int cut_n = 0;
-            float dq_n = 0.f;
-            if (w0 < w1) {
-                cut_n = P.cut[w0 * kRows + row];
-                dq_n = P.rowd1[w0 * kRows + row];
-            }
+            if (w0 < w1) cut_n = P.cut[w0 * kRows + row];
             for (int64_t w = w0; w < w1; ++w) {
                 if (w + 1 < w1) prep_a(w + 1);  // next list's A while this list's MMAs run
                 const WorkItem wi = P.work[w];
                 const int cutv = live ? cut_n : 0;
-                const float dq = dq_n;
-                if (w + 1 < w1) {
-                    cut_n = P.cut[(w + 1) * kRows + row];
-                    dq_n = P.rowd1[(w + 1) * kRows + row];
-                }
+                if (w + 1 < w1) cut_n = P.cut[(w + 1) * kRows + row];
+                // both column parts of this lane quadrant have prepared lists w and w + 1: the
+                // row's |q - r_p|^2 is the sum of their two halves (slot w & 3; a part runs at
+                // most one list ahead of its partner, so slots are never overwritten early)
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + quad), "r"(32 * kParts) : "memory");
+                float A2q = 0.f;
+#pragma unroll
+                for (int h = 0; h < kParts; ++h) A2q += s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + h * kRows + row];
+                const float dq = sqrtf(A2q);
                 const bool noaug = wi.aug == 0.0f;  // warp-uniform (per work item)
                 const float sa = wi.sA;
                 const float scale = sa * wi.sB, inv2s = 2.0f / scale;
                 float A2 = 0.f, E = 0.f;
                 if (cutv > 0) {
-                    // dq = |q - r_p| from stage 1's fix-up: exact, or fp32 with relative error
-                    // <= (d + 2) 2^-24 on dq^2 -- covered by kD1 (on A2) and kUq (on |a|)
+                    // A2 = |q - r_p|^2 in fp32 with relative error <= (d + 2) 2^-24 -- covered by
+                    // kD1 (on A2) and kUq (on |a| = sqrt(A2))
                     const float na = dq * kUq, rb = wi.radius * kUp;
-                    A2 = dq * dq;
+                    A2 = A2q;
                     E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 + kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
                 const float lb0 = A2 - E;  // lb(V) = lb0 - V * inv2s
@@ -903,7 +910,8 @@ __global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int3
     if (t < m * k) dst[static_cast<int64_t>(ids[t / k]) * k + t % k] = src[t];
 }
 
-constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 2 * kABytes + kEpiWarps * kCols * sizeof(float) + 512;
+constexpr size_t kSmemBytes =
+    1024 + kStages * kStageBytes + 2 * kABytes + (kEpiWarps * kCols + 4 * kParts * kRows) * sizeof(float) + 512;
 
 // Exact SIMT scan for the queries whose candidate buffer overflowed; the count
 // lives on the device (no host round trip).  One warp per entry, grid-stride.
@@ -1086,15 +1094,13 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     const int64_t total_work = cap_work;
     DevBuf<WorkItem> work;
     DevBuf<int32_t> cut;
-    DevBuf<float> rowd1;
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
-    RBC_CHECK(rowd1.alloc(total_work * kRows, st));
     RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
     tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.nseg.get(), po.seg_list.get(),
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
                                                    idx->radii, tc->poff,
-                                                   idx->offsets, work_off.get(), work.get(), cut.get(), rowd1.get(),
+                                                   idx->offsets, work_off.get(), work.get(), cut.get(),
                                                    tkey.get(), warm, cap_work);
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
@@ -1134,7 +1140,6 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.work_off = work_off.get();
     P.work = work.get();
     P.cut = cut.get();
-    P.rowd1 = rowd1.get();
     P.cand_lb = cand_lb.get();
     P.cand_pos = cand_pos.get();
     P.cap = cap;
