@@ -282,12 +282,15 @@ def main():
     for _ in range(3):  # direct-launch warm-up (scratch pool regrowth after the graph arena)
         step()
     torch.cuda.synchronize()
-    _lib.profile_enable(True)  # clears the records
-    for _ in range(10):
+    per_step = []
+    for _ in range(11):  # per-step phase times, median per phase
+        _lib.profile_enable(True)  # clears the records
         flush.zero_()
         step()
-    torch.cuda.synchronize()
-    phases = _lib.profile_read()
+        torch.cuda.synchronize()
+        per_step.append(_lib.profile_read())
+    phases = {name: (statistics.median(p[name][0] for p in per_step), 1 if per_step[0][name][1] else 0)
+              for name in per_step[0]}
     _lib.profile_enable(False)
     clk = clocks.stop()
 

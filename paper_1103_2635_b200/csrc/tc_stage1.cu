@@ -587,10 +587,14 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                                 take = false;
                             }
                         }
+                        unsigned hit = 0;  // the group's elements that qualify, then only those
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (take && x[j] >= T && g0 + j < P.nr) {
-                                const float lb = fmaf(-x[j], inv2s, lb0);
+                        for (int j = 0; j < 8; ++j) hit |= (take && x[j] >= T && g0 + j < P.nr ? 1u : 0u) << j;
+                        while (hit) {
+                            const int j = __ffs(hit) - 1;
+                            hit &= hit - 1;
+                            {
+                                const float lb = fmaf(-pick8(x, j), inv2s, lb0);
                                 clb[count] = lb;
                                 cp[count] = g0 + j;
                                 ++count;
@@ -674,18 +678,21 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                         sm100::tmem_ld8(tmem + tb * kN + lane_base + c0 + 8 * s, x);
                         const bool take = (gm & (1u << s)) != 0;
                         const int g0 = c0 + 8 * s;
+                        unsigned hit = 0;  // the group's elements that are not certainly far
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (take && x[j] >= Tf && g0 + j < lim) {
-                                if (rc < P.cap_rec) {
-                                    rec[rc] = off + g0 + j;
-                                    rdt[rc] = fmaf(-x[j], inv2s, qn);
-                                }
-                                ++rc;
-                                --pr;
-                                --p3;
+                        for (int j = 0; j < 8; ++j) hit |= (take && x[j] >= Tf && g0 + j < lim ? 1u : 0u) << j;
+                        const int nh = __popc(hit);
+                        while (hit) {
+                            const int j = __ffs(hit) - 1;
+                            hit &= hit - 1;
+                            if (rc < P.cap_rec) {
+                                rec[rc] = off + g0 + j;
+                                rdt[rc] = fmaf(-pick8(x, j), inv2s, qn);
                             }
+                            ++rc;
                         }
+                        pr -= nh;
+                        p3 -= nh;
                         __syncwarp();
                     }
                 }
