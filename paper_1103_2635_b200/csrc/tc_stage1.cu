@@ -768,7 +768,7 @@ __device__ __forceinline__ uint64_t group_min_u64(uint64_t v) {
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kFixQueries * kFixLanes) stage1_fixup_kernel(
+__global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stage1_fixup_kernel(
     const float *__restrict__ q64, const int32_t *__restrict__ qorder, const float *__restrict__ reps64, int64_t nq,
     int k, const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
     const float *__restrict__ lskip, const float *__restrict__ c1_lb, const int32_t *__restrict__ c1_p, int cap1,
