@@ -2,6 +2,7 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -387,6 +388,7 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
 int rbc_index_destroy(rbc_index *idx) {
     if (!idx) return RBC_OK;
     search_graph_release(idx);
+    host_buffers_release(idx);
     tc_index_release(idx);
     tc1_index_release(idx);
     void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets, idx->perm, idx->list_dists, idx->xp,
@@ -427,10 +429,71 @@ int rbc_one_shot_search(const rbc_index *idx, const float *q, int64_t nq, int32_
 }
 
 // ---- host-buffer (end-to-end) variants ---------------------------------------
+}  // extern "C"
+
+namespace rbc {
+// Device buffers of the host-buffer search, kept per index and grown on demand: a caller
+// that repeats the call hands the search identical device pointers, so the fused search
+// replays its captured graph (search.cu) instead of re-capturing.
+struct HostCallBuffers {
+    std::mutex mu;
+    float *q = nullptr;
+    uint64_t *keys = nullptr;
+    int64_t *ids = nullptr;
+    float *dists = nullptr;
+    int64_t cap_q = 0, cap_k = 0;
+    ~HostCallBuffers() {
+        cudaFree(q);
+        cudaFree(keys);
+        cudaFree(ids);
+        cudaFree(dists);
+    }
+};
+
+void host_buffers_release(const rbc_index *idx) {
+    delete static_cast<HostCallBuffers *>(idx->hostbuf);
+    idx->hostbuf = nullptr;
+}
+}  // namespace rbc
+
+extern "C" {
+
 int rbc_exact_search_host(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
                           rbc_search_stats stats, void *stream) {
     if (!idx) return fail(RBC_EINVAL, "null index");
+    if (k < 1) return fail(RBC_EINVAL, "k must be >= 1");
     cudaStream_t st = as_stream(stream);
+    if (!idx->hostbuf) idx->hostbuf = new HostCallBuffers();
+    HostCallBuffers &hb = *static_cast<HostCallBuffers *>(idx->hostbuf);
+    std::unique_lock<std::mutex> lock(hb.mu, std::try_to_lock);
+    if (lock.owns_lock() && !stats.gamma && !stats.candidates && !stats.reps_pruned_radius &&
+        !stats.reps_pruned_3gamma) {
+        if (hb.cap_q < nq * idx->d || hb.cap_k < nq * k) {
+            RBC_CUDA(cudaStreamSynchronize(st));
+            cudaFree(hb.q);
+            cudaFree(hb.keys);
+            cudaFree(hb.ids);
+            cudaFree(hb.dists);
+            hb.q = nullptr, hb.keys = nullptr, hb.ids = nullptr, hb.dists = nullptr;
+            hb.cap_q = hb.cap_k = 0;
+            const int64_t cq = nq * idx->d, ck = nq * k;
+            if (cudaMalloc(&hb.q, sizeof(float) * cq) != cudaSuccess ||
+                cudaMalloc(&hb.keys, sizeof(uint64_t) * ck) != cudaSuccess ||
+                cudaMalloc(&hb.ids, sizeof(int64_t) * ck) != cudaSuccess ||
+                cudaMalloc(&hb.dists, sizeof(float) * ck) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(RBC_ENOMEM, "host-call buffers");
+            }
+            hb.cap_q = cq, hb.cap_k = ck;
+        }
+        RBC_CHECK(copy_h2d_split(hb.q, q, sizeof(float) * nq * idx->d, st));
+        RBC_CHECK(rbc_exact_search_keys(idx, hb.q, nq, k, hb.keys, stats, stream));
+        RBC_CHECK(keys_to_output(hb.keys, nq * k, hb.ids, hb.dists, st));
+        RBC_CUDA(cudaMemcpyAsync(ids, hb.ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
+        RBC_CUDA(cudaMemcpyAsync(dists, hb.dists, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+        RBC_CUDA(cudaStreamSynchronize(st));
+        return RBC_OK;
+    }
     DevBuf<float> dq, ddist, dgamma;
     DevBuf<int64_t> dids, dcand;
     DevBuf<int32_t> dpr, dp3;

@@ -42,6 +42,8 @@ struct rbc_index {
     // captured fused-search graph + its scratch arena (search.cu), reused while a
     // caller repeats the same (queries, nq, k, outputs) call
     mutable void *graph = nullptr;
+    // device buffers of the host-buffer search entry points (abi.cu), grown on demand
+    mutable void *hostbuf = nullptr;
 };
 
 namespace rbc {
@@ -50,4 +52,5 @@ void tc_index_release(rbc_index *idx);
 int tc1_index_prepare(rbc_index *idx, cudaStream_t st);
 void tc1_index_release(rbc_index *idx);
 void search_graph_release(const rbc_index *idx);
+void host_buffers_release(const rbc_index *idx);
 }  // namespace rbc

@@ -74,10 +74,11 @@ struct Tc1Index {
     float *psimax = nullptr; // [nchunks] largest list radius of each rep chunk
     float *lskip = nullptr;  // [nr][32] list_dists at the end of each of 32 equal blocks (cutoff skip table)
     float *reps64 = nullptr; // [nr][64] representatives, zero padded (16-byte rows for the fix-up)
+    int32_t *pilots = nullptr; // [kPilots] farthest-point sample of the reps (query ordering)
     float sG = 1.f, rmax = 0.f;
 };
 
-constexpr int kPilots = 64;  // query-ordering pilots (a spread subset of the reps)
+constexpr int kPilots = 64;  // query-ordering pilots (farthest-point sample of the reps)
 
 // skip table: sample i of list p = list_dists at position min(len, (i+1) * s) - 1, s = ceil(len / 32)
 __global__ void list_skip_kernel(const int64_t *__restrict__ offsets, const float *__restrict__ list_dists, int64_t nr,
@@ -238,24 +239,70 @@ __global__ void rep_rows_kernel(const float *__restrict__ reps, int64_t nr, int 
     if (plane1) write_aug_row(base + kN * kP0 + r * kP1, static_cast<int>(r), aug);
 }
 
+// Pilot reps by farthest-point sampling (one block): start at rep 0, then repeatedly the
+// rep farthest from the chosen set.  With clustered data the pilots land one per region,
+// so queries sorted by nearest pilot fill tiles from a single region.
+__global__ void __launch_bounds__(1024) pilot_fps_kernel(const float *__restrict__ reps64, int64_t nr, int npilot,
+                                                         int32_t *__restrict__ pilots) {
+    extern __shared__ float mind[];  // [nr]
+    __shared__ unsigned long long s_best;
+    __shared__ int s_last;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) mind[p] = __int_as_float(0x7f800000);
+    if (threadIdx.x == 0) {
+        s_last = 0;
+        pilots[0] = 0;
+    }
+    __syncthreads();
+    for (int it = 1; it < npilot; ++it) {
+        const float4 *l4 = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(s_last) * 64);
+        if (threadIdx.x == 0) s_best = 0;
+        __syncthreads();
+        unsigned long long best = 0;
+        for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+            const float4 *r4 = reinterpret_cast<const float4 *>(reps64 + p * 64);
+            float a = 0.f;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const float4 x = __ldg(r4 + c), y = __ldg(l4 + c);
+                const float t0 = x.x - y.x, t1 = x.y - y.y, t2 = x.z - y.z, t3 = x.w - y.w;
+                a = fmaf(t0, t0, fmaf(t1, t1, fmaf(t2, t2, fmaf(t3, t3, a))));
+            }
+            const float m = fminf(mind[p], a);
+            mind[p] = m;
+            // farthest first, lowest position on ties (non-negative floats order as their bits)
+            const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(m)) << 32) |
+                                           (0xFFFFFFFFu - static_cast<unsigned>(p));
+            best = key > best ? key : best;
+        }
+        atomicMax(&s_best, best);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int p = static_cast<int>(0xFFFFFFFFu - static_cast<unsigned>(s_best & 0xFFFFFFFFu));
+            pilots[it] = p;
+            s_last = p;
+        }
+        __syncthreads();
+    }
+}
+
 // Query ordering: key = nearest of kPilots spread reps.  Approximate on purpose
 // (f16 products, max of q.r - |r|^2/2): it only decides which queries share a
 // tile, never a result.  Queries of one region then share their near reps, so
 // the per-tile slow paths run in lockstep.
 __global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
-                                                        const float *__restrict__ reps64, int64_t nr, int npilot,
-                                                        uint32_t *__restrict__ key, int32_t *__restrict__ ids) {
+                                                        const float *__restrict__ reps64, const int32_t *__restrict__ pilots,
+                                                        int npilot, uint32_t *__restrict__ key, int32_t *__restrict__ ids) {
     __shared__ uint4 sp[kPilots * 8];  // pilot rows, 64 f16 each
     __shared__ float sn[kPilots];      // |r|^2 / 2
     for (int t = threadIdx.x; t < npilot * 8; t += blockDim.x) {
         const int j = t >> 3, c = t & 7;
-        const float4 *row = reinterpret_cast<const float4 *>(reps64 + (static_cast<int64_t>(j) * nr / npilot) * 64) + 2 * c;
+        const float4 *row = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[j]) * 64) + 2 * c;
         const float4 a = __ldg(row), b = __ldg(row + 1);
         sp[t] = make_uint4(sm100::pack_f16x2_sat(a.x, a.y), sm100::pack_f16x2_sat(a.z, a.w),
                            sm100::pack_f16x2_sat(b.x, b.y), sm100::pack_f16x2_sat(b.z, b.w));
     }
     for (int j = threadIdx.x; j < npilot; j += blockDim.x) {
-        const float4 *row = reinterpret_cast<const float4 *>(reps64 + (static_cast<int64_t>(j) * nr / npilot) * 64);
+        const float4 *row = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[j]) * 64);
         float n = 0.f;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
@@ -1008,6 +1055,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
               cudaMalloc(&t->c64, 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->stat, 2 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->reps64, idx->nr * 64 * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&t->pilots, kPilots * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&rmax_bits, sizeof(unsigned)) == cudaSuccess;
     auto cleanup = [&](int rc) {
         cudaFree(t->rb);
@@ -1016,6 +1064,7 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaFree(t->c64);
         cudaFree(t->stat);
         cudaFree(t->reps64);
+        cudaFree(t->pilots);
         cudaFree(rmax_bits);
         delete t;
         return rc;
@@ -1034,7 +1083,13 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     chunk_psimax_kernel<<<grid_for(nchunks, 64), 64, 0, st>>>(idx->radii, idx->nr, t->psimax);
     list_skip_kernel<<<grid_for(idx->nr * 32, 256), 256, 0, st>>>(idx->offsets, idx->list_dists, idx->nr, t->lskip);
     pad_reps64_kernel<<<grid_for(idx->nr * 64, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, t->reps64);
-    note_launch(7);
+    {
+        const int npilot = static_cast<int>(idx->nr < kPilots ? idx->nr : kPilots);
+        const size_t fsmem = sizeof(float) * idx->nr;
+        cudaFuncSetAttribute(pilot_fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem));
+        pilot_fps_kernel<<<1, 1024, fsmem, st>>>(t->reps64, idx->nr, npilot, t->pilots);
+    }
+    note_launch(8);
     float stat[2] = {1.f, 0.f};
     if (cudaMemcpyAsync(stat, t->stat, sizeof(stat), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -1057,6 +1112,7 @@ void tc1_index_release(rbc_index *idx) {
     cudaFree(t->c64);
     cudaFree(t->stat);
     cudaFree(t->reps64);
+    cudaFree(t->pilots);
     delete t;
     idx->tc1 = nullptr;
 }
@@ -1089,7 +1145,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(qorder.alloc(nq, st));
     RBC_CHECK(pkey.alloc(nq, st));
     RBC_CHECK(pkey_sorted.alloc(nq, st));
-    pilot_key_kernel<<<grid_for(nq, 128), 128, 0, st>>>(q64, nq, t->reps64, idx->nr, npilot, pkey.get(), qids.get());
+    pilot_key_kernel<<<grid_for(nq, 128), 128, 0, st>>>(q64, nq, t->reps64, t->pilots, npilot, pkey.get(), qids.get());
     RBC_LAUNCHED();
     {
         size_t tb = 0;
