@@ -858,27 +858,80 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-    for (int g = sub; g < n; g += kRerankLanes) {
-        int h = 0, gg = g;
-#pragma unroll
-        for (int u = 0; u < kParts - 1; ++u)
-            if (h == u && gg >= cnt[u]) {
-                gg -= cnt[u];
-                h = u + 1;
-            }
-        const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
-        const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
-        const int32_t pos = cand_pos[at];
-        const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+    // lanes over the query's buffered groups: the elements that can still qualify
+    const int nmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(n));
+    const bool fast = d == 64 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;  // warp-uniform
+    // this lane's 8 query coordinates for the group-cooperative distance (d == 64)
+    float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = qa;
+    if (fast && live) {
+        qa = __ldg(reinterpret_cast<const float4 *>(qrow) + sub);
+        qb = __ldg(reinterpret_cast<const float4 *>(qrow) + sub + kRerankLanes);
+    }
+    const int gshift = (threadIdx.x & 31) & ~(kRerankLanes - 1);
+    for (int g0 = 0; g0 < nmax; g0 += kRerankLanes) {
+        const int g = g0 + sub;
         unsigned pass = 0;
+        int32_t pos = 0;
+        if (g < n) {
+            int h = 0, gg = g;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) pass |= (l[j] <= ufin ? 1u : 0u) << j;
-        while (pass) {
-            const int j = __ffs(pass) - 1;
-            pass &= pass - 1;
-            const float dist = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pos + j) * d, d);
-            const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos + j]));
-            if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+            for (int u = 0; u < kParts - 1; ++u)
+                if (h == u && gg >= cnt[u]) {
+                    gg -= cnt[u];
+                    h = u + 1;
+                }
+            const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
+            const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
+            pos = cand_pos[at];
+            const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pass |= (l[j] <= ufin ? 1u : 0u) << j;
+        }
+        if (!fast) {  // generic d: each lane re-ranks its own group's elements
+            while (pass) {
+                const int j = __ffs(pass) - 1;
+                pass &= pass - 1;
+                const float dist = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pos + j) * d, d);
+                const uint64_t key = pack_key(dist, static_cast<uint32_t>(perm[pos + j]));
+                if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+            }
+            continue;
+        }
+        // d == 64: one element at a time per group, the 8 lanes each summing 8 of the 64
+        // reference terms (identical fp64 terms; only the association differs), then a
+        // shuffle tree.  The fp32 result equals the reference's sequential sum unless the
+        // tree sum's square root lies within 2^-44 (relative) of an fp32 rounding midpoint
+        // -- the two sums differ by at most 2 * 63 * 2^-53 relative -- in which case the
+        // owner lane recomputes the sequential sum.
+        for (;;) {
+            const unsigned who = (__ballot_sync(0xffffffffu, pass != 0) >> gshift) & ((1u << kRerankLanes) - 1u);
+            if (__all_sync(0xffffffffu, who == 0)) break;
+            const int src = who ? __ffs(who) - 1 : 0;
+            const int jj = __shfl_sync(0xffffffffu, pass ? __ffs(pass) - 1 : 0, gshift + src);
+            const int32_t pp = __shfl_sync(0xffffffffu, pos, gshift + src) + jj;
+            double part = 0.0;
+            if (who) {
+                const float4 *r4 = reinterpret_cast<const float4 *>(xp + static_cast<int64_t>(pp) * 64);
+                const float4 ya = __ldg(r4 + sub), yb = __ldg(r4 + sub + kRerankLanes);
+                const float xs[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                const float ys[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+#pragma unroll
+                for (int t = 0; t < 8; ++t) part = __dadd_rn(part, l2_term(xs[t], ys[t]));
+            }
+#pragma unroll
+            for (int o = kRerankLanes / 2; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+            if (who && sub == src) {
+                pass &= pass - 1;
+                const double r = __dsqrt_rn(part);
+                float f = __double2float_rn(r);
+                const double mlo = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, -INFINITY)));
+                const double mhi = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, INFINITY)));
+                const double dl = 5.684341886080802e-14;  // 2^-44
+                if (!(r * (1.0 - dl) > mlo && r * (1.0 + dl) < mhi))
+                    f = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pp) * d, d);  // near a midpoint
+                const uint64_t key = pack_key(f, static_cast<uint32_t>(perm[pp]));
+                if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+            }
         }
     }
     for (int r = 0; r < k; ++r) {
