@@ -841,12 +841,14 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stag
     }
     __syncwarp();
     const float4 *qv = s_q[gq];
-    // fp32 |q - r|^2 for the lanes with `need`, one rep row at a time per group: the
-    // group's 8 lanes read the row's 256 bytes together (coalesced) and reduce by
-    // shuffles (per-lane row reads cost one L1 wavefront per lane).  Relative error
-    // <= (d + 3) 2^-24.  All 32 lanes must call it (warp-uniform trip count).
-    const float4 qa = qv[sub], qb = qv[sub + kFixLanes];
-    auto coop_sq = [&](bool need, int32_t p) -> float {
+    const float4 qa = qv[sub], qb = qv[sub + kFixLanes];  // this lane's 8 query coordinates
+    // exact distance (reference arithmetic) for the lanes with `need`, one rep row at a time
+    // per group: each of the 8 lanes sums 8 of the 64 fp64 reference terms (identical terms,
+    // only the association differs), a shuffle tree adds the partials, and the fp32 result is
+    // the reference's unless the tree sum's square root lies within 2^-44 (relative) of an fp32
+    // rounding midpoint -- the sequential and tree sums differ by at most 2 * 63 * 2^-53
+    // relative -- in which case the owner lane recomputes the sequential sum.
+    auto coop_exact = [&](bool need, int32_t p) -> float {
         float res = 0.f;
         unsigned gm = (__ballot_sync(0xffffffffu, need) >> gshift) & ((1u << kFixLanes) - 1u);
         const int cnt = __popc(gm);
@@ -855,58 +857,33 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stag
             const int src = gm ? __ffs(gm) - 1 : 0;
             gm &= gm - 1;
             const int32_t pp = __shfl_sync(0xffffffffu, p, gshift + src);
-            float part = 0.f;
+            double part = 0.0;
             if (t < cnt) {
                 const float4 *r4 = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pp) * 64);
                 const float4 ya = __ldg(r4 + sub), yb = __ldg(r4 + sub + kFixLanes);
-                const float t0 = qa.x - ya.x, t1 = qa.y - ya.y, t2 = qa.z - ya.z, t3 = qa.w - ya.w;
-                const float t4 = qb.x - yb.x, t5 = qb.y - yb.y, t6 = qb.z - yb.z, t7 = qb.w - yb.w;
-                part = fmaf(t0, t0, fmaf(t1, t1, fmaf(t2, t2, fmaf(t3, t3, 0.f))));
-                part = fmaf(t4, t4, fmaf(t5, t5, fmaf(t6, t6, fmaf(t7, t7, part))));
+                const float xs[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                const float ys[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u) part = __dadd_rn(part, l2_term(xs[u], ys[u]));
             }
 #pragma unroll
-            for (int o = kFixLanes / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            if (t < cnt && sub == src) res = part;
+            for (int o = kFixLanes / 2; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+            if (t < cnt && sub == src) {
+                const double r = __dsqrt_rn(part);
+                float f = __double2float_rn(r);
+                const double mlo = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, -INFINITY)));
+                const double mhi = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, INFINITY)));
+                const double dl = 5.684341886080802e-14;  // 2^-44
+                if (!(r * (1.0 - dl) > mlo && r * (1.0 + dl) < mhi))
+                    f = exact_dist64(qv, reps64 + static_cast<int64_t>(pp) * 64);  // near a midpoint
+                res = f;
+            }
         }
         return res;
     };
-    // ---- gamma_k over the candidates with lb <= U_k (lanes over candidates): fp32 d^2 of
-    // every candidate first, then the exact distance (reference arithmetic) only for the
-    // candidates within 2^-13 of the k-th smallest fp32 value -- a candidate above that
-    // margin has at least k candidates strictly nearer, exactly and after fp32 rounding
+    // ---- gamma_k: exact distances of the candidates with lb <= U_k (lanes over candidates)
     const float ufin = ok ? c1_u[i] : 0.f;
     const int m1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(ok ? n1 : 0));
-    float av[KT];
-#pragma unroll
-    for (int j = 0; j < KT; ++j) av[j] = __int_as_float(0x7f800000);
-    for (int e0 = 0; e0 < m1; e0 += kFixLanes) {
-        const int e = e0 + sub;
-        const bool pass = ok && e < n1 && c1_lb[i * cap1 + e] <= ufin;
-        const int32_t p = pass ? c1_p[i * cap1 + e] : 0;
-        const float a = coop_sq(pass, p);
-        if (pass) {
-            float x = a;
-#pragma unroll
-            for (int j = 0; j < KT; ++j) {
-                const float lo = fminf(av[j], x), hi = fmaxf(av[j], x);
-                av[j] = lo;
-                x = hi;
-            }
-        }
-    }
-    float vk = __int_as_float(0x7f800000);  // >= the k-th smallest fp32 value (ties pop together)
-    for (int r = 0; r < k; ++r) {
-        float m = av[0];
-#pragma unroll
-        for (int o = kFixLanes / 2; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        vk = m;
-        if (av[0] == m && m < __int_as_float(0x7f800000)) {
-#pragma unroll
-            for (int j = 0; j < KT - 1; ++j) av[j] = av[j + 1];
-            av[KT - 1] = __int_as_float(0x7f800000);
-        }
-    }
-    const float vthr = vk * (1.0f + 1.0f / 8192.0f);
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
@@ -914,9 +891,9 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stag
         const int e = e0 + sub;
         const bool pass = ok && e < n1 && c1_lb[i * cap1 + e] <= ufin;
         const int32_t p = pass ? c1_p[i * cap1 + e] : 0;
-        const float a = coop_sq(pass, p);
-        if (pass && a <= vthr) {
-            const uint64_t key = pack_key(exact_dist64(qv, reps64 + static_cast<int64_t>(p) * 64), static_cast<uint32_t>(p));
+        const float dist = coop_exact(pass, p);
+        if (pass) {
+            const uint64_t key = pack_key(dist, static_cast<uint32_t>(p));
             if (key < best[KT - 1]) sorted_insert<KT>(best, key);
 #ifdef RBC_FIX_STATS
             atomicAdd(&g_fix_stats[0], 1ull);
