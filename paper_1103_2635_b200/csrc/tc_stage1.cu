@@ -1108,7 +1108,8 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     // per-query record / segment rows, a multiple of 4 entries (16-byte aligned rows for the tile kernels)
     const int cap_rec = static_cast<int>(idx->nr < 512 ? (idx->nr + 3) & ~int64_t(3) : 512);
     DevBuf<float> q64buf, c1_lb, c1_u, rec_dt, rec_e;
-    DevBuf<int32_t> c1_p, c1_cnt, pr0, p30, rec_cnt, rec, flags, qids, qorder;
+    DevBuf<int32_t> c1_p, c1_cnt, pr0, p30, rec_cnt, rec, flags, qids;
+    DevBuf<int32_t> &qorder = out.qorder;
     DevBuf<uint32_t> pkey, pkey_sorted;
     const float *q64 = q;
     if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
