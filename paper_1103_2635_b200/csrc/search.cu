@@ -329,13 +329,14 @@ struct SearchGraph {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;
     std::unique_ptr<PruneOut> po;
-    int32_t *s1fail = nullptr;
-    int64_t *s2status = nullptr;
+    int64_t *status = nullptr;       // device status words (arena)
+    int64_t *host_status = nullptr;  // pinned read-back
     bool tc2 = false;
     ~SearchGraph() {
         if (exec) cudaGraphExecDestroy(exec);
         if (arena) cudaFree(arena);
         if (cs) cudaStreamDestroy(cs);
+        if (host_status) cudaFreeHost(host_status);
     }
 };
 
@@ -347,14 +348,15 @@ void search_graph_release(const rbc_index *idx) {
 }
 
 // enqueue the fused sequence for one chunk (q0 = 0) on st
+// status words of one fused search: [0] stage-2 work items needed, [1] overflowed rows,
+// [2] stage-1 failure flag (int32) -- one 24-byte read-back
 static int enqueue_fused(const rbc_index *idx, const float *q, int64_t m, int k, uint64_t *keys,
-                         const rbc_search_stats &stats, int64_t cap, bool tc2, PruneOut &po, DevBuf<int32_t> &s1fail,
-                         DevBuf<int64_t> &s2status, cudaStream_t st) {
-    RBC_CHECK(s1fail.alloc(1, st));
-    RBC_CHECK(s2status.alloc(2, st));
-    RBC_CUDA(cudaMemsetAsync(s1fail.get(), 0, sizeof(int32_t), st));
-    RBC_CHECK(tc_stage1(idx, q, m, k, po, s1fail.get(), st));
-    if (tc2) RBC_CHECK(tc_stage2(idx, q, m, k, po, keys, cap, s2status.get(), st));
+                         const rbc_search_stats &stats, int64_t cap, bool tc2, PruneOut &po, DevBuf<int64_t> &status,
+                         cudaStream_t st) {
+    RBC_CHECK(status.alloc(3, st));
+    RBC_CUDA(cudaMemsetAsync(status.get(), 0, 3 * sizeof(int64_t), st));
+    RBC_CHECK(tc_stage1(idx, q, m, k, po, reinterpret_cast<int32_t *>(status.get() + 2), st));
+    if (tc2) RBC_CHECK(tc_stage2(idx, q, m, k, po, keys, cap, status.get(), st));
     if (stats.gamma)
         RBC_CUDA(cudaMemcpyAsync(stats.gamma, po.gamma.get(), sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     if (stats.candidates)
@@ -416,14 +418,13 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
         g.po.reset(new PruneOut());
         g.po->pr = stats.reps_pruned_radius;
         g.po->p3 = stats.reps_pruned_3gamma;
-        DevBuf<int32_t> s1fail;
-        DevBuf<int64_t> s2status;
+        DevBuf<int64_t> status;
         const int64_t l0 = launch_count_now();
         current_arena() = &arena;
         cudaGraph_t graph = nullptr;
         int rc = cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess ? RBC_OK : RBC_ECUDA;
         if (rc == RBC_OK) {
-            rc = enqueue_fused(idx, q, nq, k, keys, stats, cap, tc2, *g.po, s1fail, s2status, g.cs);
+            rc = enqueue_fused(idx, q, nq, k, keys, stats, cap, tc2, *g.po, status, g.cs);
             const cudaError_t e = cudaStreamEndCapture(g.cs, &graph);
             if (rc == RBC_OK && e != cudaSuccess) rc = RBC_ECUDA;
         }
@@ -439,16 +440,15 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
             return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
         }
         g.launches = launch_count_now() - l0;
-        g.s1fail = s1fail.get();
-        g.s2status = s2status.get();
+        g.status = status.get();
+        if (!g.host_status) RBC_CUDA(cudaMallocHost(&g.host_status, 4 * sizeof(int64_t)));
     }
     RBC_CUDA(cudaGraphLaunch(g.exec, st));
     note_launch(static_cast<int>(g.launches));
-    int32_t f = 0;
-    int64_t s2[2] = {0, 0};
-    RBC_CUDA(cudaMemcpyAsync(&f, g.s1fail, sizeof(f), cudaMemcpyDeviceToHost, st));
-    if (tc2) RBC_CUDA(cudaMemcpyAsync(s2, g.s2status, sizeof(s2), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaMemcpyAsync(g.host_status, g.status, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaStreamSynchronize(st));
+    const int32_t f = *reinterpret_cast<const int32_t *>(g.host_status + 2);
+    const int64_t s2[2] = {g.host_status[0], g.host_status[1]};
     if (f) {  // a stage-1 buffer overflowed: the exact path recomputes everything
         if (g.exec) cudaGraphExecDestroy(g.exec);
         g.exec = nullptr;

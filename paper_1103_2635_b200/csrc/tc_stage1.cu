@@ -291,9 +291,12 @@ __global__ void __launch_bounds__(1024) pilot_fps_kernel(const float *__restrict
 // the per-tile slow paths run in lockstep.
 __global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
                                                         const float *__restrict__ reps64, const int32_t *__restrict__ pilots,
-                                                        int npilot, uint32_t *__restrict__ key, int32_t *__restrict__ ids) {
+                                                        int npilot, uint32_t *__restrict__ key,
+                                                        unsigned *__restrict__ hist) {
     __shared__ uint4 sp[kPilots * 8];  // pilot rows, 64 f16 each
     __shared__ float sn[kPilots];      // |r|^2 / 2
+    __shared__ unsigned sh[kPilots];   // this block's bucket counts
+    for (int j = threadIdx.x; j < kPilots; j += blockDim.x) sh[j] = 0;
     for (int t = threadIdx.x; t < npilot * 8; t += blockDim.x) {
         const int j = t >> 3, c = t & 7;
         const float4 *row = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[j]) * 64) + 2 * c;
@@ -312,8 +315,9 @@ __global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict_
         sn[j] = 0.5f * n;
     }
     __syncthreads();
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= nq) return;
+    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const bool live = i0 < nq;
+    const int64_t i = live ? i0 : nq - 1;
     __half2 qh[32];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
@@ -346,8 +350,39 @@ __global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict_
             bj = j;
         }
     }
-    key[i] = static_cast<uint32_t>(bj);
-    ids[i] = static_cast<int32_t>(i);
+    if (live) {
+        key[i] = static_cast<uint32_t>(bj);
+        atomicAdd(&sh[bj], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < npilot; j += blockDim.x)
+        if (sh[j]) atomicAdd(&hist[j], sh[j]);
+}
+
+// Query order from the pilot keys: a counting sort over the kPilots buckets (bucket
+// starts = exclusive scan of the histogram; each block claims a contiguous range per
+// bucket).  Order inside a bucket follows the blocks' claims -- it only shapes tiles.
+__global__ void __launch_bounds__(128) pilot_scatter_kernel(const uint32_t *__restrict__ key, int64_t nq, int npilot,
+                                                            const unsigned *__restrict__ hist,
+                                                            unsigned *__restrict__ cursor, int32_t *__restrict__ qorder) {
+    __shared__ unsigned s_start[kPilots], s_cnt[kPilots], s_base[kPilots];
+    if (threadIdx.x == 0) {
+        unsigned run = 0;
+        for (int j = 0; j < npilot; ++j) {
+            s_start[j] = run;
+            run += hist[j];
+        }
+    }
+    for (int j = threadIdx.x; j < kPilots; j += blockDim.x) s_cnt[j] = 0;
+    __syncthreads();
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int b = i < nq ? static_cast<int>(key[i]) : -1;
+    const unsigned r = b >= 0 ? atomicAdd(&s_cnt[b], 1u) : 0u;
+    __syncthreads();
+    for (int j = threadIdx.x; j < npilot; j += blockDim.x)
+        if (s_cnt[j]) s_base[j] = s_start[j] + atomicAdd(&cursor[j], s_cnt[j]);
+    __syncthreads();
+    if (b >= 0) qorder[s_base[b] + r] = static_cast<int32_t>(i);
 }
 
 __global__ void pad_reps64_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
@@ -1108,33 +1143,27 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     // per-query record / segment rows, a multiple of 4 entries (16-byte aligned rows for the tile kernels)
     const int cap_rec = static_cast<int>(idx->nr < 512 ? (idx->nr + 3) & ~int64_t(3) : 512);
     DevBuf<float> q64buf, c1_lb, c1_u, rec_dt, rec_e;
-    DevBuf<int32_t> c1_p, c1_cnt, pr0, p30, rec_cnt, rec, flags, qids;
+    DevBuf<int32_t> c1_p, c1_cnt, pr0, p30, rec_cnt, rec, flags;
     DevBuf<int32_t> &qorder = out.qorder;
-    DevBuf<uint32_t> pkey, pkey_sorted;
+    DevBuf<uint32_t> pkey;
+    DevBuf<unsigned> phist;  // [kPilots] bucket sizes, [kPilots] claim cursors
     const float *q64 = q;
     if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
         RBC_CHECK(q64buf.alloc(nq * 64, st));
         pad_rows64(q, nq, idx->d, q64buf.get(), st);
         q64 = q64buf.get();
     }
-    // query order: sort by nearest pilot (stable, so equal keys keep id order)
+    // query order: counting sort by nearest pilot
     const int npilot = static_cast<int>(idx->nr < kPilots ? idx->nr : kPilots);
-    RBC_CHECK(qids.alloc(nq, st));
     RBC_CHECK(qorder.alloc(nq, st));
     RBC_CHECK(pkey.alloc(nq, st));
-    RBC_CHECK(pkey_sorted.alloc(nq, st));
-    pilot_key_kernel<<<grid_for(nq, 128), 128, 0, st>>>(q64, nq, t->reps64, t->pilots, npilot, pkey.get(), qids.get());
+    RBC_CHECK(phist.alloc(2 * kPilots, st));
+    RBC_CUDA(cudaMemsetAsync(phist.get(), 0, 2 * kPilots * sizeof(unsigned), st));
+    pilot_key_kernel<<<grid_for(nq, 128), 128, 0, st>>>(q64, nq, t->reps64, t->pilots, npilot, pkey.get(), phist.get());
     RBC_LAUNCHED();
-    {
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, pkey.get(), pkey_sorted.get(), qids.get(), qorder.get(), nq, 0, 7,
-                                        st);
-        DevBuf<unsigned char> tmp;
-        RBC_CHECK(tmp.alloc(tb, st));
-        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, pkey.get(), pkey_sorted.get(), qids.get(), qorder.get(),
-                                                 nq, 0, 7, st));
-        note_launch();
-    }
+    pilot_scatter_kernel<<<grid_for(nq, 128), 128, 0, st>>>(pkey.get(), nq, npilot, phist.get(), phist.get() + kPilots,
+                                                           qorder.get());
+    RBC_LAUNCHED();
     RBC_CHECK(c1_lb.alloc(nq * cap1, st));
     RBC_CHECK(c1_p.alloc(nq * cap1, st));
     RBC_CHECK(c1_cnt.alloc(nq, st));
