@@ -112,7 +112,8 @@ struct S2Params {
     int k;
     int ntiles;
     const int32_t *tile_order;  // LPT order
-    const int32_t *tile_rows;   // [ntiles][128] query ids (-1 = padding)
+    const int32_t *order;       // query order: tile t holds order[128 t .. 128 t + 127] (nq entries)
+    int64_t nq;
     const int64_t *work_off;    // [ntiles + 1]
     const WorkItem *work;       // [total work]
     const int32_t *cut;         // [total work][128] per-row cutoff (0 = list not a survivor for the row)
@@ -258,7 +259,7 @@ __global__ void iota_kernel(int32_t *v, int64_t n) {
 }
 
 // union of the tile's surviving lists: count
-__global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__restrict__ rows,
+__global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__restrict__ order, int64_t nq,
                                                            const int64_t *__restrict__ seg_off,
                                                            const int32_t *__restrict__ seg_cnt,
                                                            const int32_t *__restrict__ seg_list, int64_t nr,
@@ -268,7 +269,8 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) present[p] = 0;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
+    const int32_t qi = t < nq ? order[t] : -1;
     if (qi >= 0) {  // benign races: every writer stores 1
         const int64_t s0 = seg_off[qi];
         const int cnt = seg_cnt[qi];
@@ -292,14 +294,36 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
 // union of the tile's surviving lists: work items, per-row cutoffs and stage-1
 // distances, and the tile's total work (for the LPT order)
 __global__ void __launch_bounds__(kRows) tile_fill_kernel(
-    const int32_t *__restrict__ rows, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
+    const int32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ nwork, int64_t *__restrict__ work_off,
+    int32_t *__restrict__ tile_ids, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
     const int32_t *__restrict__ seg_list, const int32_t *__restrict__ seg_len, const float *__restrict__ seg_d1,
     const uint64_t *__restrict__ order_key,
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
-    const int64_t *__restrict__ offsets, const int64_t *__restrict__ work_off, WorkItem *__restrict__ work,
+    const int64_t *__restrict__ offsets, WorkItem *__restrict__ work,
     int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key, int warm,
     int64_t cap_work) {
-    if (work_off[gridDim.x] > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
+    // this tile's first work item = sum of the earlier tiles' counts (no separate scan pass);
+    // the total decides whether the caller's capacity suffices
+    __shared__ unsigned long long s_pre, s_tot;
+    {
+        unsigned long long pre = 0, tot = 0;
+        for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) {
+            const unsigned long long v = static_cast<unsigned long long>(nwork[b]);
+            tot += v;
+            if (b < static_cast<int>(blockIdx.x)) pre += v;
+        }
+        if (threadIdx.x == 0) s_pre = s_tot = 0;
+        __syncthreads();
+        atomicAdd(&s_pre, pre);
+        atomicAdd(&s_tot, tot);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        work_off[blockIdx.x] = static_cast<int64_t>(s_pre);
+        if (blockIdx.x == gridDim.x - 1) work_off[gridDim.x] = static_cast<int64_t>(s_tot);
+        tile_ids[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
+    }
+    if (static_cast<int64_t>(s_tot) > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
@@ -313,7 +337,8 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         s_work = 0;
     }
     __syncthreads();
-    const int32_t qi = rows[blockIdx.x * kRows + threadIdx.x];
+    const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
+    const int32_t qi = tq < nq ? order[tq] : -1;
     const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
     const int cnt = qi >= 0 ? seg_cnt[qi] : 0;
     {
@@ -357,8 +382,10 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int32_t front = s_front == ~0ull ? -1 : static_cast<int32_t>(s_front & 0xFFFFFFFFu);
     // with warm-up, slot w0 is a max-only copy of the first list (k = 1: it
     // tightens the running bound before any candidate is buffered)
-    const int64_t wbase = work_off[blockIdx.x];
-    const int64_t w0 = wbase + ((warm && work_off[blockIdx.x + 1] > wbase) ? 1 : 0);
+    const int64_t wbase = static_cast<int64_t>(s_pre), wn = nwork[blockIdx.x];
+    const int64_t w0 = wbase + ((warm && wn > 0) ? 1 : 0);
+    // zero this thread's cutoff column of the tile's work items (its own later writes win)
+    for (int64_t w = wbase; w < wbase + wn; ++w) cut[w * kRows + threadIdx.x] = 0;
     // ordered compaction: front first, then the others ascending (each thread a
     // contiguous range of lists, one block scan)
     {
@@ -555,7 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&tile_empty[slot]);
             if (tile < 0) break;
-            const int32_t qi = P.tile_rows[tile * kRows + row];
+            const int64_t slot_q = static_cast<int64_t>(tile) * kRows + row;
+            const int32_t qi = slot_q < P.nq ? P.order[slot_q] : -1;
             const bool live = qi >= 0;
             // this thread's quarter of the query row (rows padded to 64 floats with zeros)
             float qv[kKd];
@@ -1096,14 +1124,11 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     //    stage-2 time and without the sort; otherwise sort by that key.
     DevBuf<uint64_t> tkey, tkey_sorted;
     DevBuf<uint32_t> gkey, skey;
-    DevBuf<int32_t> ids, order_buf, rows, tids, tile_order;
-    RBC_CHECK(rows.alloc(static_cast<int64_t>(ntiles) * kRows, st));
+    DevBuf<int32_t> ids, order_buf, tids, tile_order;
     RBC_CHECK(tkey.alloc(ntiles, st));
     RBC_CHECK(tkey_sorted.alloc(ntiles, st));
     RBC_CHECK(tids.alloc(ntiles, st));
     RBC_CHECK(tile_order.alloc(ntiles, st));
-    iota_kernel<<<grid_for(ntiles, 256), 256, 0, st>>>(tids.get(), ntiles);
-    RBC_LAUNCHED();
     size_t tb2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles, 0,
                                     40, st);
@@ -1130,9 +1155,6 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     } else {
         RBC_CHECK(tmp.alloc(tb2, st));
     }
-    tile_rows_kernel<<<grid_for(static_cast<int64_t>(ntiles) * kRows, 256), 256, 0, st>>>(
-        order, nq, static_cast<int64_t>(ntiles) * kRows, rows.get());
-    RBC_LAUNCHED();
     // 2. union of surviving lists per tile
     DevBuf<int64_t> nwork, work_off;
     RBC_CHECK(nwork.alloc(ntiles, st));
@@ -1142,16 +1164,9 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
     cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
     const int warm = k == 1 ? 1 : 0;
-    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(rows.get(), po.seg_off.get(), po.nseg.get(), po.seg_list.get(), nr,
+    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(order, nq, po.seg_off.get(), po.nseg.get(), po.seg_list.get(), nr,
                                                     nwork.get(), warm);
     RBC_LAUNCHED();
-    RBC_CUDA(cudaMemsetAsync(work_off.get(), 0, sizeof(int64_t), st));
-    size_t tb3 = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, tb3, nwork.get(), work_off.get() + 1, ntiles, st);
-    DevBuf<unsigned char> tmp3;
-    RBC_CHECK(tmp3.alloc(tb3, st));
-    RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp3.get(), tb3, nwork.get(), work_off.get() + 1, ntiles, st));
-    note_launch();
     // work arrays sized from the caller's capacity (no host round trip); an
     // undersized capacity makes every consumer kernel bail out and the caller
     // re-runs with the size reported in status[0]
@@ -1160,11 +1175,11 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     DevBuf<int32_t> cut;
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
-    RBC_CUDA(cudaMemsetAsync(cut.get(), 0, sizeof(int32_t) * total_work * kRows, st));
-    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(rows.get(), po.seg_off.get(), po.nseg.get(), po.seg_list.get(),
+    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), tids.get(), po.seg_off.get(),
+                                                   po.nseg.get(), po.seg_list.get(),
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
                                                    idx->radii, tc->poff,
-                                                   idx->offsets, work_off.get(), work.get(), cut.get(),
+                                                   idx->offsets, work.get(), cut.get(),
                                                    tkey.get(), warm, cap_work);
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
@@ -1200,7 +1215,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.k = k;
     P.ntiles = ntiles;
     P.tile_order = tile_order.get();
-    P.tile_rows = rows.get();
+    P.order = order;
+    P.nq = nq;
     P.work_off = work_off.get();
     P.work = work.get();
     P.cut = cut.get();
