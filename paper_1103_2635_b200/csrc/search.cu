@@ -440,6 +440,8 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
             return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
         }
         g.launches = launch_count_now() - l0;
+        if (getenv("RBC_DEBUG_GRAPH")) fprintf(stderr, "[graph] captured nq=%lld k=%d cap=%lld arena=%.1f MB\n",
+                                               (long long)nq, k, (long long)cap, g.arena_cap / 1e6);
         g.status = status.get();
         if (!g.host_status) RBC_CUDA(cudaMallocHost(&g.host_status, 4 * sizeof(int64_t)));
     }
