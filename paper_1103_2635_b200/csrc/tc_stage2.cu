@@ -386,21 +386,37 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int64_t w0 = wbase + ((warm && wn > 0) ? 1 : 0);
     // zero this thread's cutoff column of the tile's work items (its own later writes win)
     for (int64_t w = wbase; w < wbase + wn; ++w) cut[w * kRows + threadIdx.x] = 0;
-    // ordered compaction: front first, then the others ascending (each thread a
-    // contiguous range of lists, one block scan)
+    // work order: the lists that are some row's nearest rep first, most rows first (each
+    // row's running bound tightens early, so fewer candidate groups are buffered), then
+    // the others ascending (each thread a contiguous range of lists, one block scan)
     {
+        __shared__ unsigned long long s_fkey[kRows];
+        __shared__ int s_nf;
+        if (threadIdx.x == 0) s_nf = 0;
+        __syncthreads();
+        for (int64_t p = threadIdx.x; p < nr; p += blockDim.x)
+            if (maxlen[p] > 0 && nearcnt[p] > 0) {
+                const int slot = atomicAdd(&s_nf, 1);  // <= 128 distinct nearest reps per tile
+                s_fkey[slot] = (static_cast<unsigned long long>(kRows - nearcnt[p]) << 32) | static_cast<uint64_t>(p);
+            }
         const int64_t per = (nr + kRows - 1) / kRows;
         const int64_t pa = threadIdx.x * per, pe = min(nr, pa + per);
         int c = 0;
-        for (int64_t p = pa; p < pe; ++p) c += (maxlen[p] > 0 && p != front) ? 1 : 0;
+        for (int64_t p = pa; p < pe; ++p) c += (maxlen[p] > 0 && nearcnt[p] == 0) ? 1 : 0;
         int pos, total;
         Scan(scan_tmp).ExclusiveSum(c, pos, total);
         __syncthreads();  // every count read before nearcnt is overwritten
-        pos += front >= 0 ? 1 : 0;
+        const int nf = s_nf;
         for (int64_t p = pa; p < pe; ++p)
-            if (maxlen[p] > 0 && p != front) nearcnt[p] = pos++;  // reuse as list -> work index
+            if (maxlen[p] > 0 && nearcnt[p] == 0) nearcnt[p] = nf + pos++;  // reuse as list -> work index
+        __syncthreads();  // (an F list's rank may be 0: written only after every range is done)
+        if (threadIdx.x < nf) {
+            const unsigned long long mine = s_fkey[threadIdx.x];
+            int rank = 0;
+            for (int j = 0; j < nf; ++j) rank += s_fkey[j] < mine ? 1 : 0;
+            nearcnt[static_cast<int32_t>(mine & 0xFFFFFFFFu)] = rank;
+        }
     }
-    if (front >= 0 && threadIdx.x == 0) nearcnt[front] = 0;
     __syncthreads();
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
         if (maxlen[p] > 0) {
