@@ -36,7 +36,10 @@ int64_t stage2_work_capacity(const rbc_index *idx, int64_t nq) {
 
 void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed) {
     const int64_t ntiles = (nq + 127) / 128;
-    const int64_t per = (needed + ntiles - 1) / (ntiles > 0 ? ntiles : 1) + 4;
+    // headroom: the tile composition (and so the union sizes) varies a little from call to
+    // call, and every overflow costs a stage-2 re-run plus a graph re-capture
+    const int64_t avg = (needed + ntiles - 1) / (ntiles > 0 ? ntiles : 1);
+    const int64_t per = avg + avg / 4 + 8;
     if (per > idx->s2_work_per_tile) idx->s2_work_per_tile = per;
 }
 

@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             int count = 0;     // buffered 8-column groups
             bool overflow = false;
             const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * kParts + part);
-            float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 2;
+            float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 3;
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
             int cut_n = 0;
@@ -726,33 +726,34 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     const float ut = U * kTie;
                     int c2 = 0;
                     for (int e = 0; e < count; ++e) {
-                        const float4 a = clb[2 * e], b = clb[2 * e + 1];
-                        const float lo = fminf(fminf(fminf(a.x, a.y), fminf(a.z, a.w)), fminf(fminf(b.x, b.y), fminf(b.z, b.w)));
-                        if (lo <= ut) {
-                            clb[2 * c2] = a;
-                            clb[2 * c2 + 1] = b;
+                        const float4 a = clb[3 * e], b = clb[3 * e + 1], c = clb[3 * e + 2];
+                        const float vmax = fmaxf(fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)), fmaxf(fmaxf(b.x, b.y), fmaxf(b.z, b.w)));
+                        if (fmaf(-vmax, c.y, c.x) <= ut) {  // the group's smallest lower bound (all 8 columns)
+                            clb[3 * c2] = a;
+                            clb[3 * c2 + 1] = b;
+                            clb[3 * c2 + 2] = c;
                             cpos[c2] = cpos[e];
                             ++c2;
                         }
                     }
                     count = c2;
                 };
-                // buffer a whole 8-column group (lower bounds; +inf beyond the row's cutoff) and
-                // tighten the bound with the group's best element; the exact re-rank filters
-                auto push8 = [&](const float *v, float m, int col0, int lim) {
+                // buffer a whole 8-column group -- the raw accumulator values plus (lb0, 2/scale,
+                // valid columns): lb = lb0 - V * 2/scale, computed by the re-rank -- and tighten
+                // the bound with the group's best element; the exact re-rank filters
+                auto push8 = [&](const float *v, float m, int col0, int lim, bool block_valid) {
                     if (count < P.cap) {
-                        float l[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            l[j] = col0 + j < lim ? fmaf(-v[j], inv2s, lb0) : __int_as_float(0x7f800000);
-                        clb[2 * count] = make_float4(l[0], l[1], l[2], l[3]);
-                        clb[2 * count + 1] = make_float4(l[4], l[5], l[6], l[7]);
+                        clb[3 * count] = make_float4(v[0], v[1], v[2], v[3]);
+                        clb[3 * count + 1] = make_float4(v[4], v[5], v[6], v[7]);
+                        clb[3 * count + 2] = make_float4(lb0, inv2s, __int_as_float(min(8, lim - col0)), 0.f);
                         cpos[count] = wi.csr + col0;
                         ++count;
                     } else {
                         overflow = true;
                     }
-                    if (col0 + 8 <= lim) {  // the group's best is a valid element: its ub bounds the k-th best
+                    // the group's best is a valid element: its ub bounds the k-th best (k = 1 and a
+                    // fully valid block: the block maximum already did)
+                    if (col0 + 8 <= lim && (KT > 1 || !block_valid)) {
                         const float ub = fmaf(-m, inv2s, lb0) + 2.0f * E;
                         if (KT == 1) {
                             U = fminf(U, ub);
@@ -837,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                             const int base = off + hb + c0, llim = off + hb + lim;
 #pragma unroll
                             for (int s = 0; s < 4; ++s)
-                                if (m8[s] >= T) push8(va + 8 * s, m8[s], base + 8 * s, llim);
+                                if (m8[s] >= T) push8(va + 8 * s, m8[s], base + 8 * s, llim, c0 + 32 <= lim);
                         }
                     }
                     sm100::tc_fence_before();
@@ -925,11 +926,12 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
                     h = u + 1;
                 }
             const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
-            const float4 l0 = cand_lb[2 * at], l1 = cand_lb[2 * at + 1];
+            const float4 v0 = cand_lb[3 * at], v1 = cand_lb[3 * at + 1], mt = cand_lb[3 * at + 2];
             pos = cand_pos[at];
-            const float l[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+            const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            const int valid = __float_as_int(mt.z);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) pass |= (l[j] <= ufin ? 1u : 0u) << j;
+            for (int j = 0; j < 8; ++j) pass |= (j < valid && fmaf(-v[j], mt.y, mt.x) <= ufin ? 1u : 0u) << j;
         }
         if (!fast) {  // generic d: each lane re-ranks its own group's elements
             while (pass) {
@@ -1205,7 +1207,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     const int cap = 12 + 6 * k;  // 8-column groups per query and column part
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, cand_count, ovf_list, counters;
-    RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 8, st));
+    RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 12, st));
     RBC_CHECK(cand_pos.alloc(nq * kParts * cap, st));
     RBC_CHECK(cand_count.alloc(nq * kParts, st));
     RBC_CHECK(cand_ufin.alloc(nq * kParts, st));
