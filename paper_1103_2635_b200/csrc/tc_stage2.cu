@@ -114,7 +114,9 @@ struct S2Params {
     const int32_t *tile_order;  // LPT order
     const int32_t *order;       // query order: tile t holds order[128 t .. 128 t + 127] (nq entries)
     int64_t nq;
-    const int64_t *work_off;    // [ntiles + 1]
+    const int64_t *work_off;    // [ntiles] first work item of each tile
+    const int64_t *nwork;       // [ntiles] its work items
+    const unsigned long long *work_total;
     const WorkItem *work;       // [total work]
     const int32_t *cut;         // [total work][128] per-row cutoff (0 = list not a survivor for the row)
     float *cand_lb;
@@ -263,7 +265,8 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
                                                            const int64_t *__restrict__ seg_off,
                                                            const int32_t *__restrict__ seg_cnt,
                                                            const int32_t *__restrict__ seg_list, int64_t nr,
-                                                           int64_t *__restrict__ nwork, int warm) {
+                                                           int64_t *__restrict__ nwork, int64_t *__restrict__ work_off,
+                                                           unsigned long long *__restrict__ work_total, int warm) {
     extern __shared__ int32_t present[];
     __shared__ int s_count;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) present[p] = 0;
@@ -288,13 +291,18 @@ __global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__rest
     atomicAdd(&s_count, c);
     __syncthreads();
     // + 1 warm-up (max-only) copy of the first list when warm
-    if (threadIdx.x == 0) nwork[blockIdx.x] = s_count + (warm && s_count > 0 ? 1 : 0);
+    if (threadIdx.x == 0) {  // the tile's work items: a range claimed in the shared work array
+        const int64_t nw = s_count + (warm && s_count > 0 ? 1 : 0);
+        nwork[blockIdx.x] = nw;
+        work_off[blockIdx.x] = static_cast<int64_t>(atomicAdd(work_total, static_cast<unsigned long long>(nw)));
+    }
 }
 
 // union of the tile's surviving lists: work items, per-row cutoffs and stage-1
 // distances, and the tile's total work (for the LPT order)
 __global__ void __launch_bounds__(kRows) tile_fill_kernel(
-    const int32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ nwork, int64_t *__restrict__ work_off,
+    const int32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ nwork,
+    const int64_t *__restrict__ work_off, const unsigned long long *__restrict__ work_total,
     int32_t *__restrict__ tile_ids, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
     const int32_t *__restrict__ seg_list, const int32_t *__restrict__ seg_len, const float *__restrict__ seg_d1,
     const uint64_t *__restrict__ order_key,
@@ -302,28 +310,8 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int64_t *__restrict__ offsets, WorkItem *__restrict__ work,
     int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key, int warm,
     int64_t cap_work) {
-    // this tile's first work item = sum of the earlier tiles' counts (no separate scan pass);
-    // the total decides whether the caller's capacity suffices
-    __shared__ unsigned long long s_pre, s_tot;
-    {
-        unsigned long long pre = 0, tot = 0;
-        for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) {
-            const unsigned long long v = static_cast<unsigned long long>(nwork[b]);
-            tot += v;
-            if (b < static_cast<int>(blockIdx.x)) pre += v;
-        }
-        if (threadIdx.x == 0) s_pre = s_tot = 0;
-        __syncthreads();
-        atomicAdd(&s_pre, pre);
-        atomicAdd(&s_tot, tot);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        work_off[blockIdx.x] = static_cast<int64_t>(s_pre);
-        if (blockIdx.x == gridDim.x - 1) work_off[gridDim.x] = static_cast<int64_t>(s_tot);
-        tile_ids[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
-    }
-    if (static_cast<int64_t>(s_tot) > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
+    if (threadIdx.x == 0) tile_ids[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
+    if (static_cast<int64_t>(*work_total) > cap_work) return;  // capacity exceeded: the caller re-runs
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
@@ -382,7 +370,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int32_t front = s_front == ~0ull ? -1 : static_cast<int32_t>(s_front & 0xFFFFFFFFu);
     // with warm-up, slot w0 is a max-only copy of the first list (k = 1: it
     // tightens the running bound before any candidate is buffered)
-    const int64_t wbase = static_cast<int64_t>(s_pre), wn = nwork[blockIdx.x];
+    const int64_t wbase = work_off[blockIdx.x], wn = nwork[blockIdx.x];
     const int64_t w0 = wbase + ((warm && wn > 0) ? 1 : 0);
     // zero this thread's cutoff column of the tile's work items (its own later writes win)
     for (int64_t w = wbase; w < wbase + wn; ++w) cut[w * kRows + threadIdx.x] = 0;
@@ -472,7 +460,7 @@ __device__ __forceinline__ float pick8(const float *v, int j) {
 
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
-    if (P.work_off[P.ntiles] > P.cap_work) return;  // work arrays incomplete (see tile_fill_kernel)
+    if (static_cast<int64_t>(*P.work_total) > P.cap_work) return;  // work arrays incomplete (see tile_fill_kernel)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *sB = smem;                                   // kStages x (plane 0 | plane 1)
@@ -521,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 s_tiles[slot] = tile;
                 sm100::mbar_arrive(&tile_full[slot]);
                 if (tile < 0) break;
-                for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
+                for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w) {
                     const WorkItem wi = P.work[w];
                     for (int off = 0; off < wi.ext; off += kNmax) {
                         const int n = min(kNmax, roundup16(wi.ext - off));
@@ -550,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const int tile = s_tiles[slot];
                 sm100::mbar_arrive(&tile_empty[slot]);
                 if (tile < 0) break;
-                for (int64_t w = P.work_off[tile], w1 = P.work_off[tile + 1]; w < w1; ++w) {
+                for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w) {
                     const int ext = P.work[w].ext;
                     const uint32_t a = ai & 1;
                     S2_WAIT(&afull[a], (ai >> 1) & 1, 1);
@@ -615,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     qv[4 * c + 3] = t.w;
                 }
             }
-            const int64_t w0 = P.work_off[tile], w1 = P.work_off[tile + 1];
+            const int64_t w0 = P.work_off[tile], w1 = w0 + P.nwork[tile];
             // A operand of list w: this thread's kKd * 2 bytes of row `row` (+ the aug columns, last part)
             auto prep_a = [&](int64_t w) {
                 S2_TIME(const unsigned long long tp0 = clock64());
@@ -1039,9 +1027,9 @@ __global__ void __launch_bounds__(256) overflow_scan_kernel(const float *__restr
     }
 }
 
-__global__ void stage2_status_kernel(const int64_t *__restrict__ work_off, int ntiles,
+__global__ void stage2_status_kernel(const unsigned long long *__restrict__ work_total,
                                      const int32_t *__restrict__ ovf_count, int64_t *__restrict__ status) {
-    status[0] = work_off[ntiles];
+    status[0] = static_cast<int64_t>(*work_total);
     status[1] = *ovf_count;
 }
 
@@ -1175,15 +1163,18 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     }
     // 2. union of surviving lists per tile
     DevBuf<int64_t> nwork, work_off;
+    DevBuf<unsigned long long> work_total;
     RBC_CHECK(nwork.alloc(ntiles, st));
-    RBC_CHECK(work_off.alloc(ntiles + 1, st));
+    RBC_CHECK(work_off.alloc(ntiles, st));
+    RBC_CHECK(work_total.alloc(1, st));
+    RBC_CUDA(cudaMemsetAsync(work_total.get(), 0, sizeof(unsigned long long), st));
     const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
     if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
     cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
     cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
     const int warm = k == 1 ? 1 : 0;
     tile_count_kernel<<<ntiles, kRows, smem1, st>>>(order, nq, po.seg_off.get(), po.nseg.get(), po.seg_list.get(), nr,
-                                                    nwork.get(), warm);
+                                                    nwork.get(), work_off.get(), work_total.get(), warm);
     RBC_LAUNCHED();
     // work arrays sized from the caller's capacity (no host round trip); an
     // undersized capacity makes every consumer kernel bail out and the caller
@@ -1193,7 +1184,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     DevBuf<int32_t> cut;
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
-    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), tids.get(), po.seg_off.get(),
+    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), work_total.get(), tids.get(),
+                                                   po.seg_off.get(),
                                                    po.nseg.get(), po.seg_list.get(),
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
                                                    idx->radii, tc->poff,
@@ -1236,6 +1228,8 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.order = order;
     P.nq = nq;
     P.work_off = work_off.get();
+    P.nwork = nwork.get();
+    P.work_total = work_total.get();
     P.work = work.get();
     P.cut = cut.get();
     P.cand_lb = cand_lb.get();
@@ -1301,7 +1295,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         else overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
         RBC_LAUNCHED();
     }
-    stage2_status_kernel<<<1, 1, 0, st>>>(work_off.get(), ntiles, counters.get(), status_dev);
+    stage2_status_kernel<<<1, 1, 0, st>>>(work_total.get(), counters.get(), status_dev);
     RBC_LAUNCHED();
 #ifdef RBC_S2_TIMING
     if (getenv("RBC_DEBUG_S2")) {  // diagnostic: role timing (synchronises)
