@@ -340,10 +340,19 @@ struct SearchGraph {
     }
 };
 
+// a few captured call shapes per index (e.g. the two halves of a pipelined host call)
+struct SearchGraphCache {
+    static constexpr int kSlots = 2;
+    std::mutex mu;
+    SearchGraph slots[kSlots];
+    uint64_t last_use[kSlots] = {0, 0};
+    uint64_t tick = 0;
+};
+
 void search_graph_release(const rbc_index *idx) {
     if (!idx->graph) return;
     cudaDeviceSynchronize();
-    delete static_cast<SearchGraph *>(idx->graph);
+    delete static_cast<SearchGraphCache *>(idx->graph);
     idx->graph = nullptr;
 }
 
@@ -372,16 +381,29 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
     const bool fused = !force_exact_engine() && tc_stage1_supported(idx, k);
     if (!fused || nq == 0 || nq > (int64_t(1) << 20) || profiling_on() || getenv("RBC_NO_GRAPH"))
         return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
-    if (!idx->graph) idx->graph = new SearchGraph();
-    SearchGraph &g = *static_cast<SearchGraph *>(idx->graph);
-    std::unique_lock<std::mutex> lock(g.mu, std::try_to_lock);
+    if (!idx->graph) idx->graph = new SearchGraphCache();
+    SearchGraphCache &gc = *static_cast<SearchGraphCache *>(idx->graph);
+    std::unique_lock<std::mutex> lock(gc.mu, std::try_to_lock);
     if (!lock.owns_lock()) return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);  // concurrent caller
     const int64_t cap = stage2_work_capacity(idx, nq);
     const bool tc2 = tc_stage2_supported(idx, k);
-    const bool same = g.q == q && g.nq == nq && g.k == k && g.keys == keys && g.cap == cap && g.tc2 == tc2 &&
-                      g.stats.gamma == stats.gamma && g.stats.candidates == stats.candidates &&
-                      g.stats.reps_pruned_radius == stats.reps_pruned_radius &&
-                      g.stats.reps_pruned_3gamma == stats.reps_pruned_3gamma;
+    auto matches = [&](const SearchGraph &c) {
+        return c.q == q && c.nq == nq && c.k == k && c.keys == keys && c.cap == cap && c.tc2 == tc2 &&
+               c.stats.gamma == stats.gamma && c.stats.candidates == stats.candidates &&
+               c.stats.reps_pruned_radius == stats.reps_pruned_radius &&
+               c.stats.reps_pruned_3gamma == stats.reps_pruned_3gamma;
+    };
+    int si = -1;
+    for (int j = 0; j < SearchGraphCache::kSlots; ++j)
+        if (matches(gc.slots[j])) si = j;
+    if (si < 0) {  // least recently used slot
+        si = 0;
+        for (int j = 1; j < SearchGraphCache::kSlots; ++j)
+            if (gc.last_use[j] < gc.last_use[si]) si = j;
+    }
+    gc.last_use[si] = ++gc.tick;
+    SearchGraph &g = gc.slots[si];
+    const bool same = matches(g);
     if (!same) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         g.exec = nullptr;
