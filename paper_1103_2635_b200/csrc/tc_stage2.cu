@@ -1172,7 +1172,10 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
     cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
     cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
-    const int warm = k == 1 ? 1 : 0;
+    // max-only warm-up copy of each tile's first list (k = 1): off -- with the nearest-rep
+    // lists ordered first the bounds tighten early anyway, and the extra list cost more
+    // (stage 2 540 vs 573 us, re-rank 60 vs 52 us at cfg2); RBC_S2_WARM=1 turns it on
+    const int warm = (k == 1 && getenv("RBC_S2_WARM")) ? 1 : 0;
     tile_count_kernel<<<ntiles, kRows, smem1, st>>>(order, nq, po.seg_off.get(), po.nseg.get(), po.seg_list.get(), nr,
                                                     nwork.get(), work_off.get(), work_total.get(), warm);
     RBC_LAUNCHED();
