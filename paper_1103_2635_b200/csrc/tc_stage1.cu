@@ -75,6 +75,8 @@ struct Tc1Index {
     float *lskip = nullptr;  // [nr][32] list_dists at the end of each of 32 equal blocks (cutoff skip table)
     float *reps64 = nullptr; // [nr][64] representatives, zero padded (16-byte rows for the fix-up)
     int32_t *pilots = nullptr; // [kPilots] farthest-point sample of the reps (query ordering)
+    uint4 *prow = nullptr;     // [kPilots * 8] pilot rows as f16
+    float *pnorm = nullptr;    // [kPilots] |pilot|^2 / 2
     float sG = 1.f, rmax = 0.f;
 };
 
@@ -289,70 +291,107 @@ __global__ void __launch_bounds__(1024) pilot_fps_kernel(const float *__restrict
 // (f16 products, max of q.r - |r|^2/2): it only decides which queries share a
 // tile, never a result.  Queries of one region then share their near reps, so
 // the per-tile slow paths run in lockstep.
-__global__ void __launch_bounds__(128) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
-                                                        const float *__restrict__ reps64, const int32_t *__restrict__ pilots,
-                                                        int npilot, uint32_t *__restrict__ key,
-                                                        unsigned *__restrict__ hist) {
-    __shared__ uint4 sp[kPilots * 8];  // pilot rows, 64 f16 each
-    __shared__ float sn[kPilots];      // |r|^2 / 2
-    __shared__ unsigned sh[kPilots];   // this block's bucket counts
-    for (int j = threadIdx.x; j < kPilots; j += blockDim.x) sh[j] = 0;
-    for (int t = threadIdx.x; t < npilot * 8; t += blockDim.x) {
+// pilot rows as f16 (64 per row) and |r|^2 / 2, once per index
+__global__ void pilot_rows_kernel(const float *__restrict__ reps64, const int32_t *__restrict__ pilots, int npilot,
+                                  uint4 *__restrict__ prow, float *__restrict__ pnorm) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < npilot * 8) {
         const int j = t >> 3, c = t & 7;
         const float4 *row = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[j]) * 64) + 2 * c;
         const float4 a = __ldg(row), b = __ldg(row + 1);
-        sp[t] = make_uint4(sm100::pack_f16x2_sat(a.x, a.y), sm100::pack_f16x2_sat(a.z, a.w),
-                           sm100::pack_f16x2_sat(b.x, b.y), sm100::pack_f16x2_sat(b.z, b.w));
+        prow[t] = make_uint4(sm100::pack_f16x2_sat(a.x, a.y), sm100::pack_f16x2_sat(a.z, a.w),
+                             sm100::pack_f16x2_sat(b.x, b.y), sm100::pack_f16x2_sat(b.z, b.w));
     }
-    for (int j = threadIdx.x; j < npilot; j += blockDim.x) {
-        const float4 *row = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[j]) * 64);
+    if (t < npilot) {
+        const float4 *row = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[t]) * 64);
         float n = 0.f;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
             const float4 v = __ldg(row + c);
             n = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, n))));
         }
-        sn[j] = 0.5f * n;
+        pnorm[t] = 0.5f * n;
+    }
+}
+
+// Query ordering key: nearest of the kPilots pilots, as a small tensor-core GEMM
+// (mma.sync m16n8k16, f16 inputs, fp32 accumulate): one warp scores 16 queries against
+// all 64 pilots (argmax of q.p - |p|^2 / 2).  Approximate on purpose: it only decides
+// which queries share a tile, never a result.
+constexpr int kPilotWarps = 8;  // 128 queries per block
+__device__ __forceinline__ uint32_t f2h2(float a, float b) { return sm100::pack_f16x2_sat(a, b); }
+
+__global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
+                                                                    const uint4 *__restrict__ prow,
+                                                                    const float *__restrict__ pnorm, int npilot,
+                                                                    uint32_t *__restrict__ key,
+                                                                    unsigned *__restrict__ hist) {
+    __shared__ uint32_t sp[kPilots * 32];  // pilot rows, 64 f16 (32 words) each; absent pilots zero
+    __shared__ float sn[kPilots];
+    __shared__ unsigned sh[kPilots];
+    for (int t = threadIdx.x; t < kPilots * 8; t += blockDim.x) {
+        const uint4 v = t < npilot * 8 ? prow[t] : make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4 *>(sp)[t] = v;
+    }
+    for (int j = threadIdx.x; j < kPilots; j += blockDim.x) {
+        sh[j] = 0;
+        sn[j] = j < npilot ? pnorm[j] : __int_as_float(0x7f800000);  // absent pilots never win
     }
     __syncthreads();
-    const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    const bool live = i0 < nq;
-    const int64_t i = live ? i0 : nq - 1;
-    __half2 qh[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+    const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kPilotWarps + warp) * 16;
+    const int64_t ra = r0 + g < nq ? r0 + g : nq - 1, rb = r0 + g + 8 < nq ? r0 + g + 8 : nq - 1;
+    const float *qa = q64 + ra * 64, *qb = q64 + rb * 64;
+    float acc[8][4];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(q64 + i * 64) + c);
-        qh[2 * c] = __floats2half2_rn(v.x, v.y);
-        qh[2 * c + 1] = __floats2half2_rn(v.z, v.w);
-    }
-    float best = -__int_as_float(0x7f800000);
-    int bj = 0;
-    for (int j = 0; j < npilot; ++j) {
-        const uint4 *row = sp + j * 8;
-        __half2 acc[4];
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = __float2half2_rn(0.f);
+    for (int ks = 0; ks < 4; ++ks) {
+        const int c0 = 16 * ks + 2 * t4;
+        const float2 x0 = __ldg(reinterpret_cast<const float2 *>(qa + c0));
+        const float2 x1 = __ldg(reinterpret_cast<const float2 *>(qb + c0));
+        const float2 x2 = __ldg(reinterpret_cast<const float2 *>(qa + c0 + 8));
+        const float2 x3 = __ldg(reinterpret_cast<const float2 *>(qb + c0 + 8));
+        const uint32_t a0 = f2h2(x0.x, x0.y), a1 = f2h2(x1.x, x1.y), a2 = f2h2(x2.x, x2.y), a3 = f2h2(x3.x, x3.y);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const uint4 v = row[c];
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                __half2 r;
-                *reinterpret_cast<uint32_t *>(&r) = w[e];
-                acc[c & 3] = __hfma2(qh[4 * c + e], r, acc[c & 3]);
-            }
-        }
-        const float2 s0 = __half22float2(__hadd2(acc[0], acc[1])), s1 = __half22float2(__hadd2(acc[2], acc[3]));
-        const float score = (s0.x + s0.y) + (s1.x + s1.y) - sn[j];
-        if (score > best) {
-            best = score;
-            bj = j;
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t *prow_n = sp + (8 * j + g) * 32;  // pilot n = 8 j + g, words = dim pairs
+            const uint32_t b0 = prow_n[(16 * ks + 2 * t4) >> 1], b1 = prow_n[(16 * ks + 8 + 2 * t4) >> 1];
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};"
+                : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
+                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
         }
     }
-    if (live) {
-        key[i] = static_cast<uint32_t>(bj);
-        atomicAdd(&sh[bj], 1u);
+    // rows g (acc[.][0..1]) and g + 8 (acc[.][2..3]); columns 8 j + 2 t4 (+1)
+    float bestA = -__int_as_float(0x7f800000), bestB = bestA;
+    int jA = 0, jB = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int n = 8 * j + 2 * t4 + h;
+            const float sA = acc[j][h] - sn[n], sB = acc[j][2 + h] - sn[n];
+            if (sA > bestA) bestA = sA, jA = n;
+            if (sB > bestB) bestB = sB, jB = n;
+        }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {  // the 4 lanes of the row group
+        const float vA = __shfl_xor_sync(0xffffffffu, bestA, o), vB = __shfl_xor_sync(0xffffffffu, bestB, o);
+        const int iA = __shfl_xor_sync(0xffffffffu, jA, o), iB = __shfl_xor_sync(0xffffffffu, jB, o);
+        if (vA > bestA || (vA == bestA && iA < jA)) bestA = vA, jA = iA;
+        if (vB > bestB || (vB == bestB && iB < jB)) bestB = vB, jB = iB;
+    }
+    if (t4 == 0) {
+        if (r0 + g < nq) {
+            key[r0 + g] = static_cast<uint32_t>(jA);
+            atomicAdd(&sh[jA], 1u);
+        }
+        if (r0 + g + 8 < nq) {
+            key[r0 + g + 8] = static_cast<uint32_t>(jB);
+            atomicAdd(&sh[jB], 1u);
+        }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < npilot; j += blockDim.x)
@@ -1068,6 +1107,8 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
               cudaMalloc(&t->stat, 2 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->reps64, idx->nr * 64 * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&t->pilots, kPilots * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc(&t->prow, kPilots * 8 * sizeof(uint4)) == cudaSuccess &&
+              cudaMalloc(&t->pnorm, kPilots * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&rmax_bits, sizeof(unsigned)) == cudaSuccess;
     auto cleanup = [&](int rc) {
         cudaFree(t->rb);
@@ -1077,6 +1118,8 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaFree(t->stat);
         cudaFree(t->reps64);
         cudaFree(t->pilots);
+        cudaFree(t->prow);
+        cudaFree(t->pnorm);
         cudaFree(rmax_bits);
         delete t;
         return rc;
@@ -1100,8 +1143,9 @@ int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
         const size_t fsmem = sizeof(float) * idx->nr;
         cudaFuncSetAttribute(pilot_fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem));
         pilot_fps_kernel<<<1, 1024, fsmem, st>>>(t->reps64, idx->nr, npilot, t->pilots);
+        pilot_rows_kernel<<<grid_for(npilot * 8, 256), 256, 0, st>>>(t->reps64, t->pilots, npilot, t->prow, t->pnorm);
     }
-    note_launch(8);
+    note_launch(9);
     float stat[2] = {1.f, 0.f};
     if (cudaMemcpyAsync(stat, t->stat, sizeof(stat), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -1125,6 +1169,8 @@ void tc1_index_release(rbc_index *idx) {
     cudaFree(t->stat);
     cudaFree(t->reps64);
     cudaFree(t->pilots);
+    cudaFree(t->prow);
+    cudaFree(t->pnorm);
     delete t;
     idx->tc1 = nullptr;
 }
@@ -1159,7 +1205,8 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(pkey.alloc(nq, st));
     RBC_CHECK(phist.alloc(2 * kPilots, st));
     RBC_CUDA(cudaMemsetAsync(phist.get(), 0, 2 * kPilots * sizeof(unsigned), st));
-    pilot_key_kernel<<<grid_for(nq, 128), 128, 0, st>>>(q64, nq, t->reps64, t->pilots, npilot, pkey.get(), phist.get());
+    pilot_key_kernel<<<grid_for(nq, kPilotWarps * 16), kPilotWarps * 32, 0, st>>>(q64, nq, t->prow, t->pnorm, npilot,
+                                                                                  pkey.get(), phist.get());
     RBC_LAUNCHED();
     pilot_scatter_kernel<<<grid_for(nq, 128), 128, 0, st>>>(pkey.get(), nq, npilot, phist.get(), phist.get() + kPilots,
                                                            qorder.get());
