@@ -297,7 +297,8 @@ def main():
     os.sched_setaffinity(0, old_aff)
     # median: the host call's wall time carries OS scheduling noise; min/median/max go to stderr
     e2e_s = statistics.median(e2e_times)
-    log(f"e2e host cpus: {len(local_cpus) if local_cpus else 'unrestricted'}")
+    log(f"e2e host cpus: {len(local_cpus) if local_cpus else 'unrestricted'}; per-call ms: "
+        + " ".join(f"{1e3 * t:.2f}" for t in e2e_times))
     log(f"e2e ms: min {1e3 * min(e2e_times):.3f} median {1e3 * e2e_s:.3f} max {1e3 * max(e2e_times):.3f} "
         f"(n={len(e2e_times)})")
     if dist:
