@@ -376,10 +376,19 @@ static int enqueue_fused(const rbc_index *idx, const float *q, int64_t m, int k,
 int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
                              const rbc_search_stats &stats, cudaStream_t st);
 
+// queries per fused chunk: the per-query record and segment rows hold |R| entries each
+// (~28 B per entry), kept to ~4 GB of scratch per chunk
+static int64_t fused_chunk_limit(const rbc_index *idx) {
+    const int64_t per_query = 28 * (idx->nr + 4) + 4096;
+    int64_t lim = (int64_t(4) << 30) / per_query;
+    if (lim < 4096) lim = 4096;
+    return lim < (int64_t(1) << 20) ? lim : (int64_t(1) << 20);
+}
+
 int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
                       const rbc_search_stats &stats, cudaStream_t st) {
     const bool fused = !force_exact_engine() && tc_stage1_supported(idx, k);
-    if (!fused || nq == 0 || nq > (int64_t(1) << 20) || profiling_on() || getenv("RBC_NO_GRAPH"))
+    if (!fused || nq == 0 || nq > fused_chunk_limit(idx) || profiling_on() || getenv("RBC_NO_GRAPH"))
         return exact_search_keys_direct(idx, q, nq, k, keys, stats, st);
     if (!idx->graph) idx->graph = new SearchGraphCache();
     SearchGraphCache &gc = *static_cast<SearchGraphCache *>(idx->graph);
@@ -497,7 +506,7 @@ int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, i
     if (nq == 0) return RBC_OK;
     const bool fused = !force_exact_engine() && tc_stage1_supported(idx, k);
     // bound the stage-1 block to ~1 GiB per chunk (the fused path holds no |Q| x |R| block)
-    int64_t chunk = fused ? (int64_t(1) << 20) : (int64_t(1) << 28) / (idx->nr > 0 ? idx->nr : 1);
+    int64_t chunk = fused ? fused_chunk_limit(idx) : (int64_t(1) << 28) / (idx->nr > 0 ? idx->nr : 1);
     if (chunk < 1) chunk = 1;
     if (chunk > nq) chunk = nq;
     DevBuf<float> d1;
@@ -513,9 +522,9 @@ int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, i
             // stream-ordered with a single host round trip; rare buffer overflows re-run below
             DevBuf<int32_t> s1fail;
             DevBuf<int64_t> s2status;
-            RBC_CHECK(s1fail.alloc(1, st));
+            RBC_CHECK(s1fail.alloc(2, st));  // [0] flag, [1] diagnostic reason bits
             RBC_CHECK(s2status.alloc(2, st));
-            RBC_CUDA(cudaMemsetAsync(s1fail.get(), 0, sizeof(int32_t), st));
+            RBC_CUDA(cudaMemsetAsync(s1fail.get(), 0, 2 * sizeof(int32_t), st));
             HostClock hc;
             {
                 ProfScope ps(kPhaseStage1, st);
@@ -535,6 +544,13 @@ int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, i
             if (tc2) RBC_CUDA(cudaMemcpyAsync(s2, s2status.get(), sizeof(s2), cudaMemcpyDeviceToHost, st));
             RBC_CUDA(cudaStreamSynchronize(st));
             hc.mark("synced");
+#ifdef RBC_FAIL_WHY
+            {
+                int32_t why[2] = {0, 0};
+                cudaMemcpy(why, s1fail.get(), sizeof(why), cudaMemcpyDeviceToHost);
+                fprintf(stderr, "[s1 fail] flag %d why 0x%x\n", why[0], why[1]);
+            }
+#endif
             if (!f) {
                 if (!tc2 || s2[0] > cap) {
                     if (tc2) stage2_note_work(idx, m, s2[0]);

@@ -706,6 +706,9 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                             if (count + 8 > P.cap1) {
                                 fail = true;
                                 take = false;
+#ifdef RBC_FAIL_WHY
+                                atomicOr(P.fail + 1, 1);
+#endif
                             }
                         }
                         unsigned hit = 0;  // the group's elements that qualify, then only those
@@ -749,6 +752,10 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
             // U >= gamma_k^2 (U is an achieved k-th smallest upper bound)
             const float Uk = U;
             if (live && !(Uk < __int_as_float(0x7f800000))) fail = true;  // fewer than k candidates
+#ifdef RBC_FAIL_WHY
+            if (live && !(Uk < __int_as_float(0x7f800000))) atomicOr(P.fail + 1, 2);
+            if (live && acoef == 0.0f) atomicOr(P.fail + 1, 4);
+#endif
             const float ghi = sqrtf(Uk * kTie) * kUp;
             const float t9hi = 9.0f * ghi * ghi * (1.0f + kEps);
 
@@ -823,6 +830,9 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                 ++ti;
             }
             if (rc > P.cap_rec) fail = true;
+#ifdef RBC_FAIL_WHY
+            if (rc > P.cap_rec) atomicOr(P.fail + 1, 8);
+#endif
             if (live) {
                 // a failed row gets inert, in-range outputs: the batch is re-run on the
                 // exact path, but the fix-up and stage 2 are already queued behind this kernel
@@ -988,6 +998,9 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stag
     }
     if (ok && kth == kEmptyKey) {  // cannot happen with a consistent bound; keep the result exact anyway
         if (sub == 0) atomicExch(fail, 1);
+#ifdef RBC_FAIL_WHY
+        if (sub == 0) atomicOr(fail + 1, 16);
+#endif
         ok = false;
     }
     const float gf = ok ? key_dist(kth) : 0.f;
@@ -1186,8 +1199,10 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     const Tc1Index *t = static_cast<const Tc1Index *>(idx->tc1);
     const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
     const int cap1 = 32 + 16 * k;
-    // per-query record / segment rows, a multiple of 4 entries (16-byte aligned rows for the tile kernels)
-    const int cap_rec = static_cast<int>(idx->nr < 512 ? (idx->nr + 3) & ~int64_t(3) : 512);
+    // per-query record / segment rows: room for every representative (a query whose k-th
+    // nearest rep lies far away keeps most reps within 3 gamma_k), a multiple of 4 entries
+    // (16-byte aligned rows for the tile kernels); the caller bounds nq (fused_chunk_limit)
+    const int cap_rec = static_cast<int>((idx->nr + 3) & ~int64_t(3));
     DevBuf<float> q64buf, c1_lb, c1_u, rec_dt, rec_e;
     DevBuf<int32_t> c1_p, c1_cnt, pr0, p30, rec_cnt, rec, flags;
     DevBuf<int32_t> &qorder = out.qorder;
