@@ -217,6 +217,7 @@ def run_reference(args, rank, world):
 
 
 def main():
+    global K, METRIC
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -224,7 +225,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf", action="store_true")
+    ap.add_argument("--k", type=int, default=K, help="neighbours per query (the headline line is k=1)")
     args = ap.parse_args()
+    if args.k != K:
+        K = args.k
+        METRIC = METRIC.replace("exact 1-NN", f"exact {K}-NN")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -403,7 +408,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "cfg2: exact RBC 1-NN L2, clusters n=1M d=64 C=64 sigma=0.05, |R|=1016",
+                "config": {"workload": f"cfg2: exact RBC {K}-NN L2, clusters n=1M d=64 C=64 sigma=0.05, |R|=1016",
                            "queries_per_rank": NQ, "k": K, "n_reps": n_reps, "parallelism": f"query-shard x{world}",
                            "l2_flush": "256 MiB write between timed steps", "index_build_s": build_s,
                            "mean_candidates": float(cand_h.mean()), "flops_per_step": flops_per_step,
