@@ -899,7 +899,7 @@ __device__ __forceinline__ uint64_t group_min_u64(uint64_t v) {
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stage1_fixup_kernel(
+__global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 5 : (KT <= 8 ? 4 : 2)) stage1_fixup_kernel(
     const float *__restrict__ q64, const int32_t *__restrict__ qorder, const float *__restrict__ reps64, int64_t nq,
     int k, const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
     const float *__restrict__ lskip, const float *__restrict__ c1_lb, const int32_t *__restrict__ c1_p, int cap1,
@@ -932,8 +932,8 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stag
     // the reference's unless the tree sum's square root lies within 2^-44 (relative) of an fp32
     // rounding midpoint -- the sequential and tree sums differ by at most 2 * 63 * 2^-53
     // relative -- in which case the owner lane recomputes the sequential sum.
-    auto coop_exact = [&](bool need, int32_t p) -> float {
-        float res = 0.f;
+    auto coop_sq64 = [&](bool need, int32_t p) -> double {
+        double res = 0.0;
         unsigned gm = (__ballot_sync(0xffffffffu, need) >> gshift) & ((1u << kFixLanes) - 1u);
         const int cnt = __popc(gm);
         const int mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
@@ -952,38 +952,97 @@ __global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 6 : 4) stag
             }
 #pragma unroll
             for (int o = kFixLanes / 2; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-            if (t < cnt && sub == src) {
-                const double r = __dsqrt_rn(part);
-                float f = __double2float_rn(r);
-                const double mlo = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, -INFINITY)));
-                const double mhi = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, INFINITY)));
-                const double dl = 5.684341886080802e-14;  // 2^-44
-                if (!(r * (1.0 - dl) > mlo && r * (1.0 + dl) < mhi))
-                    f = exact_dist64(qv, reps64 + static_cast<int64_t>(pp) * 64);  // near a midpoint
-                res = f;
-            }
+            if (t < cnt && sub == src) res = part;
         }
         return res;
     };
-    // ---- gamma_k: exact distances of the candidates with lb <= U_k (lanes over candidates)
+    // the reference's fp32 distance from a tree sum of its 64 terms (see coop_sq64): taken
+    // unless the root lies within 2^-44 (relative) of an fp32 rounding midpoint, in which
+    // case the sequential sum is recomputed
+    auto verified = [&](double d2, int32_t p) -> float {
+        const double r = __dsqrt_rn(d2);
+        float f = __double2float_rn(r);
+        const double mlo = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, -INFINITY)));
+        const double mhi = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, INFINITY)));
+        const double dl = 5.684341886080802e-14;  // 2^-44
+        if (!(r * (1.0 - dl) > mlo && r * (1.0 + dl) < mhi))
+            f = exact_dist64(qv, reps64 + static_cast<int64_t>(p) * 64);  // near a midpoint
+        return f;
+    };
+    // ---- gamma_k over the candidates with lb <= U_k (lanes over candidates): the tree sums
+    // (within 2^-45 of the sequential sums) of every candidate, then fp32 keys (verified
+    // roots) only for the candidates within 2^-20 of the k-th smallest sum -- any other
+    // candidate's distance exceeds the k nearest ones' by more than 2^-21 (relative), i.e.
+    // by at least two fp32 ulps, so it cannot reach the k smallest keys (nor tie with them)
     const float ufin = ok ? c1_u[i] : 0.f;
     const int m1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(ok ? n1 : 0));
-    uint64_t best[KT];
+    double bd[KT];
+    int32_t bp[KT];
 #pragma unroll
-    for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+    for (int j = 0; j < KT; ++j) {
+        bd[j] = __longlong_as_double(0x7ff0000000000000ll);
+        bp[j] = -1;
+    }
     for (int e0 = 0; e0 < m1; e0 += kFixLanes) {
         const int e = e0 + sub;
         const bool pass = ok && e < n1 && c1_lb[i * cap1 + e] <= ufin;
         const int32_t p = pass ? c1_p[i * cap1 + e] : 0;
-        const float dist = coop_exact(pass, p);
+        const double d2 = coop_sq64(pass, p);
         if (pass) {
-            const uint64_t key = pack_key(dist, static_cast<uint32_t>(p));
-            if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+            double x = d2;
+            int32_t y = p;
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {  // sorted insert by (sum, position)
+                const bool sw = x < bd[j] || (x == bd[j] && y < bp[j]);
+                const double tx = sw ? bd[j] : x;
+                const int32_t ty = sw ? bp[j] : y;
+                if (sw) {
+                    bd[j] = x;
+                    bp[j] = y;
+                }
+                x = tx;
+                y = ty;
+            }
 #ifdef RBC_FIX_STATS
             atomicAdd(&g_fix_stats[0], 1ull);
 #endif
         }
     }
+    double dk = __longlong_as_double(0x7ff0000000000000ll);  // >= the k-th smallest sum (ties pop together)
+    {
+        double cur[KT];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) cur[j] = bd[j];
+        for (int r = 0; r < k; ++r) {
+            double m = cur[0];
+#pragma unroll
+            for (int o = kFixLanes / 2; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+            dk = m;
+            if (cur[0] == m) {
+#pragma unroll
+                for (int j = 0; j < KT - 1; ++j) cur[j] = cur[j + 1];
+                cur[KT - 1] = __longlong_as_double(0x7ff0000000000000ll);
+            }
+        }
+    }
+    const double dthr = dk * (1.0 + 1.0 / 1048576.0);  // 2^-20
+    uint64_t best[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        best[j] = kEmptyKey;
+        if (bp[j] >= 0 && bd[j] <= dthr) best[j] = pack_key(verified(bd[j], bp[j]), static_cast<uint32_t>(bp[j]));
+    }
+    // (ascending by sum and then position; the verified fp32 keys keep that order except
+    // between equal fp32 values, so re-sort)
+#pragma unroll
+    for (int a = 1; a < KT; ++a)
+#pragma unroll
+        for (int b = a; b > 0; --b)
+            if (best[b] < best[b - 1]) {
+                const uint64_t t = best[b];
+                best[b] = best[b - 1];
+                best[b - 1] = t;
+            }
     // group merge: the smallest key (nearest rep) and the k-th smallest (gamma_k)
     uint64_t first_key = kEmptyKey, kth = kEmptyKey;
     for (int r = 0; r < k; ++r) {

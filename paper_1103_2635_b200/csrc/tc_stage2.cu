@@ -318,10 +318,9 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     int32_t *nearcnt = sm + 2 * nr; // [nr]
     typedef cub::BlockScan<int, kRows> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ unsigned long long s_front, s_work;
+    __shared__ unsigned long long s_work;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) maxlen[p] = maxd1[p] = nearcnt[p] = 0;
     if (threadIdx.x == 0) {
-        s_front = ~0ull;
         s_work = 0;
     }
     __syncthreads();
@@ -358,16 +357,11 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         if (qi >= 0 && lane == __ffs(grp) - 1) atomicAdd(&nearcnt[nr_near], __popc(grp));
     }
     __syncthreads();
-    // front list = the most common nearest rep of the tile (ties: lowest position)
+    // the tile's total work (LPT key)
     unsigned long long wsum = 0;
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
-        wsum += maxlen[p];
-        if (maxlen[p] > 0 && nearcnt[p] > 0)
-            atomicMin(&s_front, (static_cast<unsigned long long>(kRows - nearcnt[p]) << 32) | static_cast<uint64_t>(p));
-    }
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) wsum += maxlen[p];
     atomicAdd(&s_work, wsum);
     __syncthreads();
-    const int32_t front = s_front == ~0ull ? -1 : static_cast<int32_t>(s_front & 0xFFFFFFFFu);
     // with warm-up, slot w0 is a max-only copy of the first list (k = 1: it
     // tightens the running bound before any candidate is buffered)
     const int64_t wbase = work_off[blockIdx.x], wn = nwork[blockIdx.x];
