@@ -238,11 +238,6 @@ __global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, i
 }
 
 // ---- tile preparation -----------------------------------------------------------------
-__global__ void tile_rows_kernel(const int32_t *__restrict__ order, int64_t nq, int64_t total, int32_t *__restrict__ rows) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t < total) rows[t] = t < nq ? order[t] : -1;
-}
-
 // query grouping key (first surviving list, nearest rep) packed into 2 * kb bits, so the
 // sort runs ceil(2 kb / 8) radix passes instead of six, plus the identity payload
 __global__ void group_key_kernel(const uint64_t *__restrict__ order_key, int64_t nq, int kb, uint32_t *__restrict__ key,
@@ -253,11 +248,6 @@ __global__ void group_key_kernel(const uint64_t *__restrict__ order_key, int64_t
     const uint32_t mask = (1u << kb) - 1u;
     key[t] = ((static_cast<uint32_t>(o >> 24) & mask) << kb) | (static_cast<uint32_t>(o) & mask);
     ids[t] = static_cast<int32_t>(t);
-}
-
-__global__ void iota_kernel(int32_t *v, int64_t n) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t < n) v[t] = static_cast<int32_t>(t);
 }
 
 // union of the tile's surviving lists: count
@@ -444,14 +434,6 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
 }
 
 // ---- the stage-2 kernel -----------------------------------------------------------------
-// v[j] for a runtime j in [0, 8) without local memory (select tree)
-__device__ __forceinline__ float pick8(const float *v, int j) {
-    const float a0 = (j & 4) ? v[4] : v[0], a1 = (j & 4) ? v[5] : v[1];
-    const float a2 = (j & 4) ? v[6] : v[2], a3 = (j & 4) ? v[7] : v[3];
-    const float b0 = (j & 2) ? a2 : a0, b1 = (j & 2) ? a3 : a1;
-    return (j & 1) ? b1 : b0;
-}
-
 template <int KT>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
     if (static_cast<int64_t>(*P.work_total) > P.cap_work) return;  // work arrays incomplete (see tile_fill_kernel)
@@ -976,19 +958,6 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
             best[KT - 1] = kEmptyKey;
         }
     }
-}
-
-__global__ void gather_query_rows_kernel(const float *__restrict__ q, const int32_t *__restrict__ ids, int64_t m, int d,
-                                         float *__restrict__ out) {
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < m * d;
-         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[t] = q[static_cast<int64_t>(ids[t / d]) * d + t % d];
-}
-
-__global__ void scatter_keys_kernel(const uint64_t *__restrict__ src, const int32_t *__restrict__ ids, int64_t m, int k,
-                                    uint64_t *__restrict__ dst) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t < m * k) dst[static_cast<int64_t>(ids[t / k]) * k + t % k] = src[t];
 }
 
 constexpr size_t kSmemBytes =
