@@ -71,6 +71,7 @@ constexpr int kABytes = kRows * (kP0 + kP1);
 
 // error-bound constants (factor-2 safety on each term; K <= 80 accumulated products)
 constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 128.0f / 4194304.0f);  // f16 rounding of a and b, fp32 accumulate
+constexpr float kAcc = 4.0f * 128.0f / 4194304.0f;                     // fp32 accumulation share of kC1
 constexpr float kC2 = 1.0f / 1048576.0f;                              // norms, aug split, epilogue rounding
 constexpr float kC4 = 1.0f / 262144.0f;                               // f16 subnormal flush (absolute, scaled)
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                       // rounding-up factor for norms
@@ -86,6 +87,7 @@ struct TcIndex {
     float *gcol = nullptr;    // [npad + tail] (|x - r_p|^2 / 2) * sB_p (fallback when -sA/sB is not an f16 normal)
     int64_t *poff = nullptr;  // [nr + 1] padded (8-row aligned) list offsets
     float *sB = nullptr;      // [nr] per-list power-of-two scale
+    float *dbmax = nullptr;   // [nr] max over the list of |b - f16(b)| (scaled residual rows, f16 rounding)
     float *reps64 = nullptr;  // [nr][64] representatives, zero padded
 };
 
@@ -106,6 +108,7 @@ struct S2Params {
     const uint8_t *xh1;
     const float *gcol;
     const float *reps64;
+    const float *dbmax;         // [nr] per-list max f16 rounding error of the B rows (scaled)
     int plane1;
     const float *q64;           // queries, rows padded to 64 floats
     const float *gamma;         // [nq] gamma_k
@@ -187,7 +190,10 @@ __global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, f
 __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *__restrict__ reps,
                                      const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff,
                                      const float *__restrict__ sB, int d, int plane1, uint8_t *__restrict__ xh0,
-                                     uint8_t *__restrict__ xh1, float *__restrict__ gcol) {
+                                     uint8_t *__restrict__ xh1, float *__restrict__ gcol, float *__restrict__ dbmax) {
+    __shared__ unsigned s_db;
+    if (threadIdx.x == 0) s_db = 0;
+    __syncthreads();
     const int64_t p = blockIdx.x;
     const int64_t len = offsets[p + 1] - offsets[p];
     const float s = sB[p];
@@ -207,6 +213,7 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
         const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ghi)) |
                              (static_cast<uint32_t>(__half_as_ushort(glo)) << 16);
         uint8_t *dst = xh0 + row * kP0;
+        float db2 = 0.f;  // |b - f16(b)|^2 of this row (scaled units)
         for (int c = 0; c < 8; ++c) {
             uint32_t w[4];
 #pragma unroll
@@ -215,6 +222,11 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
                 const float b0 = k0 < d ? __fsub_rn(x[k0], r[k0]) : 0.f;
                 const float b1 = k1 < d ? __fsub_rn(x[k1], r[k1]) : 0.f;
                 w[e] = sm100::pack_f16x2_sat(b0 * s, b1 * s);
+                __half2 h;
+                *reinterpret_cast<uint32_t *>(&h) = w[e];
+                const float2 hf2 = __half22float2(h);
+                const float e0 = b0 * s - hf2.x, e1 = b1 * s - hf2.y;
+                db2 = fmaf(e0, e0, fmaf(e1, e1, db2));
             }
             if (!plane1 && c == 7) w[3] = aug;  // columns 62, 63
             *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -226,7 +238,10 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
             *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
         }
         gcol[row] = hf * 0.5f * s;
+        atomicMax(&s_db, __float_as_uint(sqrtf(db2)));
     }
+    __syncthreads();
+    if (threadIdx.x == 0) dbmax[p] = __uint_as_float(s_db);
 }
 
 __global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
@@ -443,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     uint8_t *sA = sB + kStages * kStageBytes;             // 2 x (plane 0 | plane 1)
     float *gbuf = reinterpret_cast<float *>(sA + 2 * kABytes);  // 8 epilogue warps x 128 (fallback column)
     float *s_dq = gbuf + kEpiWarps * kCols;  // [4 list slots][kParts][128] partial |q - r_p|^2
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_dq + 4 * kParts * kRows);
+    float *s_da = s_dq + 4 * kParts * kRows;  // [4 list slots][kParts][128] partial |a - f16(a)|^2 (scaled)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_da + 4 * kParts * kRows);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + kAcc;
     uint64_t *afull = tempty + kAcc, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
@@ -608,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const uint32_t a = ai & 1;
                 S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
                 uint8_t *dst = sA + a * kABytes + row * kP0;
+                float da2 = 0.f;  // |a - f16(a)|^2 of this part (scaled units)
 #pragma unroll
                 for (int c = 0; c < kKd / 8; ++c) {
                     const float rr[8] = {rr4[2 * c].x, rr4[2 * c].y, rr4[2 * c].z, rr4[2 * c].w,
@@ -619,11 +636,17 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         const float v0 = fmaf(qv[k0], sa, -(rr[2 * e] * sa));
                         const float v1 = fmaf(qv[k0 + 1], sa, -(rr[2 * e + 1] * sa));
                         wv[e] = sm100::pack_f16x2_sat(v0, v1);
+                        __half2 h;
+                        *reinterpret_cast<uint32_t *>(&h) = wv[e];
+                        const float2 hf2 = __half22float2(h);
+                        const float e0 = v0 - hf2.x, e1 = v1 - hf2.y;
+                        da2 = fmaf(e0, e0, fmaf(e1, e1, da2));
                     }
                     const int cc = part * (kKd / 8) + c;
                     if (!P.plane1 && cc == 7) wv[3] = aug;
                     *reinterpret_cast<uint4 *>(dst + ((cc ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                 }
+                s_da[(static_cast<int>(w) & 3) * (kParts * kRows) + part * kRows + row] = da2;
                 if (P.plane1 && part == kParts - 1) {
                     uint8_t *d1p = sA + a * kABytes + kRows * kP0 + row * kP1;
                     const int sw = (row >> 2) & 1;
@@ -661,9 +684,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 // row's |q - r_p|^2 is the sum of their two halves (slot w & 3; a part runs at
                 // most one list ahead of its partner, so slots are never overwritten early)
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + quad), "r"(32 * kParts) : "memory");
-                float A2q = 0.f;
+                float A2q = 0.f, DA2 = 0.f;
 #pragma unroll
-                for (int h = 0; h < kParts; ++h) A2q += s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + h * kRows + row];
+                for (int h = 0; h < kParts; ++h) {
+                    A2q += s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + h * kRows + row];
+                    DA2 += s_da[(static_cast<int>(w) & 3) * (kParts * kRows) + h * kRows + row];
+                }
                 const float dq = sqrtf(A2q);
                 const bool noaug = wi.aug == 0.0f;  // warp-uniform (per work item)
                 const float sa = wi.sA;
@@ -674,7 +700,15 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     // kD1 (on A2) and kUq (on |a| = sqrt(A2))
                     const float na = dq * kUq, rb = wi.radius * kUp;
                     A2 = A2q;
-                    E = kC1 * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 + kC4 * rb * (2.0f / sa) + 1e-30f;
+                    // f16 rounding of the operands from the actual rounding errors: |dot(f16 a,
+                    // f16 b) - a.b| <= |da||b| + |a||db| + |da||db| (Cauchy-Schwarz), with |da|
+                    // this row's A error and |db| the list's largest B error (unscaled; +2^-23
+                    // relative for the fp32 residual rounding before the f16 conversion), x2 for
+                    // d^2 and x2 safety as in kC1; fp32 accumulation keeps its kC1 share
+                    const float da = sqrtf(DA2) * (1.0f + 1.0f / 1024.0f) / sa + dq * (1.0f / 8388608.0f);
+                    const float db = P.dbmax[wi.p] * (1.0f + 1.0f / 1024.0f) / wi.sB + rb * (1.0f / 8388608.0f);
+                    E = 4.0f * (da * rb + na * db + da * db) + kAcc * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 +
+                        kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
                 const float lb0 = A2 - E;  // lb(V) = lb0 - V * inv2s
                 // V >= T  <=>  lb = A2 - E - 2 V / scale <= U * kTie   (loosened by 2^-18 relative)
@@ -961,7 +995,7 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
 }
 
 constexpr size_t kSmemBytes =
-    1024 + kStages * kStageBytes + 2 * kABytes + (kEpiWarps * kCols + 4 * kParts * kRows) * sizeof(float) + 512;
+    1024 + kStages * kStageBytes + 2 * kABytes + (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) + 512;
 
 // Exact SIMT scan for the queries whose candidate buffer overflowed; the count
 // lives on the device (no host round trip).  One warp per entry, grid-stride.
@@ -1026,6 +1060,7 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
         cudaFree(tc->gcol);
         cudaFree(tc->poff);
         cudaFree(tc->sB);
+        cudaFree(tc->dbmax);
         cudaFree(tc->reps64);
         delete tc;
         return rc;
@@ -1035,6 +1070,7 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
               cudaMalloc(&tc->gcol, rows * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&tc->poff, (idx->nr + 1) * sizeof(int64_t)) == cudaSuccess &&
               cudaMalloc(&tc->sB, idx->nr * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&tc->dbmax, idx->nr * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&tc->reps64, idx->nr * 64 * sizeof(float)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -1050,7 +1086,8 @@ int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
     list_scale_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->radii, idx->nr, tc->sB);
     pad64_rows_kernel<<<grid_for(idx->nr * 64, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, tc->reps64);
     residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(
-        idx->xp, idx->reps, idx->offsets, tc->poff, tc->sB, idx->d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol);
+        idx->xp, idx->reps, idx->offsets, tc->poff, tc->sB, idx->d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol,
+        tc->dbmax);
     note_launch(3);
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
         return cleanup(fail(RBC_ECUDA, "tc index kernels"));
@@ -1066,6 +1103,7 @@ void tc_index_release(rbc_index *idx) {
     cudaFree(tc->gcol);
     cudaFree(tc->poff);
     cudaFree(tc->sB);
+    cudaFree(tc->dbmax);
     cudaFree(tc->reps64);
     delete tc;
     idx->tc = nullptr;
@@ -1185,6 +1223,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.xh1 = tc->xh1;
     P.gcol = tc->gcol;
     P.reps64 = tc->reps64;
+    P.dbmax = tc->dbmax;
     P.plane1 = tc->plane1 ? 1 : 0;
     P.q64 = q64;
     P.gamma = po.gamma.get();
