@@ -71,7 +71,12 @@ constexpr int kABytes = kRows * (kP0 + kP1);
 
 // error-bound constants (factor-2 safety on each term; K <= 80 accumulated products)
 constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 128.0f / 4194304.0f);  // f16 rounding of a and b, fp32 accumulate
-constexpr float kAcc = 4.0f * 128.0f / 4194304.0f;                     // fp32 accumulation share of kC1
+#ifdef RBC_S2_NOHOLD
+constexpr bool kHold = false;  // diagnostic variant
+#else
+constexpr bool kHold = true;   // k = 1: newest qualifying group held in registers
+#endif
+constexpr float kAccErr = 4.0f * 128.0f / 4194304.0f;                  // fp32 accumulation share of kC1
 constexpr float kC2 = 1.0f / 1048576.0f;                              // norms, aug split, epilogue rounding
 constexpr float kC4 = 1.0f / 262144.0f;                               // f16 subnormal flush (absolute, scaled)
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                       // rounding-up factor for norms
@@ -669,6 +674,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             float U = u_init;  // running upper bound of the k-th smallest candidate d^2
             int count = 0;     // buffered 8-column groups
             bool overflow = false;
+            // k = 1: the newest qualifying group (values, their max, (lb0, 2/scale, valid), position)
+            float hv[9];
+            float4 hm = make_float4(0.f, 0.f, 0.f, 0.f);
+            int32_t hpos = 0;
+            bool held = false;
             const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * kParts + part);
             float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 3;
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
@@ -707,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     // d^2 and x2 safety as in kC1; fp32 accumulation keeps its kC1 share
                     const float da = sqrtf(DA2) * (1.0f + 1.0f / 1024.0f) / sa + dq * (1.0f / 8388608.0f);
                     const float db = P.dbmax[wi.p] * (1.0f + 1.0f / 1024.0f) / wi.sB + rb * (1.0f / 8388608.0f);
-                    E = 4.0f * (da * rb + na * db + da * db) + kAcc * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 +
+                    E = 4.0f * (da * rb + na * db + da * db) + kAccErr * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 +
                         kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
                 const float lb0 = A2 - E;  // lb(V) = lb0 - V * inv2s
@@ -740,7 +750,29 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 // valid columns): lb = lb0 - V * 2/scale, computed by the re-rank -- and tighten
                 // the bound with the group's best element; the exact re-rank filters
                 auto push8 = [&](const float *v, float m, int col0, int lim, bool block_valid) {
-                    if (count < P.cap) {
+                    if (KT == 1 && kHold) {
+                        // k = 1: the newest qualifying group is held in registers; the one it
+                        // replaces is stored only if it can still hold the nearest candidate
+                        // (its smallest lower bound is within the current bound) -- usually the
+                        // new group has just improved on it
+                        if (held && fmaf(-hv[8], hm.y, hm.x) <= U * kTie) {
+                            if (count < P.cap) {
+                                clb[3 * count] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                                clb[3 * count + 1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                                clb[3 * count + 2] = hm;
+                                cpos[count] = hpos;
+                                ++count;
+                            } else {
+                                overflow = true;
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) hv[j] = v[j];
+                        hv[8] = m;
+                        hm = make_float4(lb0, inv2s, __int_as_float(min(8, lim - col0)), 0.f);
+                        hpos = wi.csr + col0;
+                        held = true;
+                    } else if (count < P.cap) {
                         clb[3 * count] = make_float4(v[0], v[1], v[2], v[3]);
                         clb[3 * count + 1] = make_float4(v[4], v[5], v[6], v[7]);
                         clb[3 * count + 2] = make_float4(lb0, inv2s, __int_as_float(min(8, lim - col0)), 0.f);
@@ -843,6 +875,18 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     __syncwarp();
                     if (lane == 0) sm100::mbar_arrive(&tempty[tb]);
                     ++ti;
+                }
+            }
+            // the held group joins the buffer (k = 1)
+            if (KT == 1 && kHold && held && !overflow) {
+                if (count < P.cap) {
+                    clb[3 * count] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                    clb[3 * count + 1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                    clb[3 * count + 2] = hm;
+                    cpos[count] = hpos;
+                    ++count;
+                } else {
+                    overflow = true;
                 }
             }
             // hand the buffered candidates to the exact re-rank kernel
