@@ -9,19 +9,23 @@
 // K=16 slice: operands centred on the representatives' mean c, the per-rep
 // term |r - c|^2 / 2 folded into the MMA as two extra K columns (as in
 // tc_stage2.cu), so every d^2 is known inside a rigorous interval
-// [dt - E, dt + E].  Two passes over the representatives (the accumulator
-// row of |R| columns does not fit TMEM):
-//   pass 1: the k smallest upper bounds give U_k >= gamma_k^2; every rep
-//           with lb <= U_k is buffered as a gamma candidate, and
+// [dt - E, dt + E].  The accumulator row of |R| columns does not fit TMEM, so
+// the representatives stream through in 128-column chunks:
+//   k > 1, pass 1: the k smallest upper bounds give U_k >= gamma_k^2; every
+//           rep with lb <= U_k is buffered as a gamma candidate, and
 //           gamma_k^2 lies in [U_k - 2E, U_k];
-//   pass 2: every rep is classified against 3 gamma, gamma + psi_r and
-//           gamma with that gamma interval.  Far reps (almost all) are
-//           only counted, 8 at a time through a max-reduce; certain
-//           survivors are recorded with a flag, undecided reps recorded
-//           plain.
-// No fp64 work happens here.  The fix-up kernel (one warp per query) turns
-// the gamma candidates into the exact gamma_k and nearest rep with the
-// reference arithmetic, decides the undecided reps exactly, computes the
+//   k > 1, pass 2: every rep is classified against 3 gamma and gamma + psi
+//           with that gamma interval.  Far reps (almost all) are only
+//           counted, 8 at a time through a max-reduce; the rest is recorded
+//           with its estimate.
+//   k = 1: one pass.  The running bound starts at the query's distance to its
+//           pilot (pilot_key_kernel, an upper bound of gamma^2) and tightens
+//           block by block; each block is classified against the far test
+//           with the current bound right after (the bound only decreases, so
+//           "far" stays certain under the final gamma).
+// No fp64 work happens here.  The fix-up kernel (an 8-lane group per query)
+// turns the gamma candidates into the exact gamma_k and nearest rep with the
+// reference arithmetic, decides the recorded reps exactly, computes the
 // 4 gamma cutoffs and emits the surviving segments.  No |Q| x |R| distance
 // matrix is materialised.  Any row that exhausts a buffer raises a flag and
 // the caller recomputes the batch with the exact path (search.cu), so the
@@ -126,6 +130,7 @@ struct S1Params {
     float rmax;
     const float *c64;
     const float *psimax;
+    const float *pd2;       // [nq] k = 1: upper bound of gamma_1^2 from the query's pilot
     const float *q64;
     const int32_t *qorder;  // tile slot -> query id (queries sorted by nearest pilot)
     const float *radii;
@@ -324,8 +329,11 @@ __device__ __forceinline__ uint32_t f2h2(float a, float b) { return sm100::pack_
 __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float *__restrict__ q64, int64_t nq,
                                                                     const uint4 *__restrict__ prow,
                                                                     const float *__restrict__ pnorm, int npilot,
+                                                                    const float *__restrict__ reps64,
+                                                                    const int32_t *__restrict__ pilots,
                                                                     uint32_t *__restrict__ key,
-                                                                    unsigned *__restrict__ hist) {
+                                                                    unsigned *__restrict__ hist,
+                                                                    float *__restrict__ pd2) {
     __shared__ uint32_t sp[kPilots * 32];  // pilot rows, 64 f16 (32 words) each; absent pilots zero
     __shared__ float sn[kPilots];
     __shared__ unsigned sh[kPilots];
@@ -382,6 +390,33 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
         const int iA = __shfl_xor_sync(0xffffffffu, jA, o), iB = __shfl_xor_sync(0xffffffffu, jB, o);
         if (vA > bestA || (vA == bestA && iA < jA)) bestA = vA, jA = iA;
         if (vB > bestB || (vB == bestB && iB < jB)) bestB = vB, jB = iB;
+    }
+    // |q - chosen pilot|^2 in fp32 (the 4 lanes of the row group, 16 coordinates each),
+    // rounded up by 2^-16 relative (the fp32 error is <= 66 * 2^-24): an upper bound of
+    // gamma_1^2 that seeds stage 1's running bound
+    {
+        const float4 *pa = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[jA]) * 64) + 4 * t4;
+        const float4 *pb = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[jB]) * 64) + 4 * t4;
+        const float4 *xa = reinterpret_cast<const float4 *>(qa) + 4 * t4;
+        const float4 *xb = reinterpret_cast<const float4 *>(qb) + 4 * t4;
+        float sa = 0.f, sb = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float4 u = __ldg(xa + c), v = __ldg(pa + c), w = __ldg(xb + c), z = __ldg(pb + c);
+            const float a0 = u.x - v.x, a1 = u.y - v.y, a2 = u.z - v.z, a3 = u.w - v.w;
+            const float b0 = w.x - z.x, b1 = w.y - z.y, b2 = w.z - z.z, b3 = w.w - z.w;
+            sa = fmaf(a0, a0, fmaf(a1, a1, fmaf(a2, a2, fmaf(a3, a3, sa))));
+            sb = fmaf(b0, b0, fmaf(b1, b1, fmaf(b2, b2, fmaf(b3, b3, sb))));
+        }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        if (t4 == 0) {
+            if (r0 + g < nq) pd2[r0 + g] = sa * (1.0f + 1.0f / 65536.0f) + 1e-30f;
+            if (r0 + g + 8 < nq) pd2[r0 + g + 8] = sb * (1.0f + 1.0f / 65536.0f) + 1e-30f;
+        }
     }
     if (t4 == 0) {
         if (r0 + g < nq) {
@@ -511,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
             if (tile < 0) break;
             if (lane == 0) {
                 const uint32_t bytes = P.plane1 ? kStageBytes : kN * kP0;
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = 0; pass < (P.k == 1 ? 1 : 2); ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
                         const uint32_t s = bi % kStages;
                         S1_WAIT(&empty[s], ((bi / kStages) & 1) ^ 1, 1);
@@ -537,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                 S1_WAIT(&afull[a], (ai >> 1) & 1, 3);
                 sm100::tc_fence_after();
                 const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = 0; pass < (P.k == 1 ? 1 : 2); ++pass)
                     for (int ch = 0; ch < nchunks; ++ch) {
                         const int n = min(kN, roundup16(static_cast<int>(P.nr) - ch * kN));
                         const uint32_t s = bi % kStages, tb = ti & 1;
@@ -648,10 +683,23 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
             };
             const float lb0 = qn - E;  // lb(V) = lb0 - V * inv2s
             float T = live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+            // k = 1: one pass.  The running bound starts at the pilot's distance (an upper bound
+            // of gamma_1^2), so each block can be classified against the far test right away --
+            // with a bound that only decreases, "far" stays certain under the final gamma, and
+            // the recorded rest is re-classified by the fix-up.  k > 1: two passes.
+            constexpr bool kSingle = KT == 1;
+            if (kSingle && live) {
+                U = P.pd2[qi];
+                T = threshold();
+            }
+            int pr = 0, p3 = 0, rc = 0;
+            int32_t *rec = P.rec + (live ? qi : 0) * P.cap_rec;
+            float *rdt = P.rec_dt + (live ? qi : 0) * P.cap_rec;
             for (int ch = 0; ch < nchunks; ++ch) {
                 const int off = ch * kN;
                 const int lim = min(kN, static_cast<int>(P.nr) - off);
                 const uint32_t tb = ti & 1;
+                const float psic = P.psimax[ch];
                 S1_WAIT(&tfull[tb], (ti >> 1) & 1, 8);
                 sm100::tc_fence_after();
                 for (int c0 = 0; c0 < S1_LIM(lim); c0 += 64) {
@@ -743,6 +791,46 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                         }
                         __syncwarp();
                     }
+                    if (kSingle) {  // the same block against the far test with the current bound
+                        const float ghi = sqrtf(U * kTie) * kUp;
+                        const float tpm = ghi + psic;
+                        const float thr_far = fmaxf(9.0f * ghi * ghi * (1.0f + kEps), tpm * tpm * (1.0f + kEps));
+                        const float tf = 0.5f * scale * (qn - E - thr_far);
+                        const float Tf = tf - fabsf(tf) * (1.0f / 262144.0f) - 1e-30f;
+                        const int nvb = min(64, lim - c0);
+                        if (live) {
+                            pr += nvb;  // counted far; the recorded ones are taken back below
+                            p3 += nvb;
+                        }
+                        unsigned gm2 = 0;
+#pragma unroll
+                        for (int s = 0; s < 8; ++s) gm2 |= (live && m8[s] >= Tf ? 1u : 0u) << s;
+                        unsigned gu2 = __reduce_or_sync(0xffffffffu, gm2);
+                        while (gu2) {
+                            const int s = __ffs(gu2) - 1;
+                            gu2 &= gu2 - 1;
+                            float x[8];
+                            sm100::tmem_ld8(tmem + tb * kN + lane_base + c0 + 8 * s, x);
+                            const bool take = (gm2 & (1u << s)) != 0;
+                            const int g0 = c0 + 8 * s;
+                            unsigned hit = 0;  // the group's elements that are not certainly far
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) hit |= (take && x[j] >= Tf && g0 + j < lim ? 1u : 0u) << j;
+                            const int nh = __popc(hit);
+                            while (hit) {
+                                const int j = __ffs(hit) - 1;
+                                hit &= hit - 1;
+                                if (rc < P.cap_rec) {
+                                    rec[rc] = off + g0 + j;
+                                    rdt[rc] = fmaf(-pick8(x, j), inv2s, qn);
+                                }
+                                ++rc;
+                            }
+                            pr -= nh;
+                            p3 -= nh;
+                            __syncwarp();
+                        }
+                    }
                 }
                 sm100::tc_fence_before();
                 __syncwarp();
@@ -759,11 +847,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
             const float ghi = sqrtf(Uk * kTie) * kUp;
             const float t9hi = 9.0f * ghi * ghi * (1.0f + kEps);
 
-            // ---------- pass 2: count the far reps, record the rest with their estimate ----------
-            int pr = 0, p3 = 0, rc = 0;
-            int32_t *rec = P.rec + (live ? qi : 0) * P.cap_rec;
-            float *rdt = P.rec_dt + (live ? qi : 0) * P.cap_rec;
-            for (int ch = 0; ch < nchunks; ++ch) {
+            // ---------- pass 2 (k > 1): count the far reps, record the rest with their estimate ----------
+            for (int ch = 0; ch < (kSingle ? 0 : nchunks); ++ch) {
                 const int off = ch * kN;
                 const int lim = min(kN, static_cast<int>(P.nr) - off);
                 const uint32_t tb = ti & 1;
@@ -1267,6 +1352,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     DevBuf<int32_t> &qorder = out.qorder;
     DevBuf<uint32_t> pkey;
     DevBuf<unsigned> phist;  // [kPilots] bucket sizes, [kPilots] claim cursors
+    DevBuf<float> pd2;       // [nq] upper bound of |q - nearest pilot|^2 (k = 1 seed bound)
     const float *q64 = q;
     if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
         RBC_CHECK(q64buf.alloc(nq * 64, st));
@@ -1279,8 +1365,9 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(pkey.alloc(nq, st));
     RBC_CHECK(phist.alloc(2 * kPilots, st));
     RBC_CUDA(cudaMemsetAsync(phist.get(), 0, 2 * kPilots * sizeof(unsigned), st));
-    pilot_key_kernel<<<grid_for(nq, kPilotWarps * 16), kPilotWarps * 32, 0, st>>>(q64, nq, t->prow, t->pnorm, npilot,
-                                                                                  pkey.get(), phist.get());
+    RBC_CHECK(pd2.alloc(nq, st));
+    pilot_key_kernel<<<grid_for(nq, kPilotWarps * 16), kPilotWarps * 32, 0, st>>>(
+        q64, nq, t->prow, t->pnorm, npilot, t->reps64, t->pilots, pkey.get(), phist.get(), pd2.get());
     RBC_LAUNCHED();
     pilot_scatter_kernel<<<grid_for(nq, 128), 128, 0, st>>>(pkey.get(), nq, npilot, phist.get(), phist.get() + kPilots,
                                                            qorder.get());
@@ -1314,6 +1401,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     P.rmax = t->rmax;
     P.c64 = t->c64;
     P.psimax = t->psimax;
+    P.pd2 = pd2.get();
     P.q64 = q64;
     P.qorder = qorder.get();
     P.radii = idx->radii;
