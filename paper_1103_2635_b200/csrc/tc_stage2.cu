@@ -270,50 +270,11 @@ __global__ void group_key_kernel(const uint64_t *__restrict__ order_key, int64_t
     ids[t] = static_cast<int32_t>(t);
 }
 
-// union of the tile's surviving lists: count
-__global__ void __launch_bounds__(kRows) tile_count_kernel(const int32_t *__restrict__ order, int64_t nq,
-                                                           const int64_t *__restrict__ seg_off,
-                                                           const int32_t *__restrict__ seg_cnt,
-                                                           const int32_t *__restrict__ seg_list, int64_t nr,
-                                                           int64_t *__restrict__ nwork, int64_t *__restrict__ work_off,
-                                                           unsigned long long *__restrict__ work_total, int warm) {
-    extern __shared__ int32_t present[];
-    __shared__ int s_count;
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) present[p] = 0;
-    if (threadIdx.x == 0) s_count = 0;
-    __syncthreads();
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
-    const int32_t qi = t < nq ? order[t] : -1;
-    if (qi >= 0) {  // benign races: every writer stores 1
-        const int64_t s0 = seg_off[qi];
-        const int cnt = seg_cnt[qi];
-        for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
-            uint32_t pb[kSegBatch];
-            load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, cnt - it0, pb, 0xFFFFFFFFu);
-#pragma unroll
-            for (int j = 0; j < kSegBatch; ++j)
-                if (pb[j] != 0xFFFFFFFFu) present[pb[j]] = 1;
-        }
-    }
-    __syncthreads();
-    int c = 0;
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) c += present[p];
-    atomicAdd(&s_count, c);
-    __syncthreads();
-    // + 1 warm-up (max-only) copy of the first list when warm
-    if (threadIdx.x == 0) {  // the tile's work items: a range claimed in the shared work array
-        const int64_t nw = s_count + (warm && s_count > 0 ? 1 : 0);
-        nwork[blockIdx.x] = nw;
-        work_off[blockIdx.x] = static_cast<int64_t>(atomicAdd(work_total, static_cast<unsigned long long>(nw)));
-    }
-}
-
 // union of the tile's surviving lists: work items, per-row cutoffs and stage-1
 // distances, and the tile's total work (for the LPT order)
 __global__ void __launch_bounds__(kRows) tile_fill_kernel(
-    const int32_t *__restrict__ order, int64_t nq, const int64_t *__restrict__ nwork,
-    const int64_t *__restrict__ work_off, const unsigned long long *__restrict__ work_total,
-    int32_t *__restrict__ tile_ids, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
+    const int32_t *__restrict__ order, int64_t nq, int64_t *__restrict__ nwork, int64_t *__restrict__ work_off,
+    unsigned long long *__restrict__ work_total, int32_t *__restrict__ tile_ids, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
     const int32_t *__restrict__ seg_list, const int32_t *__restrict__ seg_len, const float *__restrict__ seg_d1,
     const uint64_t *__restrict__ order_key,
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
@@ -321,17 +282,18 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key, int warm,
     int64_t cap_work) {
     if (threadIdx.x == 0) tile_ids[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
-    if (static_cast<int64_t>(*work_total) > cap_work) return;  // capacity exceeded: the caller re-runs
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
     int32_t *nearcnt = sm + 2 * nr; // [nr]
     typedef cub::BlockScan<int, kRows> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ unsigned long long s_work;
+    __shared__ unsigned long long s_work, s_off;
+    __shared__ int s_lists;
     for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) maxlen[p] = maxd1[p] = nearcnt[p] = 0;
     if (threadIdx.x == 0) {
         s_work = 0;
+        s_lists = 0;
     }
     __syncthreads();
     const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
@@ -367,14 +329,29 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         if (qi >= 0 && lane == __ffs(grp) - 1) atomicAdd(&nearcnt[nr_near], __popc(grp));
     }
     __syncthreads();
-    // the tile's total work (LPT key)
+    // the tile's total work (LPT key) and its list count; the tile claims its range of
+    // the shared work array with one atomic (an undersized array makes the tiles that do
+    // not fit skip their writes; stage 2 then bails out and the caller re-runs)
     unsigned long long wsum = 0;
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) wsum += maxlen[p];
+    int nl = 0;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+        wsum += maxlen[p];
+        nl += maxlen[p] > 0 ? 1 : 0;
+    }
     atomicAdd(&s_work, wsum);
+    atomicAdd(&s_lists, nl);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t nw = s_lists + (warm && s_lists > 0 ? 1 : 0);
+        s_off = atomicAdd(work_total, static_cast<unsigned long long>(nw));
+        nwork[blockIdx.x] = nw;
+        work_off[blockIdx.x] = static_cast<int64_t>(s_off);
+    }
     __syncthreads();
     // with warm-up, slot w0 is a max-only copy of the first list (k = 1: it
     // tightens the running bound before any candidate is buffered)
-    const int64_t wbase = work_off[blockIdx.x], wn = nwork[blockIdx.x];
+    const int64_t wbase = static_cast<int64_t>(s_off), wn = nwork[blockIdx.x];
+    if (wbase + wn > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
     const int64_t w0 = wbase + ((warm && wn > 0) ? 1 : 0);
     // zero this thread's cutoff column of the tile's work items (its own later writes win)
     for (int64_t w = wbase; w < wbase + wn; ++w) cut[w * kRows + threadIdx.x] = 0;
@@ -1213,17 +1190,13 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(work_off.alloc(ntiles, st));
     RBC_CHECK(work_total.alloc(1, st));
     RBC_CUDA(cudaMemsetAsync(work_total.get(), 0, sizeof(unsigned long long), st));
-    const size_t smem1 = sizeof(int32_t) * nr, smem3 = 3 * sizeof(int32_t) * nr;
+    const size_t smem3 = 3 * sizeof(int32_t) * nr;
     if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
     cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
-    cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
     // max-only warm-up copy of each tile's first list (k = 1): off -- with the nearest-rep
     // lists ordered first the bounds tighten early anyway, and the extra list cost more
     // (stage 2 540 vs 573 us, re-rank 60 vs 52 us at cfg2); RBC_S2_WARM=1 turns it on
     const int warm = (k == 1 && getenv("RBC_S2_WARM")) ? 1 : 0;
-    tile_count_kernel<<<ntiles, kRows, smem1, st>>>(order, nq, po.seg_off.get(), po.nseg.get(), po.seg_list.get(), nr,
-                                                    nwork.get(), work_off.get(), work_total.get(), warm);
-    RBC_LAUNCHED();
     // work arrays sized from the caller's capacity (no host round trip); an
     // undersized capacity makes every consumer kernel bail out and the caller
     // re-runs with the size reported in status[0]
