@@ -329,18 +329,39 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         if (qi >= 0 && lane == __ffs(grp) - 1) atomicAdd(&nearcnt[nr_near], __popc(grp));
     }
     __syncthreads();
-    // the tile's total work (LPT key) and its list count; the tile claims its range of
-    // the shared work array with one atomic (an undersized array makes the tiles that do
-    // not fit skip their writes; stage 2 then bails out and the caller re-runs)
+    // one pass over this thread's contiguous range of lists: the tile's total work (LPT
+    // key), its list count, the sort keys of the lists that are some row's nearest rep
+    // ("F" lists, ordered first: most rows first, so each row's running bound tightens
+    // early and fewer candidate groups are buffered) and the count of the others
+    __shared__ unsigned long long s_fkey[kRows];
+    __shared__ int s_nf;
+    if (threadIdx.x == 0) s_nf = 0;
+    __syncthreads();
+    const int64_t per = (nr + kRows - 1) / kRows;
+    const int64_t pa = threadIdx.x * per, pe = min(nr, pa + per);
     unsigned long long wsum = 0;
-    int nl = 0;
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
-        wsum += maxlen[p];
-        nl += maxlen[p] > 0 ? 1 : 0;
+    int nl = 0, c = 0;
+    for (int64_t p = pa; p < pe; ++p) {
+        const int ml = maxlen[p];
+        if (ml > 0) {
+            wsum += ml;
+            ++nl;
+            if (nearcnt[p] > 0) {
+                const int slot = atomicAdd(&s_nf, 1);  // <= 128 distinct nearest reps per tile
+                s_fkey[slot] = (static_cast<unsigned long long>(kRows - nearcnt[p]) << 32) | static_cast<uint64_t>(p);
+            } else {
+                ++c;
+            }
+        }
     }
     atomicAdd(&s_work, wsum);
     atomicAdd(&s_lists, nl);
+    int pos, total;
+    Scan(scan_tmp).ExclusiveSum(c, pos, total);
     __syncthreads();
+    // the tile claims its range of the shared work array with one atomic (an undersized
+    // array makes the tiles that do not fit skip their writes; stage 2 then bails out and
+    // the caller re-runs)
     if (threadIdx.x == 0) {
         const int64_t nw = s_lists + (warm && s_lists > 0 ? 1 : 0);
         s_off = atomicAdd(work_total, static_cast<unsigned long long>(nw));
@@ -355,39 +376,19 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int64_t w0 = wbase + ((warm && wn > 0) ? 1 : 0);
     // zero this thread's cutoff column of the tile's work items (its own later writes win)
     for (int64_t w = wbase; w < wbase + wn; ++w) cut[w * kRows + threadIdx.x] = 0;
-    // work order: the lists that are some row's nearest rep first, most rows first (each
-    // row's running bound tightens early, so fewer candidate groups are buffered), then
-    // the others ascending (each thread a contiguous range of lists, one block scan)
-    {
-        __shared__ unsigned long long s_fkey[kRows];
-        __shared__ int s_nf;
-        if (threadIdx.x == 0) s_nf = 0;
-        __syncthreads();
-        for (int64_t p = threadIdx.x; p < nr; p += blockDim.x)
-            if (maxlen[p] > 0 && nearcnt[p] > 0) {
-                const int slot = atomicAdd(&s_nf, 1);  // <= 128 distinct nearest reps per tile
-                s_fkey[slot] = (static_cast<unsigned long long>(kRows - nearcnt[p]) << 32) | static_cast<uint64_t>(p);
-            }
-        const int64_t per = (nr + kRows - 1) / kRows;
-        const int64_t pa = threadIdx.x * per, pe = min(nr, pa + per);
-        int c = 0;
-        for (int64_t p = pa; p < pe; ++p) c += (maxlen[p] > 0 && nearcnt[p] == 0) ? 1 : 0;
-        int pos, total;
-        Scan(scan_tmp).ExclusiveSum(c, pos, total);
-        __syncthreads();  // every count read before nearcnt is overwritten
-        const int nf = s_nf;
-        for (int64_t p = pa; p < pe; ++p)
-            if (maxlen[p] > 0 && nearcnt[p] == 0) nearcnt[p] = nf + pos++;  // reuse as list -> work index
-        __syncthreads();  // (an F list's rank may be 0: written only after every range is done)
-        if (threadIdx.x < nf) {
-            const unsigned long long mine = s_fkey[threadIdx.x];
-            int rank = 0;
-            for (int j = 0; j < nf; ++j) rank += s_fkey[j] < mine ? 1 : 0;
-            nearcnt[static_cast<int32_t>(mine & 0xFFFFFFFFu)] = rank;
-        }
+    // positions (nearcnt is reused as list -> work index): F lists by rank, then the others
+    const int nf = s_nf;
+    for (int64_t p = pa; p < pe; ++p)
+        if (maxlen[p] > 0 && nearcnt[p] == 0) nearcnt[p] = nf + pos++;
+    __syncthreads();  // (an F list's rank may be 0: written only after every range is done)
+    if (threadIdx.x < nf) {
+        const unsigned long long mine = s_fkey[threadIdx.x];
+        int rank = 0;
+        for (int j = 0; j < nf; ++j) rank += s_fkey[j] < mine ? 1 : 0;
+        nearcnt[static_cast<int32_t>(mine & 0xFFFFFFFFu)] = rank;
     }
     __syncthreads();
-    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) {
+    for (int64_t p = pa; p < pe; ++p) {
         if (maxlen[p] > 0) {
             WorkItem it;
             it.p = static_cast<int32_t>(p);
@@ -425,8 +426,8 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     // LPT: heavier tiles first
     if (threadIdx.x == 0) {
-        const unsigned long long wk = s_work < 0xFFFFFFFFFFull ? s_work : 0xFFFFFFFFFFull;
-        tile_key[blockIdx.x] = 0xFFFFFFFFFFull - wk;
+        const unsigned long long wk = s_work < 0xFFFFFFFFull ? s_work : 0xFFFFFFFFull;  // 32-bit LPT key
+        tile_key[blockIdx.x] = 0xFFFFFFFFull - wk;
     }
 }
 
@@ -1159,7 +1160,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(tile_order.alloc(ntiles, st));
     size_t tb2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles, 0,
-                                    40, st);
+                                    32, st);
     DevBuf<unsigned char> tmp;
     const int32_t *order = po.qorder.get();
     if (!order) {
@@ -1214,7 +1215,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                                    tkey.get(), warm, cap_work);
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
-                                             tile_order.get(), ntiles, 0, 40, st));
+                                             tile_order.get(), ntiles, 0, 32, st));
     note_launch();
     // 3. the tensor-core scan
     const int cap = 12 + 6 * k;  // 8-column groups per query and column part
