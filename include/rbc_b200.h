@@ -87,6 +87,15 @@ int rbc_pairwise_distances(const float *a, int64_t m, const float *b, int64_t p,
 int rbc_bf_search(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric, int32_t k,
                   int64_t *ids, float *dists, void *stream);
 
+/* eval.py:21-27 ball_count, :117-130 rank_error, :133-164 claim1_counts, :44-107 estimate_expansion_rate and
+ * report.py:72-95 rank_errors, batched: for query i and each of its n_thresholds thresholds t (row-major
+ * thresholds[i * n_thresholds + t]), counts[i * n_thresholds + t] = #{ j : f64(dist(q_i, x_j)) < t } when strict,
+ * <= t otherwise, with the reference's fp32 distance.  max_dist (nullable) receives max_j dist(q_i, x_j).
+ * Per-query shared state is 4*d + 140*n_thresholds bytes and must fit in 46 KB. */
+int rbc_count_within(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric,
+                     const double *thresholds, int32_t n_thresholds, int32_t strict, int64_t *counts, float *max_dist,
+                     void *stream);
+
 /* brute_force.py:189-217 bf_search_subset, batched: query i scans
  * x[subset_ids[subset_offsets[i] : subset_offsets[i+1]]] (duplicate-free,
  * validated by the caller); ids are global. */

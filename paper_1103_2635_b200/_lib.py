@@ -54,6 +54,7 @@ EXPORTS = {
     "rbc_pairwise_distances": ([_p, _i64, _p, _i64, _i32, _i32, _p, _p], ctypes.c_int),
     "rbc_bf_search": ([_p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "rbc_bf_search_subsets": ([_p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _p], ctypes.c_int),
+    "rbc_count_within": ([_p, _i64, _p, _i64, _i32, _i32, _p, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "rbc_merge_topk": ([_p, _i32, _i64, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "rbc_bernoulli_draw": ([_i64, ctypes.c_double, _u64, _u64, _u64, _u64, _p, ctypes.POINTER(_i64), _p],
                            ctypes.c_int),

@@ -296,6 +296,17 @@ int rbc_bf_search(const float *q, int64_t nq, const float *x, int64_t n, int32_t
     return keys_to_output(keys.get(), nq * k, ids, dists, st);
 }
 
+int rbc_count_within(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric,
+                     const double *thresholds, int32_t n_thresholds, int32_t strict, int64_t *counts, float *max_dist,
+                     void *stream) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (nq < 0 || n_thresholds < 0) return fail(RBC_EINVAL, "nq and n_thresholds must be >= 0");
+    if (n_thresholds > 0 && (thresholds == nullptr || counts == nullptr))
+        return fail(RBC_EINVAL, "thresholds and counts are required when n_thresholds > 0");
+    return count_within(q, nq, x, n, d, metric, thresholds, n_thresholds, strict != 0, counts, max_dist,
+                        as_stream(stream));
+}
+
 int rbc_bf_search_subsets(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric, int32_t k,
                           const int64_t *subset_ids, const int64_t *subset_offsets, int64_t *ids, float *dists,
                           void *stream) {

@@ -7,6 +7,8 @@
 // tensor-core filtered scans (tc_scan.cu).  Results are independent of the
 // work decomposition because selection is on unique key64 values
 // (brute_force.py:8-12).
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -139,6 +141,73 @@ __global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t co
         unpack_to(key, ids + t, dists + t);
         if (key == kEmptyKey && n_empty) atomicAdd(n_empty, 1);
     }
+}
+
+// ---- ball counts (eval.py:21-27 ball_count, :117-130 rank_error, :133-164 claim1_counts, :44-107
+// estimate_expansion_rate; report.py:72-95 rank_errors) ---------------------------------------------------------
+// Warp per query over all of x.  Every distance is the reference's fp32 value (exact_dist); query i counts, for
+// each of its nt thresholds, the points with f64(dist) < thr (strict) or <= thr (closed) -- numpy's comparison of
+// an fp32 row against a double.  Each lane keeps private counters in shared memory (stride 33: the final
+// column sums are conflict-free), so no n-length distance row is ever written.  Optional: the row maximum.
+template <int METRIC>
+__global__ void __launch_bounds__(256) count_within_kernel(const float *__restrict__ q, int64_t nq,
+                                                           const float *__restrict__ x, int64_t n, int d,
+                                                           const double *__restrict__ thr, int nt, int strict,
+                                                           int64_t *__restrict__ counts, float *__restrict__ dmax) {
+    extern __shared__ __align__(16) unsigned char cw_smem[];
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * nw + w;
+    if (i >= nq) return;
+    const size_t q_bytes = (static_cast<size_t>(nw) * d * sizeof(float) + 15) & ~size_t(15);
+    float *qs = reinterpret_cast<float *>(cw_smem) + static_cast<size_t>(w) * d;
+    double *ts = reinterpret_cast<double *>(cw_smem + q_bytes) + static_cast<size_t>(w) * nt;
+    uint32_t *cs = reinterpret_cast<uint32_t *>(cw_smem + q_bytes + static_cast<size_t>(nw) * nt * sizeof(double)) +
+                   static_cast<size_t>(w) * nt * 33;
+    for (int c = lane; c < d; c += 32) qs[c] = q[i * d + c];
+    for (int t = lane; t < nt; t += 32) ts[t] = thr[i * nt + t];
+    for (int t = 0; t < nt; ++t) cs[t * 33 + lane] = 0;
+    __syncwarp();
+    float mx = 0.f;
+    for (int64_t j = lane; j < n; j += 32) {
+        const float dv = exact_dist<METRIC>(qs, x + j * d, d);
+        mx = fmaxf(mx, dv);
+        const double dd = dv;
+        if (strict) {
+            for (int t = 0; t < nt; ++t) cs[t * 33 + lane] += dd < ts[t] ? 1u : 0u;
+        } else {
+            for (int t = 0; t < nt; ++t) cs[t * 33 + lane] += dd <= ts[t] ? 1u : 0u;
+        }
+    }
+    __syncwarp();
+    for (int t = lane; t < nt; t += 32) {
+        int64_t sum = 0;
+        for (int l = 0; l < 32; ++l) sum += cs[t * 33 + l];
+        counts[i * nt + t] = sum;
+    }
+    // distances are >= 0, so their bit patterns order like unsigned integers
+    const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+    if (dmax != nullptr && lane == 0) dmax[i] = __uint_as_float(m);
+}
+
+int count_within(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, const double *thr, int nt,
+                 int strict, int64_t *counts, float *dmax, cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    const size_t per_warp = static_cast<size_t>(d) * sizeof(float) + static_cast<size_t>(nt) * (sizeof(double) + 33 * 4);
+    constexpr size_t kBudget = 46 * 1024;
+    if (per_warp + 16 > kBudget) return fail(RBC_EINVAL, "count_within: too many thresholds per query for this d");
+    const int nw = static_cast<int>(std::min<size_t>(8, (kBudget - 16) / per_warp));
+    const size_t smem = ((static_cast<size_t>(nw) * d * sizeof(float) + 15) & ~size_t(15)) +
+                        static_cast<size_t>(nw) * nt * (sizeof(double) + 33 * 4);
+    const int64_t blocks = (nq + nw - 1) / nw;
+    if (blocks > 0x7FFFFFFF) return fail(RBC_EINVAL, "count_within: too many queries for one call");
+    if (metric == RBC_L2)
+        count_within_kernel<RBC_L2><<<static_cast<unsigned>(blocks), nw * 32, smem, st>>>(q, nq, x, n, d, thr, nt, strict,
+                                                                                         counts, dmax);
+    else
+        count_within_kernel<RBC_L1><<<static_cast<unsigned>(blocks), nw * 32, smem, st>>>(q, nq, x, n, d, thr, nt, strict,
+                                                                                         counts, dmax);
+    RBC_LAUNCHED();
+    return RBC_OK;
 }
 
 int unpack_keys(const uint64_t *keys, int64_t count, int64_t *ids, float *dists, int *n_empty, cudaStream_t st) {

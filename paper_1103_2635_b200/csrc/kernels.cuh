@@ -107,6 +107,9 @@ int launch_topk(const float *q, int64_t nq, int d, int metric, int k, const Src 
 int topk_sorted_all(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *out,
                     cudaStream_t st);
 
+int count_within(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, const double *thr, int nt,
+                 int strict, int64_t *counts, float *dmax, cudaStream_t st);
+
 int unpack_keys(const uint64_t *keys, int64_t count, int64_t *ids, float *dists, int *n_empty, cudaStream_t st);
 
 int merge_parts(const uint64_t *keys, int parts, int64_t nq, int k_in, int k_out, uint64_t *out, cudaStream_t st);

@@ -281,3 +281,84 @@ def one_shot_params(n: int, c: float, delta: float) -> tuple[int, int]:
         raise ValueError(f"delta must be in (0, 1), got {delta}")
     value = int(min(n, max(1, math.ceil(c * math.sqrt(n) * math.sqrt(math.log(1.0 / delta))))))
     return value, value
+
+
+# ---- RBCI index files (rbc.py:13-18 format, :228-322 writer/reader) -------------------------------------------
+#
+# Layout, all little-endian 32-bit: b"RBCI", version, variant (0 exact / 1 one-shot), metric (0 l2 / 1 l1),
+# sampling mode (0 bernoulli / 1 fixed-count), seed lo, seed hi, |R|, rep ids u32[|R|]; exact: list lengths
+# u32[|R|], ids u32[n], dists f32[n]; one-shot: s, ids u32[|R|*s]; then radii f32[|R|], n, d, X f32[n*d].
+# Files are byte-identical to the reference's, so an index built on the GPU can be loaded by the reference and
+# vice versa (tests/test_index_files.py).
+
+RBCI_MAGIC = b"RBCI"
+RBCI_VERSION = 1
+
+
+def save_index(index, path) -> None:
+    """Write an exact or one-shot index with its embedded database (rbc.py:233-258)."""
+    exact = isinstance(index, RbcExactIndex)
+    seed = int(index.reps.seed)
+    head = np.array([RBCI_VERSION, 0 if exact else 1, _lib.METRIC_CODE[index.metric.kind],
+                     0 if index.reps.sampling_mode == BERNOULLI else 1, seed & 0xFFFFFFFF,
+                     (seed >> 32) & 0xFFFFFFFF, index.reps.size], dtype="<u4")
+    parts = [RBCI_MAGIC, head, np.asarray(index.reps.rep_ids).astype("<u4")]
+    if exact:
+        ids, offsets, dists = index.flat_lists()
+        parts += [np.diff(offsets).astype("<u4"), ids.astype("<u4"), dists.astype("<f4")]
+    else:
+        parts += [np.array([index.s], "<u4"), np.asarray(index.list_ids).astype("<u4")]
+    parts += [np.asarray(index.radii).astype("<f4"), np.array([index.data.n, index.data.d], "<u4"),
+              np.asarray(index.data.values, dtype="<f4")]
+    with open(path, "wb") as fh:
+        for p in parts:
+            fh.write(p if isinstance(p, bytes) else p.tobytes())
+
+
+def load_index(path):
+    """Read an RBCI file (rbc.py:284-322): bit-exact round trip; the device copy is uploaded on first search.
+
+    ``FormatError`` on a bad magic, version or tag; ``OSError`` on a truncated file.
+    """
+    from .dataset import FormatError
+
+    with open(path, "rb") as fh:
+        buf = fh.read()
+    at = 0
+
+    def take(dtype, count):
+        nonlocal at
+        nbytes = np.dtype(dtype).itemsize * count
+        if at + nbytes > len(buf):
+            raise OSError(f"{path}: truncated index file")
+        out = np.frombuffer(buf, dtype=dtype, count=count, offset=at)
+        at += nbytes
+        return out
+
+    if bytes(take("S4", 1)[0]) != RBCI_MAGIC:
+        raise FormatError(f"{path}: bad magic, expected {RBCI_MAGIC!r}")
+    version = int(take("<u4", 1)[0])
+    if version != RBCI_VERSION:
+        raise FormatError(f"{path}: unsupported index version {version}")
+    variant, metric_code, mode_code, seed_lo, seed_hi, nr = (int(v) for v in take("<u4", 6))
+    if variant > 1 or metric_code > 1 or mode_code > 1:
+        raise FormatError(f"{path}: invalid variant/metric/mode tags")
+    reps = RepSet(take("<u4", nr).astype(np.int64), BERNOULLI if mode_code == 0 else FIXED_COUNT,
+                  seed_lo | (seed_hi << 32))
+    if variant == 0:
+        lengths = take("<u4", nr).astype(np.int64)
+        offsets = np.zeros(nr + 1, np.int64)
+        np.cumsum(lengths, out=offsets[1:])
+        total = int(offsets[-1])
+        flat_ids = take("<u4", total).astype(np.int64)
+        flat_d = take("<f4", total).astype(np.float32)
+    else:
+        s = int(take("<u4", 1)[0])
+        lists = take("<u4", nr * s).astype(np.int64).reshape(nr, s)
+    radii = take("<f4", nr).astype(np.float32)
+    n, d = (int(v) for v in take("<u4", 2))
+    data = DataMatrix(take("<f4", n * d).reshape(n, d).astype(np.float32))
+    spec = MetricSpec("l2" if metric_code == 0 else "l1", d)
+    if variant == 0:
+        return RbcExactIndex(data, spec, reps, _split(flat_ids, offsets), _split(flat_d, offsets), radii)
+    return RbcOneShotIndex(data, spec, reps, lists, s, radii)

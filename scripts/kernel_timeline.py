@@ -17,15 +17,16 @@ def main():
     from paper_1103_2635_b200 import _lib
 
     nq = int(sys.argv[1]) if len(sys.argv) > 1 else bench.NQ
+    k = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     x, q = bench.gen_inputs(0)
     index = rbc.build_exact(rbc.DataMatrix(x), bench.NR, rbc.MetricSpec("l2", bench.D), seed=bench.REP_SEED)
     sptr = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     q_dev = _lib.to_device(q)
-    keys = torch.empty((bench.NQ, 1), dtype=torch.int64, device="cuda")
+    keys = torch.empty((bench.NQ, k), dtype=torch.int64, device="cuda")
     stats = _lib.SearchStatsC(None, None, None, None)
 
     def run():
-        _lib.check(_lib.lib.rbc_exact_search_keys(index._dev.handle, _lib.ptr(q_dev), nq, 1, _lib.ptr(keys), stats,
+        _lib.check(_lib.lib.rbc_exact_search_keys(index._dev.handle, _lib.ptr(q_dev), nq, k, _lib.ptr(keys), stats,
                                                   sptr))
 
     for _ in range(3):
@@ -48,7 +49,7 @@ def main():
     r = runs[-1]
     t0 = r[0].time_range.start
     prev_end = t0
-    print(f"nq={nq}: one search, {len(r)} device ops, span {(r[-1].time_range.end - t0) / 1e3:.3f} ms")
+    print(f"nq={nq} k={k}: one search, {len(r)} device ops, span {(r[-1].time_range.end - t0) / 1e3:.3f} ms")
     for e in r:
         s, d = e.time_range.start, e.time_range.end - e.time_range.start
         gap = s - prev_end
