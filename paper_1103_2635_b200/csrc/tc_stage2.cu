@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
     const int cnt = qi >= 0 ? seg_cnt[qi] : 0;
     {
-        // warp-aggregated shared-memory atomics: the rows of a tile mostly share their
-        // lists (segments ascend by list), so lanes holding the same list combine first.
+        // shared-memory max atomics, warp-aggregated when all 32 rows hold the same list at
+        // this step (common at k = 1: segments ascend by list and the rows share lists).
         // Each row's segments are read kSegBatch at a time (independent loads in flight).
         const int lane = threadIdx.x & 31;
         const int wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
@@ -316,11 +316,20 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
             for (int j = 0; j < kSegBatch; ++j) {
                 if (it0 + j >= wmax) break;  // warp-uniform
                 const int32_t p = static_cast<int32_t>(pu[j]);
-                const unsigned grp = __match_any_sync(0xffffffffu, p);
-                const unsigned mlen = __reduce_max_sync(grp, lb[j]), md1 = __reduce_max_sync(grp, db[j]);
-                if (p >= 0 && lane == __ffs(grp) - 1) {
-                    atomicMax(&maxlen[p], static_cast<int>(mlen));
-                    atomicMax(&maxd1[p], static_cast<int>(md1));
+                // whole warp on one list: one full-mask reduction and one atomic pair.  Otherwise
+                // every lane updates on its own (a partial-mask __reduce_max_sync is a loop over
+                // the distinct masks: ~14 CREDUX per step when the rows' lists diverge, k > 1)
+                int same;
+                __match_all_sync(0xffffffffu, p, &same);
+                if (same) {
+                    const unsigned mlen = __reduce_max_sync(0xffffffffu, lb[j]), md1 = __reduce_max_sync(0xffffffffu, db[j]);
+                    if (p >= 0 && lane == 0) {
+                        atomicMax(&maxlen[p], static_cast<int>(mlen));
+                        atomicMax(&maxd1[p], static_cast<int>(md1));
+                    }
+                } else if (p >= 0) {
+                    atomicMax(&maxlen[p], static_cast<int>(lb[j]));
+                    atomicMax(&maxd1[p], static_cast<int>(db[j]));
                 }
             }
         }
