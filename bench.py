@@ -397,7 +397,7 @@ def main():
                                               _lib.ptr(d_b), sptr), "bf")
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
-        bf = {"value": m / dt, "unit": "queries/s", "sample": f"{m} queries x 1M points, k=1",
+        bf = {"value": m / dt, "unit": "queries/s", "sample": f"{m} queries x 1M points, k=1, exact SIMT scan (rbc_bf_search)",
               "rbc_speedup": (value / world) / (m / dt)}
 
     cpu = None
