@@ -972,40 +972,61 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
             }
             continue;
         }
-        // d == 64: one element at a time per group, the 8 lanes each summing 8 of the 64
-        // reference terms (identical fp64 terms; only the association differs), then a
-        // shuffle tree.  The fp32 result equals the reference's sequential sum unless the
-        // tree sum's square root lies within 2^-44 (relative) of an fp32 rounding midpoint
-        // -- the two sums differ by at most 2 * 63 * 2^-53 relative -- in which case the
-        // owner lane recomputes the sequential sum.
+        // d == 64: two elements at a time per group (two row loads in flight), the 8 lanes each
+        // summing 8 of the 64 reference terms of each (identical fp64 terms; only the
+        // association differs), then a shuffle tree.  The fp32 result equals the reference's
+        // sequential sum unless the tree sum's square root lies within 2^-44 (relative) of an
+        // fp32 rounding midpoint -- the two sums differ by at most 2 * 63 * 2^-53 relative --
+        // in which case the owner lane recomputes the sequential sum.
+        const float xs[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        auto finish = [&](double part, int32_t pp) {
+            const double r = __dsqrt_rn(part);
+            float f = __double2float_rn(r);
+            const double mlo = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, -INFINITY)));
+            const double mhi = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, INFINITY)));
+            const double dl = 5.684341886080802e-14;  // 2^-44
+            if (!(r * (1.0 - dl) > mlo && r * (1.0 + dl) < mhi))
+                f = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pp) * d, d);  // near a midpoint
+            const uint64_t key = pack_key(f, static_cast<uint32_t>(perm[pp]));
+            if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+        };
+        const unsigned gmask = (1u << kRerankLanes) - 1u;
         for (;;) {
-            const unsigned who = (__ballot_sync(0xffffffffu, pass != 0) >> gshift) & ((1u << kRerankLanes) - 1u);
-            if (__all_sync(0xffffffffu, who == 0)) break;
-            const int src = who ? __ffs(who) - 1 : 0;
-            const int jj = __shfl_sync(0xffffffffu, pass ? __ffs(pass) - 1 : 0, gshift + src);
-            const int32_t pp = __shfl_sync(0xffffffffu, pos, gshift + src) + jj;
-            double part = 0.0;
-            if (who) {
-                const float4 *r4 = reinterpret_cast<const float4 *>(xp + static_cast<int64_t>(pp) * 64);
-                const float4 ya = __ldg(r4 + sub), yb = __ldg(r4 + sub + kRerankLanes);
-                const float xs[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            // pick A: the group's first pending element; pick B: the next one after A
+            const unsigned whoA = (__ballot_sync(0xffffffffu, pass != 0) >> gshift) & gmask;
+            if (__all_sync(0xffffffffu, whoA == 0)) break;
+            const int srcA = whoA ? __ffs(whoA) - 1 : 0;
+            const unsigned passA = (whoA && sub == srcA) ? pass & (pass - 1) : pass;
+            const unsigned whoB = (__ballot_sync(0xffffffffu, passA != 0) >> gshift) & gmask;
+            const int srcB = whoB ? __ffs(whoB) - 1 : 0;
+            const int jA = __shfl_sync(0xffffffffu, pass ? __ffs(pass) - 1 : 0, gshift + srcA);
+            const int jB = __shfl_sync(0xffffffffu, passA ? __ffs(passA) - 1 : 0, gshift + srcB);
+            const int32_t ppA = __shfl_sync(0xffffffffu, pos, gshift + srcA) + jA;
+            const int32_t ppB = __shfl_sync(0xffffffffu, pos, gshift + srcB) + jB;
+            double partA = 0.0, partB = 0.0;
+            if (whoA) {
+                const float4 *rA = reinterpret_cast<const float4 *>(xp + static_cast<int64_t>(ppA) * 64);
+                const float4 *rB = reinterpret_cast<const float4 *>(xp + static_cast<int64_t>(whoB ? ppB : ppA) * 64);
+                const float4 ya = __ldg(rA + sub), yb = __ldg(rA + sub + kRerankLanes);
+                const float4 za = __ldg(rB + sub), zb = __ldg(rB + sub + kRerankLanes);
                 const float ys[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+                const float zs[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
 #pragma unroll
-                for (int t = 0; t < 8; ++t) part = __dadd_rn(part, l2_term(xs[t], ys[t]));
+                for (int t = 0; t < 8; ++t) {
+                    partA = __dadd_rn(partA, l2_term(xs[t], ys[t]));
+                    partB = __dadd_rn(partB, l2_term(xs[t], zs[t]));
+                }
             }
 #pragma unroll
-            for (int o = kRerankLanes / 2; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-            if (who && sub == src) {
+            for (int o = kRerankLanes / 2; o > 0; o >>= 1) {
+                partA = __dadd_rn(partA, __shfl_xor_sync(0xffffffffu, partA, o));
+                partB = __dadd_rn(partB, __shfl_xor_sync(0xffffffffu, partB, o));
+            }
+            pass = passA;
+            if (whoA && sub == srcA) finish(partA, ppA);
+            if (whoB && sub == srcB) {
                 pass &= pass - 1;
-                const double r = __dsqrt_rn(part);
-                float f = __double2float_rn(r);
-                const double mlo = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, -INFINITY)));
-                const double mhi = 0.5 * (static_cast<double>(f) + static_cast<double>(nextafterf(f, INFINITY)));
-                const double dl = 5.684341886080802e-14;  // 2^-44
-                if (!(r * (1.0 - dl) > mlo && r * (1.0 + dl) < mhi))
-                    f = exact_dist<RBC_L2, 8>(qrow, xp + static_cast<int64_t>(pp) * d, d);  // near a midpoint
-                const uint64_t key = pack_key(f, static_cast<uint32_t>(perm[pp]));
-                if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+                finish(partB, ppB);
             }
         }
     }
