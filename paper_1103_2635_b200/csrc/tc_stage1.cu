@@ -334,12 +334,16 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
                                                                     uint32_t *__restrict__ key,
                                                                     unsigned *__restrict__ hist,
                                                                     float *__restrict__ pd2) {
-    __shared__ uint32_t sp[kPilots * 32];  // pilot rows, 64 f16 (32 words) each; absent pilots zero
+    // pilot rows, 64 f16 (32 words) each, at a 36-word stride: the 8 row groups of an mma
+    // B fragment then read 8 different bank quads (a 32-word stride is an 8-way conflict);
+    // absent pilots zero
+    constexpr int kSpStride = 36;
+    __shared__ __align__(16) uint32_t sp[kPilots * kSpStride];
     __shared__ float sn[kPilots];
     __shared__ unsigned sh[kPilots];
     for (int t = threadIdx.x; t < kPilots * 8; t += blockDim.x) {
         const uint4 v = t < npilot * 8 ? prow[t] : make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4 *>(sp)[t] = v;
+        reinterpret_cast<uint4 *>(sp)[(t >> 3) * (kSpStride / 4) + (t & 7)] = v;
     }
     for (int j = threadIdx.x; j < kPilots; j += blockDim.x) {
         sh[j] = 0;
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
         const uint32_t a0 = f2h2(x0.x, x0.y), a1 = f2h2(x1.x, x1.y), a2 = f2h2(x2.x, x2.y), a3 = f2h2(x3.x, x3.y);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const uint32_t *prow_n = sp + (8 * j + g) * 32;  // pilot n = 8 j + g, words = dim pairs
+            const uint32_t *prow_n = sp + (8 * j + g) * kSpStride;  // pilot n = 8 j + g, words = dim pairs
             const uint32_t b0 = prow_n[(16 * ks + 2 * t4) >> 1], b1 = prow_n[(16 * ks + 8 + 2 * t4) >> 1];
             asm volatile(
                 "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
