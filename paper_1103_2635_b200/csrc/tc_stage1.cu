@@ -442,8 +442,10 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
 // bucket).  Order inside a bucket follows the blocks' claims -- it only shapes tiles.
 __global__ void __launch_bounds__(128) pilot_scatter_kernel(const uint32_t *__restrict__ key, int64_t nq, int npilot,
                                                             const unsigned *__restrict__ hist,
-                                                            unsigned *__restrict__ cursor, int32_t *__restrict__ qorder) {
+                                                            unsigned *__restrict__ cursor, int32_t *__restrict__ qorder,
+                                                            int32_t *__restrict__ zero2) {
     __shared__ unsigned s_start[kPilots], s_cnt[kPilots], s_base[kPilots];
+    if (blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;  // stage 1's two flags (no memset node)
     if (threadIdx.x == 0) {
         unsigned run = 0;
         for (int j = 0; j < npilot; ++j) {
@@ -1373,8 +1375,9 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     pilot_key_kernel<<<grid_for(nq, kPilotWarps * 16), kPilotWarps * 32, 0, st>>>(
         q64, nq, t->prow, t->pnorm, npilot, t->reps64, t->pilots, pkey.get(), phist.get(), pd2.get());
     RBC_LAUNCHED();
+    RBC_CHECK(flags.alloc(2, st));
     pilot_scatter_kernel<<<grid_for(nq, 128), 128, 0, st>>>(pkey.get(), nq, npilot, phist.get(), phist.get() + kPilots,
-                                                           qorder.get());
+                                                           qorder.get(), flags.get());
     RBC_LAUNCHED();
     RBC_CHECK(c1_lb.alloc(nq * cap1, st));
     RBC_CHECK(c1_p.alloc(nq * cap1, st));
@@ -1386,7 +1389,6 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(rec.alloc(nq * cap_rec, st));
     RBC_CHECK(rec_dt.alloc(nq * cap_rec, st));
     RBC_CHECK(rec_e.alloc(nq, st));
-    RBC_CHECK(flags.alloc(2, st));
     RBC_CHECK(out.gamma.alloc(nq, st));
     RBC_CHECK(out.nseg.alloc(nq, st));
     RBC_CHECK(out.cand.alloc(nq, st));
@@ -1396,7 +1398,6 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(out.seg_len.alloc(nq * cap_rec, st));
     RBC_CHECK(out.seg_list.alloc(nq * cap_rec, st));
     RBC_CHECK(out.seg_d1.alloc(nq * cap_rec, st));
-    RBC_CUDA(cudaMemsetAsync(flags.get(), 0, 2 * sizeof(int32_t), st));
     S1Params P;
     P.rb = t->rb;
     P.plane1 = t->plane1 ? 1 : 0;

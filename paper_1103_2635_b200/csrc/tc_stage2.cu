@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
     const int64_t *__restrict__ offsets, WorkItem *__restrict__ work,
     int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key, int warm,
-    int64_t cap_work) {
+    int64_t cap_work, int32_t *__restrict__ cand_count, int32_t *__restrict__ counters) {
     if (threadIdx.x == 0) tile_ids[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
@@ -297,6 +297,13 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     __syncthreads();
     const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
+    // stage 2's per-query group counts and its two counters start at zero (in place of two
+    // memset nodes; unconditional: the re-rank reads the counts even when stage 2 bails out)
+    if (tq < nq) {
+#pragma unroll
+        for (int h = 0; h < kParts; ++h) cand_count[kParts * tq + h] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 2) counters[threadIdx.x] = 0;
     const int32_t qi = tq < nq ? order[tq] : -1;
     const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
     const int cnt = qi >= 0 ? seg_cnt[qi] : 0;
@@ -1233,7 +1240,9 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     // re-runs with the size reported in status[0]
     const int64_t total_work = cap_work;
     DevBuf<WorkItem> work;
-    DevBuf<int32_t> cut;
+    DevBuf<int32_t> cut, cand_count, counters;
+    RBC_CHECK(cand_count.alloc(nq * kParts, st));  // zeroed by tile_fill_kernel
+    RBC_CHECK(counters.alloc(2, st));              // (overflow count, tile counter), zeroed by tile_fill_kernel
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
     tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), work_total.get(), tids.get(),
@@ -1242,7 +1251,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
                                                    idx->radii, tc->poff,
                                                    idx->offsets, work.get(), cut.get(),
-                                                   tkey.get(), warm, cap_work);
+                                                   tkey.get(), warm, cap_work, cand_count.get(), counters.get());
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
                                              tile_order.get(), ntiles, 0, 32, st));
@@ -1250,15 +1259,11 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     // 3. the tensor-core scan
     const int cap = 12 + 6 * k;  // 8-column groups per query and column part
     DevBuf<float> cand_lb, cand_ufin, q64buf;
-    DevBuf<int32_t> cand_pos, cand_count, ovf_list, counters;
+    DevBuf<int32_t> cand_pos, ovf_list;
     RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 12, st));
     RBC_CHECK(cand_pos.alloc(nq * kParts * cap, st));
-    RBC_CHECK(cand_count.alloc(nq * kParts, st));
     RBC_CHECK(cand_ufin.alloc(nq * kParts, st));
-    RBC_CUDA(cudaMemsetAsync(cand_count.get(), 0, sizeof(int32_t) * nq * kParts, st));
     RBC_CHECK(ovf_list.alloc(nq * kParts, st));
-    RBC_CHECK(counters.alloc(2, st));
-    RBC_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), st));
     const float *q64 = q;
     if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
         RBC_CHECK(q64buf.alloc(nq * 64, st));
