@@ -359,9 +359,15 @@ void search_graph_release(const rbc_index *idx) {
 // enqueue the fused sequence for one chunk (q0 = 0) on st
 // status words of one fused search: [0] stage-2 work items needed, [1] overflowed rows,
 // [2] stage-1 failure flag (int32) -- one 24-byte read-back
+// the graph's last node: the status words straight into the caller's pinned (UVA-mapped)
+// read-back buffer, instead of a device-to-host copy after the graph
+__global__ void status_to_host_kernel(const int64_t *__restrict__ status, int64_t *__restrict__ host) {
+    if (threadIdx.x < 3) host[threadIdx.x] = status[threadIdx.x];
+}
+
 static int enqueue_fused(const rbc_index *idx, const float *q, int64_t m, int k, uint64_t *keys,
                          const rbc_search_stats &stats, int64_t cap, bool tc2, PruneOut &po, DevBuf<int64_t> &status,
-                         cudaStream_t st) {
+                         int64_t *host_status, cudaStream_t st) {
     RBC_CHECK(status.alloc(3, st));
     RBC_CUDA(cudaMemsetAsync(status.get(), 0, 3 * sizeof(int64_t), st));
     RBC_CHECK(tc_stage1(idx, q, m, k, po, reinterpret_cast<int32_t *>(status.get() + 2), st));
@@ -370,6 +376,8 @@ static int enqueue_fused(const rbc_index *idx, const float *q, int64_t m, int k,
         RBC_CUDA(cudaMemcpyAsync(stats.gamma, po.gamma.get(), sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
     if (stats.candidates)
         RBC_CUDA(cudaMemcpyAsync(stats.candidates, po.cand.get(), sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, st));
+    status_to_host_kernel<<<1, 32, 0, st>>>(status.get(), host_status);
+    RBC_LAUNCHED();
     return RBC_OK;
 }
 
@@ -445,6 +453,7 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
             g.arena_cap = want;
         }
         if (!g.cs) RBC_CUDA(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+        if (!g.host_status) RBC_CUDA(cudaMallocHost(&g.host_status, 4 * sizeof(int64_t)));
         Arena arena{g.arena, g.arena_cap, 0};
         g.po.reset(new PruneOut());
         g.po->pr = stats.reps_pruned_radius;
@@ -455,7 +464,7 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
         cudaGraph_t graph = nullptr;
         int rc = cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess ? RBC_OK : RBC_ECUDA;
         if (rc == RBC_OK) {
-            rc = enqueue_fused(idx, q, nq, k, keys, stats, cap, tc2, *g.po, status, g.cs);
+            rc = enqueue_fused(idx, q, nq, k, keys, stats, cap, tc2, *g.po, status, g.host_status, g.cs);
             const cudaError_t e = cudaStreamEndCapture(g.cs, &graph);
             if (rc == RBC_OK && e != cudaSuccess) rc = RBC_ECUDA;
         }
@@ -474,11 +483,9 @@ int exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k, u
         if (getenv("RBC_DEBUG_GRAPH")) fprintf(stderr, "[graph] captured nq=%lld k=%d cap=%lld arena=%.1f MB\n",
                                                (long long)nq, k, (long long)cap, g.arena_cap / 1e6);
         g.status = status.get();
-        if (!g.host_status) RBC_CUDA(cudaMallocHost(&g.host_status, 4 * sizeof(int64_t)));
     }
     RBC_CUDA(cudaGraphLaunch(g.exec, st));
     note_launch(static_cast<int>(g.launches));
-    RBC_CUDA(cudaMemcpyAsync(g.host_status, g.status, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaStreamSynchronize(st));
     const int32_t f = *reinterpret_cast<const int32_t *>(g.host_status + 2);
     const int64_t s2[2] = {g.host_status[0], g.host_status[1]};
