@@ -22,6 +22,8 @@ struct PruneOut {
     DevBuf<float> seg_d1;      // [total] exact dist(q, r_p) of the segment's list
     DevBuf<uint64_t> order_key; // [nq] (first surviving list << 24) | nearest rep: query grouping key
     DevBuf<int32_t> qorder;     // [nq] stage-1 query order (by nearest pilot), fused path only
+    DevBuf<unsigned long long> s2_total;  // stage-2 work counter, zeroed by the fused stage 1 (pilot scatter)
+    mutable bool s2_total_zeroed = false;  // true until the first tc_stage2 call takes it
     const float *d1 = nullptr; // stage-1 distances [nq, nr] (owned by the caller)
     int64_t total_segs = 0;
     int32_t *pr = nullptr;     // optional stats outputs (caller memory)

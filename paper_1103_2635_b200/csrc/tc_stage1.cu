@@ -443,9 +443,12 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
 __global__ void __launch_bounds__(128) pilot_scatter_kernel(const uint32_t *__restrict__ key, int64_t nq, int npilot,
                                                             const unsigned *__restrict__ hist,
                                                             unsigned *__restrict__ cursor, int32_t *__restrict__ qorder,
-                                                            int32_t *__restrict__ zero2) {
+                                                            int32_t *__restrict__ zero2,
+                                                            unsigned long long *__restrict__ zero64) {
     __shared__ unsigned s_start[kPilots], s_cnt[kPilots], s_base[kPilots];
-    if (blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;  // stage 1's two flags (no memset node)
+    // stage 1's two flags and stage 2's work counter start at zero here (no memset nodes)
+    if (blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 2) *zero64 = 0ull;
     if (threadIdx.x == 0) {
         unsigned run = 0;
         for (int j = 0; j < npilot; ++j) {
@@ -1376,8 +1379,10 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
         q64, nq, t->prow, t->pnorm, npilot, t->reps64, t->pilots, pkey.get(), phist.get(), pd2.get());
     RBC_LAUNCHED();
     RBC_CHECK(flags.alloc(2, st));
+    RBC_CHECK(out.s2_total.alloc(1, st));
     pilot_scatter_kernel<<<grid_for(nq, 128), 128, 0, st>>>(pkey.get(), nq, npilot, phist.get(), phist.get() + kPilots,
-                                                           qorder.get(), flags.get());
+                                                           qorder.get(), flags.get(), out.s2_total.get());
+    out.s2_total_zeroed = true;
     RBC_LAUNCHED();
     RBC_CHECK(c1_lb.alloc(nq * cap1, st));
     RBC_CHECK(c1_p.alloc(nq * cap1, st));

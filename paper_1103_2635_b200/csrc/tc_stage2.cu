@@ -1223,11 +1223,17 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     }
     // 2. union of surviving lists per tile
     DevBuf<int64_t> nwork, work_off;
-    DevBuf<unsigned long long> work_total;
+    DevBuf<unsigned long long> work_total_own;
     RBC_CHECK(nwork.alloc(ntiles, st));
     RBC_CHECK(work_off.alloc(ntiles, st));
-    RBC_CHECK(work_total.alloc(1, st));
-    RBC_CUDA(cudaMemsetAsync(work_total.get(), 0, sizeof(unsigned long long), st));
+    unsigned long long *work_total = po.s2_total.get();
+    if (po.s2_total_zeroed) {
+        po.s2_total_zeroed = false;  // a re-run (capacity retry) zeroes its own counter
+    } else {
+        RBC_CHECK(work_total_own.alloc(1, st));
+        RBC_CUDA(cudaMemsetAsync(work_total_own.get(), 0, sizeof(unsigned long long), st));
+        work_total = work_total_own.get();
+    }
     const size_t smem3 = 3 * sizeof(int32_t) * nr;
     if (smem3 > 200 * 1024) return fail(RBC_EINVAL, "too many representatives for the tile prep");
     cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
@@ -1245,7 +1251,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(counters.alloc(2, st));              // (overflow count, tile counter), zeroed by tile_fill_kernel
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
-    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), work_total.get(), tids.get(),
+    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), work_total, tids.get(),
                                                    po.seg_off.get(),
                                                    po.nseg.get(), po.seg_list.get(),
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
@@ -1287,7 +1293,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.nq = nq;
     P.work_off = work_off.get();
     P.nwork = nwork.get();
-    P.work_total = work_total.get();
+    P.work_total = work_total;
     P.work = work.get();
     P.cut = cut.get();
     P.cand_lb = cand_lb.get();
@@ -1353,7 +1359,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         else overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
         RBC_LAUNCHED();
     }
-    stage2_status_kernel<<<1, 1, 0, st>>>(work_total.get(), counters.get(), status_dev);
+    stage2_status_kernel<<<1, 1, 0, st>>>(work_total, counters.get(), status_dev);
     RBC_LAUNCHED();
 #ifdef RBC_S2_TIMING
     if (getenv("RBC_DEBUG_S2")) {  // diagnostic: role timing (synchronises)
