@@ -368,8 +368,9 @@ __global__ void status_to_host_kernel(const int64_t *__restrict__ status, int64_
 static int enqueue_fused(const rbc_index *idx, const float *q, int64_t m, int k, uint64_t *keys,
                          const rbc_search_stats &stats, int64_t cap, bool tc2, PruneOut &po, DevBuf<int64_t> &status,
                          int64_t *host_status, cudaStream_t st) {
+    // status[2] (the stage-1 failure words) is zeroed by the pilot scatter; status[0..1] are
+    // written by stage 2's status kernel and read only when stage 2 ran
     RBC_CHECK(status.alloc(3, st));
-    RBC_CUDA(cudaMemsetAsync(status.get(), 0, 3 * sizeof(int64_t), st));
     RBC_CHECK(tc_stage1(idx, q, m, k, po, reinterpret_cast<int32_t *>(status.get() + 2), st));
     if (tc2) RBC_CHECK(tc_stage2(idx, q, m, k, po, keys, cap, status.get(), st));
     if (stats.gamma)

@@ -444,11 +444,14 @@ __global__ void __launch_bounds__(128) pilot_scatter_kernel(const uint32_t *__re
                                                             const unsigned *__restrict__ hist,
                                                             unsigned *__restrict__ cursor, int32_t *__restrict__ qorder,
                                                             int32_t *__restrict__ zero2,
-                                                            unsigned long long *__restrict__ zero64) {
+                                                            unsigned long long *__restrict__ zero64,
+                                                            int32_t *__restrict__ fail2) {
     __shared__ unsigned s_start[kPilots], s_cnt[kPilots], s_base[kPilots];
-    // stage 1's two flags and stage 2's work counter start at zero here (no memset nodes)
+    // stage 1's two flags, its failure words and stage 2's work counter start at zero here
+    // (no memset nodes; every writer of them runs after this kernel)
     if (blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2) *zero64 = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x >= 4 && threadIdx.x < 6) fail2[threadIdx.x - 4] = 0;
     if (threadIdx.x == 0) {
         unsigned run = 0;
         for (int j = 0; j < npilot; ++j) {
@@ -1381,7 +1384,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     RBC_CHECK(flags.alloc(2, st));
     RBC_CHECK(out.s2_total.alloc(1, st));
     pilot_scatter_kernel<<<grid_for(nq, 128), 128, 0, st>>>(pkey.get(), nq, npilot, phist.get(), phist.get() + kPilots,
-                                                           qorder.get(), flags.get(), out.s2_total.get());
+                                                           qorder.get(), flags.get(), out.s2_total.get(), fail_dev);
     out.s2_total_zeroed = true;
     RBC_LAUNCHED();
     RBC_CHECK(c1_lb.alloc(nq * cap1, st));
