@@ -450,3 +450,31 @@ def test_graph_replay_matches_direct(rbc, oracle, monkeypatch, k):
     for rep in run(False):
         for a, b in zip(rep, direct):
             assert np.array_equal(a, b)
+
+
+@pytest.fixture(scope="module")
+def cfg2_full(rbc):
+    """BASELINE cfg2 at full size: clusters(n = 1.1M, d = 64, seed 1, C = 64, sigma = 0.05) -> X 1M, Q 100k."""
+    full = rbc.gen_synthetic("clusters", 1_100_000, 64, 1, n_clusters=64, cluster_sigma=0.05).values
+    x, q = np.ascontiguousarray(full[:1_000_000]), np.ascontiguousarray(full[1_000_000:])
+    idx = rbc.build_exact(rbc.DataMatrix(x), 1000, rbc.MetricSpec("l2", 64), seed=0)
+    return x, q, idx
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_cfg2_full_size_tc_matches_exact_engine(rbc, oracle, cfg2_full, k):
+    """Full-size property: the tensor-core path (direct launch, graph capture, graph replay) equals the exact SIMT
+    engine on all 100k cfg2 queries (ids, distances and every stats field), and the oracle on a sample."""
+    x, q, idx = cfg2_full
+    assert idx.reps.size == 1016
+    fast, exact = _both_engines(rbc, idx, q, k)
+    for _ in range(2):  # second and third calls: graph capture, then replay
+        again = rbc.exact_query_arrays(idx, q, k)
+        for a, b in zip(again, fast):
+            assert np.array_equal(a, b)
+    for a, b in zip(fast, exact):
+        assert np.array_equal(a, b)
+    li, off, ld = idx.flat_lists()
+    sample = np.ascontiguousarray(q[::500])
+    want = oracle.exact_query(x, idx.reps.rep_ids, li, off, ld, idx.radii, sample, k)
+    assert np.array_equal(fast[0][::500], want[0]) and np.array_equal(fast[1][::500], want[1])
