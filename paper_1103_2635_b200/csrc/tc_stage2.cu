@@ -442,8 +442,16 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
     // LPT: heavier tiles first
     if (threadIdx.x == 0) {
-        const unsigned long long wk = s_work < 0xFFFFFFFFull ? s_work : 0xFFFFFFFFull;  // 32-bit LPT key
-        tile_key[blockIdx.x] = 0xFFFFFFFFull - wk;
+        // 16-bit LPT key: the work as a 5-bit exponent and 11-bit mantissa (monotonic, ~0.05%
+        // resolution), so the tile sort needs 16 key bits (two radix passes instead of four)
+        const unsigned long long wk = s_work;
+        unsigned key = 0;
+        if (wk > 0) {
+            const int e = min(63 - __clzll(static_cast<long long>(wk)), 31);
+            const unsigned m = static_cast<unsigned>(e >= 11 ? (wk >> (e - 11)) : (wk << (11 - e))) & 0x7FFu;
+            key = (static_cast<unsigned>(e) << 11) | m;
+        }
+        tile_key[blockIdx.x] = 0xFFFFull - key;
     }
 }
 
@@ -1197,7 +1205,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(tile_order.alloc(ntiles, st));
     size_t tb2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkey.get(), tkey_sorted.get(), tids.get(), tile_order.get(), ntiles, 0,
-                                    32, st);
+                                    16, st);
     DevBuf<unsigned char> tmp;
     const int32_t *order = po.qorder.get();
     if (!order) {
@@ -1260,7 +1268,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                                    tkey.get(), warm, cap_work, cand_count.get(), counters.get());
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
-                                             tile_order.get(), ntiles, 0, 32, st));
+                                             tile_order.get(), ntiles, 0, 16, st));
     note_launch();
     // 3. the tensor-core scan
     const int cap = 12 + 6 * k;  // 8-column groups per query and column part
