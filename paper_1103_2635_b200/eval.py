@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from .brute_force import _check_dims, bf_search_arrays
 from .dataset import DataMatrix, _as_values
-from .metric import MetricSpec
+from .metric import MetricSpec, pairwise_distances
 from .rbc import sample_representatives
 
 RANK_BASELINE_K = 512  # report.py:26
@@ -129,8 +129,6 @@ def rank_error(data, q, returned_id: int, spec: MetricSpec) -> int:
         raise ValueError(f"returned_id {returned_id} out of range")
     qv = np.asarray(q, dtype=np.float32).reshape(1, -1)
     _check_dims(qv, xv, spec)
-    from .metric import pairwise_distances
-
     ret = pairwise_distances(qv, xv[returned_id:returned_id + 1], spec)[0, 0]
     return int(count_within(qv, xv, spec, np.array([[ret]], np.float64), strict=True)[0, 0])
 
