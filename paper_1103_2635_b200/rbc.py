@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .dataset import DataMatrix
+from .dataset import DataMatrix, FormatError
 from .metric import MetricSpec
 
 BERNOULLI = "bernoulli"
@@ -320,8 +320,6 @@ def load_index(path):
 
     ``FormatError`` on a bad magic, version or tag; ``OSError`` on a truncated file.
     """
-    from .dataset import FormatError
-
     with open(path, "rb") as fh:
         buf = fh.read()
     at = 0
