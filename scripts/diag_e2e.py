@@ -39,7 +39,7 @@ def main():
         ts.sort()
         return ts[len(ts) // 2]
 
-    for m in (25000, 100000):
+    for m in (25000, 50000, 100000):
         t = dev_time(m)
         print(f"device nq={m}: {t:.3f} ms  {m / t / 1e3:.2f} Mq/s", flush=True)
     q_pin = torch.from_numpy(q).pin_memory()
