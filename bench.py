@@ -34,9 +34,40 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N, D, NQ, C, SIGMA, DATA_SEED, NR, REP_SEED, K = 1_000_000, 64, 100_000, 64, 0.05, 1, 1000, 0, 1
+# BASELINE.json configs: the headline (default) is cfg2; the others are
+# bench lines of their own (``--config cfgN``), committed under profiles/.
+CONFIGS = {
+    "cfg1": dict(kind="oneshot", n=10_000, d=16, nq=1_000, C=8, seed=7, n_r=100, s=100, mode="fixed-count",
+                 metric="l2", k=1, workload="cfg1: one-shot RBC 1-NN L2, clusters n=10k d=16 C=8, n_r=s=100 "
+                                           "(fixed-count), 1k queries"),
+    "cfg2": dict(kind="exact", n=1_000_000, d=64, nq=100_000, C=64, seed=1, n_r=1000, metric="l2", k=1,
+                 workload="cfg2: exact RBC 1-NN L2, clusters n=1M d=64 C=64 sigma=0.05, |R|=1016"),
+    "cfg3": dict(kind="exact", n=581_012, d=54, nq=100_000, C=8, seed=3, n_r=763, metric="l2", k=10,
+                 workload="cfg3: exact RBC 10-NN L2, Covertype-shaped clusters n=581,012 d=54 C=8, "
+                          "n_r=763 (|R|~777), 100k queries per rank"),
+    "cfg4": dict(kind="oneshot", n=2_000_000, d=21, nq=100_000, C=8, seed=4, n_r=1415, s=1415, mode="bernoulli",
+                 metric="l1", k=1, workload="cfg4: one-shot RBC 1-NN L1, Robot-shaped clusters n=2M d=21 C=8, "
+                                            "n_r=s=1415 (|R|~1455), 100k queries"),
+}
+SIGMA, REP_SEED = 0.05, 0
+CFG = CONFIGS["cfg2"]
+N, D, NQ, C, DATA_SEED, NR, K = (CFG[x] for x in ("n", "d", "nq", "C", "seed", "n_r", "k"))
 METRIC = "RBC queries/sec (exact 1-NN, n=1M d=64)"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def select_config(name: str, k=None):
+    """Point the module-level workload constants at config `name` (k overrides its k)."""
+    global CFG, N, D, NQ, C, DATA_SEED, NR, K, METRIC
+    CFG = dict(CONFIGS[name])
+    if k is not None:
+        CFG["k"] = k
+    N, D, NQ, C, DATA_SEED, NR, K = (CFG[x] for x in ("n", "d", "nq", "C", "seed", "n_r", "k"))
+    kind = "exact" if CFG["kind"] == "exact" else "one-shot"
+    nn = f"{N / 1e6:g}M" if N >= 1_000_000 else f"{N / 1e3:g}k"
+    METRIC = f"RBC queries/sec ({kind} {K}-NN{' L1' if CFG['metric'] == 'l1' else ''}, n={nn} d={D})"
+    if name == "cfg2" and K == 1:
+        METRIC = "RBC queries/sec (exact 1-NN, n=1M d=64)"  # BASELINE.json's metric string
 
 
 def log(*a):
@@ -44,6 +75,7 @@ def log(*a):
 
 
 def gen_inputs(rank: int):
+    """Reference generator ``clusters`` (dataset.py:142-148): n + nq rows, X = first n, Q = the rest."""
     rng = np.random.default_rng(DATA_SEED)
     centers = rng.random((C, D))
     assignment = rng.integers(C, size=N + NQ)
@@ -55,18 +87,28 @@ def gen_inputs(rank: int):
     return x, q
 
 
-def ncu_traffic(kernel="stage2_tc_kernel"):
-    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the newest committed
-    ncu --set full summary under profiles/ (bytes), or None."""
+def kt_of(k: int) -> int:
+    """Template width of the stage-2 / re-rank kernels serving k (tc_stage2.cu launch dispatch)."""
+    return 1 if k == 1 else 4 if k <= 4 else 8 if k <= 8 else 16
+
+
+def ncu_traffic(kernel: str, cfg: str):
+    """dram__bytes_read + dram__bytes_write per launch of exactly `kernel` (e.g. "stage2_tc_kernel<1>")
+    from the newest committed ncu --set full summary for config `cfg` under profiles/, or None.
+    Summary files: r<round>_ncu_[<cfg>_]v<ver>_kernels.txt (no cfg tag = cfg2)."""
     import glob
     import re
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_v*_kernels.txt")),
-                   key=lambda f: int(re.search(r"_v(\d+)_", f).group(1)))
-    for path in reversed(files):
+    found = []
+    for path in glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_*kernels.txt")):
+        m = re.match(r"r(\d+)_ncu_(?:(cfg\d)_)?v(\d+)_kernels\.txt$", os.path.basename(path))
+        if m and (m.group(2) or "cfg2") == cfg:
+            found.append(((int(m.group(1)), int(m.group(3))), path))
+    for _, path in sorted(found, reverse=True):
         block, total = None, 0.0
         for line in open(path):
             if line.startswith("== "):
-                block = kernel in line
+                name = line[3:].strip().split("::")[-1]
+                block = name == kernel
             elif block and "dram__bytes_" in line:
                 m = re.search(r"= ([\d.]+) (\w+)", line)
                 if m:
@@ -163,27 +205,60 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(x, q, index, budget_s=12.0):
+def _nn_label():
+    return f"{'exact' if CFG['kind'] == 'exact' else 'one-shot'} {K}-NN {CFG['metric'].upper()}"
+
+
+def oracle_index(x, index):
+    """The oracle's view of a built index (rep ids + lists)."""
+    reps = index.reps.rep_ids
+    if CFG["kind"] == "exact":
+        li, off, ld = index.flat_lists()
+        return (reps, li, off, ld, index.radii)
+    return (reps, np.asarray(index.list_ids, np.int64))
+
+
+def oracle_search(orc, x, oidx, q):
+    if CFG["kind"] == "exact":
+        reps, li, off, ld, radii = oidx
+        return orc.exact_query(x, reps, li, off, ld, radii, q, K, metric=CFG["metric"])
+    reps, lists = oidx
+    return orc.one_shot_query(x, reps, lists, q, K, metric=CFG["metric"])
+
+
+def cpu_baseline(x, q, index, cfg_name, budget_s=12.0):
     """The oracle (C restatement of the reference, OpenMP) on the host cores, bounded query sample."""
     from oracle import oracle as orc
 
     orc.build()
-    reps = index.reps.rep_ids
-    li, off, ld = index.flat_lists()
-    radii = index.radii
-    m = 256
+    oidx = oracle_index(x, index)
+    m = min(256, len(q))
     t0 = time.perf_counter()
-    orc.exact_query(x, reps, li, off, ld, radii, q[:m], K)
+    oracle_search(orc, x, oidx, q[:m])
     dt = time.perf_counter() - t0
     m2 = int(min(len(q), max(m, m * budget_s / max(dt, 1e-3))))
     t0 = time.perf_counter()
-    orc.exact_query(x, reps, li, off, ld, radii, q[:m2], K)
+    oracle_search(orc, x, oidx, q[:m2])
     dt = time.perf_counter() - t0
     return {"value": m2 / dt, "unit": "queries/s", "cores": orc.threads(), "kind": "port",
-            "sample": f"{m2} of the {len(q)} cfg2 queries, exact 1-NN via oracle/rbc_oracle.c (OpenMP)"}
+            "sample": f"{m2} of the {len(q)} {cfg_name} queries, {_nn_label()} via oracle/rbc_oracle.c (OpenMP)"}
 
 
-def run_reference(args, rank, world):
+def oracle_build(orc, x):
+    """The reference's build on the oracle (rbc.py:147-200), timed by the caller."""
+    if CFG["kind"] == "exact":
+        reps = orc.bernoulli(N, NR / N, REP_SEED)
+        li, off, ld, radii = orc.build_exact(x, reps, metric=CFG["metric"])
+        return (reps, li, off, ld, radii)
+    if CFG.get("mode") == "fixed-count":
+        reps = np.sort(np.random.default_rng(REP_SEED).choice(N, size=NR, replace=False)).astype(np.int64)
+    else:
+        reps = orc.bernoulli(N, NR / N, REP_SEED)
+    lists, _ = orc.build_one_shot(x, reps, CFG["s"], metric=CFG["metric"])
+    return (reps, lists)
+
+
+def run_reference(args, rank, world, cfg_name):
     """--impl reference: the reference algorithm's CPU restatement (oracle) on this host's cores."""
     if rank != 0:
         return
@@ -192,15 +267,14 @@ def run_reference(args, rank, world):
     orc.build()
     x, q = gen_inputs(0)
     t0 = time.perf_counter()
-    reps = orc.bernoulli(N, NR / N, REP_SEED)
-    li, off, ld, radii = orc.build_exact(x, reps)
+    oidx = oracle_build(orc, x)
     build_s = time.perf_counter() - t0
-    per_step = 1024
+    per_step = min(1024, NQ)
     times = []
     for step in range(args.warmup + args.steps):
-        lo = (step * per_step) % (NQ - per_step)
+        lo = (step * per_step) % max(1, NQ - per_step)
         t0 = time.perf_counter()
-        orc.exact_query(x, reps, li, off, ld, radii, q[lo: lo + per_step], K)
+        oracle_search(orc, x, oidx, q[lo: lo + per_step])
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             times.append(dt)
@@ -208,34 +282,39 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": "queries/s", "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2: exact RBC 1-NN L2, clusters n=1M d=64 C=64 sigma=0.05, |R|=1016",
-                       "queries_per_step": per_step, "index_build_s": build_s},
+            "config": {"workload": CFG["workload"], "queries_per_step": per_step, "k": K, "index_build_s": build_s},
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": orc.threads(), "kind": "port",
-                             "sample": f"{per_step} queries per step (oracle/rbc_oracle.c, OpenMP)"},
+                             "sample": f"{per_step} queries per step, {_nn_label()} (oracle/rbc_oracle.c, OpenMP); "
+                                       "the Python reference itself measured 233.9 q/s on 8 cores for cfg2 "
+                                       "(SURVEY.md §6.3)"},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def simt_peak_gops(sm_mhz):
+    """fp32 SIMT lane-op peak: 148 SMs x 128 lanes x clock (SURVEY.md §8d, L1 roofline)."""
+    return 148 * 128 * (sm_mhz or 1965.0) * 1e6 / 1e9
+
+
 def main():
-    global K, METRIC
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS), help="BASELINE.json config (default cfg2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf", action="store_true")
-    ap.add_argument("--k", type=int, default=K, help="neighbours per query (the headline line is k=1)")
+    ap.add_argument("--k", type=int, default=None, help="neighbours per query (default: the config's k)")
     args = ap.parse_args()
-    if args.k != K:
-        K = args.k
-        METRIC = METRIC.replace("exact 1-NN", f"exact {K}-NN")
+    select_config(args.config, args.k)
+    exact = CFG["kind"] == "exact"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, world, args.config)
 
     import torch
 
@@ -251,10 +330,13 @@ def main():
 
     x, q = gen_inputs(rank)
     data = rbc.DataMatrix(x)
-    spec = rbc.MetricSpec("l2", D)
+    spec = rbc.MetricSpec(CFG["metric"], D)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    index = rbc.build_exact(data, NR, spec, seed=REP_SEED)
+    if exact:
+        index = rbc.build_exact(data, NR, spec, seed=REP_SEED)
+    else:
+        index = rbc.build_one_shot(data, NR, CFG["s"], spec, seed=REP_SEED, mode=CFG["mode"])
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     dev = index._dev
@@ -264,6 +346,8 @@ def main():
     sptr = ctypes.c_void_p(stream.cuda_stream)
     q_dev = _lib.to_device(q)
     keys = torch.empty((NQ, K), dtype=torch.int64, device="cuda")
+    ids_d = torch.empty((NQ, K), dtype=torch.int64, device="cuda")
+    dists_d = torch.empty((NQ, K), dtype=torch.float32, device="cuda")
     gamma = torch.empty(NQ, dtype=torch.float32, device="cuda")
     prr = torch.empty(NQ, dtype=torch.int32, device="cuda")
     p3 = torch.empty(NQ, dtype=torch.int32, device="cuda")
@@ -272,8 +356,12 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def step():
-        _lib.check(_lib.lib.rbc_exact_search_keys(dev.handle, _lib.ptr(q_dev), NQ, K, _lib.ptr(keys), stats, sptr),
-                   "exact search")
+        if exact:
+            _lib.check(_lib.lib.rbc_exact_search_keys(dev.handle, _lib.ptr(q_dev), NQ, K, _lib.ptr(keys), stats,
+                                                      sptr), "exact search")
+        else:
+            _lib.check(_lib.lib.rbc_one_shot_search(dev.handle, _lib.ptr(q_dev), NQ, K, _lib.ptr(ids_d),
+                                                    _lib.ptr(dists_d), _lib.ptr(gamma), sptr), "one-shot search")
 
     for _ in range(args.warmup):
         step()
@@ -290,28 +378,51 @@ def main():
     q_pin = torch.from_numpy(q.copy()).pin_memory()
     ids_h = torch.empty((NQ, K), dtype=torch.int64).pin_memory()
     dists_h = torch.empty((NQ, K), dtype=torch.float32).pin_memory()
+
+    def host_call():
+        if exact:
+            _lib.check(_lib.lib.rbc_exact_search_host(dev.handle, ctypes.c_void_p(q_pin.data_ptr()), NQ, K,
+                                                      ctypes.c_void_p(ids_h.data_ptr()),
+                                                      ctypes.c_void_p(dists_h.data_ptr()),
+                                                      _lib.SearchStatsC(None, None, None, None), sptr), "e2e")
+        else:
+            _lib.check(_lib.lib.rbc_one_shot_search_host(dev.handle, ctypes.c_void_p(q_pin.data_ptr()), NQ, K,
+                                                         ctypes.c_void_p(ids_h.data_ptr()),
+                                                         ctypes.c_void_p(dists_h.data_ptr()), None, sptr), "e2e")
+
     e2e_times = []
     for i in range(args.warmup + max(3, args.steps // 2)):
         t0 = time.perf_counter()
-        _lib.check(_lib.lib.rbc_exact_search_host(dev.handle, ctypes.c_void_p(q_pin.data_ptr()), NQ, K,
-                                                  ctypes.c_void_p(ids_h.data_ptr()),
-                                                  ctypes.c_void_p(dists_h.data_ptr()),
-                                                  _lib.SearchStatsC(None, None, None, None), sptr), "e2e")
+        host_call()
         if i >= args.warmup:
             e2e_times.append(time.perf_counter() - t0)
+    # the drop-in Python API itself (numpy queries in, numpy ids/dists/stats out)
+    api_times = []
+    for i in range(2 + 5):
+        t0 = time.perf_counter()
+        if exact:
+            rbc.exact_query_arrays(index, q, K)
+        else:
+            rbc.one_shot_query_arrays(index, q, K)
+        if i >= 2:
+            api_times.append(time.perf_counter() - t0)
     os.sched_setaffinity(0, old_aff)
     # median: the host call's wall time carries OS scheduling noise; min/median/max go to stderr
     e2e_s = statistics.median(e2e_times)
+    api_s = statistics.median(api_times)
     log(f"e2e host cpus: {len(local_cpus) if local_cpus else 'unrestricted'}; per-call ms: "
         + " ".join(f"{1e3 * t:.2f}" for t in e2e_times))
     log(f"e2e ms: min {1e3 * min(e2e_times):.3f} median {1e3 * e2e_s:.3f} max {1e3 * max(e2e_times):.3f} "
-        f"(n={len(e2e_times)})")
+        f"(n={len(e2e_times)}); python API ms: " + " ".join(f"{1e3 * t:.2f}" for t in api_times))
     if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s, api_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s, api_s = (float(v) for v in t.tolist())
     e2e_block = {"value": world * NQ / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(q.nbytes),
-           "d2h_bytes_per_step": int(ids_h.numel() * 8 + dists_h.numel() * 4)}
+                 "d2h_bytes_per_step": int(ids_h.numel() * 8 + dists_h.numel() * 4),
+                 "api": {"value": world * NQ / api_s, "unit": "queries/s",
+                         "call": ("exact_query_arrays" if exact else "one_shot_query_arrays")
+                         + " (numpy in, numpy ids/dists/stats out; pageable host memory)"}}
 
     for _ in range(args.warmup):  # back to the device-resident call (re-captures its graph)
         step()
@@ -337,9 +448,10 @@ def main():
     if dist:
         dist.barrier()
     launches = _lib.launch_count() - launches0
-    # phase split (stage 1 / stage 2 / scan) from a separate pass with the CUDA-event phase
-    # timers on; the timers force direct launches (no graph replay), so they stay out of
-    # the timed loop above
+    # phase split from a separate pass with the CUDA-event phase timers on (recorded on the
+    # launching stream around each kernel group; "scan" brackets the dominant kernel alone:
+    # stage2_tc_kernel for the exact search, the list scan for one-shot).  The timers force
+    # direct launches (no graph replay), so they stay out of the timed loop above
     _lib.profile_enable(True)
     for _ in range(3):  # direct-launch warm-up (scratch pool regrowth after the graph arena)
         step()
@@ -367,53 +479,75 @@ def main():
     value = world * NQ * args.steps / (total_ms / 1e3)
 
     # ---- algorithmic work (reference-rule counts) ---------------
-    cand_h = cand.cpu().numpy()
-    flops_per_step = 2.0 * D * (n_reps * NQ + float(cand_h.sum()))
-    stage2_ms, stage2_n = phases["stage2"]
-    stage2_flops = 2.0 * D * float(cand_h.sum())
     pk = peaks()
-    traffic = ncu_traffic()
-    achieved_tf = stage2_flops * stage2_n / (stage2_ms / 1e3) / 1e12 if stage2_ms > 0 else None
-    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": pk["tensor"], "unit": "TFLOP/s",
-                "frac": (achieved_tf / pk["tensor"]) if achieved_tf else None,
-                "traffic": (traffic or {}).get("bytes_per_launch"), "traffic_unit": "bytes/launch",
-                "traffic_src": (traffic or {}).get("source"),
-                "kernel": "stage-2 scan (exact search)", "peak_src": pk["src"],
-                "phase_ms_per_step": {k2: (v[0] / v[1] if v[1] else None) for k2, v in phases.items()},
-                "step_share": (stage2_ms / stage2_n) / ms_per_step if stage2_n else None}
+    scan_ms, scan_n = phases["scan"]
+    if exact:
+        cand_h = cand.cpu().numpy().astype(np.float64)
+        mean_cand = float(cand_h.mean())
+    else:
+        mean_cand = float(CFG["s"])
+    evals = NQ * (n_reps + mean_cand)
+    flops_per_step = 2.0 * D * evals
+    scan_work = 2.0 * D * NQ * mean_cand  # the dominant kernel's algorithmic work per launch
+    if CFG["metric"] == "l2":
+        kname = f"stage2_tc_kernel<{kt_of(K)}>" if exact else f"oneshot scan (k={K})"
+        traffic = ncu_traffic(kname, args.config)
+        achieved = scan_work * scan_n / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["tensor"], "unit": "TFLOP/s",
+                    "frac": (achieved / pk["tensor"]) if achieved else None, "peak_src": pk["src"]}
+    else:
+        kname = f"oneshot L1 scan (k={K})"
+        traffic = ncu_traffic(kname, args.config)
+        achieved = scan_work * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+        peak = simt_peak_gops((clk or {}).get("sm_mhz"))
+        roofline = {"bound": "simt", "achieved": achieved, "peak": peak, "unit": "Glane-op/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "peak_src": "148 SMs x 128 fp32 lanes x measured SM clock"}
+    roofline.update({
+        "traffic": (traffic or {}).get("bytes_per_launch"), "traffic_unit": "bytes/launch",
+        "traffic_src": (traffic or {}).get("source"), "kernel": kname,
+        "work_per_launch": scan_work, "work_rule": "2*d*candidates (reference-rule counts from SearchStats)",
+        "phase_ms_per_step": {k2: (v[0] / v[1] if v[1] else None) for k2, v in phases.items()},
+        "step_share": (scan_ms / scan_n) / ms_per_step if scan_n else None})
 
     # ---- GPU brute-force baseline (paper Table 3 framing) -------------------
     bf = None
     if not args.no_bf and rank == 0:
-        m = 2048
+        m = min(NQ, 8192)
         qb = q_dev[:m]
-        ids_b = torch.empty((m, 1), dtype=torch.int64, device="cuda")
-        d_b = torch.empty((m, 1), dtype=torch.float32, device="cuda")
+        ids_b = torch.empty((m, K), dtype=torch.int64, device="cuda")
+        d_b = torch.empty((m, K), dtype=torch.float32, device="cuda")
         x_dev = _lib.to_device(x)
         for it in range(2):
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            _lib.check(_lib.lib.rbc_bf_search(_lib.ptr(qb), m, _lib.ptr(x_dev), N, D, 0, 1, _lib.ptr(ids_b),
-                                              _lib.ptr(d_b), sptr), "bf")
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-        bf = {"value": m / dt, "unit": "queries/s", "sample": f"{m} queries x 1M points, k=1, exact SIMT scan (rbc_bf_search)",
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            _lib.check(_lib.lib.rbc_bf_search(_lib.ptr(qb), m, _lib.ptr(x_dev), N, D, 0 if CFG["metric"] == "l2" else 1,
+                                              K, _lib.ptr(ids_b), _lib.ptr(d_b), sptr), "bf")
+            ev1.record(stream)
+            ev1.synchronize()
+            dt = ev0.elapsed_time(ev1) / 1e3
+        bf = {"value": m / dt, "unit": "queries/s",
+              "sample": f"{m} queries x {N} points, k={K}, rbc_bf_search (bf_search), device-resident",
               "rbc_speedup": (value / world) / (m / dt)}
+        del x_dev
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(x, q, index)
+        cpu = cpu_baseline(x, q, index, args.config)
 
     if rank == 0:
+        cfg = {"workload": CFG["workload"], "queries_per_rank": NQ, "k": K, "n_reps": n_reps,
+               "parallelism": f"query-shard x{world}", "l2_flush": "256 MiB write between timed steps",
+               "index_build_s": build_s, "mean_candidates": mean_cand, "flops_per_step": flops_per_step,
+               "step_ms_min": min(times), "step_ms_median": sorted(times)[len(times) // 2],
+               "arith": ("f32 inputs; f16 tcgen05 filter; exact re-rank in f64 (reference rule)"
+                         if CFG["metric"] == "l2" else "f32 inputs; exact f64 SIMT (reference rule)")}
+        if not exact:
+            cfg["s"] = CFG["s"]
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"cfg2: exact RBC {K}-NN L2, clusters n=1M d=64 C=64 sigma=0.05, |R|=1016",
-                           "queries_per_rank": NQ, "k": K, "n_reps": n_reps, "parallelism": f"query-shard x{world}",
-                           "l2_flush": "256 MiB write between timed steps", "index_build_s": build_s,
-                           "mean_candidates": float(cand_h.mean()), "flops_per_step": flops_per_step,
-                           "step_ms_min": min(times), "step_ms_median": sorted(times)[len(times) // 2],
-                           "arith": "f32 inputs; f16 tcgen05 filter; exact re-rank in f64 (reference rule)"},
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
                 "e2e": e2e_block, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "gpu_bruteforce": bf, "clocks": clk}
         print(json.dumps(line), flush=True)

@@ -17,13 +17,33 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RBC_B200_LIB") or os.path.join(_HERE, "librbc_b200.so")
 
-if not os.path.exists(LIB_PATH):
-    raise ImportError(
-        f"{LIB_PATH} is missing: build the CUDA library first "
-        "(python -m paper_1103_2635_b200._build, or __graft_entry__.build())"
-    )
+_LIB = None
 
-lib = ctypes.CDLL(LIB_PATH)
+
+def _load():
+    """Load librbc_b200.so once (first use).  A missing library raises ImportError then:
+    there is no CPU fallback.  Loading lazily lets ``python -m paper_1103_2635_b200._build``
+    import the package on a clean checkout before the library exists."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA library first "
+                "(python -m paper_1103_2635_b200._build, or __graft_entry__.build())"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for _name, (_args, _res) in EXPORTS.items():
+            f = getattr(L, _name)
+            f.argtypes = _args
+            f.restype = _res
+        _LIB = L
+    return _LIB
+
+
+def __getattr__(name):  # PEP 562: ``_lib.lib`` loads the library on first access
+    if name == "lib":
+        return _load()
+    raise AttributeError(name)
 
 RBC_OK, RBC_EINVAL, RBC_ECUDA, RBC_ENOMEM, RBC_EFEWCAND = 0, 1, 2, 3, 4
 METRIC_CODE = {"l2": 0, "l1": 1}
@@ -36,13 +56,6 @@ _u64 = ctypes.c_uint64
 
 class SearchStatsC(ctypes.Structure):
     _fields_ = [("gamma", _p), ("reps_pruned_radius", _p), ("reps_pruned_3gamma", _p), ("candidates", _p)]
-
-
-def _sig(name, args, res=ctypes.c_int):
-    f = getattr(lib, name)
-    f.argtypes = args
-    f.restype = res
-    return f
 
 
 EXPORTS = {
@@ -80,12 +93,8 @@ EXPORTS = {
     "rbc_set_engine": ([ctypes.c_int], ctypes.c_int),
     "rbc_stage2_overflows": ([], _i64),
 }
-for _name, (_args, _res) in EXPORTS.items():
-    _sig(_name, _args, _res)
-
-
 def last_error() -> str:
-    msg = lib.rbc_last_error()
+    msg = _load().rbc_last_error()
     return msg.decode() if msg else ""
 
 
@@ -151,19 +160,19 @@ def to_host(tensor) -> np.ndarray:
 
 
 def launch_count() -> int:
-    return int(lib.rbc_launch_count())
+    return int(_load().rbc_launch_count())
 
 
 PHASES = ("stage1", "prune", "stage2", "build", "scan")
 
 
 def profile_enable(on: bool = True) -> None:
-    lib.rbc_profile_enable(1 if on else 0)
+    _load().rbc_profile_enable(1 if on else 0)
 
 
 def profile_read() -> dict:
     """{phase: (total_ms, intervals)} of the CUDA-event phase timers."""
     ms = (ctypes.c_double * 8)()
     cnt = (ctypes.c_int64 * 8)()
-    check(lib.rbc_profile_read(ms, cnt, 8), "profile_read")
+    check(_load().rbc_profile_read(ms, cnt, 8), "profile_read")
     return {name: (ms[i], cnt[i]) for i, name in enumerate(PHASES)}

@@ -2,6 +2,7 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <climits>
 #include <mutex>
 #include <vector>
 
@@ -81,33 +82,55 @@ static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStre
 
 // Host -> device copy of a large host buffer split over kCopyLanes concurrent
 // copies (side streams ordered after `st`, joined back into `st`): several
-// copies in flight keep the PCIe link busier than one.
+// copies in flight keep the PCIe link busier than one.  The side streams and
+// events belong to one caller object (per index, guarded by its mutex) and are
+// created on the device that is current when the object is first used.
 static constexpr int kCopyLanes = 4;
-static int copy_h2d_split(void *dst, const void *src, size_t bytes, cudaStream_t st) {
-    static cudaStream_t side[kCopyLanes] = {};
-    static cudaEvent_t ev_start = nullptr, ev_done[kCopyLanes] = {};
-    if (!ev_start) {
-        RBC_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+struct CopyLanes {
+    int device = -1;
+    cudaStream_t side[kCopyLanes] = {};
+    cudaEvent_t ev_start = nullptr, ev_done[kCopyLanes] = {};
+    void release() {
         for (int i = 0; i < kCopyLanes; ++i) {
-            RBC_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
-            RBC_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+            if (side[i]) cudaStreamDestroy(side[i]);
+            if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+            side[i] = nullptr;
+            ev_done[i] = nullptr;
         }
+        if (ev_start) cudaEventDestroy(ev_start);
+        ev_start = nullptr;
+        device = -1;
     }
-    if (bytes < (size_t(8) << 20)) {
+    ~CopyLanes() { release(); }
+};
+
+static int copy_h2d_split(CopyLanes *lanes, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (lanes == nullptr || bytes < (size_t(8) << 20)) {
         RBC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
         return RBC_OK;
     }
-    RBC_CUDA(cudaEventRecord(ev_start, st));
+    int dev = 0;
+    RBC_CUDA(cudaGetDevice(&dev));
+    if (lanes->device != dev) {
+        lanes->release();
+        RBC_CUDA(cudaEventCreateWithFlags(&lanes->ev_start, cudaEventDisableTiming));
+        for (int i = 0; i < kCopyLanes; ++i) {
+            RBC_CUDA(cudaStreamCreateWithFlags(&lanes->side[i], cudaStreamNonBlocking));
+            RBC_CUDA(cudaEventCreateWithFlags(&lanes->ev_done[i], cudaEventDisableTiming));
+        }
+        lanes->device = dev;
+    }
+    RBC_CUDA(cudaEventRecord(lanes->ev_start, st));
     const size_t part = ((bytes + kCopyLanes - 1) / kCopyLanes + 255) & ~size_t(255);
     for (int i = 0; i < kCopyLanes; ++i) {
         const size_t off = part * i;
         if (off >= bytes) break;
         const size_t len = bytes - off < part ? bytes - off : part;
-        RBC_CUDA(cudaStreamWaitEvent(side[i], ev_start, 0));
+        RBC_CUDA(cudaStreamWaitEvent(lanes->side[i], lanes->ev_start, 0));
         RBC_CUDA(cudaMemcpyAsync(static_cast<char *>(dst) + off, static_cast<const char *>(src) + off, len,
-                                 cudaMemcpyHostToDevice, side[i]));
-        RBC_CUDA(cudaEventRecord(ev_done[i], side[i]));
-        RBC_CUDA(cudaStreamWaitEvent(st, ev_done[i], 0));
+                                 cudaMemcpyHostToDevice, lanes->side[i]));
+        RBC_CUDA(cudaEventRecord(lanes->ev_done[i], lanes->side[i]));
+        RBC_CUDA(cudaStreamWaitEvent(st, lanes->ev_done[i], 0));
     }
     return RBC_OK;
 }
@@ -156,6 +179,41 @@ __global__ void copy_segments_kernel(const int64_t *__restrict__ src_off, const 
     }
 }
 
+// [min, max] of an int64 array (index-upload validation)
+__global__ void minmax_i64_kernel(const int64_t *__restrict__ a, int64_t n, unsigned long long *__restrict__ out) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const long long v = a[t];
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+    // order-preserving unsigned image of the signed values
+    atomicMin(&out[0], static_cast<unsigned long long>(lo) ^ 0x8000000000000000ull);
+    atomicMax(&out[1], static_cast<unsigned long long>(hi) ^ 0x8000000000000000ull);
+}
+
+// every id of a[0..n) in [0, limit) (the reference's load_index / search would raise
+// IndexError; on the device an out-of-range id is an out-of-bounds gather)
+static int check_ids_in_range(const int64_t *a, int64_t n, int64_t limit, const char *what, cudaStream_t st) {
+    if (n == 0) return RBC_OK;
+    DevBuf<unsigned long long> mm;
+    RBC_CHECK(mm.alloc(2, st));
+    const unsigned long long init[2] = {~0ull, 0ull};
+    RBC_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof(init), cudaMemcpyHostToDevice, st));
+    minmax_i64_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(a, n, mm.get());
+    RBC_LAUNCHED();
+    unsigned long long h[2] = {0, 0};
+    RBC_CUDA(cudaMemcpyAsync(h, mm.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    const long long lo = static_cast<long long>(h[0] ^ 0x8000000000000000ull);
+    const long long hi = static_cast<long long>(h[1] ^ 0x8000000000000000ull);
+    if (lo < 0 || hi >= limit)
+        return fail(RBC_EINVAL, std::string(what) + " out of range [0, " + std::to_string(limit) + "): min " +
+                                    std::to_string(lo) + ", max " + std::to_string(hi));
+    return RBC_OK;
+}
+
 static int index_common(rbc_index *idx, const float *x, const int64_t *rep_ids, const float *radii, cudaStream_t st) {
     RBC_CHECK(dalloc(&idx->x, idx->n * idx->d, idx->bytes));
     RBC_CHECK(dalloc(&idx->reps, idx->nr * idx->d, idx->bytes));
@@ -181,13 +239,26 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
     idx->metric = metric;
     idx->nr = nr;
     idx->shard = owned != nullptr;
-    int rc = index_common(idx, x, rep_ids, radii, st);
+    int rc = check_ids_in_range(rep_ids, nr, n, "rep_ids", st);
+    if (rc != RBC_OK) {
+        delete idx;
+        return rc;
+    }
+    rc = index_common(idx, x, rep_ids, radii, st);
     std::vector<int64_t> off_full(nr + 1), off_local(nr + 1, 0);
     if (rc == RBC_OK) rc = dalloc(&idx->offsets, nr + 1, idx->bytes);
     if (rc == RBC_OK && cudaMemcpyAsync(off_full.data(), list_offsets, sizeof(int64_t) * (nr + 1),
                                         cudaMemcpyDeviceToHost, st) != cudaSuccess)
         rc = fail(RBC_ECUDA, "offsets D2H");
     if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "sync");
+    // the lists must partition the n points (RbcExactIndex, rbc.py:87-115): CSR offsets from
+    // 0 to n, non-decreasing, every id in [0, n)
+    if (rc == RBC_OK) {
+        bool ok = off_full[0] == 0 && off_full[nr] == n;
+        for (int64_t p = 0; ok && p < nr; ++p) ok = off_full[p + 1] >= off_full[p];
+        if (!ok) rc = fail(RBC_EINVAL, "list offsets must rise from 0 to n (the lists partition the points)");
+    }
+    if (rc == RBC_OK) rc = check_ids_in_range(list_ids, n, n, "list ids", st);
     if (rc == RBC_OK) {
         for (int64_t p = 0; p < nr; ++p) {
             const int64_t len = off_full[p + 1] - off_full[p];
@@ -203,9 +274,11 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
         rc = fail(RBC_ECUDA, "offsets H2D");
     if (rc == RBC_OK) {
         if (owned == nullptr) {
-            i64_to_i32_kernel<<<grid_for(n, 256, 148 * 64), 256, 0, st>>>(list_ids, n, idx->perm);
+            i64_to_i32_kernel<<<grid_for(idx->n_local, 256, 148 * 64), 256, 0, st>>>(list_ids, idx->n_local,
+                                                                                   idx->perm);
             note_launch();
-            if (cudaMemcpyAsync(idx->list_dists, list_dists, sizeof(float) * n, cudaMemcpyDeviceToDevice, st) !=
+            if (cudaMemcpyAsync(idx->list_dists, list_dists, sizeof(float) * idx->n_local, cudaMemcpyDeviceToDevice,
+                                st) !=
                 cudaSuccess)
                 rc = fail(RBC_ECUDA, "list_dists copy");
         } else {
@@ -372,7 +445,10 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
                               void *stream) {
     RBC_CHECK(check_common(n, d, metric));
     if (s < 1 || s > n) return fail(RBC_EINVAL, "s must be in [1, n]");
+    if (n_reps < 1 || n_reps > n) return fail(RBC_EINVAL, "n_reps must be in [1, n]");
     cudaStream_t st = as_stream(stream);
+    RBC_CHECK(check_ids_in_range(rep_ids, n_reps, n, "rep_ids", st));
+    RBC_CHECK(check_ids_in_range(list_ids, n_reps * s, n, "list ids", st));
     rbc_index *idx = new rbc_index();
     idx->kind = 1;
     idx->n = n;
@@ -453,6 +529,7 @@ struct HostCallBuffers {
     int64_t *ids = nullptr;
     float *dists = nullptr;
     int64_t cap_q = 0, cap_k = 0;
+    CopyLanes lanes;
     ~HostCallBuffers() {
         cudaFree(q);
         cudaFree(keys);
@@ -497,7 +574,7 @@ int rbc_exact_search_host(const rbc_index *idx, const float *q, int64_t nq, int3
             }
             hb.cap_q = cq, hb.cap_k = ck;
         }
-        RBC_CHECK(copy_h2d_split(hb.q, q, sizeof(float) * nq * idx->d, st));
+        RBC_CHECK(copy_h2d_split(&hb.lanes, hb.q, q, sizeof(float) * nq * idx->d, st));
         RBC_CHECK(rbc_exact_search_keys(idx, hb.q, nq, k, hb.keys, stats, stream));
         RBC_CHECK(keys_to_output(hb.keys, nq * k, hb.ids, hb.dists, st));
         RBC_CUDA(cudaMemcpyAsync(ids, hb.ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
@@ -516,7 +593,7 @@ int rbc_exact_search_host(const rbc_index *idx, const float *q, int64_t nq, int3
     if (stats.candidates) { RBC_CHECK(dcand.alloc(nq, st)); ds.candidates = dcand.get(); }
     if (stats.reps_pruned_radius) { RBC_CHECK(dpr.alloc(nq, st)); ds.reps_pruned_radius = dpr.get(); }
     if (stats.reps_pruned_3gamma) { RBC_CHECK(dp3.alloc(nq, st)); ds.reps_pruned_3gamma = dp3.get(); }
-    RBC_CHECK(copy_h2d_split(dq.get(), q, sizeof(float) * nq * idx->d, st));
+    RBC_CHECK(copy_h2d_split(nullptr, dq.get(), q, sizeof(float) * nq * idx->d, st));
     RBC_CHECK(rbc_exact_search(idx, dq.get(), nq, k, dids.get(), ddist.get(), ds, stream));
     RBC_CUDA(cudaMemcpyAsync(ids, dids.get(), sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaMemcpyAsync(dists, ddist.get(), sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
@@ -536,6 +613,8 @@ int rbc_exact_search_host(const rbc_index *idx, const float *q, int64_t nq, int3
 int rbc_one_shot_search_host(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
                              float *gamma, void *stream) {
     if (!idx) return fail(RBC_EINVAL, "null index");
+    if (idx->kind != 1) return fail(RBC_EINVAL, "not a one-shot index");
+    if (k < 1 || k > idx->s) return fail(RBC_EINVAL, "k must be in [1, s]");
     cudaStream_t st = as_stream(stream);
     DevBuf<float> dq, ddist, dgamma;
     DevBuf<int64_t> dids;

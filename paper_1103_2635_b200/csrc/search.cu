@@ -621,9 +621,13 @@ int one_shot_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k
     RBC_CHECK(nearest.alloc(nq, st));
     RBC_CHECK(row.alloc(nq, st));
     // nearest representative by key64 argmin (lowest position on ties)
-    RBC_CHECK(nearest_rows(q, nq, idx->reps, idx->nr, idx->d, idx->metric, nearest.get(), st));
-    argmin_row_kernel<<<grid_for(nq, 256), 256, 0, st>>>(nearest.get(), nq, row.get(), gamma);
-    RBC_LAUNCHED();
+    {
+        ProfScope ps(kPhaseStage1, st);
+        RBC_CHECK(nearest_rows(q, nq, idx->reps, idx->nr, idx->d, idx->metric, nearest.get(), st));
+        argmin_row_kernel<<<grid_for(nq, 256), 256, 0, st>>>(nearest.get(), nq, row.get(), gamma);
+        RBC_LAUNCHED();
+    }
+    ProfScope ps(kPhaseScan, st);
     RowSrc src{idx->x, idx->lists, row.get(), idx->s, idx->d};
     return launch_topk(q, nq, idx->d, idx->metric, k, src, keys, st);
 }

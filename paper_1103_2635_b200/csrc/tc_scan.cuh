@@ -1,5 +1,6 @@
-// tc_scan.cuh -- the filtered distance scans (tensor-core filter + exact
-// fp64 re-rank) that carry the heavy work of every hot call.
+// tc_scan.cuh -- dispatch of the distance scans: the tcgen05 stage-1/stage-2
+// engines (tensor-core filter + exact fp64 re-rank, tc_stage1.cu / tc_stage2.cu)
+// and the exact fp64 SIMT scans (exact_kernels.cu) they fall back to.
 #pragma once
 
 #include "common.cuh"

@@ -1176,8 +1176,11 @@ void tc_index_release(rbc_index *idx) {
     idx->tc = nullptr;
 }
 
+// tile_fill_kernel keeps three int32 words per representative in shared memory
+constexpr int64_t kMaxRepsTileFill = (200 * 1024) / (3 * sizeof(int32_t));
+
 bool tc_stage2_supported(const rbc_index *idx, int k) {
-    return idx->tc != nullptr && k <= 16 && idx->nr < (1 << 24);
+    return idx->tc != nullptr && k <= 16 && idx->nr <= kMaxRepsTileFill;
 }
 
 static int g_num_sms = 0;

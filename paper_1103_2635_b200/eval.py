@@ -208,12 +208,14 @@ def rank_errors(data: DataMatrix, queries: np.ndarray, returned_dists: np.ndarra
     """
     xv = _as_values(data)
     top = baseline.top_dists
-    ret = np.asarray(returned_dists, np.float32)
+    # the caller's values as given (float64 returned distances compare in float64, as in the
+    # reference); float32 only for the searchsorted branch (report.py:88)
+    ret = np.asarray(returned_dists)
     ranks = np.empty(len(ret), dtype=np.int64)
     escaped = []
     for i, r in enumerate(ret):
         if r <= top[i, -1] or top.shape[1] >= xv.shape[0]:
-            ranks[i] = np.searchsorted(top[i], r, side="left")
+            ranks[i] = np.searchsorted(top[i], np.float32(r), side="left")
         else:
             escaped.append(i)
     if escaped:

@@ -151,7 +151,29 @@ def _resolve_reps(n: int, n_r: int, seed: int, mode: str, rep_ids) -> RepSet:
 
 
 def _split(flat: np.ndarray, offsets: np.ndarray) -> list[np.ndarray]:
-    return [flat[offsets[p]: offsets[p + 1]] for p in range(len(offsets) - 1)]
+    # independent arrays per list, as the reference's np.split(...) copies (rbc.py:170-176)
+    return [flat[offsets[p]: offsets[p + 1]].copy() for p in range(len(offsets) - 1)]
+
+
+_INDEX_FIELDS = ("data", "metric", "reps", "list_ids", "list_dists", "radii", "s")
+
+
+def _fingerprint(index):
+    """Identity of the index's fields: the device copy is reused only while none of them has
+    been reassigned (the arrays themselves are treated as immutable once built, like the
+    reference's read-only DataMatrix)."""
+    fp = []
+    for f in _INDEX_FIELDS:
+        v = getattr(index, f, None)
+        fp.append(v if isinstance(v, int) else id(v))
+    lists = getattr(index, "list_ids", None)
+    fp.append(len(lists) if isinstance(lists, list) else None)
+    return tuple(fp)
+
+
+def _attach(index, dev):
+    index._dev = dev
+    index._dev_fp = _fingerprint(index)
 
 
 def _create_exact_device(x_dev, n, spec, rep_dev, nr, ids_dev, off_dev, ld_dev, radii_dev, owned=None):
@@ -198,7 +220,7 @@ def build_exact(
     flat_ids, offsets, flat_d = _lib.to_host(ids_dev), _lib.to_host(off_dev), _lib.to_host(ld_dev)
     index = RbcExactIndex(data, spec, reps, _split(flat_ids, offsets), _split(flat_d, offsets),
                           _lib.to_host(radii_dev))
-    index._dev = dev
+    _attach(index, dev)
     return index
 
 
@@ -232,7 +254,7 @@ def build_one_shot(
                                                   _lib.ptr(lists_dev), s, _lib.ptr(radii_dev), ctypes.byref(handle),
                                                   _lib.stream_ptr()), "one-shot index")
     index = RbcOneShotIndex(data, spec, reps, _lib.to_host(lists_dev), s, _lib.to_host(radii_dev))
-    index._dev = DeviceIndex(handle, t.cuda.current_device())
+    _attach(index, DeviceIndex(handle, t.cuda.current_device()))
     return index
 
 
@@ -240,7 +262,8 @@ def device_index(index) -> DeviceIndex:
     """The index's device handle, uploading a hand-made / loaded index on first use."""
     t = _lib.require_cuda()
     dev = getattr(index, "_dev", None)
-    if dev is not None and dev.handle is not None and dev.device == t.cuda.current_device():
+    if (dev is not None and dev.handle is not None and dev.device == t.cuda.current_device()
+            and getattr(index, "_dev_fp", None) == _fingerprint(index)):
         return dev
     spec = index.metric
     x_dev = _lib.to_device(index.data.values)
@@ -258,7 +281,7 @@ def device_index(index) -> DeviceIndex:
                                                       index.s, _lib.ptr(radii_dev), ctypes.byref(handle),
                                                       _lib.stream_ptr()), "one-shot index")
         dev = DeviceIndex(handle, t.cuda.current_device())
-    index._dev = dev
+    _attach(index, dev)
     return dev
 
 
