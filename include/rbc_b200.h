@@ -76,6 +76,10 @@ int rbc_set_engine(int mode);
 /* Queries of the last exact search whose candidate buffer overflowed and
  * were recomputed by the exact SIMT scan (diagnostic). */
 int64_t rbc_stage2_overflows(void);
+/* Brute-force scans (bf_search, build assignment, one-shot nearest rep, one-shot
+ * list scan) served by the tcgen05 engine since the library loaded (diagnostic:
+ * lets tests prove the tensor-core path ran). */
+int64_t rbc_tc_bf_calls(void);
 
 /* metric.py:57-76 pairwise_distances (and brute_force.py:220-251
  * distance_rows): out[m,p] = dist(a[i], b[j]), bit-exact. */
@@ -86,6 +90,16 @@ int rbc_pairwise_distances(const float *a, int64_t m, const float *b, int64_t p,
  * nearest of every query over all of x, rows sorted by key64. */
 int rbc_bf_search(const float *q, int64_t nq, const float *x, int64_t n, int32_t d, int32_t metric, int32_t k,
                   int64_t *ids, float *dists, void *stream);
+
+/* bf_search over a PREPARED operand (the same results as rbc_bf_search): the
+ * points are copied once into the tcgen05 scan's operand form (L2, d <= 64: a
+ * partition into ~sqrt(n)/2 lists of f16 residuals; otherwise a plain copy for
+ * the exact SIMT scan) so repeated searches over the same points -- the
+ * reference's report.run_baseline loop (report.py:62-95) -- skip that work.
+ * The handle is released with rbc_index_destroy. */
+int rbc_bf_prepare(const float *x, int64_t n, int32_t d, int32_t metric, rbc_index **out, void *stream);
+int rbc_bf_search_prepared(const rbc_index *bf, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
+                           void *stream);
 
 /* eval.py:21-27 ball_count, :117-130 rank_error, :133-164 claim1_counts, :44-107 estimate_expansion_rate and
  * report.py:72-95 rank_errors, batched: for query i and each of its n_thresholds thresholds t (row-major

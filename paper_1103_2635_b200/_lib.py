@@ -66,6 +66,8 @@ EXPORTS = {
     "rbc_profile_read": ([_p, _p, _i32], ctypes.c_int),
     "rbc_pairwise_distances": ([_p, _i64, _p, _i64, _i32, _i32, _p, _p], ctypes.c_int),
     "rbc_bf_search": ([_p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p, _p], ctypes.c_int),
+    "rbc_bf_prepare": ([_p, _i64, _i32, _i32, ctypes.POINTER(_p), _p], ctypes.c_int),
+    "rbc_bf_search_prepared": ([_p, _p, _i64, _i32, _p, _p, _p], ctypes.c_int),
     "rbc_bf_search_subsets": ([_p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _p], ctypes.c_int),
     "rbc_count_within": ([_p, _i64, _p, _i64, _i32, _i32, _p, _i32, _i32, _p, _p, _p], ctypes.c_int),
     "rbc_merge_topk": ([_p, _i32, _i64, _i32, _i32, _p, _p, _p], ctypes.c_int),
@@ -92,6 +94,7 @@ EXPORTS = {
     "rbc_tc_selftest": ([_p, _p, _p, _i32, _p], ctypes.c_int),
     "rbc_set_engine": ([ctypes.c_int], ctypes.c_int),
     "rbc_stage2_overflows": ([], _i64),
+    "rbc_tc_bf_calls": ([], _i64),
 }
 def last_error() -> str:
     msg = _load().rbc_last_error()

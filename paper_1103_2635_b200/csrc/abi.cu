@@ -2,6 +2,7 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <cmath>
 #include <climits>
 #include <mutex>
 #include <vector>
@@ -311,6 +312,55 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
     return RBC_OK;
 }
 
+// ---- prepared brute-force operand (kind 2) --------------------------------------------------
+// L2, d <= 64: the points are partitioned into ~sqrt(n)/2 lists around evenly spaced points
+// (the exact build's assignment + stable sort), so the tcgen05 scan multiplies residuals to a
+// nearby centre (tight f16 error bounds); every list is still scanned for every query.
+// Otherwise the operand is a plain device copy of the points for the exact SIMT scan.
+bool bf_partition_pays(int64_t nq, int64_t n, int d, int metric, int k) {
+    return metric == RBC_L2 && d <= 64 && k <= 16 && n > 65536 && nq >= 512 && n + 4096 < (int64_t(1) << 31);
+}
+
+int bf_prepare(const float *x, int64_t n, int d, int metric, rbc_index **out, cudaStream_t st) {
+    RBC_CHECK(check_common(n, d, metric));
+    if (metric == RBC_L2 && d <= 64 && n >= 1024 && n + 4096 < (int64_t(1) << 31)) {
+        int64_t nr = static_cast<int64_t>(std::sqrt(static_cast<double>(n)) / 2.0);
+        nr = nr < 1 ? 1 : nr;
+        std::vector<int64_t> rid(nr);
+        for (int64_t i = 0; i < nr; ++i) rid[i] = (i * n) / nr;
+        DevBuf<int64_t> rep_ids, list_ids, offsets;
+        DevBuf<float> list_dists, radii;
+        RBC_CHECK(rep_ids.alloc(nr, st));
+        RBC_CHECK(list_ids.alloc(n, st));
+        RBC_CHECK(offsets.alloc(nr + 1, st));
+        RBC_CHECK(list_dists.alloc(n, st));
+        RBC_CHECK(radii.alloc(nr, st));
+        RBC_CUDA(cudaMemcpyAsync(rep_ids.get(), rid.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice, st));
+        RBC_CHECK(build_exact(x, n, d, metric, rep_ids.get(), nr, list_ids.get(), offsets.get(), list_dists.get(),
+                              radii.get(), st));
+        RBC_CHECK(exact_create(x, n, d, metric, rep_ids.get(), nr, list_ids.get(), offsets.get(), list_dists.get(),
+                               radii.get(), nullptr, out, st));
+        (*out)->kind = 2;
+        return RBC_OK;
+    }
+    rbc_index *idx = new rbc_index();
+    idx->kind = 2;
+    idx->n = n;
+    idx->d = d;
+    idx->metric = metric;
+    int rc = dalloc(&idx->x, n * d, idx->bytes);
+    if (rc == RBC_OK && cudaMemcpyAsync(idx->x, x, sizeof(float) * n * d, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        rc = fail(RBC_ECUDA, "bf operand copy");
+    if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "bf operand sync");
+    if (rc != RBC_OK) {
+        rbc_index_destroy(idx);
+        return rc;
+    }
+    RBC_CUDA(cudaGetDevice(&idx->device));
+    *out = idx;
+    return RBC_OK;
+}
+
 }  // namespace rbc
 
 using namespace rbc;
@@ -365,7 +415,37 @@ int rbc_bf_search(const float *q, int64_t nq, const float *x, int64_t n, int32_t
     cudaStream_t st = as_stream(stream);
     DevBuf<uint64_t> keys;
     RBC_CHECK(keys.alloc(nq * k, st));
-    RBC_CHECK(bf_search_keys(q, nq, x, n, d, metric, k, keys.get(), st));
+    if (!force_exact_engine() && bf_partition_pays(nq, n, d, metric, k)) {
+        // large scan: partition the points once, then the tcgen05 scan over every list
+        rbc_index *bf = nullptr;
+        RBC_CHECK(bf_prepare(x, n, d, metric, &bf, st));
+        const int rc = bf->tc ? tc_bf_index_search(bf, q, nq, k, keys.get(), st)
+                              : bf_search_keys(q, nq, x, n, d, metric, k, keys.get(), st);
+        cudaStreamSynchronize(st);
+        rbc_index_destroy(bf);
+        RBC_CHECK(rc);
+    } else {
+        RBC_CHECK(bf_search_keys(q, nq, x, n, d, metric, k, keys.get(), st));
+    }
+    return keys_to_output(keys.get(), nq * k, ids, dists, st);
+}
+
+int rbc_bf_prepare(const float *x, int64_t n, int32_t d, int32_t metric, rbc_index **out, void *stream) {
+    if (!out) return fail(RBC_EINVAL, "null output handle");
+    return bf_prepare(x, n, d, metric, out, as_stream(stream));
+}
+
+int rbc_bf_search_prepared(const rbc_index *bf, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
+                           void *stream) {
+    if (!bf || bf->kind != 2) return fail(RBC_EINVAL, "not a prepared brute-force operand");
+    if (k < 1 || k > bf->n) return fail(RBC_EINVAL, "k must be in [1, n]");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<uint64_t> keys;
+    RBC_CHECK(keys.alloc(nq * k, st));
+    if (bf->tc && k <= 16 && !force_exact_engine())
+        RBC_CHECK(tc_bf_index_search(bf, q, nq, k, keys.get(), st));
+    else
+        RBC_CHECK(bf_search_keys(q, nq, bf->x, bf->n, bf->d, bf->metric, k, keys.get(), st));
     return keys_to_output(keys.get(), nq * k, ids, dists, st);
 }
 

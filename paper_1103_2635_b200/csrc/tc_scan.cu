@@ -14,12 +14,14 @@ bool force_exact_engine() { return g_engine == 1; }
 
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
                  cudaStream_t st) {
+    if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, 1)) return tc_bf_keys(q, nq, x, n, d, 1, keys, st);
     AllSrc src{x, n, d};
     return launch_topk(q, nq, d, metric, 1, src, keys, st);
 }
 
 int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
                    cudaStream_t st) {
+    if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, k)) return tc_bf_keys(q, nq, x, n, d, k, keys, st);
     if (k > kMaxWarpK) return topk_sorted_all(q, nq, x, n, d, metric, k, keys, st);
     AllSrc src{x, n, d};
     return launch_topk(q, nq, d, metric, k, src, keys, st);

@@ -42,7 +42,17 @@ bool tc_stage2_supported(const rbc_index *idx, int k);
 // status_dev[0] = work items needed (> cap_work: results invalid, re-run),
 // status_dev[1] = queries recomputed by the exact overflow scan
 int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
-              int64_t cap_work, int64_t *status_dev, cudaStream_t st);
+              int64_t cap_work, int64_t *status_dev, cudaStream_t st, int cap_groups = 0);
+
+// tcgen05 brute force (tc_stage2.cu): k nearest keys of every q row over all rows of x,
+// sorted, bit-identical to the exact scan (L2, d <= 64, k <= 16)
+bool tc_bf_supported(int64_t nq, int64_t n, int d, int metric, int k);
+int tc_bf_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int k, uint64_t *keys, cudaStream_t st);
+// tcgen05 brute force over a prepared (partitioned, kind 2) operand: every list, every query
+int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, cudaStream_t st);
+// prepared brute-force operand (abi.cu) and when preparing one per call pays off
+int bf_prepare(const float *x, int64_t n, int d, int metric, rbc_index **out, cudaStream_t st);
+bool bf_partition_pays(int64_t nq, int64_t n, int d, int metric, int k);
 int64_t &last_overflow_count();
 // stage-2 work-item capacity for nq queries, and its update from a measured need
 int64_t stage2_work_capacity(const rbc_index *idx, int64_t nq);

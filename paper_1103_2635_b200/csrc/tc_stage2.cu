@@ -39,6 +39,7 @@
 //               its half of K), candidate filter, per-half candidate buffers
 #include <cub/cub.cuh>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -126,7 +127,8 @@ struct S2Params {
     const int64_t *nwork;       // [ntiles] its work items
     const unsigned long long *work_total;
     const WorkItem *work;       // [total work]
-    const int32_t *cut;         // [total work][128] per-row cutoff (0 = list not a survivor for the row)
+    const int32_t *cut;         // [total work][128] per-row cutoff (0 = list not a survivor for the row);
+                                // null: every row scans the item's whole prefix (brute force)
     float *cand_lb;
     int32_t *cand_pos;
     int cap;
@@ -191,7 +193,10 @@ __global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, f
     sB[p] = r > 0.f ? ldexpf(1.0f, -e) : 1.0f;
 }
 
-// one block per list: f16 residual rows (pre-swizzled), folded-norm columns, fallback column
+// f16 residual rows of the lists (pre-swizzled), folded-norm columns, fallback column.
+// Grid (list, row slice): blockIdx.x = list p, blockIdx.y strides over its rows, so a
+// single long list (the brute-force scan) is prepared by many blocks.  dbmax[p] must be
+// zero on entry (max over the row slices through a float-bits atomic).
 __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *__restrict__ reps,
                                      const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff,
                                      const float *__restrict__ sB, int d, int plane1, uint8_t *__restrict__ xh0,
@@ -203,7 +208,8 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
     const int64_t len = offsets[p + 1] - offsets[p];
     const float s = sB[p];
     const float *r = reps + p * d;
-    for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
+    for (int64_t j = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < len;
+         j += static_cast<int64_t>(gridDim.y) * blockDim.x) {
         const float *x = xp + (offsets[p] + j) * d;
         const int64_t row = poff[p] + j;
         double h = 0.0;
@@ -246,7 +252,7 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
         atomicMax(&s_db, __float_as_uint(sqrtf(db2)));
     }
     __syncthreads();
-    if (threadIdx.x == 0) dbmax[p] = __uint_as_float(s_db);
+    if (threadIdx.x == 0 && s_db) atomicMax(reinterpret_cast<unsigned *>(dbmax) + p, s_db);
 }
 
 __global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
@@ -686,12 +692,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
             int cut_n = 0;
-            if (w0 < w1) cut_n = P.cut[w0 * kRows + row];
+            if (w0 < w1) cut_n = P.cut ? P.cut[w0 * kRows + row] : P.work[w0].ext;
             for (int64_t w = w0; w < w1; ++w) {
                 if (w + 1 < w1) prep_a(w + 1);  // next list's A while this list's MMAs run
                 const WorkItem wi = P.work[w];
                 const int cutv = live ? cut_n : 0;
-                if (w + 1 < w1) cut_n = P.cut[(w + 1) * kRows + row];
+                if (w + 1 < w1) cut_n = P.cut ? P.cut[(w + 1) * kRows + row] : P.work[w + 1].ext;
                 // both column parts of this lane quadrant have prepared lists w and w + 1: the
                 // row's |q - r_p|^2 is the sum of their two halves (slot w & 3; a part runs at
                 // most one list ahead of its partner, so slots are never overwritten early)
@@ -784,7 +790,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         overflow = true;
                     }
                     // the group's best is a valid element: its ub bounds the k-th best (k = 1 and a
-                    // fully valid block: the block maximum already did)
+                    // fully valid block: the block maximum already did).  (Every element's ub into
+                    // the k-best set instead, for k > 1, measured no fewer buffered groups: the
+                    // pushes follow the k-record statistics of the scan order, ~k ln(N/k).)
                     if (col0 + 8 <= lim && (KT > 1 || !block_valid)) {
                         const float ub = fmaf(-m, inv2s, lb0) + 2.0f * E;
                         if (KT == 1) {
@@ -1110,61 +1118,7 @@ void pad_rows64(const float *src, int64_t rows, int d, float *dst, cudaStream_t 
 }
 
 // ---- index-side preparation ----------------------------------------------------------------
-int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
-    if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->n_local == 0) return RBC_OK;
-    if (idx->n_local + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 work offsets
-    TcIndex *tc = new TcIndex();
-    tc->plane1 = idx->d > 62;
-    std::vector<int64_t> off(idx->nr + 1), poff(idx->nr + 1, 0);
-    RBC_CUDA(cudaMemcpyAsync(off.data(), idx->offsets, sizeof(int64_t) * (idx->nr + 1), cudaMemcpyDeviceToHost, st));
-    RBC_CUDA(cudaStreamSynchronize(st));
-    for (int64_t p = 0; p < idx->nr; ++p) poff[p + 1] = poff[p] + ((off[p + 1] - off[p] + 7) & ~int64_t(7));
-    tc->npad = poff[idx->nr];
-    const int64_t rows = tc->npad + kTailRows;
-    auto cleanup = [&](int rc) {
-        cudaFree(tc->xh0);
-        cudaFree(tc->xh1);
-        cudaFree(tc->gcol);
-        cudaFree(tc->poff);
-        cudaFree(tc->sB);
-        cudaFree(tc->dbmax);
-        cudaFree(tc->reps64);
-        delete tc;
-        return rc;
-    };
-    bool ok = cudaMalloc(&tc->xh0, rows * kP0) == cudaSuccess &&
-              (!tc->plane1 || cudaMalloc(&tc->xh1, rows * kP1) == cudaSuccess) &&
-              cudaMalloc(&tc->gcol, rows * sizeof(float)) == cudaSuccess &&
-              cudaMalloc(&tc->poff, (idx->nr + 1) * sizeof(int64_t)) == cudaSuccess &&
-              cudaMalloc(&tc->sB, idx->nr * sizeof(float)) == cudaSuccess &&
-              cudaMalloc(&tc->dbmax, idx->nr * sizeof(float)) == cudaSuccess &&
-              cudaMalloc(&tc->reps64, idx->nr * 64 * sizeof(float)) == cudaSuccess;
-    if (!ok) {
-        cudaGetLastError();
-        return cleanup(fail(RBC_ENOMEM, "tc index allocation"));
-    }
-    idx->bytes += rows * (kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (idx->nr + 1) * sizeof(int64_t) +
-                  idx->nr * (65 * sizeof(float));
-    if (cudaMemsetAsync(tc->xh0, 0, rows * kP0, st) != cudaSuccess ||
-        (tc->plane1 && cudaMemsetAsync(tc->xh1, 0, rows * kP1, st) != cudaSuccess) ||
-        cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
-        cudaMemcpyAsync(tc->poff, poff.data(), sizeof(int64_t) * (idx->nr + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return cleanup(fail(RBC_ECUDA, "tc index init"));
-    list_scale_kernel<<<grid_for(idx->nr, 256), 256, 0, st>>>(idx->radii, idx->nr, tc->sB);
-    pad64_rows_kernel<<<grid_for(idx->nr * 64, 256), 256, 0, st>>>(idx->reps, idx->nr, idx->d, tc->reps64);
-    residual_rows_kernel<<<static_cast<unsigned>(idx->nr), 256, 0, st>>>(
-        idx->xp, idx->reps, idx->offsets, tc->poff, tc->sB, idx->d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol,
-        tc->dbmax);
-    note_launch(3);
-    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
-        return cleanup(fail(RBC_ECUDA, "tc index kernels"));
-    idx->tc = tc;
-    return RBC_OK;
-}
-
-void tc_index_release(rbc_index *idx) {
-    TcIndex *tc = static_cast<TcIndex *>(idx->tc);
-    if (!tc) return;
+static void tc_free(TcIndex *tc) {
     cudaFree(tc->xh0);
     cudaFree(tc->xh1);
     cudaFree(tc->gcol);
@@ -1173,6 +1127,81 @@ void tc_index_release(rbc_index *idx) {
     cudaFree(tc->dbmax);
     cudaFree(tc->reps64);
     delete tc;
+}
+
+// Stage-2 operands of a set of lists: list p = rows [off[p], off[p+1]) of xp, centred
+// on reps[p] with radius radii[p].  off_host is the host copy of offsets_dev.
+static int tc_lists_build(const float *xp, const float *reps, const int64_t *offsets_dev,
+                          const std::vector<int64_t> &off, const float *radii, int64_t nr, int d, TcIndex **out,
+                          size_t *bytes, cudaStream_t st) {
+    TcIndex *tc = new TcIndex();
+    tc->plane1 = d > 62;
+    std::vector<int64_t> poff(nr + 1, 0);
+    int64_t maxlen = 0;
+    for (int64_t p = 0; p < nr; ++p) {
+        const int64_t len = off[p + 1] - off[p];
+        poff[p + 1] = poff[p] + ((len + 7) & ~int64_t(7));
+        maxlen = len > maxlen ? len : maxlen;
+    }
+    tc->npad = poff[nr];
+    const int64_t rows = tc->npad + kTailRows;
+    bool ok = cudaMalloc(&tc->xh0, rows * kP0) == cudaSuccess &&
+              (!tc->plane1 || cudaMalloc(&tc->xh1, rows * kP1) == cudaSuccess) &&
+              cudaMalloc(&tc->gcol, rows * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&tc->poff, (nr + 1) * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&tc->sB, nr * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&tc->dbmax, nr * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&tc->reps64, nr * 64 * sizeof(float)) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        tc_free(tc);
+        return fail(RBC_ENOMEM, "tc list operands allocation");
+    }
+    if (bytes)
+        *bytes += rows * (kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (nr + 1) * sizeof(int64_t) +
+                  nr * (66 * sizeof(float));
+    if (cudaMemsetAsync(tc->xh0, 0, rows * kP0, st) != cudaSuccess ||
+        (tc->plane1 && cudaMemsetAsync(tc->xh1, 0, rows * kP1, st) != cudaSuccess) ||
+        cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
+        cudaMemsetAsync(tc->dbmax, 0, nr * sizeof(float), st) != cudaSuccess ||
+        cudaMemcpyAsync(tc->poff, poff.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        tc_free(tc);
+        return fail(RBC_ECUDA, "tc list operands init");
+    }
+    list_scale_kernel<<<grid_for(nr, 256), 256, 0, st>>>(radii, nr, tc->sB);
+    pad64_rows_kernel<<<grid_for(nr * 64, 256), 256, 0, st>>>(reps, nr, d, tc->reps64);
+    const unsigned ysplit = static_cast<unsigned>(maxlen > 256 * 148 ? 148 : (maxlen + 255) / 256 + 0);
+    residual_rows_kernel<<<dim3(static_cast<unsigned>(nr), ysplit > 0 ? ysplit : 1), 256, 0, st>>>(
+        xp, reps, offsets_dev, tc->poff, tc->sB, d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol, tc->dbmax);
+    note_launch(3);
+    if (cudaGetLastError() != cudaSuccess) {
+        tc_free(tc);
+        return fail(RBC_ECUDA, "tc list operand kernels");
+    }
+    *out = tc;
+    return RBC_OK;
+}
+
+int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
+    if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->n_local == 0) return RBC_OK;
+    if (idx->n_local + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 work offsets
+    std::vector<int64_t> off(idx->nr + 1);
+    RBC_CUDA(cudaMemcpyAsync(off.data(), idx->offsets, sizeof(int64_t) * (idx->nr + 1), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    TcIndex *tc = nullptr;
+    RBC_CHECK(tc_lists_build(idx->xp, idx->reps, idx->offsets, off, idx->radii, idx->nr, idx->d, &tc, &idx->bytes, st));
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        tc_free(tc);
+        return fail(RBC_ECUDA, "tc index kernels");
+    }
+    idx->tc = tc;
+    return RBC_OK;
+}
+
+void tc_index_release(rbc_index *idx) {
+    TcIndex *tc = static_cast<TcIndex *>(idx->tc);
+    if (!tc) return;
+    tc_free(tc);
     idx->tc = nullptr;
 }
 
@@ -1185,8 +1214,14 @@ bool tc_stage2_supported(const rbc_index *idx, int k) {
 
 static int g_num_sms = 0;
 
+static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, const int32_t *order,
+                  int ntiles, const int32_t *tile_order, const int64_t *work_off, const int64_t *nwork,
+                  const unsigned long long *work_total, const WorkItem *work, const int32_t *cut, int64_t cap_work,
+                  int32_t *cand_count, int32_t *counters, uint64_t *keys, int64_t *status_dev, cudaStream_t st,
+                  int cap_groups);
+
 int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
-              int64_t cap_work, int64_t *status_dev, cudaStream_t st) {
+              int64_t cap_work, int64_t *status_dev, cudaStream_t st, int cap_groups) {
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
     if (g_num_sms == 0) {
         int dev = 0;
@@ -1273,8 +1308,19 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
                                              tile_order.get(), ntiles, 0, 16, st));
     note_launch();
+    return s2_run(idx, q, nq, k, po, order, ntiles, tile_order.get(), work_off.get(), nwork.get(), work_total,
+                  work.get(), cut.get(), cap_work, cand_count.get(), counters.get(), keys, status_dev, st, cap_groups);
+}
+
+// stage-2 kernel + exact re-rank + overflow scan + status over prepared work arrays
+static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, const int32_t *order,
+                  int ntiles, const int32_t *tile_order, const int64_t *work_off, const int64_t *nwork,
+                  const unsigned long long *work_total, const WorkItem *work, const int32_t *cut, int64_t cap_work,
+                  int32_t *cand_count, int32_t *counters, uint64_t *keys, int64_t *status_dev, cudaStream_t st,
+                  int cap_groups) {
+    const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
     // 3. the tensor-core scan
-    const int cap = 12 + 6 * k;  // 8-column groups per query and column part
+    const int cap = cap_groups > 0 ? cap_groups : 12 + 6 * k;  // 8-column groups per query and column part
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, ovf_list;
     RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 12, st));
@@ -1299,22 +1345,22 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     P.gamma = po.gamma.get();
     P.k = k;
     P.ntiles = ntiles;
-    P.tile_order = tile_order.get();
+    P.tile_order = tile_order;
     P.order = order;
     P.nq = nq;
-    P.work_off = work_off.get();
-    P.nwork = nwork.get();
+    P.work_off = work_off;
+    P.nwork = nwork;
     P.work_total = work_total;
-    P.work = work.get();
-    P.cut = cut.get();
+    P.work = work;
+    P.cut = cut;
     P.cand_lb = cand_lb.get();
     P.cand_pos = cand_pos.get();
     P.cap = cap;
-    P.cand_count = cand_count.get();
+    P.cand_count = cand_count;
     P.cand_ufin = cand_ufin.get();
     P.overflow_list = ovf_list.get();
-    P.overflow_count = counters.get();
-    P.tile_counter = counters.get() + 1;
+    P.overflow_count = counters;
+    P.tile_counter = counters + 1;
     P.cap_work = cap_work;
     DevBuf<unsigned long long> timing;
     P.timing = nullptr;
@@ -1348,7 +1394,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         const unsigned rgrid = grid_for(nq * kRerankLanes, kRerankThreads);
 #define RBC_RERANK(KT)                                                                                              \
     rerank_kernel<KT><<<rgrid, kRerankThreads, 0, st>>>(reinterpret_cast<const float4 *>(cand_lb.get()),           \
-                                                        cand_pos.get(), cand_count.get(),                           \
+                                                        cand_pos.get(), cand_count,                           \
                                                         cand_ufin.get(), cap, nq, q, idx->xp, idx->perm, idx->d, k, \
                                                         keys)
         if (k == 1) RBC_RERANK(1);
@@ -1364,14 +1410,26 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
         SegSubSrc src{idx->xp, idx->perm,     po.seg_start.get(), po.seg_len.get(),
                       po.seg_off.get(), po.nseg.get(), ovf_list.get(), idx->d};
         const unsigned ogrid = static_cast<unsigned>(g_num_sms * 4);
-        if (k == 1) overflow_scan_kernel<1><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
-        else if (k <= 4) overflow_scan_kernel<4><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
-        else if (k <= 8) overflow_scan_kernel<8><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
-        else overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters.get(), src, k, keys);
+        if (k == 1) overflow_scan_kernel<1><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
+        else if (k <= 4) overflow_scan_kernel<4><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
+        else if (k <= 8) overflow_scan_kernel<8><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
+        else overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
         RBC_LAUNCHED();
     }
-    stage2_status_kernel<<<1, 1, 0, st>>>(work_total, counters.get(), status_dev);
+    stage2_status_kernel<<<1, 1, 0, st>>>(work_total, counters, status_dev);
     RBC_LAUNCHED();
+    if (getenv("RBC_DEBUG_CAND")) {  // diagnostic: buffered-group counts (synchronises)
+        std::vector<int32_t> cc(nq * kParts);
+        cudaMemcpyAsync(cc.data(), cand_count, sizeof(int32_t) * nq * kParts, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        int64_t sum = 0, ovf = 0, mx = 0;
+        for (int32_t v : cc) {
+            if (v < 0) ++ovf;
+            else { sum += v; mx = v > mx ? v : mx; }
+        }
+        fprintf(stderr, "[s2] cap %d: groups mean %.2f max %lld, overflowed parts %lld of %lld\n", cap,
+                double(sum) / double(cc.size() - ovf + 1e-9), (long long)mx, (long long)ovf, (long long)cc.size());
+    }
 #ifdef RBC_S2_TIMING
     if (getenv("RBC_DEBUG_S2")) {  // diagnostic: role timing (synchronises)
         std::vector<unsigned long long> tm(148 * 12);
@@ -1389,4 +1447,387 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     return RBC_OK;
 }
 
+
+// ---- tensor-core brute force ----------------------------------------------------------------
+// bf_search (brute_force.py:165-186), the build's nearest-representative assignment
+// (rbc.py:164) and the one-shot search's nearest representative (search.py:114-115):
+// all rows of x form ONE list centred on their mean c (radius max |x - c|), and every
+// query row scans it whole through stage2_tc_kernel -- the tcgen05 distance tile with the
+// running-bound filter epilogue -- followed by the exact fp64 re-rank.  Every (q, x) pair
+// passes through the tensor cores; only the filter survivors are recomputed exactly, so
+// the keys are the reference's bit for bit.
+namespace {
+
+__global__ void bf_colsum_kernel(const float *__restrict__ x, int64_t n, int d, double *__restrict__ sum) {
+    const int k = threadIdx.x & 63, sub = threadIdx.x >> 6;
+    if (k >= d) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * 4ll + sub; i < n; i += gridDim.x * 4ll) acc += x[i * d + k];
+    atomicAdd(&sum[k], acc);
+}
+
+// centre row (the list's representative) and the CSR offsets {0, n} of the single list
+__global__ void bf_centre_kernel(const double *__restrict__ sum, int64_t n, int d, float *__restrict__ c,
+                                 int64_t *__restrict__ offsets) {
+    const int k = threadIdx.x;
+    if (k < d) c[k] = static_cast<float>(sum[k] / static_cast<double>(n));
+    if (k == 0) {
+        offsets[0] = 0;
+        offsets[1] = n;
+    }
+}
+
+// list radius: max over the rows of |x - c| (fp32 residuals, fp64 sum), rounded up
+__global__ void bf_extent_kernel(const float *__restrict__ x, int64_t n, int d, const float *__restrict__ c,
+                                 unsigned *__restrict__ rmax_bits) {
+    unsigned m = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double h = 0.0;
+        for (int k = 0; k < d; ++k) {
+            const double b = __fsub_rn(x[i * d + k], c[k]);
+            h += b * b;
+        }
+        m = max(m, __float_as_uint(static_cast<float>(sqrt(h)) * kUp));
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(rmax_bits, m);
+}
+
+// per query: one segment = the whole list (cutoff n), gamma = +inf (no seed bound),
+// |q - c| for the A-operand scale, identity tile order
+__global__ void bf_queries_kernel(const float *__restrict__ q, int64_t nq, int d, const float *__restrict__ c,
+                                  int32_t n, float *__restrict__ gamma, int32_t *__restrict__ nseg,
+                                  int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start,
+                                  int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list,
+                                  float *__restrict__ seg_d1, uint64_t *__restrict__ order_key,
+                                  int32_t *__restrict__ qorder) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i > nq) return;
+    seg_off[i] = i;
+    if (i == nq) return;
+    float h = 0.f;
+    for (int k = 0; k < d; ++k) {
+        const float t = q[i * d + k] - c[k];
+        h = fmaf(t, t, h);
+    }
+    gamma[i] = __int_as_float(0x7f800000);
+    nseg[i] = 1;
+    seg_start[i] = 0;
+    seg_len[i] = n;
+    seg_list[i] = 0;
+    seg_d1[i] = sqrtf(h);
+    order_key[i] = 0;
+    qorder[i] = static_cast<int32_t>(i);
+}
+
+__global__ void iota_i32_kernel(int32_t *__restrict__ a, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) a[i] = static_cast<int32_t>(i);
+}
+
+}  // namespace
+
+bool tc_bf_supported(int64_t nq, int64_t n, int d, int metric, int k) {
+    // one list centred on the mean: tight enough when the points are few (representative
+    // sets); large point sets use the partitioned operand (tc_bf_index_search)
+    if (metric != RBC_L2 || d < 1 || d > 64 || k < 1 || k > 16 || n < k || n > 65536) return false;
+    if (n + kTailRows + 8 >= (int64_t(1) << 31)) return false;  // int32 positions
+    return nq * n >= (int64_t(1) << 16);  // smaller problems: the exact SIMT scan is as fast
+}
+
+static std::atomic<int64_t> g_tc_bf_calls{0};
+
+int tc_bf_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int k, uint64_t *keys, cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    g_tc_bf_calls.fetch_add(1);
+    DevBuf<double> csum;
+    DevBuf<float> cen, rad;
+    DevBuf<int64_t> offsets;
+    DevBuf<int32_t> perm;
+    DevBuf<unsigned> rbits;
+    RBC_CHECK(csum.alloc(64, st));
+    RBC_CHECK(cen.alloc(64, st));
+    RBC_CHECK(rad.alloc(1, st));
+    RBC_CHECK(offsets.alloc(2, st));
+    RBC_CHECK(perm.alloc(n, st));
+    RBC_CUDA(cudaMemsetAsync(csum.get(), 0, 64 * sizeof(double), st));
+    RBC_CUDA(cudaMemsetAsync(rad.get(), 0, sizeof(float), st));
+    bf_colsum_kernel<<<grid_for(n, 4, 148 * 8), 256, 0, st>>>(x, n, d, csum.get());
+    bf_centre_kernel<<<1, 64, 0, st>>>(csum.get(), n, d, cen.get(), offsets.get());
+    bf_extent_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(x, n, d, cen.get(),
+                                                               reinterpret_cast<unsigned *>(rad.get()));
+    iota_i32_kernel<<<grid_for(n, 256), 256, 0, st>>>(perm.get(), n);
+    RBC_LAUNCHED();
+    note_launch(3);
+    TcIndex *tc = nullptr;
+    const std::vector<int64_t> off_h{0, n};
+    RBC_CHECK(tc_lists_build(x, cen.get(), offsets.get(), off_h, rad.get(), 1, d, &tc, nullptr, st));
+    rbc_index tmp;
+    tmp.kind = 0;
+    tmp.n = n;
+    tmp.d = d;
+    tmp.metric = RBC_L2;
+    tmp.nr = 1;
+    tmp.reps = cen.get();
+    tmp.radii = rad.get();
+    tmp.offsets = offsets.get();
+    tmp.perm = perm.get();
+    tmp.xp = const_cast<float *>(x);
+    tmp.n_local = n;
+    tmp.tc = tc;
+    PruneOut po;
+    int rc = RBC_OK;
+    auto run = [&]() -> int {
+        RBC_CHECK(po.gamma.alloc(nq, st));
+        RBC_CHECK(po.nseg.alloc(nq, st));
+        RBC_CHECK(po.seg_off.alloc(nq + 1, st));
+        RBC_CHECK(po.seg_start.alloc(nq, st));
+        RBC_CHECK(po.seg_len.alloc(nq, st));
+        RBC_CHECK(po.seg_list.alloc(nq, st));
+        RBC_CHECK(po.seg_d1.alloc(nq, st));
+        RBC_CHECK(po.order_key.alloc(nq, st));
+        RBC_CHECK(po.qorder.alloc(nq, st));
+        po.total_segs = nq;
+        bf_queries_kernel<<<grid_for(nq + 1, 256), 256, 0, st>>>(
+            q, nq, d, cen.get(), static_cast<int32_t>(n), po.gamma.get(), po.nseg.get(), po.seg_off.get(),
+            po.seg_start.get(), po.seg_len.get(), po.seg_list.get(), po.seg_d1.get(), po.order_key.get(),
+            po.qorder.get());
+        RBC_LAUNCHED();
+        DevBuf<int64_t> status;
+        RBC_CHECK(status.alloc(2, st));
+        const int64_t cap_work = (nq + kRows - 1) / kRows + 64;  // one work item per tile
+        const char *capenv = getenv("RBC_BF_CAP");  // diagnostic override of the candidate-group capacity
+        const int capg = capenv ? atoi(capenv) : 16 + 8 * k;
+        RBC_CHECK(tc_stage2(&tmp, q, nq, k, po, keys, cap_work, status.get(), st, capg));
+        int64_t h[2] = {0, 0};
+        RBC_CUDA(cudaMemcpyAsync(h, status.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+        RBC_CUDA(cudaStreamSynchronize(st));
+        last_overflow_count() = h[1];
+        if (h[0] > cap_work) return fail(RBC_ECUDA, "brute-force work items exceed one per tile");
+        return RBC_OK;
+    };
+    rc = run();
+    cudaStreamSynchronize(st);
+    tc_free(tc);
+    return rc;
+}
+
+
+// ---- tensor-core brute force over a partitioned operand ------------------------------------
+// bf_search at scale: x is partitioned into lists around evenly spaced points (an exact RBC
+// index, built once per prepared operand) so every f16 operand is a residual to a nearby
+// centre; the scan then visits EVERY list for every query tile -- no pruning, every
+// (q, x) pair passes through the tensor cores -- with the tile's nearest lists first so the
+// running bound is tight before the far lists stream through.
+namespace {
+
+// centre of the list representatives and |r_p - c| per list
+__global__ void bf_rep_centre_kernel(const float *__restrict__ reps, int64_t nr, int d, float *__restrict__ c) {
+    const int k = threadIdx.x;
+    if (k >= d) return;
+    double s = 0.0;
+    for (int64_t p = 0; p < nr; ++p) s += reps[p * d + k];
+    c[k] = static_cast<float>(s / static_cast<double>(nr));
+}
+
+__global__ void row_dist_kernel(const float *__restrict__ a, int64_t rows, int d, const float *__restrict__ c,
+                                float *__restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= rows) return;
+    double h = 0.0;
+    for (int k = 0; k < d; ++k) {
+        const double t = static_cast<double>(a[i * d + k]) - static_cast<double>(c[k]);
+        h += t * t;
+    }
+    out[i] = static_cast<float>(sqrt(h)) * kUp;
+}
+
+// per query: nearest-list sort key, gamma (k = 1: the exact distance to the nearest list
+// centre, a point of x, bounds the nearest neighbour; else +inf), one overflow segment = all of x
+__global__ void bf_index_queries_kernel(const uint64_t *__restrict__ near, int64_t nq, int k, int32_t n,
+                                        uint32_t *__restrict__ skey, int32_t *__restrict__ ids,
+                                        float *__restrict__ gamma, int32_t *__restrict__ nseg,
+                                        int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start,
+                                        int32_t *__restrict__ seg_len) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i > nq) return;
+    seg_off[i] = i;
+    if (i == nq) return;
+    const uint64_t key = near[i];
+    skey[i] = key_id(key);
+    ids[i] = static_cast<int32_t>(i);
+    gamma[i] = k == 1 ? key_dist(key) : __int_as_float(0x7f800000);
+    nseg[i] = 1;
+    seg_start[i] = 0;
+    seg_len[i] = n;
+}
+
+// One block per 128-query tile: every list becomes a work item (cut = whole list); the lists
+// that are some row's nearest list come first (most rows first), then the rest by position.
+// A scale from |q - c| + |r_p - c| >= |q - r_p| over the tile's rows.  Also zeroes stage 2's
+// per-query group counts and counters and writes the (identity) tile order.
+__global__ void __launch_bounds__(kRows) bf_tile_fill_kernel(
+    const int32_t *__restrict__ order, int64_t nq, const uint64_t *__restrict__ near, const float *__restrict__ qdc,
+    const float *__restrict__ rdc, int64_t nr, const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff,
+    const float *__restrict__ sB, const float *__restrict__ radii, WorkItem *__restrict__ work,
+    int64_t *__restrict__ work_off, int64_t *__restrict__ nwork, unsigned long long *__restrict__ work_total,
+    int32_t *__restrict__ tile_order, int32_t *__restrict__ cand_count, int32_t *__restrict__ counters) {
+    extern __shared__ int32_t cnt[];  // [nr]
+    typedef cub::BlockScan<int, kRows> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ unsigned long long s_fkey[kRows];
+    __shared__ int s_nf;
+    __shared__ unsigned s_dq;
+    for (int64_t p = threadIdx.x; p < nr; p += blockDim.x) cnt[p] = 0;
+    if (threadIdx.x == 0) {
+        s_nf = 0;
+        s_dq = 0;
+        tile_order[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
+        nwork[blockIdx.x] = nr;
+        work_off[blockIdx.x] = static_cast<int64_t>(blockIdx.x) * nr;
+        if (blockIdx.x == 0) *work_total = static_cast<unsigned long long>(gridDim.x) * nr;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 2) counters[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
+    const int32_t qi = tq < nq ? order[tq] : -1;
+    if (qi >= 0) {
+#pragma unroll
+        for (int h = 0; h < kParts; ++h) cand_count[kParts * static_cast<int64_t>(qi) + h] = 0;
+        atomicAdd(&cnt[key_id(near[qi])], 1);
+        atomicMax(&s_dq, __float_as_uint(qdc[qi]));
+    }
+    __syncthreads();
+    const int64_t per = (nr + kRows - 1) / kRows;
+    const int64_t pa = threadIdx.x * per, pe = min(nr, pa + per);
+    int c = 0;
+    for (int64_t p = pa; p < pe; ++p) {
+        if (cnt[p] > 0) {
+            const int slot = atomicAdd(&s_nf, 1);  // <= 128 distinct nearest lists per tile
+            s_fkey[slot] = (static_cast<unsigned long long>(kRows - cnt[p]) << 32) | static_cast<uint64_t>(p);
+        } else {
+            ++c;
+        }
+    }
+    int pos, total;
+    Scan(scan_tmp).ExclusiveSum(c, pos, total);
+    __syncthreads();
+    const int nf = s_nf;
+    const float dq = __uint_as_float(s_dq);
+    WorkItem *w0 = work + static_cast<int64_t>(blockIdx.x) * nr;
+    auto item = [&](int64_t p) {
+        WorkItem it;
+        it.p = static_cast<int32_t>(p);
+        it.ext = static_cast<int32_t>(offsets[p + 1] - offsets[p]);
+        const float m = (dq + rdc[p]) * kUp;
+        int e = 0;
+        if (m > 0.f) frexpf(m, &e);
+        it.sA = m > 0.f ? ldexpf(1.0f, -e) : 1.0f;
+        it.sB = sB[p];
+        it.radius = radii[p];
+        const float cc = it.sA / it.sB;
+        it.aug = (cc >= 6.103515625e-05f && cc <= 32768.0f) ? -cc : 0.0f;
+        it.poff = static_cast<int32_t>(poff[p]);
+        it.csr = static_cast<int32_t>(offsets[p]);
+        return it;
+    };
+    for (int64_t p = pa; p < pe; ++p)
+        if (cnt[p] == 0) w0[nf + pos++] = item(p);
+    if (threadIdx.x < nf) {
+        const unsigned long long mine = s_fkey[threadIdx.x];
+        int rank = 0;
+        for (int j = 0; j < nf; ++j) rank += s_fkey[j] < mine ? 1 : 0;
+        w0[rank] = item(static_cast<int64_t>(mine & 0xFFFFFFFFu));
+    }
+}
+
+}  // namespace
+
+int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
+    if (!tc || k < 1 || k > 16) return fail(RBC_EINVAL, "tc brute force: unsupported index or k");
+    g_tc_bf_calls.fetch_add(1);
+    const int64_t nr = idx->nr, n = idx->n_local;
+    const int d = idx->d;
+    const int ntiles = static_cast<int>((nq + kRows - 1) / kRows);
+    // 1. nearest list centre of every query (k = 1 brute force over the centres)
+    DevBuf<uint64_t> near;
+    RBC_CHECK(near.alloc(nq, st));
+    RBC_CHECK(nearest_rows(q, nq, idx->reps, nr, d, RBC_L2, near.get(), st));
+    // 2. queries ordered by nearest list; gamma; overflow segments
+    PruneOut po;
+    RBC_CHECK(po.gamma.alloc(nq, st));
+    RBC_CHECK(po.nseg.alloc(nq, st));
+    RBC_CHECK(po.seg_off.alloc(nq + 1, st));
+    RBC_CHECK(po.seg_start.alloc(nq, st));
+    RBC_CHECK(po.seg_len.alloc(nq, st));
+    DevBuf<uint32_t> skey, skey_sorted;
+    DevBuf<int32_t> ids, order;
+    RBC_CHECK(skey.alloc(nq, st));
+    RBC_CHECK(skey_sorted.alloc(nq, st));
+    RBC_CHECK(ids.alloc(nq, st));
+    RBC_CHECK(order.alloc(nq, st));
+    bf_index_queries_kernel<<<grid_for(nq + 1, 256), 256, 0, st>>>(near.get(), nq, k, static_cast<int32_t>(n),
+                                                                    skey.get(), ids.get(), po.gamma.get(),
+                                                                    po.nseg.get(), po.seg_off.get(),
+                                                                    po.seg_start.get(), po.seg_len.get());
+    RBC_LAUNCHED();
+    int kb = 1;
+    while ((int64_t(1) << kb) < nr) ++kb;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, skey.get(), skey_sorted.get(), ids.get(), order.get(), nq, 0, kb, st);
+    DevBuf<unsigned char> tmp;
+    RBC_CHECK(tmp.alloc(tb, st));
+    RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, skey.get(), skey_sorted.get(), ids.get(), order.get(), nq,
+                                             0, kb, st));
+    note_launch();
+    // 3. |q - c|, |r_p - c| for the A scales
+    DevBuf<float> cen, qdc, rdc;
+    RBC_CHECK(cen.alloc(64, st));
+    RBC_CHECK(qdc.alloc(nq, st));
+    RBC_CHECK(rdc.alloc(nr, st));
+    bf_rep_centre_kernel<<<1, 64, 0, st>>>(idx->reps, nr, d, cen.get());
+    row_dist_kernel<<<grid_for(nq, 256), 256, 0, st>>>(q, nq, d, cen.get(), qdc.get());
+    row_dist_kernel<<<grid_for(nr, 256), 256, 0, st>>>(idx->reps, nr, d, cen.get(), rdc.get());
+    RBC_LAUNCHED();
+    note_launch(2);
+    // 4. every list is a work item of every tile
+    const int64_t cap_work = static_cast<int64_t>(ntiles) * nr;
+    DevBuf<WorkItem> work;
+    DevBuf<int64_t> work_off, nwork;
+    DevBuf<unsigned long long> work_total;
+    DevBuf<int32_t> tile_order, cand_count, counters;
+    RBC_CHECK(work.alloc(cap_work, st));
+    RBC_CHECK(work_off.alloc(ntiles, st));
+    RBC_CHECK(nwork.alloc(ntiles, st));
+    RBC_CHECK(work_total.alloc(1, st));
+    RBC_CHECK(tile_order.alloc(ntiles, st));
+    RBC_CHECK(cand_count.alloc(nq * kParts, st));
+    RBC_CHECK(counters.alloc(2, st));
+    const size_t smem = sizeof(int32_t) * nr;
+    if (smem > 200 * 1024) return fail(RBC_EINVAL, "tc brute force: too many lists");
+    cudaFuncSetAttribute(bf_tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    bf_tile_fill_kernel<<<ntiles, kRows, smem, st>>>(order.get(), nq, near.get(), qdc.get(), rdc.get(), nr,
+                                                      idx->offsets, tc->poff, tc->sB, idx->radii, work.get(),
+                                                      work_off.get(), nwork.get(), work_total.get(), tile_order.get(),
+                                                      cand_count.get(), counters.get());
+    RBC_LAUNCHED();
+    // 5. the scan, exact re-rank and overflow fallback
+    DevBuf<int64_t> status;
+    RBC_CHECK(status.alloc(2, st));
+    const char *capenv = getenv("RBC_BF_CAP");  // diagnostic override of the candidate-group capacity
+    const int capg = capenv ? atoi(capenv) : 16 + 8 * k;
+    RBC_CHECK(s2_run(idx, q, nq, k, po, order.get(), ntiles, tile_order.get(), work_off.get(), nwork.get(),
+                     work_total.get(), work.get(), nullptr, cap_work, cand_count.get(), counters.get(), keys,
+                     status.get(), st, capg));
+    int64_t h[2] = {0, 0};
+    RBC_CUDA(cudaMemcpyAsync(h, status.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    last_overflow_count() = h[1];
+    return RBC_OK;
+}
 }  // namespace rbc
+
+extern "C" int64_t rbc_tc_bf_calls(void) { return rbc::g_tc_bf_calls.load(); }
