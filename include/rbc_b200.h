@@ -80,6 +80,9 @@ int64_t rbc_stage2_overflows(void);
  * list scan) served by the tcgen05 engine since the library loaded (diagnostic:
  * lets tests prove the tensor-core path ran). */
 int64_t rbc_tc_bf_calls(void);
+/* Launches of the tcgen05 list-scan kernel (stage2_tc_kernel: exact-search stage 2
+ * and every tensor-core brute force) since the library loaded (diagnostic). */
+int64_t rbc_tc_scan_calls(void);
 
 /* metric.py:57-76 pairwise_distances (and brute_force.py:220-251
  * distance_rows): out[m,p] = dist(a[i], b[j]), bit-exact. */

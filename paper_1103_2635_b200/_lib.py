@@ -95,6 +95,7 @@ EXPORTS = {
     "rbc_set_engine": ([ctypes.c_int], ctypes.c_int),
     "rbc_stage2_overflows": ([], _i64),
     "rbc_tc_bf_calls": ([], _i64),
+    "rbc_tc_scan_calls": ([], _i64),
 }
 def last_error() -> str:
     msg = _load().rbc_last_error()

@@ -313,17 +313,17 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
 }
 
 // ---- prepared brute-force operand (kind 2) --------------------------------------------------
-// L2, d <= 64: the points are partitioned into ~sqrt(n)/2 lists around evenly spaced points
+// L2, d <= 128: the points are partitioned into ~sqrt(n)/2 lists around evenly spaced points
 // (the exact build's assignment + stable sort), so the tcgen05 scan multiplies residuals to a
 // nearby centre (tight f16 error bounds); every list is still scanned for every query.
 // Otherwise the operand is a plain device copy of the points for the exact SIMT scan.
 bool bf_partition_pays(int64_t nq, int64_t n, int d, int metric, int k) {
-    return metric == RBC_L2 && d <= 64 && k <= 16 && n > 65536 && nq >= 512 && n + 4096 < (int64_t(1) << 31);
+    return metric == RBC_L2 && d <= 128 && k <= 16 && n > 65536 && nq >= 512 && n + 4096 < (int64_t(1) << 31);
 }
 
 int bf_prepare(const float *x, int64_t n, int d, int metric, rbc_index **out, cudaStream_t st) {
     RBC_CHECK(check_common(n, d, metric));
-    if (metric == RBC_L2 && d <= 64 && n >= 1024 && n + 4096 < (int64_t(1) << 31)) {
+    if (metric == RBC_L2 && d <= 128 && n >= 1024 && n + 4096 < (int64_t(1) << 31)) {
         int64_t nr = static_cast<int64_t>(std::sqrt(static_cast<double>(n)) / 2.0);
         nr = nr < 1 ? 1 : nr;
         std::vector<int64_t> rid(nr);

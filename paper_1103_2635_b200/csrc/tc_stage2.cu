@@ -56,19 +56,28 @@ namespace rbc {
 namespace {
 
 constexpr int kRows = 128;       // queries per tile = UMMA M = TMEM lanes
-constexpr int kNmax = 256;       // max UMMA N per chunk (N = 256 keeps the single MMA thread compute-bound)
+constexpr int kNmax = 256;       // largest UMMA N per chunk (N = 256 keeps the single MMA thread compute-bound)
 constexpr int kAcc = 2;          // TMEM accumulator stages (2 x 256 columns)
-constexpr int kStages = 4;       // B ring depth
 constexpr int kParts = 2;        // epilogue warps per TMEM lane quadrant (column halves / K halves)
 constexpr int kEpiWarps = 4 * kParts;
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 16 epilogue warps
-constexpr int kCols = kNmax / kParts;          // columns of each chunk per epilogue warp
-constexpr int kKd = 64 / kParts;               // A-operand dims per epilogue warp
 constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
 constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
 constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
-constexpr int kStageBytes = kNmax * (kP0 + kP1);
-constexpr int kABytes = kRows * (kP0 + kP1);
+// Per K-plane count NP (d <= 64 * NP): NP = 1 for d <= 64; NP = 2 for d <= 128 (two SW128
+// planes, 128-column chunks and a 3-stage ring so the A/B buffers fit in shared memory).
+template <int NP>
+struct S2Cfg {
+    static constexpr int kN = NP == 1 ? 256 : 128;   // UMMA N per chunk
+    static constexpr int kStages = NP == 1 ? 4 : 3;  // B ring depth
+    static constexpr int kCols = kN / kParts;        // columns of each chunk per epilogue warp
+    static constexpr int kKd = 64 * NP / kParts;     // A-operand dims per epilogue warp
+    static constexpr int kStageBytes = kN * (NP * kP0 + kP1);
+    static constexpr int kABytes = kRows * (NP * kP0 + kP1);
+    static constexpr int kTmemCols = 2 * kN;         // kAcc accumulators
+    static constexpr size_t kSmem =
+        1024 + kStages * kStageBytes + 2 * kABytes + (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) + 512;
+};
 
 // error-bound constants (factor-2 safety on each term; K <= 80 accumulated products)
 constexpr float kC1 = 4.0f * (1.0f / 1024.0f + 128.0f / 4194304.0f);  // f16 rounding of a and b, fp32 accumulate
@@ -77,7 +86,8 @@ constexpr bool kHold = false;  // diagnostic variant
 #else
 constexpr bool kHold = true;   // k = 1: newest qualifying group held in registers
 #endif
-constexpr float kAccErr = 4.0f * 128.0f / 4194304.0f;                  // fp32 accumulation share of kC1
+constexpr float kAccErr = 4.0f * 128.0f / 4194304.0f;                  // fp32 accumulation share of kC1 (K <= 80;
+                                                                       // doubled for the K <= 144 of NP = 2)
 constexpr float kC2 = 1.0f / 1048576.0f;                              // norms, aug split, epilogue rounding
 constexpr float kC4 = 1.0f / 262144.0f;                               // f16 subnormal flush (absolute, scaled)
 constexpr float kUp = 1.0f + 1.0f / 1048576.0f;                       // rounding-up factor for norms
@@ -87,14 +97,16 @@ constexpr float kUq = 1.0f + 1.0f / 65536.0f;                          // ... an
 
 struct TcIndex {
     int64_t npad = 0;
-    bool plane1 = false;      // aug columns in a separate 16-wide plane (d > 62)
-    uint8_t *xh0 = nullptr;   // [npad + tail][128 B] f16 residual rows (+aug when d <= 62), SW128 pre-swizzled
+    int np = 1;               // 64-wide K planes (d <= 64 np)
+    int64_t rows = 0;         // rows per plane (npad + tail)
+    bool plane1 = false;      // aug columns in a separate 16-wide plane (d > 64 np - 2)
+    uint8_t *xh0 = nullptr;   // [np][rows][128 B] f16 residual rows (+aug in the last plane when d <= 64 np - 2), SW128
     uint8_t *xh1 = nullptr;   // [npad + tail][32 B] aug plane, SW32 pre-swizzled (d > 62 only)
     float *gcol = nullptr;    // [npad + tail] (|x - r_p|^2 / 2) * sB_p (fallback when -sA/sB is not an f16 normal)
     int64_t *poff = nullptr;  // [nr + 1] padded (8-row aligned) list offsets
     float *sB = nullptr;      // [nr] per-list power-of-two scale
     float *dbmax = nullptr;   // [nr] max over the list of |b - f16(b)| (scaled residual rows, f16 rounding)
-    float *reps64 = nullptr;  // [nr][64] representatives, zero padded
+    float *reps64 = nullptr;  // [nr][64 np] representatives, zero padded
 };
 
 // one (tile, list) work item, 32 bytes
@@ -111,12 +123,13 @@ struct __align__(16) WorkItem {
 
 struct S2Params {
     const uint8_t *xh0;
+    int64_t plane_bytes;        // byte stride between the K planes of xh0
     const uint8_t *xh1;
     const float *gcol;
     const float *reps64;
     const float *dbmax;         // [nr] per-list max f16 rounding error of the B rows (scaled)
     int plane1;
-    const float *q64;           // queries, rows padded to 64 floats
+    const float *q64;           // queries, rows padded to 64 NP floats
     const float *gamma;         // [nq] gamma_k
     int k;
     int ntiles;
@@ -199,7 +212,8 @@ __global__ void list_scale_kernel(const float *__restrict__ radii, int64_t nr, f
 // zero on entry (max over the row slices through a float-bits atomic).
 __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *__restrict__ reps,
                                      const int64_t *__restrict__ offsets, const int64_t *__restrict__ poff,
-                                     const float *__restrict__ sB, int d, int plane1, uint8_t *__restrict__ xh0,
+                                     const float *__restrict__ sB, int d, int np, int64_t plane_bytes, int plane1,
+                                     uint8_t *__restrict__ xh0,
                                      uint8_t *__restrict__ xh1, float *__restrict__ gcol, float *__restrict__ dbmax) {
     __shared__ unsigned s_db;
     if (threadIdx.x == 0) s_db = 0;
@@ -223,9 +237,9 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
         const __half glo = __float2half_rn(gp - __half2float(ghi));
         const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ghi)) |
                              (static_cast<uint32_t>(__half_as_ushort(glo)) << 16);
-        uint8_t *dst = xh0 + row * kP0;
         float db2 = 0.f;  // |b - f16(b)|^2 of this row (scaled units)
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 8 * np; ++c) {
+            uint8_t *dst = xh0 + (c >> 3) * plane_bytes + row * kP0;
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -239,8 +253,8 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
                 const float e0 = b0 * s - hf2.x, e1 = b1 * s - hf2.y;
                 db2 = fmaf(e0, e0, fmaf(e1, e1, db2));
             }
-            if (!plane1 && c == 7) w[3] = aug;  // columns 62, 63
-            *reinterpret_cast<uint4 *>(dst + ((c ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            if (!plane1 && c == 8 * np - 1) w[3] = aug;  // last two columns of the last plane
+            *reinterpret_cast<uint4 *>(dst + (((c & 7) ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         if (plane1) {
             uint8_t *d1p = xh1 + row * kP1;
@@ -255,11 +269,13 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
     if (threadIdx.x == 0 && s_db) atomicMax(reinterpret_cast<unsigned *>(dbmax) + p, s_db);
 }
 
-__global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst) {
+// rows of src [rows][d] -> dst [rows][w], zero padded (w = 64 or 128)
+__global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst,
+                                  int w = 64) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t >= rows * 64) return;
-    const int64_t r = t >> 6;
-    const int c = static_cast<int>(t & 63);
+    if (t >= rows * w) return;
+    const int64_t r = t / w;
+    const int c = static_cast<int>(t - r * w);
     dst[t] = c < d ? src[r * d + c] : 0.f;
 }
 
@@ -462,8 +478,12 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
 }
 
 // ---- the stage-2 kernel -----------------------------------------------------------------
-template <int KT>
+template <int KT, int NP>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
+    using Cfg = S2Cfg<NP>;
+    constexpr int kN = Cfg::kN, kStages = Cfg::kStages, kCols = Cfg::kCols, kKd = Cfg::kKd;
+    constexpr int kStageBytes = Cfg::kStageBytes, kABytes = Cfg::kABytes;
+    constexpr float kAccErrNP = kAccErr * NP;
     if (static_cast<int64_t>(*P.work_total) > P.cap_work) return;  // work arrays incomplete (see tile_fill_kernel)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (sm100::smem_u32(smem_raw) & 1023)) & 1023);
@@ -496,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         }
         sm100::fence_barrier_init();
     }
-    if (warp == 1) sm100::tmem_alloc<512>(s_tmem);
+    if (warp == 1) sm100::tmem_alloc<Cfg::kTmemCols>(s_tmem);
     sm100::tc_fence_before();
     __syncthreads();
     sm100::tc_fence_after();
@@ -516,17 +536,21 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 if (tile < 0) break;
                 for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w) {
                     const WorkItem wi = P.work[w];
-                    for (int off = 0; off < wi.ext; off += kNmax) {
-                        const int n = min(kNmax, roundup16(wi.ext - off));
+                    for (int off = 0; off < wi.ext; off += kN) {
+                        const int n = min(kN, roundup16(wi.ext - off));
                         const uint32_t s = bi % kStages;
                         S2_WAIT(&empty[s], ((bi / kStages) & 1) ^ 1, 0);
                         uint8_t *dst = sB + s * kStageBytes;
                         const uint32_t b0 = static_cast<uint32_t>(n) * kP0;
                         const uint32_t b1 = P.plane1 ? static_cast<uint32_t>(n) * kP1 : 0u;
-                        sm100::mbar_arrive_expect_tx(&full[s], b0 + b1);
-                        sm100::bulk_g2s(dst, P.xh0 + (static_cast<int64_t>(wi.poff) + off) * kP0, b0, &full[s]);
+                        sm100::mbar_arrive_expect_tx(&full[s], NP * b0 + b1);
+#pragma unroll
+                        for (int j = 0; j < NP; ++j)
+                            sm100::bulk_g2s(dst + j * kN * kP0,
+                                            P.xh0 + j * P.plane_bytes + (static_cast<int64_t>(wi.poff) + off) * kP0, b0,
+                                            &full[s]);
                         if (b1)
-                            sm100::bulk_g2s(dst + kNmax * kP0, P.xh1 + (static_cast<int64_t>(wi.poff) + off) * kP1, b1,
+                            sm100::bulk_g2s(dst + NP * kN * kP0, P.xh1 + (static_cast<int64_t>(wi.poff) + off) * kP1, b1,
                                             &full[s]);
                         ++bi;
                     }
@@ -549,22 +573,25 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     S2_WAIT(&afull[a], (ai >> 1) & 1, 1);
                     sm100::tc_fence_after();
                     const uint32_t a0 = sm100::smem_u32(sA + a * kABytes);
-                    for (int off = 0; off < ext; off += kNmax) {
-                        const int n = min(kNmax, roundup16(ext - off));
+                    for (int off = 0; off < ext; off += kN) {
+                        const int n = min(kN, roundup16(ext - off));
                         const uint32_t s = bi % kStages, tb = ti % kAcc;
                         S2_WAIT(&full[s], (bi / kStages) & 1, 2);
                         S2_WAIT(&tempty[tb], ((ti / kAcc) & 1) ^ 1, 3);
                         sm100::tc_fence_after();
                         const uint32_t idesc = sm100::idesc_f16_f32(kRows, static_cast<uint32_t>(n));
                         const uint32_t b0 = sm100::smem_u32(sB + s * kStageBytes);
-                        const uint32_t d_tmem = tmem + tb * kNmax;
+                        const uint32_t d_tmem = tmem + tb * kN;
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + kk * 32),
-                                            sm100::umma_desc_sw128(b0 + kk * 32), idesc, kk > 0);
+                        for (int j = 0; j < NP; ++j)
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                sm100::umma_f16(d_tmem, sm100::umma_desc_sw128(a0 + j * kRows * kP0 + kk * 32),
+                                                sm100::umma_desc_sw128(b0 + j * kN * kP0 + kk * 32), idesc,
+                                                (j | kk) > 0);
                         if (P.plane1)
-                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(a0 + kRows * kP0),
-                                            sm100::umma_desc_sw32(b0 + kNmax * kP0), idesc, 1);
+                            sm100::umma_f16(d_tmem, sm100::umma_desc_sw32(a0 + NP * kRows * kP0),
+                                            sm100::umma_desc_sw32(b0 + NP * kN * kP0), idesc, 1);
                         sm100::umma_commit(&empty[s]);
                         sm100::umma_commit(&tfull[tb]);
                         ++bi;
@@ -595,13 +622,16 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             const int32_t qi = slot_q < P.nq ? P.order[slot_q] : -1;
             const bool live = qi >= 0;
             // this thread's quarter of the query row (rows padded to 64 floats with zeros)
-            float qv[kKd];
-            {
-                const float4 *src =
-                    reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(live ? qi : 0) * 64 + part * kKd);
+            // (NP = 2: 64 floats per thread would not fit beside the epilogue's registers;
+            // prep_a then re-reads the row from L1)
+            constexpr int kQv = NP == 1 ? kKd : 4;
+            float qv[kQv];
+            const float4 *qsrc =
+                reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(live ? qi : 0) * (64 * NP) + part * kKd);
+            if (NP == 1) {
 #pragma unroll
-                for (int c = 0; c < kKd / 4; ++c) {
-                    const float4 t = live ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int c = 0; c < kQv / 4; ++c) {
+                    const float4 t = live ? __ldg(qsrc + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                     qv[4 * c] = t.x;
                     qv[4 * c + 1] = t.y;
                     qv[4 * c + 2] = t.z;
@@ -614,40 +644,20 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 S2_TIME(const unsigned long long tp0 = clock64());
                 S2_TIME(++tw[11]);
                 const WorkItem wi = P.work[w];
-                const float4 *rep4 = reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * 64 + part * kKd);
-                float4 rr4[kKd / 4];
-#pragma unroll
-                for (int c = 0; c < kKd / 4; ++c) rr4[c] = __ldg(rep4 + c);
+                const float4 *rep4 =
+                    reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * (64 * NP) + part * kKd);
                 const __half ac = __float2half_rn(wi.aug);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 const float sa = wi.sA;
-                // this part's share of |q - r_p|^2 (fp32; with the other part's, the A2 term of
-                // the error bound -- same (d + 2) 2^-24 relative error budget as kD1 / kUq)
-                {
-                    float n0 = 0.f, n1 = 0.f;
-#pragma unroll
-                    for (int c = 0; c < kKd / 4; ++c) {
-                        const float t0 = qv[4 * c] - rr4[c].x, t1 = qv[4 * c + 1] - rr4[c].y;
-                        const float t2 = qv[4 * c + 2] - rr4[c].z, t3 = qv[4 * c + 3] - rr4[c].w;
-                        n0 = fmaf(t0, t0, fmaf(t1, t1, n0));
-                        n1 = fmaf(t2, t2, fmaf(t3, t3, n1));
-                    }
-                    s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + part * kRows + row] = n0 + n1;
-                }
                 const uint32_t a = ai & 1;
-                S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
-                uint8_t *dst = sA + a * kABytes + row * kP0;
-                float da2 = 0.f;  // |a - f16(a)|^2 of this part (scaled units)
-#pragma unroll
-                for (int c = 0; c < kKd / 8; ++c) {
-                    const float rr[8] = {rr4[2 * c].x, rr4[2 * c].y, rr4[2 * c].z, rr4[2 * c].w,
-                                         rr4[2 * c + 1].x, rr4[2 * c + 1].y, rr4[2 * c + 1].z, rr4[2 * c + 1].w};
+                // one 16-byte chunk (8 dims) of this thread's K range: f16 residuals, their rounding
+                // error, and the chunk's share of |q - r_p|^2
+                auto chunk = [&](int c, const float *qq, const float *rr, float &nq2, float &da2) {
                     uint32_t wv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int k0 = c * 8 + 2 * e;
-                        const float v0 = fmaf(qv[k0], sa, -(rr[2 * e] * sa));
-                        const float v1 = fmaf(qv[k0 + 1], sa, -(rr[2 * e + 1] * sa));
+                        const float v0 = fmaf(qq[2 * e], sa, -(rr[2 * e] * sa));
+                        const float v1 = fmaf(qq[2 * e + 1], sa, -(rr[2 * e + 1] * sa));
                         wv[e] = sm100::pack_f16x2_sat(v0, v1);
                         __half2 h;
                         *reinterpret_cast<uint32_t *>(&h) = wv[e];
@@ -655,13 +665,63 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         const float e0 = v0 - hf2.x, e1 = v1 - hf2.y;
                         da2 = fmaf(e0, e0, fmaf(e1, e1, da2));
                     }
-                    const int cc = part * (kKd / 8) + c;
-                    if (!P.plane1 && cc == 7) wv[3] = aug;
+                    // global 16-byte chunk index -> (plane, chunk in the 128-byte row)
+                    const int g = part * (kKd / 8) + c, pl = g >> 3, cc = g & 7;
+                    if (!P.plane1 && g == 8 * NP - 1) wv[3] = aug;
+                    uint8_t *dst = sA + a * kABytes + pl * kRows * kP0 + row * kP0;
                     *reinterpret_cast<uint4 *>(dst + ((cc ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                };
+                float da2 = 0.f;  // |a - f16(a)|^2 of this part (scaled units)
+                if constexpr (NP == 1) {
+                    float4 rr4[kKd / 4];
+#pragma unroll
+                    for (int c = 0; c < kKd / 4; ++c) rr4[c] = __ldg(rep4 + c);
+                    // this part's share of |q - r_p|^2 (fp32; with the other part's, the A2 term of
+                    // the error bound -- same (d + 2) 2^-24 relative error budget as kD1 / kUq)
+                    {
+                        float n0 = 0.f, n1 = 0.f;
+#pragma unroll
+                        for (int c = 0; c < kKd / 4; ++c) {
+                            const float t0 = qv[4 * c] - rr4[c].x, t1 = qv[4 * c + 1] - rr4[c].y;
+                            const float t2 = qv[4 * c + 2] - rr4[c].z, t3 = qv[4 * c + 3] - rr4[c].w;
+                            n0 = fmaf(t0, t0, fmaf(t1, t1, n0));
+                            n1 = fmaf(t2, t2, fmaf(t3, t3, n1));
+                        }
+                        s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + part * kRows + row] = n0 + n1;
+                    }
+                    S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
+#pragma unroll
+                    for (int c = 0; c < kKd / 8; ++c) {
+                        const float rr[8] = {rr4[2 * c].x, rr4[2 * c].y, rr4[2 * c].z, rr4[2 * c].w,
+                                             rr4[2 * c + 1].x, rr4[2 * c + 1].y, rr4[2 * c + 1].z, rr4[2 * c + 1].w};
+                        float nd = 0.f;
+                        chunk(c, qv + 8 * c, rr, nd, da2);
+                    }
+                } else {
+                    // NP = 2: 64 dims per thread, streamed 8 at a time (query and rep rows from L1)
+                    S2_WAIT(&aempty[a], ((ai >> 1) & 1) ^ 1, 4);
+                    float n0 = 0.f, n1 = 0.f;
+#pragma unroll 2
+                    for (int c = 0; c < kKd / 8; ++c) {
+                        const float4 r0 = __ldg(rep4 + 2 * c), r1 = __ldg(rep4 + 2 * c + 1);
+                        const float4 q0 = live ? __ldg(qsrc + 2 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 q1 = live ? __ldg(qsrc + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                        const float qq[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float t0 = qq[2 * e] - rr[2 * e], t1 = qq[2 * e + 1] - rr[2 * e + 1];
+                            n0 = fmaf(t0, t0, n0);
+                            n1 = fmaf(t1, t1, n1);
+                        }
+                        float nd = 0.f;
+                        chunk(c, qq, rr, nd, da2);
+                    }
+                    s_dq[(static_cast<int>(w) & 3) * (kParts * kRows) + part * kRows + row] = n0 + n1;
                 }
                 s_da[(static_cast<int>(w) & 3) * (kParts * kRows) + part * kRows + row] = da2;
                 if (P.plane1 && part == kParts - 1) {
-                    uint8_t *d1p = sA + a * kABytes + kRows * kP0 + row * kP1;
+                    uint8_t *d1p = sA + a * kABytes + NP * kRows * kP0 + row * kP1;
                     const int sw = (row >> 2) & 1;
                     *reinterpret_cast<uint4 *>(d1p + ((0 ^ sw) << 4)) = make_uint4(aug, 0, 0, 0);
                     *reinterpret_cast<uint4 *>(d1p + ((1 ^ sw) << 4)) = make_uint4(0, 0, 0, 0);
@@ -725,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     // d^2 and x2 safety as in kC1; fp32 accumulation keeps its kC1 share
                     const float da = sqrtf(DA2) * (1.0f + 1.0f / 1024.0f) / sa + dq * (1.0f / 8388608.0f);
                     const float db = P.dbmax[wi.p] * (1.0f + 1.0f / 1024.0f) / wi.sB + rb * (1.0f / 8388608.0f);
-                    E = 4.0f * (da * rb + na * db + da * db) + kAccErr * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 +
+                    E = 4.0f * (da * rb + na * db + da * db) + kAccErrNP * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 +
                         kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
                 const float lb0 = A2 - E;  // lb(V) = lb0 - V * inv2s
@@ -814,8 +874,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         T = threshold();
                     }
                 };
-                for (int off = 0; off < wi.ext; off += kNmax) {
-                    const int n = min(kNmax, roundup16(wi.ext - off));
+                for (int off = 0; off < wi.ext; off += kN) {
+                    const int n = min(kN, roundup16(wi.ext - off));
                     const int hb = part * kCols;  // this warp's first column in the chunk
                     if (noaug) {
                         // rare: per-column norm term subtracted here instead of in the MMA
@@ -833,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
 #else
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
 #endif
-                    const uint32_t tbase = tmem + tb * kNmax + hb + (static_cast<uint32_t>(quad * 32) << 16);
+                    const uint32_t tbase = tmem + tb * kN + hb + (static_cast<uint32_t>(quad * 32) << 16);
                     for (int c0 = 0; c0 < wlim; c0 += 32) {
                         uint32_t ra[32];
                         sm100::tmem_ld32_async(tbase + c0, ra);
@@ -917,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
 #endif
     sm100::tc_fence_before();
     __syncthreads();
-    if (warp == 1) sm100::tmem_dealloc<512>(tmem);
+    if (warp == 1) sm100::tmem_dealloc<Cfg::kTmemCols>(tmem);
 }
 
 // Exact re-rank (reference arithmetic) of the buffered candidate groups of both
@@ -1069,8 +1129,6 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
     }
 }
 
-constexpr size_t kSmemBytes =
-    1024 + kStages * kStageBytes + 2 * kABytes + (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) + 512;
 
 // Exact SIMT scan for the queries whose candidate buffer overflowed; the count
 // lives on the device (no host round trip).  One warp per entry, grid-stride.
@@ -1079,12 +1137,12 @@ __global__ void __launch_bounds__(256) overflow_scan_kernel(const float *__restr
                                                             const int32_t *__restrict__ ovf_list,
                                                             const int32_t *__restrict__ ovf_count, SegSubSrc src, int k,
                                                             uint64_t *__restrict__ keys) {
-    __shared__ float qs_all[8 * 64];
+    __shared__ float qs_all[8 * 128];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = *ovf_count;
     for (int64_t i = blockIdx.x * 8 + w; i < n; i += static_cast<int64_t>(gridDim.x) * 8) {
         const int64_t qi = ovf_list[i];
-        float *qs = qs_all + w * 64;
+        float *qs = qs_all + w * 128;
         for (int c = lane; c < d; c += 32) qs[c] = q[qi * d + c];
         __syncwarp();
         uint64_t best[KT];
@@ -1135,7 +1193,8 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
                           const std::vector<int64_t> &off, const float *radii, int64_t nr, int d, TcIndex **out,
                           size_t *bytes, cudaStream_t st) {
     TcIndex *tc = new TcIndex();
-    tc->plane1 = d > 62;
+    tc->np = d > 64 ? 2 : 1;
+    tc->plane1 = d > 64 * tc->np - 2;
     std::vector<int64_t> poff(nr + 1, 0);
     int64_t maxlen = 0;
     for (int64_t p = 0; p < nr; ++p) {
@@ -1145,22 +1204,24 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
     }
     tc->npad = poff[nr];
     const int64_t rows = tc->npad + kTailRows;
-    bool ok = cudaMalloc(&tc->xh0, rows * kP0) == cudaSuccess &&
+    tc->rows = rows;
+    const int np = tc->np;
+    bool ok = cudaMalloc(&tc->xh0, np * rows * kP0) == cudaSuccess &&
               (!tc->plane1 || cudaMalloc(&tc->xh1, rows * kP1) == cudaSuccess) &&
               cudaMalloc(&tc->gcol, rows * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&tc->poff, (nr + 1) * sizeof(int64_t)) == cudaSuccess &&
               cudaMalloc(&tc->sB, nr * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&tc->dbmax, nr * sizeof(float)) == cudaSuccess &&
-              cudaMalloc(&tc->reps64, nr * 64 * sizeof(float)) == cudaSuccess;
+              cudaMalloc(&tc->reps64, nr * 64 * np * sizeof(float)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         tc_free(tc);
         return fail(RBC_ENOMEM, "tc list operands allocation");
     }
     if (bytes)
-        *bytes += rows * (kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (nr + 1) * sizeof(int64_t) +
-                  nr * (66 * sizeof(float));
-    if (cudaMemsetAsync(tc->xh0, 0, rows * kP0, st) != cudaSuccess ||
+        *bytes += rows * (np * kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (nr + 1) * sizeof(int64_t) +
+                  nr * ((64 * np + 2) * sizeof(float));
+    if (cudaMemsetAsync(tc->xh0, 0, np * rows * kP0, st) != cudaSuccess ||
         (tc->plane1 && cudaMemsetAsync(tc->xh1, 0, rows * kP1, st) != cudaSuccess) ||
         cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
         cudaMemsetAsync(tc->dbmax, 0, nr * sizeof(float), st) != cudaSuccess ||
@@ -1169,10 +1230,11 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
         return fail(RBC_ECUDA, "tc list operands init");
     }
     list_scale_kernel<<<grid_for(nr, 256), 256, 0, st>>>(radii, nr, tc->sB);
-    pad64_rows_kernel<<<grid_for(nr * 64, 256), 256, 0, st>>>(reps, nr, d, tc->reps64);
+    pad64_rows_kernel<<<grid_for(nr * 64 * np, 256), 256, 0, st>>>(reps, nr, d, tc->reps64, 64 * np);
     const unsigned ysplit = static_cast<unsigned>(maxlen > 256 * 148 ? 148 : (maxlen + 255) / 256 + 0);
     residual_rows_kernel<<<dim3(static_cast<unsigned>(nr), ysplit > 0 ? ysplit : 1), 256, 0, st>>>(
-        xp, reps, offsets_dev, tc->poff, tc->sB, d, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol, tc->dbmax);
+        xp, reps, offsets_dev, tc->poff, tc->sB, d, np, rows * kP0, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol,
+        tc->dbmax);
     note_launch(3);
     if (cudaGetLastError() != cudaSuccess) {
         tc_free(tc);
@@ -1183,7 +1245,7 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
 }
 
 int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
-    if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->n_local == 0) return RBC_OK;
+    if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 128 || idx->n_local == 0) return RBC_OK;
     if (idx->n_local + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 work offsets
     std::vector<int64_t> off(idx->nr + 1);
     RBC_CUDA(cudaMemcpyAsync(off.data(), idx->offsets, sizeof(int64_t) * (idx->nr + 1), cudaMemcpyDeviceToHost, st));
@@ -1313,11 +1375,14 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
 }
 
 // stage-2 kernel + exact re-rank + overflow scan + status over prepared work arrays
+static std::atomic<int64_t> g_tc_scan_calls{0};
+
 static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, const int32_t *order,
                   int ntiles, const int32_t *tile_order, const int64_t *work_off, const int64_t *nwork,
                   const unsigned long long *work_total, const WorkItem *work, const int32_t *cut, int64_t cap_work,
                   int32_t *cand_count, int32_t *counters, uint64_t *keys, int64_t *status_dev, cudaStream_t st,
                   int cap_groups) {
+    g_tc_scan_calls.fetch_add(1);
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
     // 3. the tensor-core scan
     const int cap = cap_groups > 0 ? cap_groups : 12 + 6 * k;  // 8-column groups per query and column part
@@ -1328,14 +1393,16 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
     RBC_CHECK(cand_ufin.alloc(nq * kParts, st));
     RBC_CHECK(ovf_list.alloc(nq * kParts, st));
     const float *q64 = q;
-    if (idx->d != 64 || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
-        RBC_CHECK(q64buf.alloc(nq * 64, st));
-        pad64_rows_kernel<<<grid_for(nq * 64, 256), 256, 0, st>>>(q, nq, idx->d, q64buf.get());
+    const int qw = 64 * tc->np;
+    if (idx->d != qw || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
+        RBC_CHECK(q64buf.alloc(nq * qw, st));
+        pad64_rows_kernel<<<grid_for(nq * qw, 256), 256, 0, st>>>(q, nq, idx->d, q64buf.get(), qw);
         RBC_LAUNCHED();
         q64 = q64buf.get();
     }
     S2Params P;
     P.xh0 = tc->xh0;
+    P.plane_bytes = tc->rows * kP0;
     P.xh1 = tc->xh1;
     P.gcol = tc->gcol;
     P.reps64 = tc->reps64;
@@ -1377,16 +1444,25 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
-    auto launch = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-        kern<<<grid, kThreads, kSmemBytes, st>>>(P);
+    auto launch = [&](auto kern, size_t smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kThreads, smem, st>>>(P);
     };
     {
         ProfScope ps(kPhaseScan, st);
-        if (k == 1) launch(stage2_tc_kernel<1>);
-        else if (k <= 4) launch(stage2_tc_kernel<4>);
-        else if (k <= 8) launch(stage2_tc_kernel<8>);
-        else launch(stage2_tc_kernel<16>);
+        if (tc->np == 1) {
+            constexpr size_t sm = S2Cfg<1>::kSmem;
+            if (k == 1) launch(stage2_tc_kernel<1, 1>, sm);
+            else if (k <= 4) launch(stage2_tc_kernel<4, 1>, sm);
+            else if (k <= 8) launch(stage2_tc_kernel<8, 1>, sm);
+            else launch(stage2_tc_kernel<16, 1>, sm);
+        } else {
+            constexpr size_t sm = S2Cfg<2>::kSmem;
+            if (k == 1) launch(stage2_tc_kernel<1, 2>, sm);
+            else if (k <= 4) launch(stage2_tc_kernel<4, 2>, sm);
+            else if (k <= 8) launch(stage2_tc_kernel<8, 2>, sm);
+            else launch(stage2_tc_kernel<16, 2>, sm);
+        }
     }
     RBC_LAUNCHED();
     // 4. exact re-rank of the buffered candidates
@@ -1429,6 +1505,24 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
         }
         fprintf(stderr, "[s2] cap %d: groups mean %.2f max %lld, overflowed parts %lld of %lld\n", cap,
                 double(sum) / double(cc.size() - ovf + 1e-9), (long long)mx, (long long)ovf, (long long)cc.size());
+        // MMA work: columns scanned per tile (chunks rounded to 16) x 128 rows, and the tile spread
+        std::vector<int64_t> nw(ntiles), wo(ntiles);
+        unsigned long long wt = 0;
+        cudaMemcpy(nw.data(), nwork, sizeof(int64_t) * ntiles, cudaMemcpyDeviceToHost);
+        cudaMemcpy(wo.data(), work_off, sizeof(int64_t) * ntiles, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&wt, work_total, sizeof(wt), cudaMemcpyDeviceToHost);
+        std::vector<WorkItem> wi(wt);
+        cudaMemcpy(wi.data(), work, sizeof(WorkItem) * wt, cudaMemcpyDeviceToHost);
+        double cols = 0, tmax = 0, items = 0;
+        for (int t = 0; t < ntiles; ++t) {
+            double tc = 0;
+            for (int64_t w = wo[t]; w < wo[t] + nw[t]; ++w) tc += (wi[w].ext + 15) / 16 * 16;
+            cols += tc;
+            items += nw[t];
+            tmax = tc > tmax ? tc : tmax;
+        }
+        fprintf(stderr, "[s2] tiles %d: work items/tile %.1f, MMA pairs %.4g (cols/tile mean %.0f max %.0f)\n", ntiles,
+                items / ntiles, cols * 128, cols / ntiles, tmax);
     }
 #ifdef RBC_S2_TIMING
     if (getenv("RBC_DEBUG_S2")) {  // diagnostic: role timing (synchronises)
@@ -1459,10 +1553,10 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
 namespace {
 
 __global__ void bf_colsum_kernel(const float *__restrict__ x, int64_t n, int d, double *__restrict__ sum) {
-    const int k = threadIdx.x & 63, sub = threadIdx.x >> 6;
+    const int k = threadIdx.x & 127, sub = threadIdx.x >> 7;
     if (k >= d) return;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * 4ll + sub; i < n; i += gridDim.x * 4ll) acc += x[i * d + k];
+    for (int64_t i = blockIdx.x * 2ll + sub; i < n; i += gridDim.x * 2ll) acc += x[i * d + k];
     atomicAdd(&sum[k], acc);
 }
 
@@ -1531,7 +1625,7 @@ __global__ void iota_i32_kernel(int32_t *__restrict__ a, int64_t n) {
 bool tc_bf_supported(int64_t nq, int64_t n, int d, int metric, int k) {
     // one list centred on the mean: tight enough when the points are few (representative
     // sets); large point sets use the partitioned operand (tc_bf_index_search)
-    if (metric != RBC_L2 || d < 1 || d > 64 || k < 1 || k > 16 || n < k || n > 65536) return false;
+    if (metric != RBC_L2 || d < 1 || d > 128 || k < 1 || k > 16 || n < k || n > 65536) return false;
     if (n + kTailRows + 8 >= (int64_t(1) << 31)) return false;  // int32 positions
     return nq * n >= (int64_t(1) << 16);  // smaller problems: the exact SIMT scan is as fast
 }
@@ -1546,15 +1640,15 @@ int tc_bf_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int
     DevBuf<int64_t> offsets;
     DevBuf<int32_t> perm;
     DevBuf<unsigned> rbits;
-    RBC_CHECK(csum.alloc(64, st));
-    RBC_CHECK(cen.alloc(64, st));
+    RBC_CHECK(csum.alloc(128, st));
+    RBC_CHECK(cen.alloc(128, st));
     RBC_CHECK(rad.alloc(1, st));
     RBC_CHECK(offsets.alloc(2, st));
     RBC_CHECK(perm.alloc(n, st));
-    RBC_CUDA(cudaMemsetAsync(csum.get(), 0, 64 * sizeof(double), st));
+    RBC_CUDA(cudaMemsetAsync(csum.get(), 0, 128 * sizeof(double), st));
     RBC_CUDA(cudaMemsetAsync(rad.get(), 0, sizeof(float), st));
-    bf_colsum_kernel<<<grid_for(n, 4, 148 * 8), 256, 0, st>>>(x, n, d, csum.get());
-    bf_centre_kernel<<<1, 64, 0, st>>>(csum.get(), n, d, cen.get(), offsets.get());
+    bf_colsum_kernel<<<grid_for(n, 2, 148 * 8), 256, 0, st>>>(x, n, d, csum.get());
+    bf_centre_kernel<<<1, 128, 0, st>>>(csum.get(), n, d, cen.get(), offsets.get());
     bf_extent_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(x, n, d, cen.get(),
                                                                reinterpret_cast<unsigned *>(rad.get()));
     iota_i32_kernel<<<grid_for(n, 256), 256, 0, st>>>(perm.get(), n);
@@ -1785,10 +1879,10 @@ int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, 
     note_launch();
     // 3. |q - c|, |r_p - c| for the A scales
     DevBuf<float> cen, qdc, rdc;
-    RBC_CHECK(cen.alloc(64, st));
+    RBC_CHECK(cen.alloc(128, st));
     RBC_CHECK(qdc.alloc(nq, st));
     RBC_CHECK(rdc.alloc(nr, st));
-    bf_rep_centre_kernel<<<1, 64, 0, st>>>(idx->reps, nr, d, cen.get());
+    bf_rep_centre_kernel<<<1, 128, 0, st>>>(idx->reps, nr, d, cen.get());
     row_dist_kernel<<<grid_for(nq, 256), 256, 0, st>>>(q, nq, d, cen.get(), qdc.get());
     row_dist_kernel<<<grid_for(nr, 256), 256, 0, st>>>(idx->reps, nr, d, cen.get(), rdc.get());
     RBC_LAUNCHED();
@@ -1831,3 +1925,4 @@ int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, 
 }  // namespace rbc
 
 extern "C" int64_t rbc_tc_bf_calls(void) { return rbc::g_tc_bf_calls.load(); }
+extern "C" int64_t rbc_tc_scan_calls(void) { return rbc::g_tc_scan_calls.load(); }

@@ -141,22 +141,22 @@ def _prepared_search(rbc, x, q, kind, k):
     try:
         ids = torch.empty((q.shape[0], k), dtype=torch.int64, device="cuda")
         ds = torch.empty((q.shape[0], k), dtype=torch.float32, device="cuda")
+        c0 = _calls()
         _lib.check(_lib.lib.rbc_bf_search_prepared(h, _lib.ptr(q_dev), q.shape[0], k, _lib.ptr(ids), _lib.ptr(ds), sp),
                    "search")
-        return ids.cpu().numpy(), ds.cpu().numpy()
+        return ids.cpu().numpy(), ds.cpu().numpy(), _calls() > c0
     finally:
         _lib.lib.rbc_index_destroy(h)
 
 
 @pytest.mark.parametrize("d,kind,k", [(64, "l2", 1), (64, "l2", 16), (21, "l2", 5), (7, "l2", 3), (21, "l1", 4),
-                                      (100, "l2", 2), (64, "l2", 40)])
+                                      (100, "l2", 2), (64, "l2", 40), (160, "l2", 3)])
 def test_tc_bf_prepared_vs_oracle(rbc, oracle, d, kind, k):
-    # the prepared operand: partitioned tcgen05 scan for L2 d <= 64 k <= 16, else the exact SIMT scan
+    # the prepared operand: partitioned tcgen05 scan for L2 d <= 128 k <= 16, else the exact SIMT scan
     full = oracle.gen_clusters(70_000 + 700, d, 17 + d, n_clusters=12, cluster_sigma=0.05)
     x, q = full[:70_000], full[70_000:]
-    c0 = _calls()
-    ids, dists = _prepared_search(rbc, x, q, kind, k)
-    assert (_calls() > c0) == (kind == "l2" and d <= 64 and k <= 16)
+    ids, dists, tc_ran = _prepared_search(rbc, x, q, kind, k)
+    assert tc_ran == (kind == "l2" and d <= 128 and k <= 16)
     oi, od = oracle.bf_topk(q, x, k, kind)
     assert np.array_equal(ids, oi) and np.array_equal(dists, od)
 
@@ -167,3 +167,37 @@ def test_tc_bf_prepared_rejects_wrong_handle(rbc):
     from paper_1103_2635_b200 import _lib
 
     assert _lib.lib.rbc_bf_search_prepared(None, None, 1, 1, None, None, None) != 0
+
+
+def _scans():
+    from paper_1103_2635_b200 import _lib
+
+    return _lib.lib.rbc_tc_scan_calls()
+
+
+@pytest.mark.parametrize("d", [65, 96, 126, 127, 128])
+@pytest.mark.parametrize("k", [1, 10])
+def test_tc_stage2_wide_d_vs_oracle(rbc, oracle, d, k):
+    # d in (64, 128]: two K planes (and the separate aug plane for d > 126) on the tensor cores
+    full = oracle.gen_clusters(30_000 + 500, d, 5 + d, n_clusters=8, cluster_sigma=0.05)
+    x, q = full[:30_000], full[30_000:]
+    idx = rbc.build_exact(rbc.DataMatrix(x), 173, rbc.MetricSpec("l2", d), seed=3)
+    s0 = _scans()
+    got = rbc.exact_query_arrays(idx, q, k)
+    assert _scans() > s0, "stage 2 did not run on the tensor cores"
+    li, off, ld = idx.flat_lists()
+    want = oracle.exact_query(x, idx.reps.rep_ids, li, off, ld, idx.radii, q, k)
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g).astype(np.asarray(w).dtype), w)
+
+
+@pytest.mark.parametrize("d", [100, 128])
+def test_tc_bf_wide_d_vs_oracle(rbc, oracle, d):
+    x = oracle.gen_clusters(80_000, d, 9 + d, n_clusters=8, cluster_sigma=0.05)
+    q = np.concatenate([uniform(500, d, d), x[::400] + np.float32(0.001)]).astype(np.float32)
+    for k in (1, 5, 16):
+        c0 = _calls()
+        ids, dists = rbc.brute_force.bf_search_arrays(q, x, rbc.MetricSpec("l2", d), k)
+        assert _calls() > c0
+        oi, od = oracle.bf_topk(q, x, k, "l2")
+        assert np.array_equal(ids, oi) and np.array_equal(dists, od)
