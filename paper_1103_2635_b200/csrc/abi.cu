@@ -464,7 +464,7 @@ int rbc_bf_search_subsets(const float *q, int64_t nq, const float *x, int64_t n,
                           const int64_t *subset_ids, const int64_t *subset_offsets, int64_t *ids, float *dists,
                           void *stream) {
     RBC_CHECK(check_common(n, d, metric));
-    if (k < 1 || k > kMaxWarpK) return fail(RBC_EINVAL, "subset scan supports 1 <= k <= 64");
+    if (k < 1) return fail(RBC_EINVAL, "k must be >= 1");
     cudaStream_t st = as_stream(stream);
     DevBuf<uint64_t> keys;
     RBC_CHECK(keys.alloc(nq * k, st));
@@ -571,7 +571,7 @@ int64_t rbc_index_device_bytes(const rbc_index *idx) { return idx ? static_cast<
 int rbc_exact_search_keys(const rbc_index *idx, const float *q, int64_t nq, int32_t k, uint64_t *keys,
                           rbc_search_stats stats, void *stream) {
     if (!idx || idx->kind != 0) return fail(RBC_EINVAL, "not an exact index");
-    if (k < 1 || k > idx->nr || k > kMaxWarpK) return fail(RBC_EINVAL, "k must be in [1, min(|R|, 64)]");
+    if (k < 1 || k > idx->nr) return fail(RBC_EINVAL, "k must be in [1, |R|]");
     return exact_search_keys(idx, q, nq, k, keys, stats, as_stream(stream));
 }
 
@@ -587,7 +587,7 @@ int rbc_exact_search(const rbc_index *idx, const float *q, int64_t nq, int32_t k
 int rbc_one_shot_search(const rbc_index *idx, const float *q, int64_t nq, int32_t k, int64_t *ids, float *dists,
                         float *gamma, void *stream) {
     if (!idx || idx->kind != 1) return fail(RBC_EINVAL, "not a one-shot index");
-    if (k < 1 || k > idx->s || k > kMaxWarpK) return fail(RBC_EINVAL, "k must be in [1, min(s, 64)]");
+    if (k < 1 || k > idx->s) return fail(RBC_EINVAL, "k must be in [1, s]");
     cudaStream_t st = as_stream(stream);
     DevBuf<uint64_t> keys;
     RBC_CHECK(keys.alloc(nq * k, st));

@@ -11,6 +11,8 @@
 
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -115,6 +117,123 @@ static int launch_topk_kt(const float *q, int64_t nq, int d, int metric, int k, 
     return RBC_OK;
 }
 
+// ---- k > 64: every candidate key of a query batch, segmented radix sort ------------------
+// The reference accepts any k <= |R| (exact, search.py:167-170) or k <= s (one-shot,
+// search.py:104-105).  Above the register top-k width the candidates' exact keys are
+// materialised per query (batches of <= 2^27 keys), sorted per query with CUB, and the
+// first k kept (missing entries = empty keys when a query has fewer than k candidates).
+template <class Src>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) count_cand_kernel(int64_t nq, Src src, int64_t *__restrict__ cnt) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + w;
+    if (i >= nq) return;
+    int64_t c = 0;
+    src.for_each(i, lane, [&](const float *, uint32_t) { ++c; });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[i] = c;
+}
+
+template <int METRIC, class Src>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) cand_keys_kernel(const float *__restrict__ q, int64_t q0,
+                                                                        int64_t rows, int d, Src src,
+                                                                        const int64_t *__restrict__ off,
+                                                                        uint64_t *__restrict__ keys) {
+    extern __shared__ float qs_all[];
+    __shared__ unsigned long long pos[kWarpsPerBlock];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + w;
+    if (r >= rows) return;
+    const int64_t i = q0 + r;
+    float *qs = qs_all + w * d;
+    for (int c = lane; c < d; c += 32) qs[c] = q[i * d + c];
+    if (lane == 0) pos[w] = 0;
+    __syncwarp();
+    uint64_t *dst = keys + (off[i] - off[q0]);
+    src.for_each(i, lane, [&](const float *__restrict__ row, uint32_t id) {
+        const unsigned long long p = atomicAdd(&pos[w], 1ull);
+        dst[p] = pack_key(exact_dist<METRIC>(qs, row, d), id);
+    });
+}
+
+__global__ void rebase_offsets_kernel(const int64_t *__restrict__ off, int64_t q0, int64_t rows,
+                                      int64_t *__restrict__ out) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t <= rows) out[t] = off[q0 + t] - off[q0];
+}
+
+__global__ void take_k_kernel(const uint64_t *__restrict__ sorted, const int64_t *__restrict__ off, int64_t q0,
+                              int64_t rows, int k, uint64_t *__restrict__ out) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= rows * k) return;
+    const int64_t r = t / k, j = t % k;
+    const int64_t a = off[q0 + r] - off[q0], n = off[q0 + r + 1] - off[q0 + r];
+    out[(q0 + r) * k + j] = j < n ? sorted[a + j] : kEmptyKey;
+}
+
+template <class Src>
+static int topk_large(const float *q, int64_t nq, int d, int metric, int k, const Src &src, uint64_t *out,
+                      cudaStream_t st) {
+    const size_t qsmem = sizeof(float) * kWarpsPerBlock * d;
+    if (qsmem > 48 * 1024) return fail(RBC_EINVAL, "dimension too large for the exact scan kernel");
+    DevBuf<int64_t> cnt, off;
+    RBC_CHECK(cnt.alloc(nq, st));
+    RBC_CHECK(off.alloc(nq + 1, st));
+    count_cand_kernel<Src><<<grid_for(nq, kWarpsPerBlock), kWarpsPerBlock * 32, 0, st>>>(nq, src, cnt.get());
+    RBC_LAUNCHED();
+    RBC_CUDA(cudaMemsetAsync(off.get(), 0, sizeof(int64_t), st));
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, cnt.get(), off.get() + 1, nq, st);
+    {
+        DevBuf<unsigned char> tmp;
+        RBC_CHECK(tmp.alloc(tb, st));
+        RBC_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, cnt.get(), off.get() + 1, nq, st));
+    }
+    std::vector<int64_t> h(nq + 1);
+    RBC_CUDA(cudaMemcpyAsync(h.data(), off.get(), sizeof(int64_t) * (nq + 1), cudaMemcpyDeviceToHost, st));
+    RBC_CUDA(cudaStreamSynchronize(st));
+    const int64_t budget = int64_t(1) << 27;  // keys per batch (1 GiB of key64)
+    int64_t maxb = 0;
+    for (int64_t q0 = 0; q0 < nq;) {  // largest batch, for the buffer sizes
+        int64_t q1 = q0 + 1;
+        while (q1 < nq && q1 - q0 < 65535 && h[q1 + 1] - h[q0] <= budget) ++q1;
+        maxb = h[q1] - h[q0] > maxb ? h[q1] - h[q0] : maxb;
+        q0 = q1;
+    }
+    DevBuf<uint64_t> keys, sorted;
+    DevBuf<int64_t> boff;
+    RBC_CHECK(keys.alloc(maxb, st));
+    RBC_CHECK(sorted.alloc(maxb, st));
+    RBC_CHECK(boff.alloc(65536, st));
+    for (int64_t q0 = 0; q0 < nq;) {
+        int64_t q1 = q0 + 1;
+        while (q1 < nq && q1 - q0 < 65535 && h[q1 + 1] - h[q0] <= budget) ++q1;
+        const int64_t rows = q1 - q0, total = h[q1] - h[q0];
+        if (metric == RBC_L2)
+            cand_keys_kernel<RBC_L2, Src><<<grid_for(rows, kWarpsPerBlock), kWarpsPerBlock * 32, qsmem, st>>>(
+                q, q0, rows, d, src, off.get(), keys.get());
+        else
+            cand_keys_kernel<RBC_L1, Src><<<grid_for(rows, kWarpsPerBlock), kWarpsPerBlock * 32, qsmem, st>>>(
+                q, q0, rows, d, src, off.get(), keys.get());
+        RBC_LAUNCHED();
+        rebase_offsets_kernel<<<grid_for(rows + 1, 256), 256, 0, st>>>(off.get(), q0, rows, boff.get());
+        RBC_LAUNCHED();
+        size_t sb = 0;
+        cub::DeviceSegmentedRadixSort::SortKeys(nullptr, sb, keys.get(), sorted.get(), total, static_cast<int>(rows),
+                                                boff.get(), boff.get() + 1, 0, 64, st);
+        DevBuf<unsigned char> tmp;
+        RBC_CHECK(tmp.alloc(sb, st));
+        RBC_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(tmp.get(), sb, keys.get(), sorted.get(), total,
+                                                         static_cast<int>(rows), boff.get(), boff.get() + 1, 0, 64,
+                                                         st));
+        note_launch();
+        take_k_kernel<<<grid_for(rows * k, 256), 256, 0, st>>>(sorted.get(), off.get(), q0, rows, k, out);
+        RBC_LAUNCHED();
+        q0 = q1;
+    }
+    return RBC_OK;
+}
+
 template <class Src>
 int launch_topk(const float *q, int64_t nq, int d, int metric, int k, const Src &src, uint64_t *out,
                 cudaStream_t st) {
@@ -123,7 +242,7 @@ int launch_topk(const float *q, int64_t nq, int d, int metric, int k, const Src 
     if (k <= 4) return launch_topk_kt<Src, 4>(q, nq, d, metric, k, src, out, st);
     if (k <= 16) return launch_topk_kt<Src, 16>(q, nq, d, metric, k, src, out, st);
     if (k <= kMaxWarpK) return launch_topk_kt<Src, kMaxWarpK>(q, nq, d, metric, k, src, out, st);
-    return fail(RBC_EINVAL, "launch_topk: k too large for the warp path");
+    return topk_large(q, nq, d, metric, k, src, out, st);
 }
 
 template int launch_topk<AllSrc>(const float *, int64_t, int, int, int, const AllSrc &, uint64_t *, cudaStream_t);

@@ -220,12 +220,12 @@ def local_shard_keys(sh: ShardedExactIndex, q_dev, nq: int, k: int):
 
 def exact_query_sharded(sh: ShardedExactIndex, queries, k: int = 1, group=None):
     """Exact k-NN over the rep-sharded index: local scan + key merge (same outputs as exact_query_arrays)."""
-    from .search import MAX_K, _queries
+    from .search import _queries
 
     qv = _queries(queries)
     n_reps = sh.index.reps.size
-    if not 1 <= k <= min(n_reps, MAX_K):
-        raise ValueError(f"k must be in [1, {min(n_reps, MAX_K)}], got {k}")
+    if not 1 <= k <= n_reps:
+        raise ValueError(f"k must be in [1, |R|={n_reps}], got {k}")
     if qv.shape[1] != sh.index.metric.dim:
         raise ValueError(f"dimension mismatch: queries d={qv.shape[1]}, metric dim={sh.index.metric.dim}")
     nq = qv.shape[0]

@@ -21,7 +21,7 @@ from . import _lib
 from .brute_force import NeighborList, resolve_workers
 from .rbc import RbcExactIndex, RbcOneShotIndex, device_index
 
-MAX_K = 64
+MAX_K = None  # no cap: k > 64 runs the exact materialise-and-sort top-k (csrc/exact_kernels.cu topk_large)
 
 
 @dataclass
@@ -81,8 +81,6 @@ def exact_query_arrays(index: RbcExactIndex, queries, k: int = 1, q_dev=None):
         raise ValueError(f"k must be in [1, |R|={n_reps}] so the stage-1 bound exists, got {k}")
     if k > index.data.n:
         raise ValueError(f"k={k} exceeds database size {index.data.n}")
-    if k > MAX_K:
-        raise ValueError(f"k={k} above the supported maximum {MAX_K}")
     if qv.shape[1] != index.metric.dim:
         raise ValueError(f"dimension mismatch: queries d={qv.shape[1]}, metric dim={index.metric.dim}")
     t = _lib.require_cuda()
@@ -130,8 +128,6 @@ def one_shot_query_arrays(index: RbcOneShotIndex, queries, k: int = 1, q_dev=Non
     qv = _queries(queries)
     if not 1 <= k <= index.s:
         raise ValueError(f"k must be in [1, s={index.s}], got {k}")
-    if k > MAX_K:
-        raise ValueError(f"k={k} above the supported maximum {MAX_K}")
     if qv.shape[1] != index.metric.dim:
         raise ValueError(f"dimension mismatch: queries d={qv.shape[1]}, metric dim={index.metric.dim}")
     t = _lib.require_cuda()
