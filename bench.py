@@ -89,7 +89,7 @@ def gen_inputs(rank: int):
 
 def kt_of(k: int) -> int:
     """Template width of the stage-2 / re-rank kernels serving k (tc_stage2.cu launch dispatch)."""
-    return 1 if k == 1 else 4 if k <= 4 else 8 if k <= 8 else 16
+    return 1 if k == 1 else 4 if k <= 4 else 8 if k <= 8 else 16 if k <= 16 else 32
 
 
 def ncu_traffic(kernel: str, cfg: str):
@@ -490,7 +490,7 @@ def main():
     flops_per_step = 2.0 * D * evals
     scan_work = 2.0 * D * NQ * mean_cand  # the dominant kernel's algorithmic work per launch
     if CFG["metric"] == "l2":
-        kname = f"stage2_tc_kernel<{kt_of(K)}>" if exact else f"oneshot scan (k={K})"
+        kname = f"stage2_tc_kernel<{kt_of(K)}, {1 if D <= 64 else 2}>" if exact else f"oneshot scan (k={K})"
         traffic = ncu_traffic(kname, args.config)
         achieved = scan_work * scan_n / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
         roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["tensor"], "unit": "TFLOP/s",

@@ -318,7 +318,7 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
 // nearby centre (tight f16 error bounds); every list is still scanned for every query.
 // Otherwise the operand is a plain device copy of the points for the exact SIMT scan.
 bool bf_partition_pays(int64_t nq, int64_t n, int d, int metric, int k) {
-    return metric == RBC_L2 && d <= 128 && k <= 16 && n > 65536 && nq >= 512 && n + 4096 < (int64_t(1) << 31);
+    return metric == RBC_L2 && d <= 128 && k <= 32 && n > 65536 && nq >= 512 && n + 4096 < (int64_t(1) << 31);
 }
 
 int bf_prepare(const float *x, int64_t n, int d, int metric, rbc_index **out, cudaStream_t st) {
@@ -442,7 +442,7 @@ int rbc_bf_search_prepared(const rbc_index *bf, const float *q, int64_t nq, int3
     cudaStream_t st = as_stream(stream);
     DevBuf<uint64_t> keys;
     RBC_CHECK(keys.alloc(nq * k, st));
-    if (bf->tc && k <= 16 && !force_exact_engine())
+    if (bf->tc && k <= 32 && !force_exact_engine())
         RBC_CHECK(tc_bf_index_search(bf, q, nq, k, keys.get(), st));
     else
         RBC_CHECK(bf_search_keys(q, nq, bf->x, bf->n, bf->d, bf->metric, k, keys.get(), st));

@@ -1271,7 +1271,7 @@ void tc_index_release(rbc_index *idx) {
 constexpr int64_t kMaxRepsTileFill = (200 * 1024) / (3 * sizeof(int32_t));
 
 bool tc_stage2_supported(const rbc_index *idx, int k) {
-    return idx->tc != nullptr && k <= 16 && idx->nr <= kMaxRepsTileFill;
+    return idx->tc != nullptr && k <= 32 && idx->nr <= kMaxRepsTileFill;
 }
 
 static int g_num_sms = 0;
@@ -1455,13 +1455,15 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
             if (k == 1) launch(stage2_tc_kernel<1, 1>, sm);
             else if (k <= 4) launch(stage2_tc_kernel<4, 1>, sm);
             else if (k <= 8) launch(stage2_tc_kernel<8, 1>, sm);
-            else launch(stage2_tc_kernel<16, 1>, sm);
+            else if (k <= 16) launch(stage2_tc_kernel<16, 1>, sm);
+            else launch(stage2_tc_kernel<32, 1>, sm);
         } else {
             constexpr size_t sm = S2Cfg<2>::kSmem;
             if (k == 1) launch(stage2_tc_kernel<1, 2>, sm);
             else if (k <= 4) launch(stage2_tc_kernel<4, 2>, sm);
             else if (k <= 8) launch(stage2_tc_kernel<8, 2>, sm);
-            else launch(stage2_tc_kernel<16, 2>, sm);
+            else if (k <= 16) launch(stage2_tc_kernel<16, 2>, sm);
+            else launch(stage2_tc_kernel<32, 2>, sm);
         }
     }
     RBC_LAUNCHED();
@@ -1476,7 +1478,8 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
         if (k == 1) RBC_RERANK(1);
         else if (k <= 4) RBC_RERANK(4);
         else if (k <= 8) RBC_RERANK(8);
-        else RBC_RERANK(16);
+        else if (k <= 16) RBC_RERANK(16);
+        else RBC_RERANK(32);
 #undef RBC_RERANK
         RBC_LAUNCHED();
     }
@@ -1489,7 +1492,8 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
         if (k == 1) overflow_scan_kernel<1><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
         else if (k <= 4) overflow_scan_kernel<4><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
         else if (k <= 8) overflow_scan_kernel<8><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
-        else overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
+        else if (k <= 16) overflow_scan_kernel<16><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
+        else overflow_scan_kernel<32><<<ogrid, 256, 0, st>>>(q, idx->d, ovf_list.get(), counters, src, k, keys);
         RBC_LAUNCHED();
     }
     stage2_status_kernel<<<1, 1, 0, st>>>(work_total, counters, status_dev);
@@ -1625,7 +1629,7 @@ __global__ void iota_i32_kernel(int32_t *__restrict__ a, int64_t n) {
 bool tc_bf_supported(int64_t nq, int64_t n, int d, int metric, int k) {
     // one list centred on the mean: tight enough when the points are few (representative
     // sets); large point sets use the partitioned operand (tc_bf_index_search)
-    if (metric != RBC_L2 || d < 1 || d > 128 || k < 1 || k > 16 || n < k || n > 65536) return false;
+    if (metric != RBC_L2 || d < 1 || d > 128 || k < 1 || k > 32 || n < k || n > 65536) return false;
     if (n + kTailRows + 8 >= (int64_t(1) << 31)) return false;  // int32 positions
     return nq * n >= (int64_t(1) << 16);  // smaller problems: the exact SIMT scan is as fast
 }
@@ -1841,7 +1845,7 @@ __global__ void __launch_bounds__(kRows) bf_tile_fill_kernel(
 int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, cudaStream_t st) {
     if (nq == 0) return RBC_OK;
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
-    if (!tc || k < 1 || k > 16) return fail(RBC_EINVAL, "tc brute force: unsupported index or k");
+    if (!tc || k < 1 || k > 32) return fail(RBC_EINVAL, "tc brute force: unsupported index or k");
     g_tc_bf_calls.fetch_add(1);
     const int64_t nr = idx->nr, n = idx->n_local;
     const int d = idx->d;

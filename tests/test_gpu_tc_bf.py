@@ -44,7 +44,7 @@ def _exact_engine(rbc, fn):
 
 
 @pytest.mark.parametrize("d", [1, 5, 16, 21, 54, 62, 63, 64])
-@pytest.mark.parametrize("k", [1, 4, 10, 16])
+@pytest.mark.parametrize("k", [1, 4, 10, 16, 32])
 def test_tc_bf_vs_oracle(rbc, oracle, d, k):
     x = oracle.gen_clusters(6000, d, 11 + d, n_clusters=7, cluster_sigma=0.08)
     q = np.concatenate([uniform(90, d, 5 * d), x[::200] + np.float32(0.001)]).astype(np.float32)
@@ -156,7 +156,7 @@ def test_tc_bf_prepared_vs_oracle(rbc, oracle, d, kind, k):
     full = oracle.gen_clusters(70_000 + 700, d, 17 + d, n_clusters=12, cluster_sigma=0.05)
     x, q = full[:70_000], full[70_000:]
     ids, dists, tc_ran = _prepared_search(rbc, x, q, kind, k)
-    assert tc_ran == (kind == "l2" and d <= 128 and k <= 16)
+    assert tc_ran == (kind == "l2" and d <= 128 and k <= 32)
     oi, od = oracle.bf_topk(q, x, k, kind)
     assert np.array_equal(ids, oi) and np.array_equal(dists, od)
 
@@ -201,3 +201,18 @@ def test_tc_bf_wide_d_vs_oracle(rbc, oracle, d):
         assert _calls() > c0
         oi, od = oracle.bf_topk(q, x, k, "l2")
         assert np.array_equal(ids, oi) and np.array_equal(dists, od)
+
+
+@pytest.mark.parametrize("k", [17, 24, 32])
+@pytest.mark.parametrize("d", [20, 64, 100])
+def test_tc_stage2_k_up_to_32_vs_oracle(rbc, oracle, k, d):
+    full = oracle.gen_clusters(30_000 + 400, d, 2 + d, n_clusters=10, cluster_sigma=0.05)
+    x, q = full[:30_000], full[30_000:]
+    idx = rbc.build_exact(rbc.DataMatrix(x), 173, rbc.MetricSpec("l2", d), seed=5)
+    s0 = _scans()
+    got = rbc.exact_query_arrays(idx, q, k)
+    assert _scans() > s0, "stage 2 did not run on the tensor cores"
+    li, off, ld = idx.flat_lists()
+    want = oracle.exact_query(x, idx.reps.rep_ids, li, off, ld, idx.radii, q, k)
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g).astype(np.asarray(w).dtype), w)
