@@ -528,7 +528,7 @@ def main():
         torch.cuda.synchronize()
         t_prep = time.perf_counter() - t_prep
         launches0 = _lib.lib.rbc_tc_bf_calls()
-        times = []
+        bf_times = []
         for it in range(3):
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -537,8 +537,8 @@ def main():
                        "bf")
             ev1.record(stream)
             ev1.synchronize()
-            times.append(ev0.elapsed_time(ev1) / 1e3)
-        dt = statistics.median(times[1:])
+            bf_times.append(ev0.elapsed_time(ev1) / 1e3)
+        dt = statistics.median(bf_times[1:])
         tc_used = _lib.lib.rbc_tc_bf_calls() > launches0
         _lib.lib.rbc_index_destroy(bfh)
         bf_flops = 2.0 * D * m * N  # algorithmic: every (query, point) pair, 2 d flops

@@ -70,8 +70,9 @@ int rbc_profile_enable(int on);
 int rbc_profile_read(double *ms, int64_t *count, int32_t n_phases);
 
 /* Engine selection for the heavy scans: 0 = auto (tcgen05 filter + exact
- * fp64 re-rank where supported, the default), 1 = exact fp64 SIMT only.
- * Both produce identical results; 1 exists for A/B checks. */
+ * fp64 re-rank where supported and the scan is large enough to pay, the
+ * default), 1 = exact fp64 SIMT only, 2 = tcgen05 wherever supported, at any
+ * size.  All produce identical results; 1 and 2 exist for A/B checks. */
 int rbc_set_engine(int mode);
 /* Queries of the last exact search whose candidate buffer overflowed and
  * were recomputed by the exact SIMT scan (diagnostic). */

@@ -318,7 +318,8 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
 // nearby centre (tight f16 error bounds); every list is still scanned for every query.
 // Otherwise the operand is a plain device copy of the points for the exact SIMT scan.
 bool bf_partition_pays(int64_t nq, int64_t n, int d, int metric, int k) {
-    return metric == RBC_L2 && d <= 128 && k <= 32 && n > 65536 && nq >= 512 && n + 4096 < (int64_t(1) << 31);
+    return metric == RBC_L2 && d <= 128 && k <= 32 && n > 65536 && nq >= 512 && nq * n >= tc_min_pairs() &&
+           n + 4096 < (int64_t(1) << 31);
 }
 
 int bf_prepare(const float *x, int64_t n, int d, int metric, rbc_index **out, cudaStream_t st) {
@@ -544,6 +545,20 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
         if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
             rc = fail(RBC_ECUDA, "one-shot index");
     }
+    // L2: the s-lists as tensor-core operands (rows gathered per list; perm aliases lists)
+    if (rc == RBC_OK && metric == RBC_L2 && d <= 128 && n_reps * static_cast<int64_t>(s) + 4096 < (int64_t(1) << 31)) {
+        const int64_t total = n_reps * static_cast<int64_t>(s);
+        rc = dalloc(&idx->offsets, n_reps + 1, idx->bytes);
+        if (rc == RBC_OK) rc = dalloc(&idx->xp, total * d, idx->bytes);
+        if (rc == RBC_OK) {
+            gather_rows_i32_kernel<<<grid_for(total * d, 256, 148 * 64), 256, 0, st>>>(idx->x, idx->lists, total, d,
+                                                                                      idx->xp);
+            note_launch();
+            idx->perm = idx->lists;
+            idx->n_local = total;
+            rc = tc_one_shot_prepare(idx, idx->xp, st);
+        }
+    }
     if (rc != RBC_OK) {
         rbc_index_destroy(idx);
         return rc;
@@ -558,8 +573,8 @@ int rbc_index_destroy(rbc_index *idx) {
     host_buffers_release(idx);
     tc_index_release(idx);
     tc1_index_release(idx);
-    void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets, idx->perm, idx->list_dists, idx->xp,
-                    idx->lists};
+    void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets,
+                    idx->perm == idx->lists ? nullptr : idx->perm, idx->list_dists, idx->xp, idx->lists};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete idx;

@@ -8,9 +8,14 @@
 
 namespace rbc {
 
-static int g_engine = 0;  // 0 = auto (tensor cores where supported), 1 = exact SIMT only
+static int g_engine = 0;  // 0 = auto, 1 = exact SIMT only, 2 = tensor cores wherever supported (tests)
 
 bool force_exact_engine() { return g_engine == 1; }
+
+// Brute-force-shaped scans below this many (query, point) pairs stay on the exact SIMT scan
+// in auto mode: the tensor-core path's operand preparation and host round trips cost more
+// than the scan (e.g. cfg1's 1k x 100 one-shot search: 0.03 ms SIMT vs 0.26 ms).
+int64_t tc_min_pairs() { return g_engine == 2 ? 0 : (int64_t(1) << 24); }
 
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
                  cudaStream_t st) {
@@ -68,7 +73,7 @@ int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const P
 }  // namespace rbc
 
 extern "C" int rbc_set_engine(int mode) {
-    if (mode != 0 && mode != 1) return rbc::fail(RBC_EINVAL, "engine must be 0 (auto) or 1 (exact)");
+    if (mode < 0 || mode > 2) return rbc::fail(RBC_EINVAL, "engine must be 0 (auto), 1 (exact) or 2 (tensor cores)");
     rbc::g_engine = mode;
     return RBC_OK;
 }

@@ -50,6 +50,12 @@ bool tc_bf_supported(int64_t nq, int64_t n, int d, int metric, int k);
 int tc_bf_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int k, uint64_t *keys, cudaStream_t st);
 // tcgen05 brute force over a prepared (partitioned, kind 2) operand: every list, every query
 int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, cudaStream_t st);
+// tcgen05 one-shot list scan (tc_stage2.cu): operands of the s-lists (xp_lists = the
+// points of every list, gathered, [nr * s][d]) and the scan of each query's own list
+int tc_one_shot_prepare(rbc_index *idx, const float *xp_lists, cudaStream_t st);
+bool tc_one_shot_supported(const rbc_index *idx, int64_t nq, int k);
+int tc_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
+                     cudaStream_t st);
 // prepared brute-force operand (abi.cu) and when preparing one per call pays off
 int bf_prepare(const float *x, int64_t n, int d, int metric, rbc_index **out, cudaStream_t st);
 bool bf_partition_pays(int64_t nq, int64_t n, int d, int metric, int k);
@@ -60,5 +66,7 @@ void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed);
 
 // engine selection (RBC_ENGINE env: "auto" (default) | "exact")
 bool force_exact_engine();
+// minimum (query, point) pairs for the brute-force-shaped tensor-core scans (0 in mode 2)
+int64_t tc_min_pairs();
 
 }  // namespace rbc

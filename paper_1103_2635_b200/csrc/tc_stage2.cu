@@ -1631,7 +1631,7 @@ bool tc_bf_supported(int64_t nq, int64_t n, int d, int metric, int k) {
     // sets); large point sets use the partitioned operand (tc_bf_index_search)
     if (metric != RBC_L2 || d < 1 || d > 128 || k < 1 || k > 32 || n < k || n > 65536) return false;
     if (n + kTailRows + 8 >= (int64_t(1) << 31)) return false;  // int32 positions
-    return nq * n >= (int64_t(1) << 16);  // smaller problems: the exact SIMT scan is as fast
+    return nq * n >= tc_min_pairs();  // smaller problems: the exact SIMT scan is faster
 }
 
 static std::atomic<int64_t> g_tc_bf_calls{0};
@@ -1925,6 +1925,99 @@ int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, 
     RBC_CUDA(cudaStreamSynchronize(st));
     last_overflow_count() = h[1];
     return RBC_OK;
+}
+
+// ---- one-shot list scan on the tensor cores ---------------------------------------------------
+// one_shot_query_batch (search.py:90-141): each query scans exactly the s-list of its nearest
+// representative.  The s-lists are stored like exact-index lists (rows gathered per list,
+// f16 residuals to the list's rep; the lists overlap, so a point can sit in several), the
+// queries are grouped by nearest rep, and each row's only segment is its own list (cutoff
+// s; 0 for the tile's other lists), so the scan is exactly L_{r_q}.
+namespace {
+
+__global__ void one_shot_offsets_kernel(int64_t nr, int s, int64_t *__restrict__ off) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p <= nr) off[p] = p * s;
+}
+
+__global__ void one_shot_segments_kernel(const uint64_t *__restrict__ near, int64_t nq, int s,
+                                         float *__restrict__ gamma, int32_t *__restrict__ nseg,
+                                         int64_t *__restrict__ seg_off, int64_t *__restrict__ seg_start,
+                                         int32_t *__restrict__ seg_len, int32_t *__restrict__ seg_list,
+                                         float *__restrict__ seg_d1, uint64_t *__restrict__ order_key) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i > nq) return;
+    seg_off[i] = i;
+    if (i == nq) return;
+    const uint64_t key = near[i];
+    const uint32_t p = key_id(key);
+    gamma[i] = __int_as_float(0x7f800000);  // no seed bound (the rep need not be in its own list)
+    nseg[i] = 1;
+    seg_start[i] = static_cast<int64_t>(p) * s;
+    seg_len[i] = s;
+    seg_list[i] = static_cast<int32_t>(p);
+    seg_d1[i] = key_dist(key);
+    order_key[i] = (static_cast<uint64_t>(p) << 24) | p;
+}
+
+}  // namespace
+
+int tc_one_shot_prepare(rbc_index *idx, const float *xp_lists, cudaStream_t st) {
+    if (idx->kind != 1 || idx->metric != RBC_L2 || idx->d > 128) return RBC_OK;
+    const int64_t total = idx->nr * static_cast<int64_t>(idx->s);
+    if (total + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 positions
+    std::vector<int64_t> off(idx->nr + 1);
+    for (int64_t p = 0; p <= idx->nr; ++p) off[p] = p * idx->s;
+    one_shot_offsets_kernel<<<grid_for(idx->nr + 1, 256), 256, 0, st>>>(idx->nr, idx->s, idx->offsets);
+    RBC_LAUNCHED();
+    TcIndex *tc = nullptr;
+    RBC_CHECK(tc_lists_build(xp_lists, idx->reps, idx->offsets, off, idx->radii, idx->nr, idx->d, &tc, &idx->bytes,
+                             st));
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        tc_free(tc);
+        return fail(RBC_ECUDA, "one-shot tc operands");
+    }
+    idx->tc = tc;
+    return RBC_OK;
+}
+
+bool tc_one_shot_supported(const rbc_index *idx, int64_t nq, int k) {
+    return idx->tc != nullptr && idx->kind == 1 && k <= 32 && k <= idx->s && idx->nr <= kMaxRepsTileFill &&
+           nq * idx->s >= tc_min_pairs();
+}
+
+int tc_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
+                     cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    g_tc_bf_calls.fetch_add(1);
+    PruneOut po;
+    RBC_CHECK(po.gamma.alloc(nq, st));
+    RBC_CHECK(po.nseg.alloc(nq, st));
+    RBC_CHECK(po.seg_off.alloc(nq + 1, st));
+    RBC_CHECK(po.seg_start.alloc(nq, st));
+    RBC_CHECK(po.seg_len.alloc(nq, st));
+    RBC_CHECK(po.seg_list.alloc(nq, st));
+    RBC_CHECK(po.seg_d1.alloc(nq, st));
+    RBC_CHECK(po.order_key.alloc(nq, st));
+    po.total_segs = nq;
+    one_shot_segments_kernel<<<grid_for(nq + 1, 256), 256, 0, st>>>(near, nq, idx->s, po.gamma.get(), po.nseg.get(),
+                                                                     po.seg_off.get(), po.seg_start.get(),
+                                                                     po.seg_len.get(), po.seg_list.get(),
+                                                                     po.seg_d1.get(), po.order_key.get());
+    RBC_LAUNCHED();
+    DevBuf<int64_t> status;
+    RBC_CHECK(status.alloc(2, st));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const int64_t cap = stage2_work_capacity(idx, nq);
+        RBC_CHECK(tc_stage2(idx, q, nq, k, po, keys, cap, status.get(), st));
+        int64_t h[2] = {0, 0};
+        RBC_CUDA(cudaMemcpyAsync(h, status.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+        RBC_CUDA(cudaStreamSynchronize(st));
+        last_overflow_count() = h[1];
+        if (h[0] <= cap) return RBC_OK;
+        stage2_note_work(idx, nq, h[0]);
+    }
+    return fail(RBC_ECUDA, "one-shot scan: work capacity");
 }
 }  // namespace rbc
 

@@ -23,8 +23,13 @@ def rbc():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1103_2635_b200 as m
+    from paper_1103_2635_b200 import _lib
 
-    return m
+    # engine 2: the tensor-core scans at every size (auto mode keeps small brute-force-shaped
+    # scans on the exact SIMT kernels, where they are faster)
+    _lib.lib.rbc_set_engine(2)
+    yield m
+    _lib.lib.rbc_set_engine(0)
 
 
 def _calls():
@@ -40,7 +45,7 @@ def _exact_engine(rbc, fn):
     try:
         return fn()
     finally:
-        _lib.lib.rbc_set_engine(0)
+        _lib.lib.rbc_set_engine(2)
 
 
 @pytest.mark.parametrize("d", [1, 5, 16, 21, 54, 62, 63, 64])
@@ -216,3 +221,40 @@ def test_tc_stage2_k_up_to_32_vs_oracle(rbc, oracle, k, d):
     want = oracle.exact_query(x, idx.reps.rep_ids, li, off, ld, idx.radii, q, k)
     for g, w in zip(got, want):
         assert np.array_equal(np.asarray(g).astype(np.asarray(w).dtype), w)
+
+
+@pytest.mark.parametrize("d", [16, 64, 100])
+@pytest.mark.parametrize("k", [1, 5, 32])
+def test_tc_one_shot_scan_vs_oracle(rbc, oracle, d, k):
+    # the one-shot list scan on the tensor cores: exactly the nearest rep's s-list per query
+    full = oracle.gen_clusters(40_000 + 2_000, d, 21 + d, n_clusters=8, cluster_sigma=0.05)
+    x, q = full[:40_000], full[40_000:]
+    idx = rbc.build_one_shot(rbc.DataMatrix(x), 200, 300, rbc.MetricSpec("l2", d), seed=2)
+    s0 = _scans()
+    got = rbc.one_shot_query_arrays(idx, q, k)
+    assert _scans() > s0, "the one-shot scan did not run on the tensor cores"
+    want = oracle.one_shot_query(x, idx.reps.rep_ids, idx.list_ids, q, k)
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g).astype(np.asarray(w).dtype), w)
+    exact = _exact_engine(rbc, lambda: rbc.one_shot_query_arrays(idx, q, k))
+    for g, w in zip(got, exact):
+        assert np.array_equal(g, w)
+
+
+def test_auto_engine_size_threshold(rbc, oracle):
+    # auto mode: a small brute force stays on the exact scan, a large one takes the tensor cores
+    from paper_1103_2635_b200 import _lib
+
+    x = oracle.gen_clusters(20_000, 16, 3, n_clusters=4, cluster_sigma=0.05)
+    _lib.lib.rbc_set_engine(0)
+    try:
+        c0 = _calls()
+        rbc.brute_force.bf_search_arrays(x[:50], x, rbc.MetricSpec("l2", 16), 1)
+        assert _calls() == c0
+        big = oracle.gen_clusters(100_000, 16, 4, n_clusters=4, cluster_sigma=0.05)
+        ids, dists = rbc.brute_force.bf_search_arrays(big[:1000], big, rbc.MetricSpec("l2", 16), 3)
+        assert _calls() > c0
+        oi, od = oracle.bf_topk(big[:1000], big, 3, "l2")
+        assert np.array_equal(ids, oi) and np.array_equal(dists, od)
+    finally:
+        _lib.lib.rbc_set_engine(2)
