@@ -162,6 +162,20 @@ int rbc_index_exact_create_shard(const float *x, int64_t n, int32_t d, int32_t m
                                  int64_t n_reps, const int64_t *list_ids, const int64_t *list_offsets,
                                  const float *list_dists, const float *radii, const uint8_t *owned_mask,
                                  rbc_index **out, void *stream);
+/* Sharded build: the representative shard of one rank
+ * built from the entries it RECEIVED, without the full point set.  Every rank holds
+ * all representatives (rows reps[n_reps,d], ids, global radii); the rank's m entries
+ * are (ids[m], owner rep position[m], dist[m], rows[m,d]) in increasing id order, as the
+ * all-to-all of the per-rank assignments delivers them.  The lists of the owned reps are
+ * sorted by (dist, id) (rbc.py:168), the others stay empty; search with
+ * rbc_exact_search_keys and merge over the ranks (rbc_merge_topk). */
+int rbc_index_exact_create_local(const float *reps, const int64_t *rep_ids, int64_t n_reps, const float *radii,
+                                 int64_t n_total, int32_t d, int32_t metric, const float *rows, const int64_t *ids,
+                                 const int64_t *owner, const float *dist, int64_t m, rbc_index **out, void *stream);
+/* radii[p] = max dist over the entries owned by p (0 if none): a rank's share of the
+ * list radii (rbc.py:172-175), combined across ranks with an all-reduce(MAX). */
+int rbc_local_list_radii(const int64_t *owner, const float *dist, int64_t m, int64_t n_reps, float *radii,
+                         void *stream);
 int rbc_index_destroy(rbc_index *idx);
 /* Bytes of device memory held by the index. */
 int64_t rbc_index_device_bytes(const rbc_index *idx);

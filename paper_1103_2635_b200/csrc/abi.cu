@@ -76,6 +76,9 @@ int bernoulli(int64_t n, double p, uint64_t st_hi, uint64_t st_lo, uint64_t inc_
               int64_t *count_host, cudaStream_t st);
 int build_exact(const float *x, int64_t n, int d, int metric, const int64_t *rep_ids, int64_t nr, int64_t *list_ids,
                 int64_t *offsets, float *list_dists, float *radii, cudaStream_t st);
+int build_local_lists(const int64_t *owner, const float *dist, int64_t m, int64_t nr, int64_t *order,
+                      int64_t *offsets, float *sorted_dists, cudaStream_t st);
+int local_list_radii(const int64_t *owner, const float *dist, int64_t m, int64_t nr, float *radii, cudaStream_t st);
 int build_one_shot(const float *x, int64_t n, int d, int metric, const int64_t *rep_ids, int64_t nr, int s,
                    int64_t *lists, float *radii, cudaStream_t st);
 
@@ -177,6 +180,19 @@ __global__ void copy_segments_kernel(const int64_t *__restrict__ src_off, const 
     for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
         perm[dst_off[p] + j] = static_cast<int32_t>(list_ids[src_off[p] + j]);
         ldist[dst_off[p] + j] = list_dists[src_off[p] + j];
+    }
+}
+
+// sorted entry i of a local shard: id and row of received entry order[i]
+__global__ void gather_local_kernel(const int64_t *__restrict__ order, const int64_t *__restrict__ ids,
+                                    const float *__restrict__ rows, int64_t m, int d, int32_t *__restrict__ perm,
+                                    float *__restrict__ xp) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < m * d;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = t / d, c = t - i * d;
+        const int64_t j = order[i];
+        xp[t] = rows[j * d + c];
+        if (c == 0) perm[i] = static_cast<int32_t>(ids[j]);
     }
 }
 
@@ -519,6 +535,67 @@ int rbc_index_exact_create_shard(const float *x, int64_t n, int32_t d, int32_t m
     if (!owned_mask) return fail(RBC_EINVAL, "owned_mask is required");
     return exact_create(x, n, d, metric, rep_ids, n_reps, list_ids, list_offsets, list_dists, radii, owned_mask, out,
                         as_stream(stream));
+}
+
+int rbc_local_list_radii(const int64_t *owner, const float *dist, int64_t m, int64_t n_reps, float *radii,
+                         void *stream) {
+    if (n_reps < 1 || m < 0) return fail(RBC_EINVAL, "n_reps must be >= 1 and m >= 0");
+    cudaStream_t st = as_stream(stream);
+    RBC_CHECK(check_ids_in_range(owner, m, n_reps, "owner", st));
+    return local_list_radii(owner, dist, m, n_reps, radii, st);
+}
+
+int rbc_index_exact_create_local(const float *reps, const int64_t *rep_ids, int64_t n_reps, const float *radii,
+                                 int64_t n_total, int32_t d, int32_t metric, const float *rows, const int64_t *ids,
+                                 const int64_t *owner, const float *dist, int64_t m, rbc_index **out, void *stream) {
+    RBC_CHECK(check_common(n_total, d, metric));
+    if (n_reps < 1 || n_reps > n_total) return fail(RBC_EINVAL, "n_reps must be in [1, n]");
+    if (m < 0 || m > n_total) return fail(RBC_EINVAL, "m must be in [0, n]");
+    if (!out) return fail(RBC_EINVAL, "null output handle");
+    cudaStream_t st = as_stream(stream);
+    RBC_CHECK(check_ids_in_range(rep_ids, n_reps, n_total, "rep_ids", st));
+    RBC_CHECK(check_ids_in_range(ids, m, n_total, "ids", st));
+    RBC_CHECK(check_ids_in_range(owner, m, n_reps, "owner", st));
+    rbc_index *idx = new rbc_index();
+    idx->kind = 0;
+    idx->n = n_total;
+    idx->d = d;
+    idx->metric = metric;
+    idx->nr = n_reps;
+    idx->shard = true;
+    idx->n_local = m;
+    int rc = dalloc(&idx->reps, n_reps * d, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->rep_ids, n_reps, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->radii, n_reps, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->offsets, n_reps + 1, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->perm, m, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->list_dists, m, idx->bytes);
+    if (rc == RBC_OK) rc = dalloc(&idx->xp, m * d, idx->bytes);
+    if (rc == RBC_OK &&
+        (cudaMemcpyAsync(idx->reps, reps, sizeof(float) * n_reps * d, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+         cudaMemcpyAsync(idx->rep_ids, rep_ids, sizeof(int64_t) * n_reps, cudaMemcpyDeviceToDevice, st) !=
+             cudaSuccess ||
+         cudaMemcpyAsync(idx->radii, radii, sizeof(float) * n_reps, cudaMemcpyDeviceToDevice, st) != cudaSuccess))
+        rc = fail(RBC_ECUDA, "shard index copies");
+    DevBuf<int64_t> order;
+    if (rc == RBC_OK) rc = order.alloc(m, st);
+    if (rc == RBC_OK) rc = build_local_lists(owner, dist, m, n_reps, order.get(), idx->offsets, idx->list_dists, st);
+    if (rc == RBC_OK && m > 0) {
+        gather_local_kernel<<<grid_for(m * d, 256, 148 * 64), 256, 0, st>>>(order.get(), ids, rows, m, d, idx->perm,
+                                                                            idx->xp);
+        note_launch();
+        if (cudaGetLastError() != cudaSuccess) rc = fail(RBC_ECUDA, "shard gather");
+    }
+    if (rc == RBC_OK) rc = cudaGetDevice(&idx->device) == cudaSuccess ? RBC_OK : fail(RBC_ECUDA, "device");
+    if (rc == RBC_OK) rc = tc_index_prepare(idx, st);
+    if (rc == RBC_OK) rc = tc1_index_prepare(idx, st);
+    if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "shard index sync");
+    if (rc != RBC_OK) {
+        rbc_index_destroy(idx);
+        return rc;
+    }
+    *out = idx;
+    return RBC_OK;
 }
 
 int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metric, const int64_t *rep_ids,

@@ -101,6 +101,13 @@ int gather_rows(const float *x, const int64_t *ids, int64_t rows, int d, float *
     return RBC_OK;
 }
 
+// (owner, dist) -> assignment key (dist bits << 32 | rep pos)
+__global__ void pack_assign_kernel(const int64_t *__restrict__ owner, const float *__restrict__ dist, int64_t m,
+                                   uint64_t *__restrict__ assign) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < m) assign[i] = pack_key(dist[i], static_cast<uint32_t>(owner[i]));
+}
+
 // assignment key (dist bits, rep pos) -> sort key (rep pos << 32 | dist bits), payload id
 __global__ void owner_sort_keys_kernel(const uint64_t *__restrict__ assign, int64_t n, uint64_t *__restrict__ keys,
                                        uint32_t *__restrict__ vals) {
@@ -202,4 +209,59 @@ int build_one_shot(const float *x, int64_t n, int d, int metric, const int64_t *
     return RBC_OK;
 }
 
+
+// ---- lists of a representative shard from received (owner, dist) entries ----------------------
+// The sharded build (distributed.py build_exact_distributed): every rank assigns its slice
+// of X, the entries travel to the rank owning their representative, and each rank sorts
+// what it received.  Entries arrive in increasing id order (contiguous id slices,
+// concatenated in rank order), so one stable sort on (owner << 32 | f32 bits(dist))
+// reproduces lexsort((id, dist, owner)) (rbc.py:168) for the owned lists.
+int build_local_lists(const int64_t *owner, const float *dist, int64_t m, int64_t nr, int64_t *order,
+                      int64_t *offsets, float *sorted_dists, cudaStream_t st) {
+    DevBuf<uint64_t> assign, keys, skeys;
+    DevBuf<uint32_t> vals, svals;
+    DevBuf<float> radii;
+    RBC_CHECK(assign.alloc(m, st));
+    RBC_CHECK(keys.alloc(m, st));
+    RBC_CHECK(skeys.alloc(m, st));
+    RBC_CHECK(vals.alloc(m, st));
+    RBC_CHECK(svals.alloc(m, st));
+    RBC_CHECK(radii.alloc(nr, st));
+    if (m > 0) {
+        pack_assign_kernel<<<grid_for(m, 256), 256, 0, st>>>(owner, dist, m, assign.get());
+        RBC_LAUNCHED();
+        owner_sort_keys_kernel<<<grid_for(m, 256), 256, 0, st>>>(assign.get(), m, keys.get(), vals.get());
+        RBC_LAUNCHED();
+        int owner_bits = 1;
+        while ((int64_t(1) << owner_bits) < nr) ++owner_bits;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.get(), skeys.get(), vals.get(), svals.get(), m, 0,
+                                        32 + owner_bits, st);
+        DevBuf<unsigned char> tmp;
+        RBC_CHECK(tmp.alloc(tb, st));
+        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, keys.get(), skeys.get(), vals.get(), svals.get(), m, 0,
+                                                 32 + owner_bits, st));
+        note_launch();
+        finish_lists_kernel<<<grid_for(m, 256), 256, 0, st>>>(skeys.get(), svals.get(), m, order, sorted_dists);
+        RBC_LAUNCHED();
+    }
+    segment_offsets_kernel<<<grid_for(nr + 1, 256), 256, 0, st>>>(skeys.get(), m, nr, offsets, radii.get());
+    RBC_LAUNCHED();
+    return RBC_OK;
+}
+
+// radii[p] = max(radii[p], dist of every entry owned by p) (dist >= 0: float bits order)
+__global__ void list_radii_kernel(const int64_t *__restrict__ owner, const float *__restrict__ dist, int64_t m,
+                                  float *__restrict__ radii) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < m) atomicMax(reinterpret_cast<unsigned *>(radii) + owner[i], __float_as_uint(dist[i]));
+}
+
+int local_list_radii(const int64_t *owner, const float *dist, int64_t m, int64_t nr, float *radii, cudaStream_t st) {
+    RBC_CUDA(cudaMemsetAsync(radii, 0, sizeof(float) * nr, st));
+    if (m == 0) return RBC_OK;
+    list_radii_kernel<<<grid_for(m, 256), 256, 0, st>>>(owner, dist, m, radii);
+    RBC_LAUNCHED();
+    return RBC_OK;
+}
 }  // namespace rbc

@@ -98,6 +98,12 @@ def _dist():
     return dist
 
 
+def _world(group=None) -> int:
+    """World size of the group, 1 when no process group is initialised (single process)."""
+    dist = _dist()
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
 def merge_shard_keys(local_keys, k: int, group=None, merge_fn=None):
     """Exact global top-k from every rank's local top-k key rows.
 
@@ -107,7 +113,7 @@ def merge_shard_keys(local_keys, k: int, group=None, merge_fn=None):
     P-way merge for k > 1 (default: the on-device ``rbc_merge_topk``).
     """
     dist = _dist()
-    world = dist.get_world_size(group)
+    world = _world(group)
     if world == 1:
         return local_keys
     if k == 1:
@@ -140,7 +146,7 @@ def device_merge_keys(stacked, k: int):
 
 def sum_over_ranks(tensor, group=None):
     dist = _dist()
-    if dist.get_world_size(group) > 1:
+    if _world(group) > 1:
         dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
     return tensor
 
@@ -148,7 +154,7 @@ def sum_over_ranks(tensor, group=None):
 def gather_query_shards(local, nq: int, group=None):
     """All-gather per-rank query-slice results (rows) into the full [nq, ...] tensor on every rank."""
     dist = _dist()
-    world = dist.get_world_size(group)
+    world = _world(group)
     if world == 1:
         return local
     sl = query_slices(nq, world)
@@ -167,16 +173,34 @@ def gather_query_shards(local, nq: int, group=None):
 class ShardedExactIndex:
     """One rank's representative shard of an exact index (all reps, the owned lists)."""
 
-    index: object          # the full RbcExactIndex (host arrays; identical on every rank)
+    index: object          # the full RbcExactIndex (host arrays), or None after a sharded build
     plan: np.ndarray       # shard of every rep position
     rank: int
     world: int
     dev: object = None     # DeviceIndex of the shard
+    list_sizes: np.ndarray = None  # global list length of every rep
+    rep_ids: np.ndarray = None
+    radii: np.ndarray = None
+    metric: object = None
+
+    def __post_init__(self):
+        if self.index is not None:
+            if self.list_sizes is None:
+                self.list_sizes = np.array([len(a) for a in self.index.list_ids], np.int64)
+            if self.rep_ids is None:
+                self.rep_ids = self.index.reps.rep_ids
+            if self.radii is None:
+                self.radii = np.asarray(self.index.radii, np.float32)
+            if self.metric is None:
+                self.metric = self.index.metric
+
+    @property
+    def n_reps(self) -> int:
+        return int(len(self.rep_ids))
 
     @property
     def owned_points(self) -> int:
-        sizes = np.array([len(a) for a in self.index.list_ids], np.int64)
-        return int(sizes[self.plan == self.rank].sum())
+        return int(np.asarray(self.list_sizes)[self.plan == self.rank].sum())
 
 
 def shard_exact_index(index, rank: int, world: int) -> ShardedExactIndex:
@@ -204,6 +228,107 @@ def build_exact_sharded(data, n_r, spec, seed, rank: int, world: int, **kw) -> S
     return sh
 
 
+def exchange_to_owners(ids, owner, dist, rows, plan, group=None):
+    """All-to-all of assignment entries to the rank that owns their representative.
+
+    ``ids`` int64 [m], ``owner`` int64 [m] (rep positions), ``dist`` float32 [m], ``rows``
+    float32 [m, d]: torch tensors on the collective's device (CUDA for NCCL, CPU for gloo).
+    Each source sends its entries for a destination in their local order (a stable
+    partition), and the received blocks are concatenated in source-rank order -- so with
+    contiguous ascending id slices per rank the received entries are in increasing id
+    order, which the local stable sort relies on (rbc_index_exact_create_local).
+    Returns the received (ids, owner, dist, rows).
+    """
+    import torch
+
+    dist_ = _dist()
+    world = dist_.get_world_size(group)
+    plan_t = torch.as_tensor(np.asarray(plan, np.int64), device=owner.device)
+    dest = plan_t[owner]
+    order = torch.sort(dest, stable=True).indices
+    send = torch.bincount(dest, minlength=world).to(torch.int64)
+    recv = torch.empty_like(send)
+    dist_.all_to_all_single(recv, send, group=group)
+    sc, rc = send.tolist(), recv.tolist()
+
+    def a2a(t):
+        out = t.new_empty((sum(rc),) + tuple(t.shape[1:]))
+        dist_.all_to_all_single(out, t[order].contiguous(), rc, sc, group=group)
+        return out
+
+    return a2a(ids), a2a(owner), a2a(dist), a2a(rows)
+
+
+def build_exact_distributed(x_local, id_lo: int, n_total: int, n_r: int, spec, seed: int, rank: int, world: int,
+                            group=None, mode: str = "bernoulli", rep_ids=None) -> ShardedExactIndex:
+    """Sharded exact build: each rank holds only its id slice
+    x_local = X[id_lo : id_lo + m] and ends with the ownership lists of its rep shard.
+
+    1. every rank draws the same representatives (rbc.py:62-84) and all-reduces their rows;
+    2. each rank assigns its slice to the nearest representative (the tcgen05 brute force of
+       every point over the reps: rbc.py:164);
+    3. list sizes all-reduce(SUM) -> the same LPT rep-shard plan on every rank;
+    4. all-to-all of (id, owner, dist, row) to the owning rank;
+    5. list radii: local max, all-reduce(MAX) (rbc.py:172-175);
+    6. the received entries become the shard's lists (stable radix sort on (owner, dist)).
+    Per-rank device memory holds the slice and the shard, about 2/P of the points.
+    The concatenated shard lists equal the single-GPU build's lists, bit for bit.
+    """
+    import torch
+
+    from .rbc import _resolve_reps, DeviceIndex
+
+    dist_ = _dist()
+    t = _lib.require_cuda()
+    xl = _lib.to_device(np.ascontiguousarray(x_local, np.float32))
+    m, d = int(xl.shape[0]), int(xl.shape[1])
+    if d != spec.dim:
+        raise ValueError(f"dimension mismatch: data d={d}, metric dim={spec.dim}")
+    reps = _resolve_reps(n_total, n_r, seed, mode, rep_ids)
+    rid = np.asarray(reps.rep_ids, np.int64)
+    nr = int(rid.size)
+    rid_dev = _lib.to_device(rid)
+    # 1. representative rows: each rep row is contributed by the one rank whose slice holds it
+    rows = torch.zeros((nr, d), dtype=torch.float32, device="cuda")
+    mine = np.flatnonzero((rid >= id_lo) & (rid < id_lo + m))
+    if mine.size:
+        rows[torch.as_tensor(mine, device="cuda")] = xl[torch.as_tensor(rid[mine] - id_lo, device="cuda")]
+    if world > 1:
+        dist_.all_reduce(rows, op=dist_.ReduceOp.SUM, group=group)
+    # 2. nearest representative of every local point (key64 argmin: lowest position on ties)
+    owner = torch.empty((m, 1), dtype=torch.int64, device="cuda")
+    dists = torch.empty((m, 1), dtype=torch.float32, device="cuda")
+    if m:
+        _lib.check(_lib.lib.rbc_bf_search(_lib.ptr(xl), m, _lib.ptr(rows), nr, d, spec.code, 1, _lib.ptr(owner),
+                                          _lib.ptr(dists), _lib.stream_ptr()), "shard assignment")
+    owner, dists = owner.view(-1), dists.view(-1)
+    # 3. global list sizes -> plan
+    sizes = torch.bincount(owner, minlength=nr).to(torch.int64)
+    if world > 1:
+        dist_.all_reduce(sizes, op=dist_.ReduceOp.SUM, group=group)
+    sizes_h = _lib.to_host(sizes)
+    plan = rep_shard_plan(sizes_h, world)
+    # 4. entries to their owner shard
+    ids = torch.arange(id_lo, id_lo + m, dtype=torch.int64, device="cuda")
+    if world > 1:
+        ids, owner, dists, xl = exchange_to_owners(ids, owner, dists, xl, plan, group)
+    # 5. radii
+    radii = torch.empty(nr, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib.rbc_local_list_radii(_lib.ptr(owner), _lib.ptr(dists), int(owner.numel()), nr,
+                                             _lib.ptr(radii), _lib.stream_ptr()), "list radii")
+    if world > 1:
+        dist_.all_reduce(radii, op=dist_.ReduceOp.MAX, group=group)
+    # 6. the shard index
+    handle = ctypes.c_void_p()
+    _lib.check(_lib.lib.rbc_index_exact_create_local(_lib.ptr(rows), _lib.ptr(rid_dev), nr, _lib.ptr(radii), n_total, d,
+                                                     spec.code, _lib.ptr(xl), _lib.ptr(ids), _lib.ptr(owner),
+                                                     _lib.ptr(dists), int(owner.numel()), ctypes.byref(handle),
+                                                     _lib.stream_ptr()), "shard index create")
+    dev = DeviceIndex(handle, t.cuda.current_device())
+    return ShardedExactIndex(None, plan, rank, world, dev, list_sizes=sizes_h, rep_ids=rid,
+                             radii=_lib.to_host(radii), metric=spec)
+
+
 def local_shard_keys(sh: ShardedExactIndex, q_dev, nq: int, k: int):
     """This rank's local top-k key rows [nq, k] (int64, EMPTY_KEY = none) and search stats tensors."""
     t = _lib.require_cuda()
@@ -223,11 +348,11 @@ def exact_query_sharded(sh: ShardedExactIndex, queries, k: int = 1, group=None):
     from .search import _queries
 
     qv = _queries(queries)
-    n_reps = sh.index.reps.size
+    n_reps = sh.n_reps
     if not 1 <= k <= n_reps:
         raise ValueError(f"k must be in [1, |R|={n_reps}], got {k}")
-    if qv.shape[1] != sh.index.metric.dim:
-        raise ValueError(f"dimension mismatch: queries d={qv.shape[1]}, metric dim={sh.index.metric.dim}")
+    if qv.shape[1] != sh.metric.dim:
+        raise ValueError(f"dimension mismatch: queries d={qv.shape[1]}, metric dim={sh.metric.dim}")
     nq = qv.shape[0]
     keys, (gamma, prr, p3, cand) = local_shard_keys(sh, _lib.to_device(qv), nq, k)
     merged = merge_shard_keys(keys, k, group)
@@ -258,7 +383,7 @@ def exact_query_qsharded(index, queries, k: int = 1, rank: int = 0, world: int =
 
 
 __all__ = [
-    "ShardedExactIndex", "build_exact_sharded", "exact_query_qsharded", "exact_query_sharded",
+    "ShardedExactIndex", "build_exact_distributed", "build_exact_sharded", "exchange_to_owners", "exact_query_qsharded", "exact_query_sharded",
     "gather_query_shards", "merge_shard_keys", "owned_mask", "query_slices", "rep_shard_plan",
     "shard_exact_index", "unpack_keys_host",
 ]

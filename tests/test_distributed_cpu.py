@@ -124,3 +124,62 @@ def test_unpack_keys_host_roundtrip():
     dists = np.array([[0.0, 1.5, np.inf]], np.float32)
     got_ids, got_d = D.unpack_keys_host(_pack(ids, dists))
     assert np.array_equal(got_ids, ids) and np.array_equal(got_d, dists)
+
+
+def _build_worker(rank, world, port, result_dir):
+    """Sharded-build host logic: slice assignment (oracle), size all-reduce, LPT plan, all-to-all of
+    (id, owner, dist, row) to the owner shard, radii all-reduce(MAX)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as orc
+
+        x = orc.gen_clusters(3_001, 6, 17, n_clusters=5, cluster_sigma=0.05)
+        reps = orc.bernoulli(3_001, 60 / 3_001, 1)
+        lo, hi = D.query_slices(x.shape[0], world)[rank]
+        xl = x[lo:hi]
+        rows = torch.zeros((len(reps), 6), dtype=torch.float32)
+        mine = np.flatnonzero((reps >= lo) & (reps < hi))
+        rows[torch.as_tensor(mine)] = torch.from_numpy(xl[reps[mine] - lo])
+        dist.all_reduce(rows, op=dist.ReduceOp.SUM)
+        own, dd = orc.bf_topk(xl, rows.numpy(), 1)
+        owner = torch.from_numpy(np.asarray(own).reshape(-1).astype(np.int64))
+        dists = torch.from_numpy(np.asarray(dd).reshape(-1).astype(np.float32))
+        sizes = torch.bincount(owner, minlength=len(reps)).to(torch.int64)
+        dist.all_reduce(sizes, op=dist.ReduceOp.SUM)
+        plan = D.rep_shard_plan(sizes.numpy(), world)
+        ids = torch.arange(lo, hi, dtype=torch.int64)
+        r_ids, r_owner, r_dist, r_rows = D.exchange_to_owners(ids, owner, dists, torch.from_numpy(xl), plan)
+        radii = torch.zeros(len(reps), dtype=torch.float32)
+        radii.scatter_reduce_(0, r_owner, r_dist, reduce="amax")
+        dist.all_reduce(radii, op=dist.ReduceOp.MAX)
+        np.savez(os.path.join(result_dir, f"b{rank}.npz"), ids=r_ids.numpy(), owner=r_owner.numpy(),
+                 dist=r_dist.numpy(), rows=r_rows.numpy(), radii=radii.numpy(), plan=plan, sizes=sizes.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_build_exchange_equals_single_build(tmp_path, oracle):
+    world = 2
+    mp.start_processes(_build_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    x = oracle.gen_clusters(3_001, 6, 17, n_clusters=5, cluster_sigma=0.05)
+    reps = oracle.bernoulli(3_001, 60 / 3_001, 1)
+    li, off, ld, radii = oracle.build_exact(x, reps)
+    seen = np.zeros(x.shape[0], np.int64)
+    for r in range(world):
+        z = np.load(tmp_path / f"b{r}.npz")
+        assert np.array_equal(z["sizes"], np.diff(off)), "global list sizes"
+        assert np.array_equal(z["radii"], radii), "all-reduced radii equal the single build's"
+        assert np.all(np.diff(z["ids"]) > 0), "entries must arrive in increasing id order"
+        assert np.array_equal(z["rows"], x[z["ids"]]), "rows travel with their ids"
+        assert np.all(z["plan"][z["owner"]] == r), "every received entry belongs to this shard"
+        # the local stable sort (rbc_index_exact_create_local) = lexsort((id, dist, owner))
+        o = np.lexsort((z["ids"], z["dist"], z["owner"]))
+        for p in np.flatnonzero(z["plan"] == r):
+            sel = z["owner"][o] == p
+            assert np.array_equal(z["ids"][o][sel], li[off[p]: off[p + 1]]), f"list {p} ids"
+            assert np.array_equal(z["dist"][o][sel], ld[off[p]: off[p + 1]]), f"list {p} dists"
+        seen[z["ids"]] += 1
+    assert np.all(seen == 1), "every point lands on exactly one shard"
