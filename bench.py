@@ -48,6 +48,11 @@ CONFIGS = {
     "cfg4": dict(kind="oneshot", n=2_000_000, d=21, nq=100_000, C=8, seed=4, n_r=1415, s=1415, mode="bernoulli",
                  metric="l1", k=1, workload="cfg4: one-shot RBC 1-NN L1, Robot-shaped clusters n=2M d=21 C=8, "
                                             "n_r=s=1415 (|R|~1455), 100k queries"),
+    "cfg5": dict(kind="exact", n=16_000_000, d=128, nq=10_000, C=64, seed=5, n_r=4000, metric="l2", k=10,
+                 rep_shard=True,
+                 workload="cfg5: exact RBC 10-NN L2, clusters n=16M d=128 C=64 sigma=0.05, n_r=4000 (|R|~4000), "
+                          "X sharded by representative over the GPUs (sharded build + per-query key merge), "
+                          "10k queries per step served by all ranks"),
 }
 SIGMA, REP_SEED = 0.05, 0
 CFG = CONFIGS["cfg2"]
@@ -85,6 +90,154 @@ def gen_inputs(rank: int):
         r2 = np.random.default_rng(1000 + rank)
         q = np.ascontiguousarray((centers[r2.integers(C, size=NQ)] + SIGMA * r2.standard_normal((NQ, D))).astype(np.float32))
     return x, q
+
+
+def gen_inputs_chunked(rows_per_chunk: int = 1 << 20):
+    """gen_inputs for large n: the same random stream (centres, assignment, then the normals
+    row-major), drawn in row chunks straight into float32 so the float64 temporaries stay small."""
+    rng = np.random.default_rng(DATA_SEED)
+    centers = rng.random((C, D))
+    assignment = rng.integers(C, size=N + NQ)
+    full = np.empty((N + NQ, D), np.float32)
+    for r0 in range(0, N + NQ, rows_per_chunk):
+        r1 = min(N + NQ, r0 + rows_per_chunk)
+        full[r0:r1] = centers[assignment[r0:r1]] + SIGMA * rng.standard_normal((r1 - r0, D))
+    return full[:N], full[N:]
+
+
+def run_rep_shard(args, rank, world, local):
+    """cfg5: the database sharded by representative over the ranks.  The
+    build is the sharded build (each rank assigns its id slice, all-to-all to the owner
+    shard); every rank searches ALL queries over its shard and the per-query top-k keys are
+    merged over NCCL (all_gather + rbc_merge_topk).  value = queries / max-over-ranks time
+    (strong scaling: the work per query is split over the ranks)."""
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1103_2635_b200 as rbc
+    from paper_1103_2635_b200 import _lib
+    from paper_1103_2635_b200 import distributed as Dm
+
+    x, q = gen_inputs_chunked()
+    lo, hi = Dm.query_slices(N, world)[rank]
+    spec = rbc.MetricSpec("l2", D)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh = Dm.build_exact_distributed(x[lo:hi], lo, N, NR, spec, REP_SEED, rank, world)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    q_dev = _lib.to_device(q)
+    keys = torch.empty((NQ, K), dtype=torch.int64, device="cuda")
+    cand = torch.empty(NQ, dtype=torch.int64, device="cuda")
+    stats = _lib.SearchStatsC(None, None, None, cand.data_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        _lib.check(_lib.lib.rbc_exact_search_keys(sh.dev.handle, _lib.ptr(q_dev), NQ, K, _lib.ptr(keys), stats,
+                                                  sptr), "shard search")
+        return Dm.merge_shard_keys(keys, K)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # e2e: the Python API (numpy queries in, numpy ids/dists/stats out, merge included)
+    e2e_times = []
+    for i in range(1 + max(2, min(args.steps, 5))):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        Dm.exact_query_sharded(sh, q, K)
+        if i >= 1:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_times)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    times = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.zero_()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        step()
+        ev1.record(stream)
+        ev1.synchronize()
+        times.append(ev0.elapsed_time(ev1))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = _lib.launch_count() - launches0
+    # phase split of this rank's search (stage-2 scan alone = the dominant kernel)
+    _lib.profile_enable(True)
+    _lib.check(_lib.lib.rbc_exact_search_keys(sh.dev.handle, _lib.ptr(q_dev), NQ, K, _lib.ptr(keys), stats, sptr), "p")
+    torch.cuda.synchronize()
+    _lib.profile_enable(True)
+    _lib.check(_lib.lib.rbc_exact_search_keys(sh.dev.handle, _lib.ptr(q_dev), NQ, K, _lib.ptr(keys), stats, sptr), "p")
+    torch.cuda.synchronize()
+    phases = _lib.profile_read()
+    _lib.profile_enable(False)
+    clk = clocks.stop()
+    total_ms = sum(times)
+    cand_local = float(cand.sum().item())
+    if dist:
+        t = torch.tensor([total_ms, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_s = (float(v) for v in t.tolist())
+        c = torch.tensor([cand_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        cand_total = float(c.item())
+    else:
+        cand_total = cand_local
+    value = NQ * args.steps / (total_ms / 1e3)
+    pk = peaks()
+    scan_ms = phases["scan"][0]
+    scan_work = 2.0 * D * cand_local
+    achieved = scan_work / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["tensor"], "unit": "TFLOP/s",
+                "frac": achieved / pk["tensor"] if achieved else None, "peak_src": pk["src"], "traffic": None,
+                "traffic_unit": "bytes/launch", "traffic_src": None, "kernel": f"stage2_tc_kernel<{kt_of(K)}, 2>",
+                "work_per_launch": scan_work, "work_rule": "2*d*candidates on this rank (reference-rule counts)",
+                "phase_ms_per_step": {k2: v[0] for k2, v in phases.items()}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # exact RBC returns the brute-force k-NN (SPEC acceptance 1): the oracle's brute force
+        # over all 16M points on the host cores, a small query sample
+        from oracle import oracle as orc
+
+        orc.build()
+        m = 8
+        t0 = time.perf_counter()
+        orc.bf_topk(q[:m], x, K)
+        dt = time.perf_counter() - t0
+        cpu = {"value": m / dt, "unit": "queries/s", "cores": orc.threads(), "kind": "port",
+               "sample": f"{m} of the {NQ} cfg5 queries, brute-force {K}-NN over all {N} points via "
+                         "oracle/rbc_oracle.c (OpenMP) -- the oracle's RBC build of 16M x 128 takes ~10 min"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": CFG["workload"], "queries_per_step": NQ, "k": K, "n_reps": sh.n_reps,
+                           "parallelism": f"rep-shard x{world}", "l2_flush": "256 MiB write between timed steps",
+                           "index_build_s": build_s, "mean_candidates": cand_total / NQ,
+                           "shard_points": sh.owned_points,
+                           "arith": "f32 inputs; f16 tcgen05 filter (two K planes); exact re-rank in f64"},
+                "e2e": {"value": NQ / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(q.nbytes),
+                        "d2h_bytes_per_step": int(NQ * K * 12 + NQ * 24),
+                        "call": "distributed.exact_query_sharded (numpy in/out, NCCL merge)"},
+                "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "gpu_bruteforce": None,
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
 
 
 def kt_of(k: int) -> int:
@@ -315,6 +468,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world, args.config)
+    if CFG.get("rep_shard"):
+        return run_rep_shard(args, rank, world, local)
 
     import torch
 

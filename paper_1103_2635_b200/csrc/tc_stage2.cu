@@ -801,15 +801,33 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 auto compact = [&]() {
                     const float ut = U * kTie;
                     int c2 = 0;
-                    for (int e = 0; e < count; ++e) {
-                        const float4 a = clb[3 * e], b = clb[3 * e + 1], c = clb[3 * e + 2];
-                        const float vmax = fmaxf(fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)), fmaxf(fmaxf(b.x, b.y), fmaxf(b.z, b.w)));
-                        if (fmaf(-vmax, c.y, c.x) <= ut) {  // the group's smallest lower bound (all 8 columns)
-                            clb[3 * c2] = a;
-                            clb[3 * c2 + 1] = b;
-                            clb[3 * c2 + 2] = c;
-                            cpos[c2] = cpos[e];
-                            ++c2;
+                    // kCB groups loaded before any is written back: the loads are independent (in
+                    // flight together) and every write-back slot c2 <= e precedes the batch's
+                    // unread entries, so nothing is overwritten before it is read
+                    constexpr int kCB = KT == 1 ? 1 : 4;  // (k = 1 rarely compacts: no registers for it)
+                    for (int e0 = 0; e0 < count; e0 += kCB) {
+                        float4 a[kCB], b[kCB], c[kCB];
+                        int32_t ps[kCB];
+#pragma unroll
+                        for (int j = 0; j < kCB; ++j) {
+                            const int e = e0 + j < count ? e0 + j : e0;
+                            a[j] = clb[3 * e];
+                            b[j] = clb[3 * e + 1];
+                            c[j] = clb[3 * e + 2];
+                            ps[j] = cpos[e];
+                        }
+#pragma unroll
+                        for (int j = 0; j < kCB; ++j) {
+                            const float vmax = fmaxf(fmaxf(fmaxf(a[j].x, a[j].y), fmaxf(a[j].z, a[j].w)),
+                                                     fmaxf(fmaxf(b[j].x, b[j].y), fmaxf(b[j].z, b[j].w)));
+                            // the group's smallest lower bound (all 8 columns)
+                            if (e0 + j < count && fmaf(-vmax, c[j].y, c[j].x) <= ut) {
+                                clb[3 * c2] = a[j];
+                                clb[3 * c2 + 1] = b[j];
+                                clb[3 * c2 + 2] = c[j];
+                                cpos[c2] = ps[j];
+                                ++c2;
+                            }
                         }
                     }
                     count = c2;
@@ -865,10 +883,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                 ubk[t] = lo;
                                 x = hi;
                             }
-                            float kth = ubk[0];
+                            float kth = ubk[KT - 1];
+                            if (P.k != KT) {
 #pragma unroll
-                            for (int t = 0; t < KT; ++t)
-                                if (t == P.k - 1) kth = ubk[t];
+                                for (int t = 0; t < KT; ++t)
+                                    if (t == P.k - 1) kth = ubk[t];
+                            }
                             U = fminf(u_init, kth);
                         }
                         T = threshold();
@@ -1385,7 +1405,10 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
     g_tc_scan_calls.fetch_add(1);
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
     // 3. the tensor-core scan
-    const int cap = cap_groups > 0 ? cap_groups : 12 + 6 * k;  // 8-column groups per query and column part
+    // 8-column groups per query and column part.  k > 1 buffers ~k ln(N/k) groups per part
+    // (the k-record events of the scan); a compaction (a pass over the buffer) runs when it
+    // fills, so the capacity is sized to make that rare
+    const int cap = cap_groups > 0 ? cap_groups : (k == 1 ? 18 : (16 + 24 * k < 512 ? 16 + 24 * k : 512));
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, ovf_list;
     RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 12, st));
@@ -1455,6 +1478,7 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
             if (k == 1) launch(stage2_tc_kernel<1, 1>, sm);
             else if (k <= 4) launch(stage2_tc_kernel<4, 1>, sm);
             else if (k <= 8) launch(stage2_tc_kernel<8, 1>, sm);
+            else if (k == 10) launch(stage2_tc_kernel<10, 1>, sm);  // the k of cfg3/cfg5: no k-th select
             else if (k <= 16) launch(stage2_tc_kernel<16, 1>, sm);
             else launch(stage2_tc_kernel<32, 1>, sm);
         } else {
@@ -1462,6 +1486,7 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
             if (k == 1) launch(stage2_tc_kernel<1, 2>, sm);
             else if (k <= 4) launch(stage2_tc_kernel<4, 2>, sm);
             else if (k <= 8) launch(stage2_tc_kernel<8, 2>, sm);
+            else if (k == 10) launch(stage2_tc_kernel<10, 2>, sm);  // the k of cfg3/cfg5: no k-th select
             else if (k <= 16) launch(stage2_tc_kernel<16, 2>, sm);
             else launch(stage2_tc_kernel<32, 2>, sm);
         }
@@ -1674,30 +1699,30 @@ int tc_bf_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int
     tmp.xp = const_cast<float *>(x);
     tmp.n_local = n;
     tmp.tc = tc;
-    PruneOut po;
-    int rc = RBC_OK;
-    auto run = [&]() -> int {
-        RBC_CHECK(po.gamma.alloc(nq, st));
-        RBC_CHECK(po.nseg.alloc(nq, st));
-        RBC_CHECK(po.seg_off.alloc(nq + 1, st));
-        RBC_CHECK(po.seg_start.alloc(nq, st));
-        RBC_CHECK(po.seg_len.alloc(nq, st));
-        RBC_CHECK(po.seg_list.alloc(nq, st));
-        RBC_CHECK(po.seg_d1.alloc(nq, st));
-        RBC_CHECK(po.order_key.alloc(nq, st));
-        RBC_CHECK(po.qorder.alloc(nq, st));
-        po.total_segs = nq;
-        bf_queries_kernel<<<grid_for(nq + 1, 256), 256, 0, st>>>(
-            q, nq, d, cen.get(), static_cast<int32_t>(n), po.gamma.get(), po.nseg.get(), po.seg_off.get(),
+    // queries in batches of <= 1M rows (the candidate buffers are ~2.3 KB per query at k = 1)
+    auto run = [&](const float *qb, int64_t m, uint64_t *kb) -> int {
+        PruneOut po;
+        RBC_CHECK(po.gamma.alloc(m, st));
+        RBC_CHECK(po.nseg.alloc(m, st));
+        RBC_CHECK(po.seg_off.alloc(m + 1, st));
+        RBC_CHECK(po.seg_start.alloc(m, st));
+        RBC_CHECK(po.seg_len.alloc(m, st));
+        RBC_CHECK(po.seg_list.alloc(m, st));
+        RBC_CHECK(po.seg_d1.alloc(m, st));
+        RBC_CHECK(po.order_key.alloc(m, st));
+        RBC_CHECK(po.qorder.alloc(m, st));
+        po.total_segs = m;
+        bf_queries_kernel<<<grid_for(m + 1, 256), 256, 0, st>>>(
+            qb, m, d, cen.get(), static_cast<int32_t>(n), po.gamma.get(), po.nseg.get(), po.seg_off.get(),
             po.seg_start.get(), po.seg_len.get(), po.seg_list.get(), po.seg_d1.get(), po.order_key.get(),
             po.qorder.get());
         RBC_LAUNCHED();
         DevBuf<int64_t> status;
         RBC_CHECK(status.alloc(2, st));
-        const int64_t cap_work = (nq + kRows - 1) / kRows + 64;  // one work item per tile
+        const int64_t cap_work = (m + kRows - 1) / kRows + 64;  // one work item per tile
         const char *capenv = getenv("RBC_BF_CAP");  // diagnostic override of the candidate-group capacity
         const int capg = capenv ? atoi(capenv) : 16 + 8 * k;
-        RBC_CHECK(tc_stage2(&tmp, q, nq, k, po, keys, cap_work, status.get(), st, capg));
+        RBC_CHECK(tc_stage2(&tmp, qb, m, k, po, kb, cap_work, status.get(), st, capg));
         int64_t h[2] = {0, 0};
         RBC_CUDA(cudaMemcpyAsync(h, status.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
         RBC_CUDA(cudaStreamSynchronize(st));
@@ -1705,7 +1730,10 @@ int tc_bf_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int
         if (h[0] > cap_work) return fail(RBC_ECUDA, "brute-force work items exceed one per tile");
         return RBC_OK;
     };
-    rc = run();
+    const int64_t batch = int64_t(1) << 20;
+    int rc = RBC_OK;
+    for (int64_t q0 = 0; q0 < nq && rc == RBC_OK; q0 += batch)
+        rc = run(q + q0 * d, nq - q0 < batch ? nq - q0 : batch, keys + q0 * k);
     cudaStreamSynchronize(st);
     tc_free(tc);
     return rc;
@@ -1842,7 +1870,19 @@ __global__ void __launch_bounds__(kRows) bf_tile_fill_kernel(
 
 }  // namespace
 
+static int tc_bf_index_search_batch(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
+                                    cudaStream_t st);
+
 int tc_bf_index_search(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys, cudaStream_t st) {
+    const int64_t batch = int64_t(1) << 20;  // candidate buffers ~2.3 KB per query at k = 1
+    for (int64_t q0 = 0; q0 < nq; q0 += batch)
+        RBC_CHECK(tc_bf_index_search_batch(idx, q + q0 * idx->d, nq - q0 < batch ? nq - q0 : batch, k,
+                                           keys + q0 * k, st));
+    return RBC_OK;
+}
+
+static int tc_bf_index_search_batch(const rbc_index *idx, const float *q, int64_t nq, int k, uint64_t *keys,
+                                    cudaStream_t st) {
     if (nq == 0) return RBC_OK;
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
     if (!tc || k < 1 || k > 32) return fail(RBC_EINVAL, "tc brute force: unsupported index or k");

@@ -1,4 +1,4 @@
-"""Profiling driver: build the cfg2 index, run `--iters` exact searches (for ncu / launch lists)."""
+"""Profiling driver: build a config's exact index (default cfg2), run `--iters` exact searches (for ncu / launch lists)."""
 import argparse
 import os
 import sys
@@ -11,8 +11,11 @@ import bench  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=2)
-    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--config", default="cfg2")
     args = ap.parse_args()
+    bench.select_config(args.config, args.k)
+    args.k = bench.K
     import ctypes
 
     import torch
@@ -22,6 +25,8 @@ def main():
 
     x, q = bench.gen_inputs(0)
     index = rbc.build_exact(rbc.DataMatrix(x), bench.NR, rbc.MetricSpec("l2", bench.D), seed=bench.REP_SEED)
+    torch.cuda.synchronize()
+    print("built", file=sys.stderr)
     q_dev = _lib.to_device(q)
     keys = torch.empty((bench.NQ, args.k), dtype=torch.int64, device="cuda")
     stats = _lib.SearchStatsC(None, None, None, None)
