@@ -70,9 +70,12 @@ int rbc_profile_enable(int on);
 int rbc_profile_read(double *ms, int64_t *count, int32_t n_phases);
 
 /* Engine selection for the heavy scans: 0 = auto (tcgen05 filter + exact
- * fp64 re-rank where supported and the scan is large enough to pay, the
- * default), 1 = exact fp64 SIMT only, 2 = tcgen05 wherever supported, at any
- * size.  All produce identical results; 1 and 2 exist for A/B checks. */
+ * fp64 re-rank for L2, the fp32 SIMT filter + exact fp64 re-rank for L1 and
+ * where the tensor cores do not apply, each where the scan is large enough to
+ * pay; the default), 1 = exact fp64 SIMT only, 2 = the filtered engines
+ * wherever supported, at any size, 3 = the fp32 SIMT filter for every
+ * brute-force-shaped scan (L2 too).  All produce identical results; 1-3 exist
+ * for A/B checks. */
 int rbc_set_engine(int mode);
 /* Queries of the last exact search whose candidate buffer overflowed and
  * were recomputed by the exact SIMT scan (diagnostic). */
@@ -84,6 +87,9 @@ int64_t rbc_tc_bf_calls(void);
 /* Launches of the tcgen05 list-scan kernel (stage2_tc_kernel: exact-search stage 2
  * and every tensor-core brute force) since the library loaded (diagnostic). */
 int64_t rbc_tc_scan_calls(void);
+/* Launches of the fp32 SIMT filter scan (simt_scan_kernel: the L1 engine, and small
+ * L2 scans) since the library loaded (diagnostic). */
+int64_t rbc_simt_scan_calls(void);
 
 /* metric.py:57-76 pairwise_distances (and brute_force.py:220-251
  * distance_rows): out[m,p] = dist(a[i], b[j]), bit-exact. */

@@ -622,19 +622,21 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
         if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
             rc = fail(RBC_ECUDA, "one-shot index");
     }
-    // L2: the s-lists as tensor-core operands (rows gathered per list; perm aliases lists)
-    if (rc == RBC_OK && metric == RBC_L2 && d <= 128 && n_reps * static_cast<int64_t>(s) + 4096 < (int64_t(1) << 31)) {
+    // the s-lists' rows gathered per list (xp; perm aliases lists): the operand of the SIMT
+    // filter scan, and for L2 the source of the tensor-core operands
+    if (rc == RBC_OK && d <= 128 && n_reps * static_cast<int64_t>(s) + 4096 < (int64_t(1) << 31)) {
         const int64_t total = n_reps * static_cast<int64_t>(s);
-        rc = dalloc(&idx->offsets, n_reps + 1, idx->bytes);
-        if (rc == RBC_OK) rc = dalloc(&idx->xp, total * d, idx->bytes);
+        rc = dalloc(&idx->xp, total * d, idx->bytes);
         if (rc == RBC_OK) {
             gather_rows_i32_kernel<<<grid_for(total * d, 256, 148 * 64), 256, 0, st>>>(idx->x, idx->lists, total, d,
                                                                                       idx->xp);
             note_launch();
             idx->perm = idx->lists;
             idx->n_local = total;
-            rc = tc_one_shot_prepare(idx, idx->xp, st);
         }
+        if (rc == RBC_OK && metric == RBC_L2) rc = dalloc(&idx->offsets, n_reps + 1, idx->bytes);
+        if (rc == RBC_OK && metric == RBC_L2) rc = tc_one_shot_prepare(idx, idx->xp, st);
+        if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "one-shot list rows");
     }
     if (rc != RBC_OK) {
         rbc_index_destroy(idx);

@@ -198,12 +198,9 @@ int build_one_shot(const float *x, int64_t n, int d, int metric, const int64_t *
     RBC_CHECK(reps.alloc(nr * d, st));
     RBC_CHECK(keys.alloc(nr * s, st));
     RBC_CHECK(gather_rows(x, rep_ids, nr, d, reps.get(), st));
-    if (s <= kMaxWarpK) {
-        AllSrc src{x, n, d};
-        RBC_CHECK(launch_topk(reps.get(), nr, d, metric, s, src, keys.get(), st));
-    } else {
-        RBC_CHECK(topk_sorted_all(reps.get(), nr, x, n, d, metric, s, keys.get(), st));
-    }
+    // the s nearest points of every rep: bf_search(reps, X, s) (rbc.py:196-200) through the
+    // brute-force dispatch (tensor cores / SIMT filter / exact)
+    RBC_CHECK(bf_search_keys(reps.get(), nr, x, n, d, metric, s, keys.get(), st));
     one_shot_finish_kernel<<<grid_for(nr * s, 256), 256, 0, st>>>(keys.get(), nr, s, lists, radii);
     RBC_LAUNCHED();
     return RBC_OK;

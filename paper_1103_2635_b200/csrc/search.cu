@@ -630,6 +630,8 @@ int one_shot_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k
     ProfScope ps(kPhaseScan, st);
     if (!force_exact_engine() && tc_one_shot_supported(idx, nq, k))
         return tc_one_shot_scan(idx, q, nq, k, nearest.get(), keys, st);
+    if (!force_exact_engine() && simt_one_shot_supported(idx, nq, k))
+        return simt_one_shot_scan(idx, q, nq, k, nearest.get(), keys, st);
     RowSrc src{idx->x, idx->lists, row.get(), idx->s, idx->d};
     return launch_topk(q, nq, idx->d, idx->metric, k, src, keys, st);
 }

@@ -8,18 +8,26 @@
 
 namespace rbc {
 
-static int g_engine = 0;  // 0 = auto, 1 = exact SIMT only, 2 = tensor cores wherever supported (tests)
+// 0 = auto, 1 = exact SIMT only, 2 = the filtered engines (tensor cores, else the fp32 SIMT
+// filter) wherever supported, 3 = the fp32 SIMT filter for every brute-force-shaped scan
+// (tests: the L2 SIMT path)
+static int g_engine = 0;
 
 bool force_exact_engine() { return g_engine == 1; }
 
 // Brute-force-shaped scans below this many (query, point) pairs stay on the exact SIMT scan
 // in auto mode: the tensor-core path's operand preparation and host round trips cost more
 // than the scan (e.g. cfg1's 1k x 100 one-shot search: 0.03 ms SIMT vs 0.26 ms).
-int64_t tc_min_pairs() { return g_engine == 2 ? 0 : (int64_t(1) << 24); }
+int64_t tc_min_pairs() { return g_engine == 2 ? 0 : g_engine == 3 ? INT64_MAX : (int64_t(1) << 24); }
+// ... and the fp32 SIMT filter pays from a few million pairs (its grouping and launch
+// sequence cost ~20 us)
+int64_t simt_min_pairs() { return g_engine >= 2 ? 0 : (int64_t(1) << 22); }
 
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
                  cudaStream_t st) {
     if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, 1)) return tc_bf_keys(q, nq, x, n, d, 1, keys, st);
+    if (!force_exact_engine() && simt_supported(d, 1) && nq * n >= simt_min_pairs())
+        return simt_dense_topk(q, nq, x, n, d, metric, 1, nullptr, keys, st);
     AllSrc src{x, n, d};
     return launch_topk(q, nq, d, metric, 1, src, keys, st);
 }
@@ -27,6 +35,8 @@ int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, i
 int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
                    cudaStream_t st) {
     if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, k)) return tc_bf_keys(q, nq, x, n, d, k, keys, st);
+    if (!force_exact_engine() && simt_supported(d, k) && nq * n >= simt_min_pairs())
+        return simt_dense_topk(q, nq, x, n, d, metric, k, nullptr, keys, st);
     if (k > kMaxWarpK) return topk_sorted_all(q, nq, x, n, d, metric, k, keys, st);
     AllSrc src{x, n, d};
     return launch_topk(q, nq, d, metric, k, src, keys, st);
@@ -73,7 +83,8 @@ int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const P
 }  // namespace rbc
 
 extern "C" int rbc_set_engine(int mode) {
-    if (mode < 0 || mode > 2) return rbc::fail(RBC_EINVAL, "engine must be 0 (auto), 1 (exact) or 2 (tensor cores)");
+    if (mode < 0 || mode > 3)
+        return rbc::fail(RBC_EINVAL, "engine must be 0 (auto), 1 (exact), 2 (filtered engines) or 3 (SIMT filter)");
     rbc::g_engine = mode;
     return RBC_OK;
 }

@@ -64,9 +64,20 @@ int64_t &last_overflow_count();
 int64_t stage2_work_capacity(const rbc_index *idx, int64_t nq);
 void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed);
 
+// fp32 SIMT filter + exact fp64 re-rank (simt_scan.cu): the L1 engine, and L2 where the
+// tensor-core scans do not apply (d <= 128, k <= 32)
+bool simt_supported(int d, int k);
+bool simt_one_shot_supported(const rbc_index *idx, int64_t nq, int k);
+int simt_dense_topk(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k,
+                    const int32_t *pid, uint64_t *keys, cudaStream_t st);
+int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
+                       cudaStream_t st);
+
 // engine selection (RBC_ENGINE env: "auto" (default) | "exact")
 bool force_exact_engine();
 // minimum (query, point) pairs for the brute-force-shaped tensor-core scans (0 in mode 2)
 int64_t tc_min_pairs();
+// minimum (query, point) pairs for the fp32 SIMT filter scans (0 in modes 2 and 3)
+int64_t simt_min_pairs();
 
 }  // namespace rbc
