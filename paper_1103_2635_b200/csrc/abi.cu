@@ -622,22 +622,24 @@ int rbc_index_one_shot_create(const float *x, int64_t n, int32_t d, int32_t metr
         if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
             rc = fail(RBC_ECUDA, "one-shot index");
     }
-    // the s-lists' rows gathered per list (xp; perm aliases lists): the operand of the SIMT
-    // filter scan, and for L2 the source of the tensor-core operands
-    if (rc == RBC_OK && d <= 128 && n_reps * static_cast<int64_t>(s) + 4096 < (int64_t(1) << 31)) {
+    // the SIMT filter's operands: padded representatives and the s-lists' rows gathered per
+    // list (x4)
+    if (rc == RBC_OK) rc = simt_index_prepare(idx, st);
+    // L2: the s-lists as tensor-core operands (rows gathered per list; perm aliases lists)
+    if (rc == RBC_OK && metric == RBC_L2 && d <= 128 && n_reps * static_cast<int64_t>(s) + 4096 < (int64_t(1) << 31)) {
         const int64_t total = n_reps * static_cast<int64_t>(s);
-        rc = dalloc(&idx->xp, total * d, idx->bytes);
+        rc = dalloc(&idx->offsets, n_reps + 1, idx->bytes);
+        if (rc == RBC_OK) rc = dalloc(&idx->xp, total * d, idx->bytes);
         if (rc == RBC_OK) {
             gather_rows_i32_kernel<<<grid_for(total * d, 256, 148 * 64), 256, 0, st>>>(idx->x, idx->lists, total, d,
                                                                                       idx->xp);
             note_launch();
             idx->perm = idx->lists;
             idx->n_local = total;
+            rc = tc_one_shot_prepare(idx, idx->xp, st);
         }
-        if (rc == RBC_OK && metric == RBC_L2) rc = dalloc(&idx->offsets, n_reps + 1, idx->bytes);
-        if (rc == RBC_OK && metric == RBC_L2) rc = tc_one_shot_prepare(idx, idx->xp, st);
-        if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "one-shot list rows");
     }
+    if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "one-shot index operands");
     if (rc != RBC_OK) {
         rbc_index_destroy(idx);
         return rc;
@@ -653,7 +655,8 @@ int rbc_index_destroy(rbc_index *idx) {
     tc_index_release(idx);
     tc1_index_release(idx);
     void *ptrs[] = {idx->x, idx->reps, idx->rep_ids, idx->radii, idx->offsets,
-                    idx->perm == idx->lists ? nullptr : idx->perm, idx->list_dists, idx->xp, idx->lists};
+                    idx->perm == idx->lists ? nullptr : idx->perm, idx->list_dists, idx->xp, idx->lists,
+                    idx->reps4, idx->x4};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete idx;

@@ -36,6 +36,11 @@ struct rbc_index {
     // one-shot: [nr, s] point ids
     int32_t *lists = nullptr;
 
+    // fp32 SIMT filter operands (simt_scan.cu), rows padded to d4 = d rounded up to 4:
+    // the representatives and (one-shot) the s-lists' rows gathered per list
+    float *reps4 = nullptr;  // [nr, d4]
+    float *x4 = nullptr;     // [nr * s, d4]
+
     // stage-2 work-item capacity learned from previous searches (tile unions)
     mutable int64_t s2_work_per_tile = 24;
 

@@ -623,7 +623,7 @@ int one_shot_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k
     // nearest representative by key64 argmin (lowest position on ties)
     {
         ProfScope ps(kPhaseStage1, st);
-        RBC_CHECK(nearest_rows(q, nq, idx->reps, idx->nr, idx->d, idx->metric, nearest.get(), st));
+        RBC_CHECK(nearest_rows(q, nq, idx->reps, idx->nr, idx->d, idx->metric, nearest.get(), st, idx->reps4));
         argmin_row_kernel<<<grid_for(nq, 256), 256, 0, st>>>(nearest.get(), nq, row.get(), gamma);
         RBC_LAUNCHED();
     }

@@ -1,12 +1,12 @@
 // simt_scan.cu -- the fp32 SIMT filter with an exact fp64 re-rank: the L1 engine (north
 // star: "L1 is an all-SIMT path"), and the L2 engine wherever the tensor-core scans do not
-// pay (small problems, d > 128).
+// apply (d > 128) or do not pay (small scans).
 //
-// Every (query, point) pair is evaluated once in fp32 on the FP32 pipe; only pairs whose
-// fp32 distance can still reach the query's k best are recomputed with the reference
-// arithmetic (common.cuh exact_dist: fp64, coordinate order, one rounding to fp32,
-// metric.py:36-54) and enter an exact key64 top-k (brute_force.py:62-82).  The filter is
-// rigorous, so the keys are the reference's bit for bit:
+// Every (query, point) pair is evaluated once in fp32; only pairs whose fp32 distance can
+// still reach the query's k best are recomputed with the reference arithmetic
+// (common.cuh exact_dist: fp64, coordinate order, one rounding to fp32, metric.py:36-54)
+// and enter an exact key64 top-k (brute_force.py:62-82).  The filter is rigorous, so the
+// keys are the reference's bit for bit:
 //
 //   S  = fp32 sum of |a_k - b_k| (L1) or (a_k - b_k)^2 (L2, FMA), any summation order
 //   |S - D| <= gamma_{d+1} D + d 2^-148       (D = the real-valued sum)
@@ -14,20 +14,23 @@
 //
 // so a point with S > T = S_k (1 + (4 d + 16) 2^-24) + d 1e-35, S_k the k-th smallest
 // fp32 sum seen so far, has a reference distance strictly above k already-seen points'
-// and cannot be in the answer.  Points that pass are queued per thread (shared memory)
-// and re-checked against the (tighter) bound once per tile before the exact fp64
-// evaluation, so a warp pays for ~one exact distance per tile instead of one per lane.
+// and cannot be in the answer.
 //
-// Work decomposition.  A CTA (256 threads) owns one work item: up to 256 queries and a
-// contiguous range of point rows.  Point tiles are staged in shared memory with
-// cp.async (two stages); every thread holds its query in registers and reads the tile
-// rows as warp broadcasts.  When an item has fewer than 256 queries the point range is
-// split over R = 256 / queries thread slices and the slices' exact top-k lists are
-// merged at the end.
-//   * dense items (bf_search, nearest representative, build assignment): all queries x
-//     all rows, query blocks x point splits (splits merged by merge_parts);
+// Work decomposition.  A CTA (8 warps) owns one work item: up to 32 x QPT queries (lane
+// l holds queries l, l + 32, ..., coordinates in registers) and a range of point rows,
+// staged through shared memory in tiles (cp.async, two stages) with a 16-byte aligned row
+// stride d4 = d rounded up to 4 (zero padded; |0 - 0| adds nothing).  Warp w scans tile
+// rows w, w + 8, ...: every lane of a warp reads the same row (a shared-memory broadcast)
+// and uses it for QPT queries.  After each tile the warps publish their per-query bounds
+// and all adopt the minimum (any warp's k-th smallest sum bounds the union's), so the
+// eight-way split filters as tightly as one scan; the warps' exact lists are merged at
+// the end.
+//   * dense items (bf_search, nearest representative, build assignment): query chunks x
+//     point splits (splits merged by merge_parts);
 //   * grouped items (one-shot search, search.py:114-120): queries sorted by nearest
-//     representative, one item per (representative, 256 of its queries) x its s-list.
+//     representative, one item per (representative, chunk of its queries) x its s-list.
+// Points that pass the filter are queued per lane in shared memory and drained after the
+// bound exchange, so most stale candidates are dropped before the exact fp64 evaluation.
 #include <cub/cub.cuh>
 
 #include <atomic>
@@ -41,45 +44,35 @@ namespace rbc {
 
 namespace {
 
-constexpr int kST = 256;   // threads per CTA = most queries per work item
-constexpr int kQLen = 8;   // pending candidates per thread (shared memory queue)
+constexpr int kW = 8;        // warps per CTA (point slices)
+constexpr int kT = 32 * kW;
+constexpr int kQLen = 8;     // queued candidates per lane
 
 struct __align__(16) ScanItem {
     int32_t qbeg;  // first position in qorder
-    int32_t qcnt;  // queries (<= kST x QPT)
+    int32_t qcnt;  // queries (<= 32 x QPT)
     int32_t pbeg;  // first point row
     int32_t pcnt;  // point rows
 };
 
 struct SimtParams {
-    const float *q;
+    const float *q;          // queries [nq][d]
     int64_t nq;
     int d;
-    int d4;                  // row stride of the shared-memory tiles (d rounded up to 4)
-    int tp;                  // points per tile
-    const int32_t *qorder;   // grouped: query of each position
-    const float *p;          // point rows [*][d]
-    const int32_t *pid;      // id of each point row (nullptr: the row index)
+    int d4;                  // row stride of p (d rounded up to 4)
+    int tp;                  // rows per tile
+    const int32_t *qorder;   // grouped: query of each sorted position
     const ScanItem *items;   // grouped items (nullptr: dense)
     const int32_t *nitems;
+    const float *p;          // point rows [*][d4], 16-byte aligned
+    const int32_t *pid;      // id of each point row (nullptr: the row index)
+    int64_t nqc;             // dense: query chunks
     int64_t np;              // dense: point rows
     int64_t pchunk;          // dense: rows per split (< 2^31)
-    int nqb;                 // dense: query blocks
-    int qblk;                // dense: queries per block
     int k;
-    uint64_t *out;           // [slot][nq][k]
+    int qpt;                 // queries per lane (host side: selects the instantiation)
+    uint64_t *out;           // [split][nq][k]
 };
-
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // packed fp32 pairs (FADD2 / FFMA2 on sm_100)
 __device__ __forceinline__ uint64_t f2u(float2 v) { return *reinterpret_cast<const uint64_t *>(&v); }
@@ -107,7 +100,7 @@ __device__ __forceinline__ void acc2(float2 q, float2 x, float2 &acc) {
     }
 }
 
-// one fp32 sum into a running top-KT of fp32 sums; returns the new threshold T
+// one fp32 sum into the running top-KT of fp32 sums; returns the new threshold T
 template <int KT>
 __device__ __forceinline__ float topk_push(float (&sv)[KT], float S, int k, float fac, float absl) {
     float x = S;
@@ -126,15 +119,23 @@ __device__ __forceinline__ float topk_push(float (&sv)[KT], float S, int k, floa
     return fmaf(kth, fac, absl);
 }
 
-// QPT queries per thread (each tile row read from shared memory once for all of them),
-// DMAX >= d coordinates held in registers per query
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int METRIC, int DMAX, int KT, int QPT>
-__global__ void __launch_bounds__(kST) simt_scan_kernel(const SimtParams P) {
+__global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel(const SimtParams P) {
     extern __shared__ __align__(16) float smem[];
-    // item
     int64_t qbeg, pbeg;
     int qcnt, pcnt;
-    int slot = 0;
+    int64_t slot = 0;
     if (P.items) {
         if (static_cast<int>(blockIdx.x) >= *P.nitems) return;
         const ScanItem it = P.items[blockIdx.x];
@@ -143,48 +144,34 @@ __global__ void __launch_bounds__(kST) simt_scan_kernel(const SimtParams P) {
         pbeg = it.pbeg;
         pcnt = it.pcnt;
     } else {
-        const int qb = static_cast<int>(blockIdx.x % P.nqb);
-        slot = static_cast<int>(blockIdx.x / P.nqb);
-        qbeg = static_cast<int64_t>(qb) * P.qblk;
-        qcnt = static_cast<int>(min(static_cast<int64_t>(P.qblk), P.nq - qbeg));
-        pbeg = static_cast<int64_t>(slot) * P.pchunk;
+        const int64_t chunk = blockIdx.x % P.nqc;
+        slot = blockIdx.x / P.nqc;
+        qbeg = chunk * 32 * QPT;
+        qcnt = static_cast<int>(min(static_cast<int64_t>(32 * QPT), P.nq - qbeg));
+        pbeg = slot * P.pchunk;
         pcnt = static_cast<int>(min(P.pchunk, P.np - pbeg));
     }
     const int d = P.d, d4 = P.d4, tp = P.tp, k = P.k;
-    const int tid = threadIdx.x;
-    // nqt query threads (QPT queries each) x R point slices; the slices' exact lists are
-    // merged through shared memory at the end
-    const int nqt = (qcnt + QPT - 1) / QPT;
-    const int R = max(1, min(kST / nqt, kST / k));
-    const bool active = tid < nqt * R;
-    const int qslot = active ? tid % nqt : 0, slice = active ? tid / nqt : 0;
-    int qpos[QPT];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float *tiles = smem;                                            // [2][tp][d4]
+    float *tsh = smem + 2 * tp * d4;                                // [kW][32 QPT] published bounds
+    float *qs_s = tsh + kW * 32 * QPT;                              // [kQLen][kT] queued sums
+    uint32_t *qs_r = reinterpret_cast<uint32_t *>(qs_s + kQLen * kT);  // [kQLen][kT] (u << 28) | row
     const float *qg[QPT];
     float2 qv[QPT][DMAX / 2];
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
-        qpos[u] = qslot + u * nqt;
-        const int pos = qpos[u] < qcnt ? qpos[u] : qslot;  // a missing query repeats the thread's first
+        const int pos = 32 * u + lane < qcnt ? 32 * u + lane : 0;  // a missing query repeats the first
         const int64_t qi = P.qorder ? P.qorder[qbeg + pos] : qbeg + pos;
         qg[u] = P.q + qi * d;
 #pragma unroll
         for (int c = 0; c < DMAX / 2; ++c)
             qv[u][c] = make_float2(2 * c < d ? __ldg(qg[u] + 2 * c) : 0.f, 2 * c + 1 < d ? __ldg(qg[u] + 2 * c + 1) : 0.f);
     }
-
-    float *tiles = smem;                                              // [2][tp][d4]
-    float *qs_s = smem + 2 * tp * d4;                                 // [kQLen][kST] pending fp32 sums
-    uint32_t *qs_r = reinterpret_cast<uint32_t *>(qs_s + kQLen * kST);  // [kQLen][kST] (query << 31) | row
-    // zero the pad columns once (cp.async writes only columns < d)
-    if (d4 != d)
-        for (int e = tid; e < 2 * tp; e += kST)
-            for (int c = d; c < d4; ++c) tiles[e * d4 + c] = 0.f;
-
     const float fac = 1.0f + static_cast<float>(4 * d + 16) * (1.0f / 16777216.0f);
     const float absl = static_cast<float>(d) * 1e-35f;
-    float sv[QPT][KT];
+    float sv[QPT][KT], T[QPT];
     uint64_t ek[QPT][KT];
-    float T[QPT];
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
         T[u] = __int_as_float(0x7f800000);
@@ -195,148 +182,129 @@ __global__ void __launch_bounds__(kST) simt_scan_kernel(const SimtParams P) {
         }
     }
     int qn = 0;
-
-    auto issue = [&](int t0, int buf) {
-        const int tn = min(tp, pcnt - t0);
-        const float *src = P.p + (pbeg + t0) * d;
-        float *dst = tiles + buf * tp * d4;
-        const int total = tn * d;
-        for (int e = tid; e < total; e += kST) {
-            const int r = e / d, c = e - r * d;
-            cp_async4(dst + r * d4 + c, src + e);
+    // exact fp64 evaluation of the queued points that still qualify
+    auto drain = [&]() {
+        for (int e = 0; e < qn; ++e) {
+            const float sq = qs_s[e * kT + tid];
+            const uint32_t rw = qs_r[e * kT + tid];
+            const int u = static_cast<int>(rw >> 28);
+            float Tu = T[0];
+            const float *qq = qg[0];
+#pragma unroll
+            for (int v = 1; v < QPT; ++v)
+                if (u == v) {
+                    Tu = T[v];
+                    qq = qg[v];
+                }
+            if (sq <= Tu) {
+                const int64_t row = pbeg + static_cast<int64_t>(rw & 0x0FFFFFFFu);
+                const uint32_t id = P.pid ? static_cast<uint32_t>(P.pid[row]) : static_cast<uint32_t>(row);
+                const uint64_t key = pack_key(exact_dist<METRIC>(qq, P.p + row * d4, d), id);
+#pragma unroll
+                for (int v = 0; v < QPT; ++v)
+                    if (u == v && key < ek[v][KT - 1]) sorted_insert<KT>(ek[v], key);
+            }
         }
+        qn = 0;
+    };
+    // tile copies: the tile's rows are contiguous and 16-byte aligned (padded stride d4)
+    auto tile_rows = [&](int t0) { return min(t0 == 0 ? 2 * kW : tp, pcnt - t0); };
+    auto issue = [&](int t0, int buf) {
+        const int tn = tile_rows(t0);
+        const float4 *src = reinterpret_cast<const float4 *>(P.p + (pbeg + t0) * d4);
+        float4 *dst = reinterpret_cast<float4 *>(tiles + buf * tp * d4);
+        for (int e = tid; e < tn * (d4 >> 2); e += kT) cp_async16(dst + e, src + e);
         cp_async_commit();
     };
 
-    const int ntiles = (pcnt + tp - 1) / tp;
-    __syncthreads();  // pad zeros before the first cp.async lands next to them
-    if (ntiles > 0) issue(0, 0);
-    for (int t = 0; t < ntiles; ++t) {
-        const int buf = t & 1;
-        if (t + 1 < ntiles) {
-            issue((t + 1) * tp, buf ^ 1);
+    // tiles: a short first one (two rows per warp: after its bound exchange every query
+    // starts from the best of 16 rows, so the later tiles rarely queue a candidate), then
+    // tp rows each
+    int t = 0;
+    if (pcnt > 0) issue(0, 0);
+    for (int t0 = 0; t0 < pcnt; t0 += tile_rows(t0), ++t) {
+        const int buf = t & 1, tn = tile_rows(t0);
+        if (t0 + tn < pcnt) {
+            issue(t0 + tn, buf ^ 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        if (active) {
-            const int t0 = t * tp;
-            const int tn = min(tp, pcnt - t0);
-            const float *tile = tiles + buf * tp * d4;
-            // the inner loop leaves early only when the queue may overflow; the queue is drained
-            // at one site (the exact fp64 evaluation is inlined once)
-            int j = slice;
-            for (;;) {
-                for (; j < tn; j += R) {
-                    const float4 *xr = reinterpret_cast<const float4 *>(tile + j * d4);
-                    float2 acc[QPT][2];
+        const float *tile = tiles + buf * tp * d4;
+        for (int j = warp; j < tn; j += kW) {
+            const float4 *xr = reinterpret_cast<const float4 *>(tile + j * d4);
+            float2 acc[QPT][2];
 #pragma unroll
-                    for (int u = 0; u < QPT; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
+            for (int u = 0; u < QPT; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int c = 0; c < DMAX / 4; ++c) {
-                        if (4 * c < d) {
-                            const float4 x = xr[c];
-#pragma unroll
-                            for (int u = 0; u < QPT; ++u) {
-                                acc2<METRIC>(qv[u][2 * c], make_float2(x.x, x.y), acc[u][0]);
-                                acc2<METRIC>(qv[u][2 * c + 1], make_float2(x.z, x.w), acc[u][1]);
-                            }
-                        }
-                    }
+            for (int c = 0; c < DMAX / 4; ++c) {
+                if (4 * c < d) {
+                    const float4 x = xr[c];
 #pragma unroll
                     for (int u = 0; u < QPT; ++u) {
-                        const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
-                        if (S < sv[u][KT - 1]) T[u] = topk_push<KT>(sv[u], S, k, fac, absl);
-                        if (S <= T[u]) {
-                            qs_s[qn * kST + tid] = S;
-                            qs_r[qn * kST + tid] = (static_cast<uint32_t>(u) << 31) | static_cast<uint32_t>(t0 + j);
-                            ++qn;
-                        }
-                    }
-                    if (qn > kQLen - QPT) {
-                        j += R;
-                        break;
+                        acc2<METRIC>(qv[u][2 * c], make_float2(x.x, x.y), acc[u][0]);
+                        acc2<METRIC>(qv[u][2 * c + 1], make_float2(x.z, x.w), acc[u][1]);
                     }
                 }
-                // exact fp64 evaluation of the queued points that can still qualify
-                for (int e = 0; e < qn; ++e) {
-                    const float s = qs_s[e * kST + tid];
-                    const uint32_t rw = qs_r[e * kST + tid];
-                    const int u = static_cast<int>(rw >> 31);
-                    float Tu = T[0];
-#pragma unroll
-                    for (int v = 1; v < QPT; ++v)
-                        if (u == v) Tu = T[v];
-                    if (s <= Tu) {
-                        const int64_t row = static_cast<int64_t>(rw & 0x7FFFFFFFu) + pbeg;
-                        const uint32_t id = P.pid ? static_cast<uint32_t>(P.pid[row]) : static_cast<uint32_t>(row);
-                        const float *qq = qg[0];
-#pragma unroll
-                        for (int v = 1; v < QPT; ++v)
-                            if (u == v) qq = qg[v];
-                        const uint64_t key = pack_key(exact_dist<METRIC>(qq, P.p + row * d, d), id);
-#pragma unroll
-                        for (int v = 0; v < QPT; ++v)
-                            if (u == v && key < ek[v][KT - 1]) sorted_insert<KT>(ek[v], key);
-                    }
-                }
-                qn = 0;
-                if (j >= tn) break;
             }
-        }
-        __syncthreads();  // the buffer is refilled by the next issue
-    }
-    // merge the slices' exact lists (R > 1) and write the k best keys
-    if (R == 1) {
-        if (active)
 #pragma unroll
-            for (int u = 0; u < QPT; ++u)
-                if (qpos[u] < qcnt) {
-                    const int64_t qi = P.qorder ? P.qorder[qbeg + qpos[u]] : qbeg + qpos[u];
-                    uint64_t *outq = P.out + (static_cast<int64_t>(slot) * P.nq + qi) * k;
-#pragma unroll
-                    for (int j = 0; j < KT; ++j)
-                        if (j < k) outq[j] = ek[u][j];
+            for (int u = 0; u < QPT; ++u) {
+                const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
+                if (S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
+                if (S <= T[u]) {
+                    qs_s[qn * kT + tid] = S;
+                    qs_r[qn * kT + tid] = (static_cast<uint32_t>(u) << 28) | static_cast<uint32_t>(t0 + j);
+                    ++qn;
                 }
-        return;
+            }
+            if (__any_sync(0xffffffffu, qn > kQLen - QPT)) drain();
+        }
+        // bound exchange: every warp adopts the smallest published bound of each query
+#pragma unroll
+        for (int u = 0; u < QPT; ++u) tsh[warp * 32 * QPT + 32 * u + lane] = T[u];
+        __syncthreads();  // (also: the buffer is refilled by the next issue)
+#pragma unroll
+        for (int u = 0; u < QPT; ++u) {
+            float m = T[u];
+#pragma unroll
+            for (int w = 0; w < kW; ++w) m = fminf(m, tsh[w * 32 * QPT + 32 * u + lane]);
+            T[u] = m;
+        }
+        drain();
     }
-    uint64_t *mk = reinterpret_cast<uint64_t *>(smem);  // [R][qcnt][k] (the tiles are done)
-    if (active)
-#pragma unroll
-        for (int u = 0; u < QPT; ++u)
-            if (qpos[u] < qcnt)
-#pragma unroll
-                for (int j = 0; j < KT; ++j)
-                    if (j < k) mk[(static_cast<int64_t>(slice) * qcnt + qpos[u]) * k + j] = ek[u][j];
+    // merge the warps' exact lists: mk[w][pos][k] (the tiles are done)
     __syncthreads();
-    for (int qp = tid; qp < qcnt; qp += kST) {
+    uint64_t *mk = reinterpret_cast<uint64_t *>(smem);
+#pragma unroll
+    for (int u = 0; u < QPT; ++u)
+        if (32 * u + lane < qcnt)
+#pragma unroll
+            for (int j = 0; j < KT; ++j)
+                if (j < k) mk[(static_cast<int64_t>(warp) * qcnt + 32 * u + lane) * k + j] = ek[u][j];
+    __syncthreads();
+    for (int qp = tid; qp < qcnt; qp += kT) {
         uint64_t best[KT];
 #pragma unroll
         for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
-        for (int s = 0; s < R; ++s)
+        for (int w = 0; w < kW; ++w)
             for (int j = 0; j < k; ++j) {
-                const uint64_t key = mk[(static_cast<int64_t>(s) * qcnt + qp) * k + j];
-                if (key >= best[KT - 1]) break;  // each slice's list ascends
+                const uint64_t key = mk[(static_cast<int64_t>(w) * qcnt + qp) * k + j];
+                if (key >= best[KT - 1]) break;  // each warp's list ascends
                 sorted_insert<KT>(best, key);
             }
         const int64_t qi = P.qorder ? P.qorder[qbeg + qp] : qbeg + qp;
-        uint64_t *outq = P.out + (static_cast<int64_t>(slot) * P.nq + qi) * k;
+        uint64_t *outq = P.out + (slot * P.nq + qi) * k;
 #pragma unroll
         for (int j = 0; j < KT; ++j)
             if (j < k) outq[j] = best[j];
     }
 }
 
-// ---- one-shot grouping: queries by nearest representative --------------------------------
+// ---- one-shot grouping: queries sorted by nearest representative --------------------------
 __global__ void near_hist_kernel(const uint64_t *__restrict__ near, int64_t nq, int32_t *__restrict__ cnt) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < nq) atomicAdd(&cnt[key_id(near[i])], 1);
-}
-
-__global__ void near_chunks_kernel(const int32_t *__restrict__ cnt, int64_t nr, int qb, int32_t *__restrict__ nchunk) {
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (r < nr) nchunk[r] = (cnt[r] + qb - 1) / qb;
 }
 
 __global__ void near_scatter_kernel(const uint64_t *__restrict__ near, int64_t nq, const int32_t *__restrict__ start,
@@ -345,6 +313,23 @@ __global__ void near_scatter_kernel(const uint64_t *__restrict__ near, int64_t n
     if (i >= nq) return;
     const uint32_t r = key_id(near[i]);
     qorder[start[r] + atomicAdd(&fill[r], 1)] = static_cast<int32_t>(i);
+}
+
+// rows [rows][d] -> [rows][d4] (zero padded), optionally gathered: src row = ids[r]
+__global__ void pad_rows_kernel(const float *__restrict__ src, const int32_t *__restrict__ ids, int64_t rows, int d,
+                                int d4, float *__restrict__ dst) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < rows * d4;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = t / d4;
+        const int c = static_cast<int>(t - r * d4);
+        const int64_t sr = ids ? ids[r] : r;
+        dst[t] = c < d ? src[sr * d + c] : 0.f;
+    }
+}
+
+__global__ void near_chunks_kernel(const int32_t *__restrict__ cnt, int64_t nr, int qb, int32_t *__restrict__ nchunk) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r < nr) nchunk[r] = (cnt[r] + qb - 1) / qb;
 }
 
 __global__ void near_items_kernel(const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
@@ -365,69 +350,67 @@ __global__ void near_items_kernel(const int32_t *__restrict__ cnt, const int32_t
     if (r == nr - 1) *nitems = istart[r] + nc;
 }
 
-int simt_dmax(int d) { return d <= 24 ? 24 : d <= 32 ? 32 : d <= 64 ? 64 : 128; }
+int simt_dmax(int d) { return d <= 24 ? 24 : d <= 64 ? 64 : 128; }
 int simt_kt(int k) { return k <= 1 ? 1 : k <= 4 ? 4 : k <= 16 ? 16 : 32; }
-// two queries per thread where their coordinates fit the registers (and the merge buffer
-// of two queries x k keys per thread fits shared memory)
-int simt_qpt(int d, int k) { return d <= 32 && k <= 16 ? 2 : 1; }
+// queries per lane: each shared-memory row read serves QPT queries, as registers allow
+// (grouped items with small groups use one: a lane slot left empty costs a full scan)
+int simt_qpt(int d, int k, bool small_groups = false) { return d <= 64 && k <= 16 && !small_groups ? 2 : 1; }
+int simt_tp(int d4) { return d4 <= 32 ? 128 : 64; }
 
-int simt_tp(int d4) { return d4 <= 64 ? 128 : 64; }
-
-size_t simt_smem(int d4, int tp, int k, int qpt) {
+size_t simt_smem(int d4, int k, int qpt) {
+    const int tp = simt_tp(d4);
     const size_t tiles = 2 * static_cast<size_t>(tp) * d4 * sizeof(float);
-    const size_t merge = static_cast<size_t>(kST) * qpt * k * sizeof(uint64_t);
-    return (tiles > merge ? tiles : merge) + kQLen * kST * (sizeof(float) + sizeof(int32_t));
+    const size_t merge = static_cast<size_t>(kW) * 32 * qpt * k * sizeof(uint64_t);
+    return (tiles > merge ? tiles : merge) + kW * 32 * qpt * sizeof(float) + kQLen * kT * 2 * sizeof(float);
 }
 
 template <int METRIC, int DMAX, int KT, int QPT>
-int launch_kt(const SimtParams &P, unsigned grid, size_t smem, cudaStream_t st) {
-    auto *fn = simt_scan_kernel<METRIC, DMAX, KT, QPT>;
+int launch_kt(const SimtParams &P, unsigned grid, cudaStream_t st) {
+    const size_t smem = simt_smem(P.d4, P.k, QPT);
+    auto *fn = simt_tile_kernel<METRIC, DMAX, KT, QPT>;
     if (smem > 48 * 1024)
         RBC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    fn<<<grid, kST, smem, st>>>(P);
+    fn<<<grid, kT, smem, st>>>(P);
     RBC_LAUNCHED();
     return RBC_OK;
 }
 
-template <int METRIC, int DMAX>
-int launch_dmax(const SimtParams &P, unsigned grid, size_t smem, cudaStream_t st) {
-    if constexpr (DMAX <= 32) {
-        if (simt_qpt(P.d, P.k) == 2) {
-            switch (simt_kt(P.k)) {
-                case 1: return launch_kt<METRIC, DMAX, 1, 2>(P, grid, smem, st);
-                case 4: return launch_kt<METRIC, DMAX, 4, 2>(P, grid, smem, st);
-                default: return launch_kt<METRIC, DMAX, 16, 2>(P, grid, smem, st);
-            }
-        }
-        return launch_kt<METRIC, DMAX, 32, 1>(P, grid, smem, st);
-    } else {
-        switch (simt_kt(P.k)) {
-            case 1: return launch_kt<METRIC, DMAX, 1, 1>(P, grid, smem, st);
-            case 4: return launch_kt<METRIC, DMAX, 4, 1>(P, grid, smem, st);
-            case 16: return launch_kt<METRIC, DMAX, 16, 1>(P, grid, smem, st);
-            default: return launch_kt<METRIC, DMAX, 32, 1>(P, grid, smem, st);
-        }
+template <int METRIC, int DMAX, int QPT>
+int launch_qpt(const SimtParams &P, unsigned grid, cudaStream_t st) {
+    switch (simt_kt(P.k)) {
+        case 1: return launch_kt<METRIC, DMAX, 1, QPT>(P, grid, st);
+        case 4: return launch_kt<METRIC, DMAX, 4, QPT>(P, grid, st);
+        default: return launch_kt<METRIC, DMAX, 16, QPT>(P, grid, st);
     }
 }
 
+template <int METRIC, int DMAX>
+int launch_dmax(const SimtParams &P, unsigned grid, cudaStream_t st) {
+    if (P.k > 16) return launch_kt<METRIC, DMAX, 32, 1>(P, grid, st);
+    if constexpr (DMAX <= 64) {
+        if (P.qpt == 2) return launch_qpt<METRIC, DMAX, 2>(P, grid, st);
+    }
+    return launch_qpt<METRIC, DMAX, 1>(P, grid, st);
+}
+
 template <int METRIC>
-int launch_metric(const SimtParams &P, unsigned grid, size_t smem, cudaStream_t st) {
+int launch_metric(const SimtParams &P, unsigned grid, cudaStream_t st) {
     switch (simt_dmax(P.d)) {
-        case 24: return launch_dmax<METRIC, 24>(P, grid, smem, st);
-        case 32: return launch_dmax<METRIC, 32>(P, grid, smem, st);
-        case 64: return launch_dmax<METRIC, 64>(P, grid, smem, st);
-        default: return launch_dmax<METRIC, 128>(P, grid, smem, st);
+        case 24: return launch_dmax<METRIC, 24>(P, grid, st);
+        case 64: return launch_dmax<METRIC, 64>(P, grid, st);
+        default: return launch_dmax<METRIC, 128>(P, grid, st);
     }
 }
 
 std::atomic<int64_t> g_simt_calls{0};
 
-int simt_launch(SimtParams P, int metric, unsigned grid, cudaStream_t st) {
+int simt_launch(SimtParams P, int metric, int64_t grid, cudaStream_t st) {
     g_simt_calls.fetch_add(1);
+    if (grid > 0x7FFFFFFF) return fail(RBC_EINVAL, "simt scan: too many queries for one call");
     P.d4 = (P.d + 3) & ~3;
     P.tp = simt_tp(P.d4);
-    const size_t smem = simt_smem(P.d4, P.tp, P.k, simt_qpt(P.d, P.k));
-    return metric == RBC_L2 ? launch_metric<RBC_L2>(P, grid, smem, st) : launch_metric<RBC_L1>(P, grid, smem, st);
+    return metric == RBC_L2 ? launch_metric<RBC_L2>(P, static_cast<unsigned>(grid), st)
+                            : launch_metric<RBC_L1>(P, static_cast<unsigned>(grid), st);
 }
 
 }  // namespace
@@ -435,54 +418,72 @@ int simt_launch(SimtParams P, int metric, unsigned grid, cudaStream_t st) {
 bool simt_supported(int d, int k) { return d >= 1 && d <= 128 && k >= 1 && k <= 32; }
 
 bool simt_one_shot_supported(const rbc_index *idx, int64_t nq, int k) {
-    return idx->kind == 1 && idx->xp != nullptr && simt_supported(idx->d, k) && k <= idx->s &&
-           idx->nr * static_cast<int64_t>(idx->s) < (int64_t(1) << 31) && nq < (int64_t(1) << 31) &&
+    return idx->kind == 1 && idx->x4 != nullptr && simt_supported(idx->d, k) && k <= idx->s &&
+           nq < (int64_t(1) << 31) && idx->nr * static_cast<int64_t>(idx->s) < (int64_t(1) << 31) &&
+           idx->s < (1 << 28) &&
            nq * idx->s >= simt_min_pairs();
 }
 
+int simt_pad_rows(const float *src, const int32_t *ids, int64_t rows, int d, float *dst, cudaStream_t st) {
+    if (rows == 0) return RBC_OK;
+    const int d4 = (d + 3) & ~3;
+    pad_rows_kernel<<<grid_for(rows * d4, 256, 148 * 64), 256, 0, st>>>(src, ids, rows, d, d4, dst);
+    RBC_LAUNCHED();
+    return RBC_OK;
+}
+
 // k nearest keys (ascending) of every q row over the rows of x; ids = row index (pid
-// nullptr) or pid[row]
+// nullptr) or pid[row].  x4: x with the padded stride, when the caller has it.
 int simt_dense_topk(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k,
-                    const int32_t *pid, uint64_t *keys, cudaStream_t st) {
+                    const int32_t *pid, uint64_t *keys, cudaStream_t st, const float *x4) {
     if (nq == 0) return RBC_OK;
     if (!simt_supported(d, k)) return fail(RBC_EINVAL, "simt scan: unsupported d or k");
-    // queries per CTA: kST x QPT / Rt (Rt point slices per query thread), the fewest slices
-    // giving >= ~600 CTAs; point splits (merged by merge_parts) only when the queries alone
-    // cannot fill the GPU
+    if (n >= (int64_t(1) << 31)) return fail(RBC_EINVAL, "simt scan: too many points for one call");
+    const int d4 = (d + 3) & ~3;
+    DevBuf<float> padded;
+    if (!x4) {
+        if (d4 == d && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+            x4 = x;
+        } else {
+            RBC_CHECK(padded.alloc(n * d4, st));
+            RBC_CHECK(simt_pad_rows(x, nullptr, n, d, padded.get(), st));
+            x4 = padded.get();
+        }
+    }
+    // query chunks of 32 QPT x point splits: splits (merged by merge_parts) only when the
+    // chunks alone leave the GPU short of ~4 CTAs per SM, each split >= 4 tiles
     const int qpt = simt_qpt(d, k);
-    int qblk = kST * qpt;
-    while (qblk > 32 * qpt && (nq + qblk - 1) / qblk < 600 && qblk / 2 >= 32 * qpt && kST * qpt / (qblk / 2) <= kST / k)
-        qblk /= 2;
-    const int64_t nqb = (nq + qblk - 1) / qblk;
-    int64_t splits = (600 + nqb - 1) / nqb;
-    const int64_t max_splits = (n + 2047) / 2048;
+    const int qb = 32 * qpt;
+    const int64_t nqc = (nq + qb - 1) / qb;
+    int64_t splits = (148 * 4 + nqc - 1) / nqc;
+    const int64_t max_splits = (n + 4 * simt_tp(d4) - 1) / (4 * simt_tp(d4));
     if (splits > max_splits) splits = max_splits;
     if (splits < 1) splits = 1;
+    if (splits < (n >> 27) + 1) splits = (n >> 27) + 1;  // rows of a split < 2^28 (queue encoding)
     const int64_t pchunk = (n + splits - 1) / splits;
     splits = (n + pchunk - 1) / pchunk;
-    if (nqb * splits > 0x7FFFFFFF || n >= (int64_t(1) << 31))
-        return fail(RBC_EINVAL, "simt scan: problem too large for one call");
     DevBuf<uint64_t> part;
     if (splits > 1) RBC_CHECK(part.alloc(splits * nq * k, st));
     SimtParams P{};
     P.q = q;
     P.nq = nq;
     P.d = d;
-    P.p = x;
+    P.d4 = d4;
+    P.p = x4;
     P.pid = pid;
+    P.nqc = nqc;
     P.np = n;
     P.pchunk = pchunk;
-    P.nqb = static_cast<int>(nqb);
-    P.qblk = qblk;
     P.k = k;
+    P.qpt = qpt;
     P.out = splits > 1 ? part.get() : keys;
-    RBC_CHECK(simt_launch(P, metric, static_cast<unsigned>(nqb * splits), st));
+    RBC_CHECK(simt_launch(P, metric, nqc * splits, st));
     if (splits > 1) RBC_CHECK(merge_parts(part.get(), static_cast<int>(splits), nq, k, k, keys, st));
     return RBC_OK;
 }
 
 // one-shot list scan: query i scans the s-list of its nearest representative key_id(near[i])
-// (rows [p s, p s + s) of idx->xp, ids idx->lists)
+// (rows [r s, r s + s) of idx->x4, ids idx->lists)
 int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
                        cudaStream_t st) {
     if (nq == 0) return RBC_OK;
@@ -497,7 +498,8 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
     RBC_CHECK(istart.alloc(nr, st));
     RBC_CHECK(qorder.alloc(nq, st));
     RBC_CHECK(nitems.alloc(1, st));
-    const int qb = kST * simt_qpt(idx->d, k);
+    const int qpt = simt_qpt(idx->d, k, nq < 96 * idx->nr);  // mean group below 96 queries
+    const int qb = 32 * qpt;
     const int64_t max_items = std::min<int64_t>(nr, nq) + nq / qb + 1;
     RBC_CHECK(items.alloc(max_items, st));
     RBC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * nr, st));
@@ -524,13 +526,34 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
     P.nq = nq;
     P.d = idx->d;
     P.qorder = qorder.get();
-    P.p = idx->xp;
-    P.pid = idx->lists;
     P.items = items.get();
     P.nitems = nitems.get();
+    P.p = idx->x4;
+    P.pid = idx->lists;
     P.k = k;
+    P.qpt = qpt;
     P.out = keys;
-    return simt_launch(P, idx->metric, static_cast<unsigned>(max_items), st);
+    return simt_launch(P, idx->metric, max_items, st);
+}
+
+// padded SIMT operands of an index: the representatives (both kinds) and, one-shot, the
+// s-lists' rows gathered per list
+int simt_index_prepare(rbc_index *idx, cudaStream_t st) {
+    if (idx->d > 128) return RBC_OK;
+    const int d4 = (idx->d + 3) & ~3;
+    if (cudaMalloc(&idx->reps4, sizeof(float) * idx->nr * d4) != cudaSuccess)
+        return fail(RBC_ENOMEM, "simt operands (representatives)");
+    idx->bytes += sizeof(float) * idx->nr * d4;
+    RBC_CHECK(simt_pad_rows(idx->reps, nullptr, idx->nr, idx->d, idx->reps4, st));
+    if (idx->kind == 1) {
+        const int64_t rows = idx->nr * static_cast<int64_t>(idx->s);
+        if (rows >= (int64_t(1) << 31)) return RBC_OK;
+        if (cudaMalloc(&idx->x4, sizeof(float) * rows * d4) != cudaSuccess)
+            return fail(RBC_ENOMEM, "simt operands (list rows)");
+        idx->bytes += sizeof(float) * rows * d4;
+        RBC_CHECK(simt_pad_rows(idx->x, idx->lists, rows, idx->d, idx->x4, st));
+    }
+    return RBC_OK;
 }
 
 }  // namespace rbc

@@ -24,10 +24,10 @@ int64_t tc_min_pairs() { return g_engine == 2 ? 0 : g_engine == 3 ? INT64_MAX : 
 int64_t simt_min_pairs() { return g_engine >= 2 ? 0 : (int64_t(1) << 22); }
 
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
-                 cudaStream_t st) {
+                 cudaStream_t st, const float *x4) {
     if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, 1)) return tc_bf_keys(q, nq, x, n, d, 1, keys, st);
     if (!force_exact_engine() && simt_supported(d, 1) && nq * n >= simt_min_pairs())
-        return simt_dense_topk(q, nq, x, n, d, metric, 1, nullptr, keys, st);
+        return simt_dense_topk(q, nq, x, n, d, metric, 1, nullptr, keys, st, x4);
     AllSrc src{x, n, d};
     return launch_topk(q, nq, d, metric, 1, src, keys, st);
 }

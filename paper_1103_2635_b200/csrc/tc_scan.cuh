@@ -12,8 +12,9 @@ struct PruneOut;
 
 // k=1 key64 argmin of every q row over the rows of x (build assignment,
 // one-shot nearest rep, bf_search k=1).  keys[i] = (f32 bits(dist) << 32) | j.
+// x4: optional copy of x with rows padded to d rounded up to 4 (the SIMT engine's layout)
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
-                 cudaStream_t st);
+                 cudaStream_t st, const float *x4 = nullptr);
 
 // bf_search core: k nearest keys per query row over all of x, sorted.
 int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
@@ -69,7 +70,8 @@ void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed);
 bool simt_supported(int d, int k);
 bool simt_one_shot_supported(const rbc_index *idx, int64_t nq, int k);
 int simt_dense_topk(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k,
-                    const int32_t *pid, uint64_t *keys, cudaStream_t st);
+                    const int32_t *pid, uint64_t *keys, cudaStream_t st, const float *x4 = nullptr);
+int simt_index_prepare(rbc_index *idx, cudaStream_t st);
 int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
                        cudaStream_t st);
 
