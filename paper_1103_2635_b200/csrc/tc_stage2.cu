@@ -64,6 +64,7 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 16 epilogue war
 constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
 constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
 constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
+constexpr int kLSlots = 4;       // per-list data ring slots
 // Per K-plane count NP (d <= 64 * NP): NP = 1 for d <= 64; NP = 2 for d <= 128 (two SW128
 // planes, 128-column chunks and a 3-stage ring so the A/B buffers fit in shared memory).
 template <int NP>
@@ -75,8 +76,13 @@ struct S2Cfg {
     static constexpr int kStageBytes = kN * (NP * kP0 + kP1);
     static constexpr int kABytes = kRows * (NP * kP0 + kP1);
     static constexpr int kTmemCols = 2 * kN;         // kAcc accumulators
-    static constexpr size_t kSmem =
-        1024 + kStages * kStageBytes + 2 * kABytes + (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) + 512;
+    // per-list data ring (work item + representative row + its B rounding error), staged by the
+    // producer one list ahead so no role waits on a dependent global load at a list switch
+    static constexpr int kRepStride = 64 * NP + 4;                        // floats per rep row
+    static constexpr int kLSlotBytes = 32 + kRepStride * 4;               // WorkItem + rep row
+    static constexpr size_t kSmem = 1024 + kStages * kStageBytes + 2 * kABytes +
+                                    (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) +
+                                    kLSlots * kLSlotBytes + 512;
 };
 
 // error-bound constants (factor-2 safety on each term; K <= 80 accumulated products)
@@ -106,7 +112,7 @@ struct TcIndex {
     int64_t *poff = nullptr;  // [nr + 1] padded (8-row aligned) list offsets
     float *sB = nullptr;      // [nr] per-list power-of-two scale
     float *dbmax = nullptr;   // [nr] max over the list of |b - f16(b)| (scaled residual rows, f16 rounding)
-    float *reps64 = nullptr;  // [nr][64 np] representatives, zero padded
+    float *reps64 = nullptr;  // [nr][64 np + 4] representatives, zero padded; [64 np] = dbmax[p]
 };
 
 // one (tile, list) work item, 32 bytes
@@ -269,7 +275,12 @@ __global__ void residual_rows_kernel(const float *__restrict__ xp, const float *
     if (threadIdx.x == 0 && s_db) atomicMax(reinterpret_cast<unsigned *>(dbmax) + p, s_db);
 }
 
-// rows of src [rows][d] -> dst [rows][w], zero padded (w = 64 or 128)
+__global__ void rep_dbmax_kernel(const float *__restrict__ dbmax, int64_t nr, int stride, float *__restrict__ reps) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p < nr) reps[p * stride + stride - 4] = dbmax[p];
+}
+
+// rows of src [rows][d] -> dst [rows][w], zero padded (w = 64, 128, or those + 4)
 __global__ void pad64_rows_kernel(const float *__restrict__ src, int64_t rows, int d, float *__restrict__ dst,
                                   int w = 64) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -492,10 +503,19 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     float *gbuf = reinterpret_cast<float *>(sA + 2 * kABytes);  // 8 epilogue warps x 128 (fallback column)
     float *s_dq = gbuf + kEpiWarps * kCols;  // [4 list slots][kParts][128] partial |q - r_p|^2
     float *s_da = s_dq + 4 * kParts * kRows;  // [4 list slots][kParts][128] partial |a - f16(a)|^2 (scaled)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_da + 4 * kParts * kRows);
+    uint8_t *lring = reinterpret_cast<uint8_t *>(s_da + 4 * kParts * kRows);  // [kLSlots] per-list data
+    uint64_t *bars = reinterpret_cast<uint64_t *>(lring + kLSlots * Cfg::kLSlotBytes);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + kAcc;
     uint64_t *afull = tempty + kAcc, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(tile_empty + 2);
+    uint64_t *lfull = tile_empty + 2, *lempty = lfull + kLSlots;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(lempty + kLSlots);
+    // list data of ring position li: its work item and representative row (+ dbmax at [64 NP])
+    auto lslot_wi = [&](uint32_t li) -> const WorkItem & {
+        return *reinterpret_cast<const WorkItem *>(lring + (li % kLSlots) * Cfg::kLSlotBytes);
+    };
+    auto lslot_rep = [&](uint32_t li) {
+        return reinterpret_cast<const float *>(lring + (li % kLSlots) * Cfg::kLSlotBytes + 32);
+    };
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);  // 2-slot ring of tile ids
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -514,6 +534,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             sm100::mbar_init(&tile_full[b], 1);
             sm100::mbar_init(&tile_empty[b], 1 + kEpiWarps);  // MMA lane + epilogue warps
         }
+        for (int l = 0; l < kLSlots; ++l) {
+            sm100::mbar_init(&lfull[l], 1);
+            sm100::mbar_init(&lempty[l], kEpiWarps);
+        }
         sm100::fence_barrier_init();
     }
     if (warp == 1) sm100::tmem_alloc<Cfg::kTmemCols>(s_tmem);
@@ -525,7 +549,20 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     if (warp == 0) {
         // ===== scheduler + producer =====
         if (lane == 0) {
-            uint32_t bi = 0;
+            uint32_t bi = 0, li = 0;
+            // list data of work item w into the next ring slot (the epilogue prepares list w + 1's
+            // A operand while list w's chunks run, so w + 1's data is issued before w's chunks)
+            auto issue_list = [&](int64_t w) {
+                const uint32_t sl = li % kLSlots;
+                sm100::mbar_wait(&lempty[sl], ((li / kLSlots) & 1) ^ 1);
+                uint8_t *dst = lring + sl * Cfg::kLSlotBytes;
+                const int32_t p = P.work[w].p;
+                sm100::mbar_arrive_expect_tx(&lfull[sl], Cfg::kLSlotBytes);
+                sm100::bulk_g2s(dst, P.work + w, 32, &lfull[sl]);
+                sm100::bulk_g2s(dst + 32, P.reps64 + static_cast<int64_t>(p) * Cfg::kRepStride, Cfg::kRepStride * 4,
+                                &lfull[sl]);
+                ++li;
+            };
             for (uint32_t it = 0;; ++it) {
                 const uint32_t slot = it & 1;
                 sm100::mbar_wait(&tile_empty[slot], ((it >> 1) & 1) ^ 1);
@@ -534,7 +571,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 s_tiles[slot] = tile;
                 sm100::mbar_arrive(&tile_full[slot]);
                 if (tile < 0) break;
-                for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w) {
+                const int64_t wt0 = P.work_off[tile], wt1 = wt0 + P.nwork[tile];
+                if (wt0 < wt1) issue_list(wt0);
+                for (int64_t w = wt0, w1 = wt1; w < w1; ++w) {
+                    if (w + 1 < w1) issue_list(w + 1);
                     const WorkItem wi = P.work[w];
                     for (int off = 0; off < wi.ext; off += kN) {
                         const int n = min(kN, roundup16(wi.ext - off));
@@ -560,15 +600,16 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            uint32_t bi = 0, ti = 0, ai = 0;
+            uint32_t bi = 0, ti = 0, ai = 0, li = 0;
             for (uint32_t it = 0;; ++it) {
                 const uint32_t slot = it & 1;
                 sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
                 const int tile = s_tiles[slot];
                 sm100::mbar_arrive(&tile_empty[slot]);
                 if (tile < 0) break;
-                for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w) {
-                    const int ext = P.work[w].ext;
+                for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w, ++li) {
+                    sm100::mbar_wait(&lfull[li % kLSlots], (li / kLSlots) & 1);
+                    const int ext = lslot_wi(li).ext;
                     const uint32_t a = ai & 1;
                     S2_WAIT(&afull[a], (ai >> 1) & 1, 1);
                     sm100::tc_fence_after();
@@ -610,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         const int part = (warp - 2) >> 2;
         const int row = quad * 32 + lane;
         float *g = gbuf + (warp - 2) * kCols;
-        uint32_t ti = 0, ai = 0;
+        uint32_t ti = 0, ai = 0, li0 = 0;  // li0: ring position of the tile's first list
         for (uint32_t it = 0;; ++it) {
             const uint32_t slot = it & 1;
             sm100::mbar_wait(&tile_full[slot], (it >> 1) & 1);
@@ -643,9 +684,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             auto prep_a = [&](int64_t w) {
                 S2_TIME(const unsigned long long tp0 = clock64());
                 S2_TIME(++tw[11]);
-                const WorkItem wi = P.work[w];
-                const float4 *rep4 =
-                    reinterpret_cast<const float4 *>(P.reps64 + static_cast<int64_t>(wi.p) * (64 * NP) + part * kKd);
+                const uint32_t lw = li0 + static_cast<uint32_t>(w - w0);
+                sm100::mbar_wait(&lfull[lw % kLSlots], (lw / kLSlots) & 1);
+                const WorkItem wi = lslot_wi(lw);
+                const float4 *rep4 = reinterpret_cast<const float4 *>(lslot_rep(lw) + part * kKd);
                 const __half ac = __float2half_rn(wi.aug);
                 const uint32_t aug = static_cast<uint32_t>(__half_as_ushort(ac)) * 0x00010001u;
                 const float sa = wi.sA;
@@ -675,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 if constexpr (NP == 1) {
                     float4 rr4[kKd / 4];
 #pragma unroll
-                    for (int c = 0; c < kKd / 4; ++c) rr4[c] = __ldg(rep4 + c);
+                    for (int c = 0; c < kKd / 4; ++c) rr4[c] = rep4[c];
                     // this part's share of |q - r_p|^2 (fp32; with the other part's, the A2 term of
                     // the error bound -- same (d + 2) 2^-24 relative error budget as kD1 / kUq)
                     {
@@ -703,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     float n0 = 0.f, n1 = 0.f;
 #pragma unroll 2
                     for (int c = 0; c < kKd / 8; ++c) {
-                        const float4 r0 = __ldg(rep4 + 2 * c), r1 = __ldg(rep4 + 2 * c + 1);
+                        const float4 r0 = rep4[2 * c], r1 = rep4[2 * c + 1];
                         const float4 q0 = live ? __ldg(qsrc + 2 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
                         const float4 q1 = live ? __ldg(qsrc + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
                         const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
@@ -755,7 +797,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             if (w0 < w1) cut_n = P.cut ? P.cut[w0 * kRows + row] : P.work[w0].ext;
             for (int64_t w = w0; w < w1; ++w) {
                 if (w + 1 < w1) prep_a(w + 1);  // next list's A while this list's MMAs run
-                const WorkItem wi = P.work[w];
+                const uint32_t lw = li0 + static_cast<uint32_t>(w - w0);  // (waited for by prep_a(w))
+                const WorkItem wi = lslot_wi(lw);
                 const int cutv = live ? cut_n : 0;
                 if (w + 1 < w1) cut_n = P.cut ? P.cut[(w + 1) * kRows + row] : P.work[w + 1].ext;
                 // both column parts of this lane quadrant have prepared lists w and w + 1: the
@@ -784,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     // relative for the fp32 residual rounding before the f16 conversion), x2 for
                     // d^2 and x2 safety as in kC1; fp32 accumulation keeps its kC1 share
                     const float da = sqrtf(DA2) * (1.0f + 1.0f / 1024.0f) / sa + dq * (1.0f / 8388608.0f);
-                    const float db = P.dbmax[wi.p] * (1.0f + 1.0f / 1024.0f) / wi.sB + rb * (1.0f / 8388608.0f);
+                    const float db = lslot_rep(lw)[64 * NP] * (1.0f + 1.0f / 1024.0f) / wi.sB + rb * (1.0f / 8388608.0f);
                     E = 4.0f * (da * rb + na * db + da * db) + kAccErrNP * na * rb + kC2 * (A2 + rb * rb) + kD1 * A2 +
                         kC4 * rb * (2.0f / sa) + 1e-30f;
                 }
@@ -909,7 +952,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     // valid columns of this row, relative to this warp's part of the chunk
                     const int lim = min(min(cutv - off, n) - hb, kCols);
 #ifdef RBC_S2_NOEPI
-                    const int wlim = 0;  // diagnostic: pipeline without epilogue work (results invalid)
+                    // diagnostic: pipeline without epilogue work in the search (results invalid; the
+                    // build's brute force keeps its epilogue so the index is still right)
+                    const int wlim = P.cut ? 0 : __reduce_max_sync(0xffffffffu, max(lim, 0));
 #else
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
 #endif
@@ -919,7 +964,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         sm100::tmem_ld32_async(tbase + c0, ra);
                         sm100::tmem_wait_ld(ra);
 #if defined(RBC_S2_LEVEL) && RBC_S2_LEVEL == 1
-                        {  // diagnostic: TMEM loads only
+                        if (P.cut) {  // diagnostic: TMEM loads only (search only)
                             uint32_t x = 0;
 #pragma unroll
                             for (int j = 0; j < 32; ++j) x ^= ra[j];
@@ -950,8 +995,10 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                             }
                         }
 #if defined(RBC_S2_LEVEL) && RBC_S2_LEVEL == 2
-                        if (ma == 1234.5f) count += 1;  // diagnostic: loads + reductions, no candidates
-                        continue;
+                        if (P.cut) {  // diagnostic: loads + reductions, no candidates (search only)
+                            if (ma == 1234.5f) count += 1;
+                            continue;
+                        }
 #endif
                         if (ma >= T) {
                             if (count + 4 > P.cap && !overflow) compact();
@@ -966,7 +1013,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     if (lane == 0) sm100::mbar_arrive(&tempty[tb]);
                     ++ti;
                 }
+                // list w's ring slot is free once every epilogue warp is past it
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(&lempty[lw % kLSlots]);
             }
+            li0 += static_cast<uint32_t>(w1 - w0);
             // the held group joins the buffer (k = 1)
             if (KT == 1 && kHold && held && !overflow) {
                 if (count < P.cap) {
@@ -1232,7 +1283,7 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
               cudaMalloc(&tc->poff, (nr + 1) * sizeof(int64_t)) == cudaSuccess &&
               cudaMalloc(&tc->sB, nr * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&tc->dbmax, nr * sizeof(float)) == cudaSuccess &&
-              cudaMalloc(&tc->reps64, nr * 64 * np * sizeof(float)) == cudaSuccess;
+              cudaMalloc(&tc->reps64, nr * (64 * np + 4) * sizeof(float)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         tc_free(tc);
@@ -1240,7 +1291,7 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
     }
     if (bytes)
         *bytes += rows * (np * kP0 + (tc->plane1 ? kP1 : 0) + sizeof(float)) + (nr + 1) * sizeof(int64_t) +
-                  nr * ((64 * np + 2) * sizeof(float));
+                  nr * ((64 * np + 6) * sizeof(float));
     if (cudaMemsetAsync(tc->xh0, 0, np * rows * kP0, st) != cudaSuccess ||
         (tc->plane1 && cudaMemsetAsync(tc->xh1, 0, rows * kP1, st) != cudaSuccess) ||
         cudaMemsetAsync(tc->gcol, 0, rows * sizeof(float), st) != cudaSuccess ||
@@ -1250,12 +1301,14 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
         return fail(RBC_ECUDA, "tc list operands init");
     }
     list_scale_kernel<<<grid_for(nr, 256), 256, 0, st>>>(radii, nr, tc->sB);
-    pad64_rows_kernel<<<grid_for(nr * 64 * np, 256), 256, 0, st>>>(reps, nr, d, tc->reps64, 64 * np);
+    pad64_rows_kernel<<<grid_for(nr * (64 * np + 4), 256), 256, 0, st>>>(reps, nr, d, tc->reps64, 64 * np + 4);
     const unsigned ysplit = static_cast<unsigned>(maxlen > 256 * 148 ? 148 : (maxlen + 255) / 256 + 0);
     residual_rows_kernel<<<dim3(static_cast<unsigned>(nr), ysplit > 0 ? ysplit : 1), 256, 0, st>>>(
         xp, reps, offsets_dev, tc->poff, tc->sB, d, np, rows * kP0, tc->plane1 ? 1 : 0, tc->xh0, tc->xh1, tc->gcol,
         tc->dbmax);
-    note_launch(3);
+    // dbmax[p] beside the representative row (one bulk copy brings both to the stage-2 kernel)
+    rep_dbmax_kernel<<<grid_for(nr, 256), 256, 0, st>>>(tc->dbmax, nr, 64 * np + 4, tc->reps64);
+    note_launch(4);
     if (cudaGetLastError() != cudaSuccess) {
         tc_free(tc);
         return fail(RBC_ECUDA, "tc list operand kernels");

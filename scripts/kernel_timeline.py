@@ -15,18 +15,26 @@ def main():
 
     import paper_1103_2635_b200 as rbc
     from paper_1103_2635_b200 import _lib
+    from paper_1103_2635_b200.rbc import device_index
 
     nq = int(sys.argv[1]) if len(sys.argv) > 1 else bench.NQ
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     x, q = bench.gen_inputs(0)
-    index = rbc.build_exact(rbc.DataMatrix(x), bench.NR, rbc.MetricSpec("l2", bench.D), seed=bench.REP_SEED)
+    cache = os.environ.get("RBC_INDEX_CACHE")  # diagnostic library variants load the normal build's index
+    if cache and os.path.exists(cache):
+        index = rbc.load_index(cache)
+    else:
+        index = rbc.build_exact(rbc.DataMatrix(x), bench.NR, rbc.MetricSpec("l2", bench.D), seed=bench.REP_SEED)
+        if cache:
+            rbc.save_index(index, cache)
+    device_index(index)  # upload (a loaded index uploads on first use)
     sptr = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     q_dev = _lib.to_device(q)
     keys = torch.empty((bench.NQ, k), dtype=torch.int64, device="cuda")
     stats = _lib.SearchStatsC(None, None, None, None)
 
     def run():
-        _lib.check(_lib.lib.rbc_exact_search_keys(index._dev.handle, _lib.ptr(q_dev), nq, k, _lib.ptr(keys), stats,
+        _lib.check(_lib.lib.rbc_exact_search_keys(device_index(index).handle, _lib.ptr(q_dev), nq, k, _lib.ptr(keys), stats,
                                                   sptr))
 
     for _ in range(3):
