@@ -583,6 +583,13 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                         uint8_t *dst = sB + s * kStageBytes;
                         const uint32_t b0 = static_cast<uint32_t>(n) * kP0;
                         const uint32_t b1 = P.plane1 ? static_cast<uint32_t>(n) * kP1 : 0u;
+#ifdef RBC_S2_NOLOAD
+                        if (P.cut) {  // diagnostic: no B traffic in the search (stale operands, results invalid)
+                            sm100::mbar_arrive(&full[s]);
+                            ++bi;
+                            continue;
+                        }
+#endif
                         sm100::mbar_arrive_expect_tx(&full[s], NP * b0 + b1);
 #pragma unroll
                         for (int j = 0; j < NP; ++j)
