@@ -90,6 +90,11 @@ int64_t rbc_tc_scan_calls(void);
 /* Launches of the fp32 SIMT filter scan (simt_scan_kernel: the L1 engine, and small
  * L2 scans) since the library loaded (diagnostic). */
 int64_t rbc_simt_scan_calls(void);
+/* Large-k selections (k > 32: one-shot build s-lists, bf_search with large k) served by
+ * the sampled-threshold engine, and the queries it handed to the exact full sort
+ * (diagnostic). */
+int64_t rbc_select_calls(void);
+int64_t rbc_select_fallbacks(void);
 
 /* metric.py:57-76 pairwise_distances (and brute_force.py:220-251
  * distance_rows): out[m,p] = dist(a[i], b[j]), bit-exact. */

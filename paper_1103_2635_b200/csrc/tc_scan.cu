@@ -37,6 +37,8 @@ int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d,
     if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, k)) return tc_bf_keys(q, nq, x, n, d, k, keys, st);
     if (!force_exact_engine() && simt_supported(d, k) && nq * n >= simt_min_pairs())
         return simt_dense_topk(q, nq, x, n, d, metric, k, nullptr, keys, st);
+    if (!force_exact_engine() && select_large_supported(nq, n, d, k))
+        return select_topk_large(q, nq, x, n, d, metric, k, keys, st);
     if (k > kMaxWarpK) return topk_sorted_all(q, nq, x, n, d, metric, k, keys, st);
     AllSrc src{x, n, d};
     return launch_topk(q, nq, d, metric, k, src, keys, st);

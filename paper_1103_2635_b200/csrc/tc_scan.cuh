@@ -75,6 +75,12 @@ int simt_index_prepare(rbc_index *idx, cudaStream_t st);
 int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
                        cudaStream_t st);
 
+// k nearest keys for large k (select.cu): a sampled fp32 threshold, one counting and
+// collecting pass, a segmented sort of the collected exact keys (k > 32)
+bool select_large_supported(int64_t nq, int64_t n, int d, int k);
+int select_topk_large(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
+                      cudaStream_t st);
+
 // engine selection (RBC_ENGINE env: "auto" (default) | "exact")
 bool force_exact_engine();
 // minimum (query, point) pairs for the brute-force-shaped tensor-core scans (0 in mode 2)

@@ -144,3 +144,52 @@ def test_simt_exact_build_assignment_l1(rbc, oracle):
     assert np.array_equal(np.concatenate(idx.list_ids), list_ids)
     assert np.array_equal(np.concatenate(idx.list_dists), list_dists)
     assert np.array_equal(idx.radii, radii)
+
+
+def _select_calls():
+    from paper_1103_2635_b200 import _lib
+
+    return _lib.lib.rbc_select_calls(), _lib.lib.rbc_select_fallbacks()
+
+
+@pytest.mark.parametrize("metric", ["l1", "l2"])
+@pytest.mark.parametrize("s", [33, 150, 600])
+def test_select_one_shot_build_vs_oracle(rbc, oracle, metric, s):
+    # the one-shot build's s-lists for s > 32 go through the sampled-threshold selection
+    d = 21 if metric == "l1" else 16
+    x = oracle.gen_clusters(40_000, d, 50 + s, n_clusters=8, cluster_sigma=0.05)
+    c0, _ = _select_calls()
+    idx = rbc.build_one_shot(rbc.DataMatrix(x), 120, s, rbc.MetricSpec(metric, d), seed=2)
+    assert _select_calls()[0] > c0, "the large-k selection did not run"
+    lists, radii = oracle.build_one_shot(x, idx.reps.rep_ids, s, metric)
+    assert np.array_equal(np.asarray(idx.list_ids), lists) and np.array_equal(idx.radii, radii)
+
+
+@pytest.mark.parametrize("metric", ["l1", "l2"])
+@pytest.mark.parametrize("k", [40, 100, 512])
+def test_select_bf_large_k_vs_oracle(rbc, oracle, metric, k):
+    d = 12
+    x = oracle.gen_clusters(30_000, d, 9, n_clusters=5, cluster_sigma=0.06)
+    x = np.concatenate([x, x[:500]])  # exact duplicates: ties broken by the lowest id
+    q = np.concatenate([uniform(40, d, 11), x[::997] + np.float32(0.002)]).astype(np.float32)
+    ids, dists = rbc.brute_force.bf_search_arrays(q, x, rbc.MetricSpec(metric, d), k)
+    oi, od = oracle.bf_topk(q, x, k, metric)
+    assert np.array_equal(ids, oi) and np.array_equal(dists, od)
+
+
+def test_select_unrepresentative_sample_falls_back(rbc, oracle):
+    # every sampled row (ids divisible by the stride) is far away and the rest sits next to
+    # the queries: the sampled threshold is far too loose, the collection overflows and the
+    # exact full sort takes over -- the keys must still be the reference's
+    k, d = 160, 4
+    stride = k // 8
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((20_000, d)) * 0.01).astype(np.float32)
+    x[::stride] += np.float32(50.0)
+    q = (rng.standard_normal((6, d)) * 0.01).astype(np.float32)
+    _, f0 = _select_calls()
+    for metric in ("l1", "l2"):
+        ids, dists = rbc.brute_force.bf_search_arrays(q, x, rbc.MetricSpec(metric, d), k)
+        oi, od = oracle.bf_topk(q, x, k, metric)
+        assert np.array_equal(ids, oi) and np.array_equal(dists, od)
+    assert _select_calls()[1] > f0, "expected the exact fallback"
