@@ -651,7 +651,12 @@ def main():
         roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["tensor"], "unit": "TFLOP/s",
                     "frac": (achieved / pk["tensor"]) if achieved else None, "peak_src": pk["src"]}
     else:
-        kname = f"oneshot L1 scan (k={K})"
+        # the one-shot list scan on the fp32 SIMT filter engine (simt_scan.cu simt_tile_kernel<metric,
+        # DMAX, KT, QPT>; grouped items use one query per lane when the mean group is below 96)
+        dmax = 24 if D <= 24 else 64 if D <= 64 else 128
+        kt = 1 if K <= 1 else 4 if K <= 4 else 16 if K <= 16 else 32
+        qpt = 2 if (D <= 64 and K <= 16 and NQ >= 96 * n_reps) else 1
+        kname = f"simt_tile_kernel<1, {dmax}, {kt}, {qpt}>"
         traffic = ncu_traffic(kname, args.config)
         achieved = scan_work * scan_n / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
         peak = simt_peak_gops((clk or {}).get("sm_mhz"))
@@ -682,7 +687,7 @@ def main():
         _lib.check(_lib.lib.rbc_bf_prepare(_lib.ptr(x_dev), N, D, metric_code, ctypes.byref(bfh), sptr), "bf prepare")
         torch.cuda.synchronize()
         t_prep = time.perf_counter() - t_prep
-        launches0 = _lib.lib.rbc_tc_bf_calls()
+        launches0, simt0 = _lib.lib.rbc_tc_bf_calls(), _lib.lib.rbc_simt_scan_calls()
         bf_times = []
         for it in range(3):
             torch.cuda.synchronize()
@@ -695,14 +700,17 @@ def main():
             bf_times.append(ev0.elapsed_time(ev1) / 1e3)
         dt = statistics.median(bf_times[1:])
         tc_used = _lib.lib.rbc_tc_bf_calls() > launches0
+        simt_used = _lib.lib.rbc_simt_scan_calls() > simt0
         _lib.lib.rbc_index_destroy(bfh)
         bf_flops = 2.0 * D * m * N  # algorithmic: every (query, point) pair, 2 d flops
         bf = {"value": m / dt, "unit": "queries/s",
               "sample": f"{m} queries x {N} points, k={K}, rbc_bf_search_prepared (bf_search over a prepared "
                         f"operand), device-resident",
-              "engine": "tcgen05 f16 filter + exact fp64 re-rank" if tc_used else "exact fp64 SIMT",
+              "engine": ("tcgen05 f16 filter + exact fp64 re-rank" if tc_used else
+                         "fp32 SIMT filter + exact fp64 re-rank" if simt_used else "exact fp64 SIMT"),
               "prepare_s": t_prep, "ms": dt * 1e3, "achieved_tflops": bf_flops / dt / 1e12,
-              "frac_of_peak": bf_flops / dt / 1e12 / pk["tensor"],
+              "frac_of_peak": (bf_flops / dt / 1e12 / pk["tensor"] if CFG["metric"] == "l2" else
+                               bf_flops / dt / 1e9 / simt_peak_gops((clk or {}).get("sm_mhz"))),
               "rbc_speedup": (value / world) / (m / dt)}
         del x_dev
 
@@ -716,7 +724,8 @@ def main():
                "index_build_s": build_s, "mean_candidates": mean_cand, "flops_per_step": flops_per_step,
                "step_ms_min": min(times), "step_ms_median": sorted(times)[len(times) // 2],
                "arith": ("f32 inputs; f16 tcgen05 filter; exact re-rank in f64 (reference rule)"
-                         if CFG["metric"] == "l2" else "f32 inputs; exact f64 SIMT (reference rule)")}
+                         if CFG["metric"] == "l2" else
+                         "f32 inputs; fp32 SIMT filter; exact re-rank in f64 (reference rule)")}
         if not exact:
             cfg["s"] = CFG["s"]
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,

@@ -81,5 +81,38 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+TORCH_SRC = os.path.join(PKG, "torch_ext", "rbc_torch_ops.cpp")
+TORCH_LIB = os.path.join(PKG, "librbc_torch_ops.so")
+
+
+def build_torch_ops(force: bool = False) -> str:
+    """torch.ops.rbc_b200.* (torch_ext/rbc_torch_ops.cpp): registered operators over the C-ABI,
+    linked against librbc_b200.so (found next to it via $ORIGIN)."""
+    deps = [TORCH_SRC, os.path.join(ROOT, "include", "rbc_b200.h"), os.path.abspath(__file__)]
+    if (not force and os.path.exists(TORCH_LIB)
+            and all(os.path.getmtime(p) <= os.path.getmtime(TORCH_LIB) for p in deps)):
+        return TORCH_LIB
+    import torch
+    from torch.utils import cpp_extension
+
+    cxx = shutil.which("g++") or "g++"
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    cmd = [cxx, "-O2", "-std=c++17", "-fPIC", "-shared", TORCH_SRC, "-o", TORCH_LIB + ".tmp",
+           f"-D_GLIBCXX_USE_CXX11_ABI={abi}", "-DTORCH_EXTENSION_NAME=rbc_torch_ops",
+           "-I", os.path.join(ROOT, "include")]
+    for inc in cpp_extension.include_paths(device_type="cuda"):
+        cmd += ["-isystem", inc]
+    for lib in cpp_extension.library_paths(device_type="cuda"):
+        cmd += ["-L", lib, f"-Wl,-rpath,{lib}"]
+    cmd += ["-L", PKG, "-lrbc_b200", "-Wl,-rpath,$ORIGIN", "-lc10", "-ltorch", "-ltorch_cpu", "-ltorch_cuda",
+            "-lc10_cuda"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"torch ops build failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(TORCH_LIB + ".tmp", TORCH_LIB)
+    return TORCH_LIB
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_torch_ops(force="--force" in sys.argv))

@@ -105,3 +105,18 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("device present")
     with pytest.raises(RuntimeError, match="CUDA device"):
         rbc.pairwise_distances(np.zeros((2, 3), np.float32), np.zeros((2, 3), np.float32), rbc.MetricSpec("l2", 3))
+
+
+def test_torch_ops_registered():
+    # torch.ops.rbc_b200.* (torch_ext/rbc_torch_ops.cpp) load and carry the hot-path schemas;
+    # no compute without a GPU
+    from paper_1103_2635_b200 import torch_ops
+
+    ops = torch_ops.load()
+    for name, args in (("bf_search", "queries, Tensor data, int metric, int k"),
+                       ("pairwise_distances", "a, Tensor b, int metric"),
+                       ("exact_search", "index, Tensor queries, int k"),
+                       ("one_shot_search", "index, Tensor queries, int k")):
+        schema = str(getattr(ops, name).default._schema)
+        assert schema.startswith(f"rbc_b200::{name}("), schema
+        assert args in schema, schema
