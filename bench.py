@@ -242,7 +242,7 @@ def run_rep_shard(args, rank, world, local):
 
 def kt_of(k: int) -> int:
     """Template width of the stage-2 / re-rank kernels serving k (tc_stage2.cu launch dispatch)."""
-    return 1 if k == 1 else 4 if k <= 4 else 8 if k <= 8 else 16 if k <= 16 else 32
+    return 1 if k == 1 else 4 if k <= 4 else 8 if k <= 8 else 10 if k == 10 else 16 if k <= 16 else 32
 
 
 def ncu_traffic(kernel: str, cfg: str):
@@ -561,6 +561,17 @@ def main():
             rbc.one_shot_query_arrays(index, q, K)
         if i >= 2:
             api_times.append(time.perf_counter() - t0)
+    # the reference-shaped call (list[NeighborList], list[SearchStats]: one dataclass pair per query)
+    nb = min(NQ, 10_000)
+    batch_times = []
+    for i in range(1 + 3):
+        t0 = time.perf_counter()
+        if exact:
+            rbc.exact_query_batch(index, q[:nb], K)
+        else:
+            rbc.one_shot_query_batch(index, q[:nb], K)
+        if i >= 1:
+            batch_times.append(time.perf_counter() - t0)
     os.sched_setaffinity(0, old_aff)
     # median: the host call's wall time carries OS scheduling noise; min/median/max go to stderr
     e2e_s = statistics.median(e2e_times)
@@ -577,7 +588,11 @@ def main():
                  "d2h_bytes_per_step": int(ids_h.numel() * 8 + dists_h.numel() * 4),
                  "api": {"value": world * NQ / api_s, "unit": "queries/s",
                          "call": ("exact_query_arrays" if exact else "one_shot_query_arrays")
-                         + " (numpy in, numpy ids/dists/stats out; pageable host memory)"}}
+                         + " (numpy in, numpy ids/dists/stats out; pageable host memory)"},
+                 "api_batch": {"value": nb / statistics.median(batch_times), "unit": "queries/s",
+                               "sample": f"{nb} queries per call",
+                               "call": ("exact_query_batch" if exact else "one_shot_query_batch")
+                               + " (the reference's return types: a NeighborList and SearchStats per query)"}}
 
     for _ in range(args.warmup):  # back to the device-resident call (re-captures its graph)
         step()
