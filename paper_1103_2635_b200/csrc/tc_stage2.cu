@@ -65,6 +65,8 @@ constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies m
 constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
 constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
 constexpr int kLSlots = 4;       // per-list data ring slots
+constexpr int kMaxSplit = 4;     // k > 1: a heavy tile's work items are split over up to 4 CTAs
+constexpr int kMaxSlots = kParts * kMaxSplit;  // candidate slots per query (column parts x splits)
 // Per K-plane count NP (d <= 64 * NP): NP = 1 for d <= 64; NP = 2 for d <= 128 (two SW128
 // planes, 128-column chunks and a 3-stage ring so the A/B buffers fit in shared memory).
 template <int NP>
@@ -140,6 +142,9 @@ struct S2Params {
     int k;
     int ntiles;
     const int32_t *tile_order;  // LPT order
+    const int4 *vt;             // virtual tiles {tile, first work item, end, split} in LPT order (nullptr: whole tiles)
+    const int32_t *nvt;         // their count (device)
+    int nslot;                  // candidate slots per query: kParts x splits
     const int32_t *order;       // query order: tile t holds order[128 t .. 128 t + 127] (nq entries)
     int64_t nq;
     const int64_t *work_off;    // [ntiles] first work item of each tile
@@ -151,8 +156,8 @@ struct S2Params {
     float *cand_lb;
     int32_t *cand_pos;
     int cap;
-    int32_t *cand_count;        // [nq][kParts] buffered groups, -1 = overflow
-    float *cand_ufin;           // [nq][kParts] final k-th best upper bound (with tie slack)
+    int32_t *cand_count;        // [nq][nslot] buffered groups, -1 = overflow
+    float *cand_ufin;           // [nq][nslot] final k-th best upper bound (with tie slack)
     int32_t *overflow_list;
     int32_t *overflow_count;
     int32_t *tile_counter;
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     int64_t nr, const float *__restrict__ sB, const float *__restrict__ radii, const int64_t *__restrict__ poff,
     const int64_t *__restrict__ offsets, WorkItem *__restrict__ work,
     int32_t *__restrict__ cut, uint64_t *__restrict__ tile_key, int warm,
-    int64_t cap_work, int32_t *__restrict__ cand_count, int32_t *__restrict__ counters) {
+    int64_t cap_work, int32_t *__restrict__ cand_count, int nslot, int32_t *__restrict__ counters) {
     if (threadIdx.x == 0) tile_ids[blockIdx.x] = static_cast<int32_t>(blockIdx.x);
     extern __shared__ int32_t sm[];
     int32_t *maxlen = sm;           // [nr]
@@ -332,10 +337,8 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
     // stage 2's per-query group counts and its two counters start at zero (in place of two
     // memset nodes; unconditional: the re-rank reads the counts even when stage 2 bails out)
-    if (tq < nq) {
-#pragma unroll
-        for (int h = 0; h < kParts; ++h) cand_count[kParts * tq + h] = 0;
-    }
+    if (tq < nq)
+        for (int h = 0; h < nslot; ++h) cand_count[nslot * tq + h] = 0;
     if (blockIdx.x == 0 && threadIdx.x < 2) counters[threadIdx.x] = 0;
     const int32_t qi = tq < nq ? order[tq] : -1;
     const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
@@ -488,6 +491,62 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     }
 }
 
+// k > 1: heavy tiles (a few queries whose k-th nearest representative lies in another region
+// scan almost every list) are split over several CTAs: the tile's work items in up to
+// `maxsplit` contiguous ranges, each a virtual tile with its own candidate slots (split index),
+// merged by the re-rank.  A tile is split when its work exceeds half an SM's share; the work
+// comes back from the LPT key (16-bit exponent/mantissa code of tile_fill_kernel).
+__device__ __forceinline__ double lpt_work(uint64_t tkey) {
+    const unsigned key = 0xFFFFu - static_cast<unsigned>(tkey);
+    if (key == 0) return 0.0;
+    return ldexp(static_cast<double>(0x800u | (key & 0x7FFu)), static_cast<int>(key >> 11) - 11);
+}
+
+__global__ void __launch_bounds__(1024) split_plan_kernel(const int32_t *__restrict__ tile_order,
+                                                          const uint64_t *__restrict__ tkey_sorted, int ntiles,
+                                                          const int64_t *__restrict__ work_off,
+                                                          const int64_t *__restrict__ nwork, int maxsplit, int nsm,
+                                                          int4 *__restrict__ vt, int32_t *__restrict__ nvt) {
+    typedef cub::BlockReduce<double, 1024> Red;
+    typedef cub::BlockScan<int, 1024> Scan;
+    __shared__ typename Red::TempStorage red_tmp;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ double s_total;
+    __shared__ int s_base;
+    double part = 0.0;
+    for (int i = threadIdx.x; i < ntiles; i += blockDim.x) part += lpt_work(tkey_sorted[i]);
+    const double tot = Red(red_tmp).Sum(part);
+    if (threadIdx.x == 0) {
+        s_total = tot;
+        s_base = 0;
+    }
+    __syncthreads();
+    const double half_share = s_total / (2.0 * nsm);
+    for (int i0 = 0; i0 < ntiles; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        int S = 0, tile = 0;
+        int64_t wo = 0, nw = 0;
+        if (i < ntiles) {
+            tile = tile_order[i];
+            wo = work_off[tile];
+            nw = nwork[tile];
+            const double W = lpt_work(tkey_sorted[i]);
+            S = 1;
+            if (half_share > 0.0 && W > half_share) S = min(maxsplit, static_cast<int>(W / half_share) + 1);
+            if (S > nw) S = nw > 1 ? static_cast<int>(nw) : 1;
+        }
+        int pos, total;
+        Scan(scan_tmp).ExclusiveSum(S, pos, total);
+        const int base = s_base;
+        for (int sp = 0; sp < S; ++sp)
+            vt[base + pos + sp] = make_int4(tile, static_cast<int>(wo + nw * sp / S), static_cast<int>(wo + nw * (sp + 1) / S), sp);
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *nvt = s_base;
+}
+
 // ---- the stage-2 kernel -----------------------------------------------------------------
 template <int KT, int NP>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
@@ -517,6 +576,19 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         return reinterpret_cast<const float *>(lring + (li % kLSlots) * Cfg::kLSlotBytes + 32);
     };
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);  // 2-slot ring of tile ids
+    // work items [w0, w1) of scheduled entry t (a virtual tile when heavy tiles are split) and
+    // its split index (candidate slots split * kParts + part)
+    auto work_range = [&](int t, int64_t &w0, int64_t &w1) -> int {
+        if (P.vt) {
+            const int4 e = P.vt[t];
+            w0 = e.y;
+            w1 = e.z;
+            return e.w;
+        }
+        w0 = P.work_off[t];
+        w1 = w0 + P.nwork[t];
+        return 0;
+    };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     S2_TIME(unsigned long long tw[12] = {});
@@ -567,11 +639,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const uint32_t slot = it & 1;
                 sm100::mbar_wait(&tile_empty[slot], ((it >> 1) & 1) ^ 1);
                 const int t = atomicAdd(P.tile_counter, 1);
-                const int tile = t < P.ntiles ? P.tile_order[t] : -1;
+                const int tile = P.vt ? (t < *P.nvt ? t : -1) : (t < P.ntiles ? P.tile_order[t] : -1);
                 s_tiles[slot] = tile;
                 sm100::mbar_arrive(&tile_full[slot]);
                 if (tile < 0) break;
-                const int64_t wt0 = P.work_off[tile], wt1 = wt0 + P.nwork[tile];
+                int64_t wt0, wt1;
+                work_range(tile, wt0, wt1);
                 if (wt0 < wt1) issue_list(wt0);
                 for (int64_t w = wt0, w1 = wt1; w < w1; ++w) {
                     if (w + 1 < w1) issue_list(w + 1);
@@ -614,7 +687,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 const int tile = s_tiles[slot];
                 sm100::mbar_arrive(&tile_empty[slot]);
                 if (tile < 0) break;
-                for (int64_t w = P.work_off[tile], w1 = w + P.nwork[tile]; w < w1; ++w, ++li) {
+                int64_t w, w1;
+                work_range(tile, w, w1);
+                for (; w < w1; ++w, ++li) {
                     sm100::mbar_wait(&lfull[li % kLSlots], (li / kLSlots) & 1);
                     const int ext = lslot_wi(li).ext;
                     const uint32_t a = ai & 1;
@@ -666,7 +741,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(&tile_empty[slot]);
             if (tile < 0) break;
-            const int64_t slot_q = static_cast<int64_t>(tile) * kRows + row;
+            int64_t w0, w1;
+            const int split = work_range(tile, w0, w1);
+            const int64_t slot_q = static_cast<int64_t>(P.vt ? P.vt[tile].x : tile) * kRows + row;
             const int32_t qi = slot_q < P.nq ? P.order[slot_q] : -1;
             const bool live = qi >= 0;
             // this thread's quarter of the query row (rows padded to 64 floats with zeros)
@@ -686,7 +763,6 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     qv[4 * c + 3] = t.w;
                 }
             }
-            const int64_t w0 = P.work_off[tile], w1 = w0 + P.nwork[tile];
             // A operand of list w: this thread's kKd * 2 bytes of row `row` (+ the aug columns, last part)
             auto prep_a = [&](int64_t w) {
                 S2_TIME(const unsigned long long tp0 = clock64());
@@ -796,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             float4 hm = make_float4(0.f, 0.f, 0.f, 0.f);
             int32_t hpos = 0;
             bool held = false;
-            const int64_t slot_id = (static_cast<int64_t>(live ? qi : 0) * kParts + part);
+            const int64_t slot_id = static_cast<int64_t>(live ? qi : 0) * P.nslot + split * kParts + part;
             float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 3;
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
             // per-list row data, prefetched one list ahead
@@ -1070,7 +1146,7 @@ template <int KT>
 __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__restrict__ cand_lb,
                                                      const int32_t *__restrict__ cand_pos,
                                                      const int32_t *__restrict__ cand_count,
-                                                     const float *__restrict__ cand_ufin, int cap, int64_t nq,
+                                                     const float *__restrict__ cand_ufin, int cap, int nslot, int64_t nq,
                                                      const float *__restrict__ q, const float *__restrict__ xp,
                                                      const int32_t *__restrict__ perm, int d, int k,
                                                      uint64_t *__restrict__ out_keys) {
@@ -1078,17 +1154,21 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
     const int64_t i = (blockIdx.x * static_cast<int64_t>(kRerankThreads) + threadIdx.x) / kRerankLanes;
     if ((blockIdx.x * static_cast<int64_t>(kRerankThreads) + (threadIdx.x & ~31)) / kRerankLanes >= nq) return;
     bool live = i < nq;
-    int cnt[kParts];
+    // slots: column parts x splits of a heavy tile (k > 1).  The final bound is the smallest of
+    // the slots' bounds: each is at least the k-th best of the union (it bounds the k-th best of
+    // its own share).  Split slots that buffered nothing may be unwritten: their bound is skipped.
+    int cnt[kMaxSlots];
     float ufin = __int_as_float(0x7f800000);
 #pragma unroll
-    for (int h = 0; h < kParts; ++h) {
-        cnt[h] = live ? cand_count[kParts * i + h] : 0;
+    for (int h = 0; h < kMaxSlots; ++h) {
+        cnt[h] = (live && h < nslot) ? cand_count[static_cast<int64_t>(nslot) * i + h] : 0;
         if (cnt[h] < 0) live = false;  // overflowed: recomputed by the exact scan
-        if (live) ufin = fminf(ufin, cand_ufin[kParts * i + h]);
+        if (live && h < nslot && (h < kParts || cnt[h] > 0))
+            ufin = fminf(ufin, cand_ufin[static_cast<int64_t>(nslot) * i + h]);
     }
     int n = 0;
 #pragma unroll
-    for (int h = 0; h < kParts; ++h) n += live ? cnt[h] : 0;
+    for (int h = 0; h < kMaxSlots; ++h) n += live ? cnt[h] : 0;
     const float *qrow = q + (live ? i : 0) * d;
     uint64_t best[KT];
 #pragma unroll
@@ -1110,12 +1190,12 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
         if (g < n) {
             int h = 0, gg = g;
 #pragma unroll
-            for (int u = 0; u < kParts - 1; ++u)
+            for (int u = 0; u < kMaxSlots - 1; ++u)
                 if (h == u && gg >= cnt[u]) {
                     gg -= cnt[u];
                     h = u + 1;
                 }
-            const int64_t at = (static_cast<int64_t>(kParts) * i + h) * cap + gg;
+            const int64_t at = (static_cast<int64_t>(nslot) * i + h) * cap + gg;
             const float4 v0 = cand_lb[3 * at], v1 = cand_lb[3 * at + 1], mt = cand_lb[3 * at + 2];
             pos = cand_pos[at];
             const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
@@ -1360,7 +1440,7 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
                   int ntiles, const int32_t *tile_order, const int64_t *work_off, const int64_t *nwork,
                   const unsigned long long *work_total, const WorkItem *work, const int32_t *cut, int64_t cap_work,
                   int32_t *cand_count, int32_t *counters, uint64_t *keys, int64_t *status_dev, cudaStream_t st,
-                  int cap_groups);
+                  int cap_groups, int nslot, const int4 *vt, const int32_t *nvt);
 
 int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
               int64_t cap_work, int64_t *status_dev, cudaStream_t st, int cap_groups) {
@@ -1433,9 +1513,12 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     // undersized capacity makes every consumer kernel bail out and the caller
     // re-runs with the size reported in status[0]
     const int64_t total_work = cap_work;
+    // k > 1: heavy tiles split over up to kMaxSplit CTAs (RBC_S2_NOSPLIT=1: off)
+    const int nsplit = (k > 1 && cap_work < (int64_t(1) << 31) && !getenv("RBC_S2_NOSPLIT")) ? kMaxSplit : 1;
+    const int nslot = kParts * nsplit;
     DevBuf<WorkItem> work;
     DevBuf<int32_t> cut, cand_count, counters;
-    RBC_CHECK(cand_count.alloc(nq * kParts, st));  // zeroed by tile_fill_kernel
+    RBC_CHECK(cand_count.alloc(nq * nslot, st));  // zeroed by tile_fill_kernel
     RBC_CHECK(counters.alloc(2, st));              // (overflow count, tile counter), zeroed by tile_fill_kernel
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
@@ -1445,13 +1528,23 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
                                                    idx->radii, tc->poff,
                                                    idx->offsets, work.get(), cut.get(),
-                                                   tkey.get(), warm, cap_work, cand_count.get(), counters.get());
+                                                   tkey.get(), warm, cap_work, cand_count.get(), nslot, counters.get());
     RBC_LAUNCHED();
     RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb2, tkey.get(), tkey_sorted.get(), tids.get(),
                                              tile_order.get(), ntiles, 0, 16, st));
     note_launch();
+    DevBuf<int4> vt;
+    DevBuf<int32_t> nvt;
+    if (nsplit > 1) {
+        RBC_CHECK(vt.alloc(static_cast<int64_t>(ntiles) * nsplit, st));
+        RBC_CHECK(nvt.alloc(1, st));
+        split_plan_kernel<<<1, 1024, 0, st>>>(tile_order.get(), tkey_sorted.get(), ntiles, work_off.get(), nwork.get(),
+                                              nsplit, g_num_sms, vt.get(), nvt.get());
+        RBC_LAUNCHED();
+    }
     return s2_run(idx, q, nq, k, po, order, ntiles, tile_order.get(), work_off.get(), nwork.get(), work_total,
-                  work.get(), cut.get(), cap_work, cand_count.get(), counters.get(), keys, status_dev, st, cap_groups);
+                  work.get(), cut.get(), cap_work, cand_count.get(), counters.get(), keys, status_dev, st, cap_groups,
+                  nslot, nsplit > 1 ? vt.get() : nullptr, nsplit > 1 ? nvt.get() : nullptr);
 }
 
 // stage-2 kernel + exact re-rank + overflow scan + status over prepared work arrays
@@ -1461,7 +1554,7 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
                   int ntiles, const int32_t *tile_order, const int64_t *work_off, const int64_t *nwork,
                   const unsigned long long *work_total, const WorkItem *work, const int32_t *cut, int64_t cap_work,
                   int32_t *cand_count, int32_t *counters, uint64_t *keys, int64_t *status_dev, cudaStream_t st,
-                  int cap_groups) {
+                  int cap_groups, int nslot, const int4 *vt, const int32_t *nvt) {
     g_tc_scan_calls.fetch_add(1);
     const TcIndex *tc = static_cast<const TcIndex *>(idx->tc);
     // 3. the tensor-core scan
@@ -1471,10 +1564,10 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
     const int cap = cap_groups > 0 ? cap_groups : (k == 1 ? 18 : (16 + 24 * k < 512 ? 16 + 24 * k : 512));
     DevBuf<float> cand_lb, cand_ufin, q64buf;
     DevBuf<int32_t> cand_pos, ovf_list;
-    RBC_CHECK(cand_lb.alloc(nq * kParts * cap * 12, st));
-    RBC_CHECK(cand_pos.alloc(nq * kParts * cap, st));
-    RBC_CHECK(cand_ufin.alloc(nq * kParts, st));
-    RBC_CHECK(ovf_list.alloc(nq * kParts, st));
+    RBC_CHECK(cand_lb.alloc(nq * nslot * cap * 12, st));
+    RBC_CHECK(cand_pos.alloc(nq * nslot * cap, st));
+    RBC_CHECK(cand_ufin.alloc(nq * nslot, st));
+    RBC_CHECK(ovf_list.alloc(nq * nslot, st));
     const float *q64 = q;
     const int qw = 64 * tc->np;
     if (idx->d != qw || (reinterpret_cast<uintptr_t>(q) & 15) != 0) {
@@ -1496,6 +1589,9 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
     P.k = k;
     P.ntiles = ntiles;
     P.tile_order = tile_order;
+    P.vt = vt;
+    P.nvt = nvt;
+    P.nslot = nslot;
     P.order = order;
     P.nq = nq;
     P.work_off = work_off;
@@ -1526,7 +1622,8 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const unsigned grid = static_cast<unsigned>(ntiles < g_num_sms ? ntiles : g_num_sms);
+    const int64_t entries = vt ? static_cast<int64_t>(ntiles) * (nslot / kParts) : ntiles;
+    const unsigned grid = static_cast<unsigned>(entries < g_num_sms ? entries : g_num_sms);
     auto launch = [&](auto kern, size_t smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<grid, kThreads, smem, st>>>(P);
@@ -1558,7 +1655,7 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
 #define RBC_RERANK(KT)                                                                                              \
     rerank_kernel<KT><<<rgrid, kRerankThreads, 0, st>>>(reinterpret_cast<const float4 *>(cand_lb.get()),           \
                                                         cand_pos.get(), cand_count,                           \
-                                                        cand_ufin.get(), cap, nq, q, idx->xp, idx->perm, idx->d, k, \
+                                                        cand_ufin.get(), cap, nslot, nq, q, idx->xp, idx->perm, idx->d, k, \
                                                         keys)
         if (k == 1) RBC_RERANK(1);
         else if (k <= 4) RBC_RERANK(4);
@@ -1584,8 +1681,8 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
     stage2_status_kernel<<<1, 1, 0, st>>>(work_total, counters, status_dev);
     RBC_LAUNCHED();
     if (getenv("RBC_DEBUG_CAND")) {  // diagnostic: buffered-group counts (synchronises)
-        std::vector<int32_t> cc(nq * kParts);
-        cudaMemcpyAsync(cc.data(), cand_count, sizeof(int32_t) * nq * kParts, cudaMemcpyDeviceToHost, st);
+        std::vector<int32_t> cc(nq * nslot);
+        cudaMemcpyAsync(cc.data(), cand_count, sizeof(int32_t) * nq * nslot, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         int64_t sum = 0, ovf = 0, mx = 0;
         for (int32_t v : cc) {
@@ -2019,7 +2116,7 @@ static int tc_bf_index_search_batch(const rbc_index *idx, const float *q, int64_
     const int capg = capenv ? atoi(capenv) : 16 + 8 * k;
     RBC_CHECK(s2_run(idx, q, nq, k, po, order.get(), ntiles, tile_order.get(), work_off.get(), nwork.get(),
                      work_total.get(), work.get(), nullptr, cap_work, cand_count.get(), counters.get(), keys,
-                     status.get(), st, capg));
+                     status.get(), st, capg, kParts, nullptr, nullptr));
     int64_t h[2] = {0, 0};
     RBC_CUDA(cudaMemcpyAsync(h, status.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaStreamSynchronize(st));
