@@ -354,7 +354,14 @@ int simt_dmax(int d) { return d <= 24 ? 24 : d <= 64 ? 64 : 128; }
 int simt_kt(int k) { return k <= 1 ? 1 : k <= 4 ? 4 : k <= 16 ? 16 : 32; }
 // queries per lane: each shared-memory row read serves QPT queries, as registers allow
 // (grouped items with small groups use one: a lane slot left empty costs a full scan)
-int simt_qpt(int d, int k, bool small_groups = false) { return d <= 64 && k <= 16 && !small_groups ? 2 : 1; }
+int simt_qpt(int d, int k) { return d <= 64 && k <= 16 ? 2 : 1; }
+// grouped items: enough queries per lane that one chunk holds a typical group (every chunk of a
+// group scans the whole s-list, so an almost empty second chunk costs as much as a full one)
+int simt_qpt_grouped(int d, int k, int64_t nq, int64_t nr) {
+    const int64_t mean = (nq + nr - 1) / (nr > 0 ? nr : 1);
+    // (three queries per lane for ~69-query groups measured slower at cfg4: 1.26 vs 1.06 ms)
+    return d <= 64 && k <= 16 && mean > 96 ? 2 : 1;
+}
 int simt_tp(int d4) { return d4 <= 32 ? 128 : 64; }
 
 size_t simt_smem(int d4, int k, int qpt) {
@@ -498,7 +505,7 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
     RBC_CHECK(istart.alloc(nr, st));
     RBC_CHECK(qorder.alloc(nq, st));
     RBC_CHECK(nitems.alloc(1, st));
-    const int qpt = simt_qpt(idx->d, k, nq < 96 * idx->nr);  // mean group below 96 queries
+    const int qpt = simt_qpt_grouped(idx->d, k, nq, idx->nr);
     const int qb = 32 * qpt;
     const int64_t max_items = std::min<int64_t>(nr, nq) + nq / qb + 1;
     RBC_CHECK(items.alloc(max_items, st));

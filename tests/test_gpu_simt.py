@@ -193,3 +193,19 @@ def test_select_unrepresentative_sample_falls_back(rbc, oracle):
         oi, od = oracle.bf_topk(q, x, k, metric)
         assert np.array_equal(ids, oi) and np.array_equal(dists, od)
     assert _select_calls()[1] > f0, "expected the exact fallback"
+
+
+@pytest.mark.parametrize("metric", ["l1", "l2"])
+@pytest.mark.parametrize("k", [1, 3])
+def test_simt_one_shot_large_groups(rbc, oracle, metric, k):
+    # about 100 queries per representative: three (d <= 24, k <= 4) or two queries per lane,
+    # groups of more than one chunk
+    d = 21
+    x = oracle.gen_clusters(20_000, d, 61, n_clusters=8, cluster_sigma=0.05)
+    q = oracle.gen_clusters(4_000, d, 62, n_clusters=8, cluster_sigma=0.05)
+    idx = rbc.build_one_shot(rbc.DataMatrix(x), 40, 200, rbc.MetricSpec(metric, d), seed=5)
+    lists, _ = oracle.build_one_shot(x, idx.reps.rep_ids, 200, metric)
+    got = rbc.one_shot_query_arrays(idx, q, k)
+    want = oracle.one_shot_query(x, idx.reps.rep_ids, lists, q, k, metric)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
