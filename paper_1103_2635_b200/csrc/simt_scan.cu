@@ -232,33 +232,45 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
         }
         __syncthreads();
         const float *tile = tiles + buf * tp * d4;
-        for (int j = warp; j < tn; j += kW) {
-            const float4 *xr = reinterpret_cast<const float4 *>(tile + j * d4);
-            float2 acc[QPT][2];
+        // kRows tile rows per step (a warp's rows j, j + kW, ...): every row's loads are issued
+        // before any arithmetic (independent registers, predicated instead of branched), so the
+        // shared-memory latency overlaps across rows and chunks
+        constexpr int kRowsStep = DMAX * (QPT + 2) <= 128 ? 2 : 1;
+        for (int j = warp; j < tn; j += kRowsStep * kW) {
+            float4 xs[kRowsStep][DMAX / 4];
 #pragma unroll
-            for (int u = 0; u < QPT; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
+            for (int rr = 0; rr < kRowsStep; ++rr) {
+                const int jr = j + rr * kW < tn ? j + rr * kW : j;
+                const float4 *xr = reinterpret_cast<const float4 *>(tile + jr * d4);
 #pragma unroll
-            for (int c = 0; c < DMAX / 4; ++c) {
-                if (4 * c < d) {
-                    const float4 x = xr[c];
+                for (int c = 0; c < DMAX / 4; ++c) xs[rr][c] = 4 * c < d ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int rr = 0; rr < kRowsStep; ++rr) {
+                if (j + rr * kW >= tn) break;  // warp-uniform
+                float2 acc[QPT][2];
+#pragma unroll
+                for (int u = 0; u < QPT; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < DMAX / 4; ++c) {
 #pragma unroll
                     for (int u = 0; u < QPT; ++u) {
-                        acc2<METRIC>(qv[u][2 * c], make_float2(x.x, x.y), acc[u][0]);
-                        acc2<METRIC>(qv[u][2 * c + 1], make_float2(x.z, x.w), acc[u][1]);
+                        acc2<METRIC>(qv[u][2 * c], make_float2(xs[rr][c].x, xs[rr][c].y), acc[u][0]);
+                        acc2<METRIC>(qv[u][2 * c + 1], make_float2(xs[rr][c].z, xs[rr][c].w), acc[u][1]);
                     }
                 }
-            }
 #pragma unroll
-            for (int u = 0; u < QPT; ++u) {
-                const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
-                if (S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
-                if (S <= T[u]) {
-                    qs_s[qn * kT + tid] = S;
-                    qs_r[qn * kT + tid] = (static_cast<uint32_t>(u) << 28) | static_cast<uint32_t>(t0 + j);
-                    ++qn;
+                for (int u = 0; u < QPT; ++u) {
+                    const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
+                    if (S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
+                    if (S <= T[u]) {
+                        qs_s[qn * kT + tid] = S;
+                        qs_r[qn * kT + tid] = (static_cast<uint32_t>(u) << 28) | static_cast<uint32_t>(t0 + j + rr * kW);
+                        ++qn;
+                    }
                 }
+                if (__any_sync(0xffffffffu, qn > kQLen - QPT)) drain();
             }
-            if (__any_sync(0xffffffffu, qn > kQLen - QPT)) drain();
         }
         // bound exchange: every warp adopts the smallest published bound of each query
 #pragma unroll
