@@ -1142,8 +1142,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
 constexpr int kRerankLanes = 8;
 constexpr int kRerankThreads = 256;
 
-template <int KT>
-__global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__restrict__ cand_lb,
+template <int KT, int DL>
+__global__ void __launch_bounds__(kRerankThreads, KT == 1 ? 4 : 0) rerank_kernel(const float4 *__restrict__ cand_lb,
                                                      const int32_t *__restrict__ cand_pos,
                                                      const int32_t *__restrict__ cand_count,
                                                      const float *__restrict__ cand_ufin, int cap, int nslot, int64_t nq,
@@ -1157,31 +1157,78 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
     // slots: column parts x splits of a heavy tile (k > 1).  The final bound is the smallest of
     // the slots' bounds: each is at least the k-th best of the union (it bounds the k-th best of
     // its own share).  Split slots that buffered nothing may be unwritten: their bound is skipped.
-    int cnt[kMaxSlots];
+    constexpr int kSlots = KT == 1 ? kParts : kMaxSlots;  // k = 1 never splits tiles
+    const int ns = KT == 1 ? kParts : nslot;
+    int cnt[kSlots];
     float ufin = __int_as_float(0x7f800000);
 #pragma unroll
-    for (int h = 0; h < kMaxSlots; ++h) {
-        cnt[h] = (live && h < nslot) ? cand_count[static_cast<int64_t>(nslot) * i + h] : 0;
+    for (int h = 0; h < kSlots; ++h) {
+        cnt[h] = (live && h < ns) ? cand_count[static_cast<int64_t>(ns) * i + h] : 0;
         if (cnt[h] < 0) live = false;  // overflowed: recomputed by the exact scan
-        if (live && h < nslot && (h < kParts || cnt[h] > 0))
-            ufin = fminf(ufin, cand_ufin[static_cast<int64_t>(nslot) * i + h]);
+        if (live && h < ns && (h < kParts || cnt[h] > 0))
+            ufin = fminf(ufin, cand_ufin[static_cast<int64_t>(ns) * i + h]);
     }
     int n = 0;
 #pragma unroll
-    for (int h = 0; h < kMaxSlots; ++h) n += live ? cnt[h] : 0;
+    for (int h = 0; h < kSlots; ++h) n += live ? cnt[h] : 0;
     const float *qrow = q + (live ? i : 0) * d;
     uint64_t best[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
     // lanes over the query's buffered groups: the elements that can still qualify
     const int nmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(n));
-    const bool fast = d == 64 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;  // warp-uniform
-    // this lane's 8 query coordinates for the group-cooperative distance (d == 64)
-    float4 qa = make_float4(0.f, 0.f, 0.f, 0.f), qb = qa;
-    if (fast && live) {
-        qa = __ldg(reinterpret_cast<const float4 *>(qrow) + sub);
-        qb = __ldg(reinterpret_cast<const float4 *>(qrow) + sub + kRerankLanes);
+    // group-cooperative exact distances for d <= 8 DL: lane `sub` owns coordinates
+    // [sub DL, sub DL + DL) (zero beyond d: exact zero terms do not change the sum)
+    const bool fast = d <= kRerankLanes * DL;  // warp-uniform
+    const bool vec = fast && (d & 3) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(xp) & 15) == 0;
+    // coordinates of lane `sub`: 16-byte rows -> float4 number sub + 8 t4 (the group's loads
+    // of one row are contiguous 128-byte runs); otherwise the run [sub DL, sub DL + DL)
+    auto coord = [&](int t) { return vec ? 4 * (sub + kRerankLanes * (t >> 2)) + (t & 3) : sub * DL + t; };
+    const bool full = vec && d == kRerankLanes * DL;  // every lane's coordinates inside the row
+    float xs[DL];
+    if (full) {
+#pragma unroll
+        for (int t = 0; t < DL; t += 4) {
+            const float4 v = live ? __ldg(reinterpret_cast<const float4 *>(qrow) + sub + kRerankLanes * (t >> 2))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            xs[t] = v.x;
+            xs[t + 1] = v.y;
+            xs[t + 2] = v.z;
+            xs[t + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < DL; ++t) xs[t] = (fast && live && coord(t) < d) ? __ldg(qrow + coord(t)) : 0.f;
     }
+    // this lane's DL coordinates of point row p
+    auto load_row = [&](int32_t p, float (&ys)[DL]) {
+        const float *row = xp + static_cast<int64_t>(p) * d;
+        if (full) {
+            const float4 *r4 = reinterpret_cast<const float4 *>(row) + sub;
+#pragma unroll
+            for (int t = 0; t < DL; t += 4) {
+                const float4 v = __ldg(r4 + kRerankLanes * (t >> 2));
+                ys[t] = v.x;
+                ys[t + 1] = v.y;
+                ys[t + 2] = v.z;
+                ys[t + 3] = v.w;
+            }
+        } else if (vec) {
+#pragma unroll
+            for (int t = 0; t < DL; t += 4) {
+                const float4 v = coord(t) < d ? __ldg(reinterpret_cast<const float4 *>(row + coord(t)))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                ys[t] = v.x;
+                ys[t + 1] = v.y;
+                ys[t + 2] = v.z;
+                ys[t + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < DL; ++t) ys[t] = coord(t) < d ? __ldg(row + coord(t)) : 0.f;
+        }
+    };
     const int gshift = (threadIdx.x & 31) & ~(kRerankLanes - 1);
     for (int g0 = 0; g0 < nmax; g0 += kRerankLanes) {
         const int g = g0 + sub;
@@ -1190,12 +1237,12 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
         if (g < n) {
             int h = 0, gg = g;
 #pragma unroll
-            for (int u = 0; u < kMaxSlots - 1; ++u)
+            for (int u = 0; u < kSlots - 1; ++u)
                 if (h == u && gg >= cnt[u]) {
                     gg -= cnt[u];
                     h = u + 1;
                 }
-            const int64_t at = (static_cast<int64_t>(nslot) * i + h) * cap + gg;
+            const int64_t at = (static_cast<int64_t>(ns) * i + h) * cap + gg;
             const float4 v0 = cand_lb[3 * at], v1 = cand_lb[3 * at + 1], mt = cand_lb[3 * at + 2];
             pos = cand_pos[at];
             const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
@@ -1213,13 +1260,12 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
             }
             continue;
         }
-        // d == 64: two elements at a time per group (two row loads in flight), the 8 lanes each
-        // summing 8 of the 64 reference terms of each (identical fp64 terms; only the
+        // d <= 8 DL: two elements at a time per group (two row loads in flight), the 8 lanes each
+        // summing DL of the reference terms of each (identical fp64 terms; only the
         // association differs), then a shuffle tree.  The fp32 result equals the reference's
         // sequential sum unless the tree sum's square root lies within 2^-44 (relative) of an
-        // fp32 rounding midpoint -- the two sums differ by at most 2 * 63 * 2^-53 relative --
+        // fp32 rounding midpoint -- the two sums differ by at most 2 * 127 * 2^-53 relative --
         // in which case the owner lane recomputes the sequential sum.
-        const float xs[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
         auto finish = [&](double part, int32_t pp) {
             const double r = __dsqrt_rn(part);
             float f = __double2float_rn(r);
@@ -1246,14 +1292,11 @@ __global__ void __launch_bounds__(kRerankThreads) rerank_kernel(const float4 *__
             const int32_t ppB = __shfl_sync(0xffffffffu, pos, gshift + srcB) + jB;
             double partA = 0.0, partB = 0.0;
             if (whoA) {
-                const float4 *rA = reinterpret_cast<const float4 *>(xp + static_cast<int64_t>(ppA) * 64);
-                const float4 *rB = reinterpret_cast<const float4 *>(xp + static_cast<int64_t>(whoB ? ppB : ppA) * 64);
-                const float4 ya = __ldg(rA + sub), yb = __ldg(rA + sub + kRerankLanes);
-                const float4 za = __ldg(rB + sub), zb = __ldg(rB + sub + kRerankLanes);
-                const float ys[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
-                const float zs[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+                float ys[DL], zs[DL];
+                load_row(ppA, ys);
+                load_row(whoB ? ppB : ppA, zs);
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
+                for (int t = 0; t < DL; ++t) {
                     partA = __dadd_rn(partA, l2_term(xs[t], ys[t]));
                     partB = __dadd_rn(partB, l2_term(xs[t], zs[t]));
                 }
@@ -1653,13 +1696,20 @@ static int s2_run(const rbc_index *idx, const float *q, int64_t nq, int k, const
     {
         const unsigned rgrid = grid_for(nq * kRerankLanes, kRerankThreads);
 #define RBC_RERANK(KT)                                                                                              \
-    rerank_kernel<KT><<<rgrid, kRerankThreads, 0, st>>>(reinterpret_cast<const float4 *>(cand_lb.get()),           \
-                                                        cand_pos.get(), cand_count,                           \
-                                                        cand_ufin.get(), cap, nslot, nq, q, idx->xp, idx->perm, idx->d, k, \
-                                                        keys)
+    do {                                                                                                            \
+        if (idx->d <= 64)                                                                                           \
+            rerank_kernel<KT, 8><<<rgrid, kRerankThreads, 0, st>>>(                                                  \
+                reinterpret_cast<const float4 *>(cand_lb.get()), cand_pos.get(), cand_count, cand_ufin.get(), cap,    \
+                nslot, nq, q, idx->xp, idx->perm, idx->d, k, keys);                                                  \
+        else                                                                                                        \
+            rerank_kernel<KT, 16><<<rgrid, kRerankThreads, 0, st>>>(                                                 \
+                reinterpret_cast<const float4 *>(cand_lb.get()), cand_pos.get(), cand_count, cand_ufin.get(), cap,    \
+                nslot, nq, q, idx->xp, idx->perm, idx->d, k, keys);                                                  \
+    } while (0)
         if (k == 1) RBC_RERANK(1);
         else if (k <= 4) RBC_RERANK(4);
         else if (k <= 8) RBC_RERANK(8);
+        else if (k == 10) RBC_RERANK(10);
         else if (k <= 16) RBC_RERANK(16);
         else RBC_RERANK(32);
 #undef RBC_RERANK

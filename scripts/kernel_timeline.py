@@ -17,6 +17,8 @@ def main():
     from paper_1103_2635_b200 import _lib
     from paper_1103_2635_b200.rbc import device_index
 
+    if len(sys.argv) > 3:  # optional config name (default cfg2)
+        bench.select_config(sys.argv[3], int(sys.argv[2]) if len(sys.argv) > 2 else None)
     nq = int(sys.argv[1]) if len(sys.argv) > 1 else bench.NQ
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     x, q = bench.gen_inputs(0)
