@@ -81,7 +81,7 @@ struct S2Cfg {
     // per-list data ring (work item + representative row + its B rounding error), staged by the
     // producer one list ahead so no role waits on a dependent global load at a list switch
     static constexpr int kRepStride = 64 * NP + 4;                        // floats per rep row
-    static constexpr int kLSlotBytes = 32 + kRepStride * 4;               // WorkItem + rep row
+    static constexpr int kLSlotBytes = 32 + kRepStride * 4 + kRows * 4;  // WorkItem + rep row + row cutoffs
     static constexpr size_t kSmem = 1024 + kStages * kStageBytes + 2 * kABytes +
                                     (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) +
                                     kLSlots * kLSlotBytes + 512;
@@ -575,6 +575,9 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     auto lslot_rep = [&](uint32_t li) {
         return reinterpret_cast<const float *>(lring + (li % kLSlots) * Cfg::kLSlotBytes + 32);
     };
+    auto lslot_cut = [&](uint32_t li) {  // the list's per-row cutoffs (work item's cut row)
+        return reinterpret_cast<const int32_t *>(lring + (li % kLSlots) * Cfg::kLSlotBytes + 32 + Cfg::kRepStride * 4);
+    };
     int *s_tiles = reinterpret_cast<int *>(s_tmem + 1);  // 2-slot ring of tile ids
     // work items [w0, w1) of scheduled entry t (a virtual tile when heavy tiles are split) and
     // its split index (candidate slots split * kParts + part)
@@ -629,10 +632,12 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 sm100::mbar_wait(&lempty[sl], ((li / kLSlots) & 1) ^ 1);
                 uint8_t *dst = lring + sl * Cfg::kLSlotBytes;
                 const int32_t p = P.work[w].p;
-                sm100::mbar_arrive_expect_tx(&lfull[sl], Cfg::kLSlotBytes);
+                sm100::mbar_arrive_expect_tx(&lfull[sl], 32 + Cfg::kRepStride * 4 + (P.cut ? kRows * 4 : 0));
                 sm100::bulk_g2s(dst, P.work + w, 32, &lfull[sl]);
                 sm100::bulk_g2s(dst + 32, P.reps64 + static_cast<int64_t>(p) * Cfg::kRepStride, Cfg::kRepStride * 4,
                                 &lfull[sl]);
+                if (P.cut)
+                    sm100::bulk_g2s(dst + 32 + Cfg::kRepStride * 4, P.cut + w * kRows, kRows * 4, &lfull[sl]);
                 ++li;
             };
             for (uint32_t it = 0;; ++it) {
@@ -875,15 +880,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             const int64_t slot_id = static_cast<int64_t>(live ? qi : 0) * P.nslot + split * kParts + part;
             float4 *clb = reinterpret_cast<float4 *>(P.cand_lb) + slot_id * P.cap * 3;
             int32_t *cpos = P.cand_pos + slot_id * P.cap;
-            // per-list row data, prefetched one list ahead
-            int cut_n = 0;
-            if (w0 < w1) cut_n = P.cut ? P.cut[w0 * kRows + row] : P.work[w0].ext;
             for (int64_t w = w0; w < w1; ++w) {
                 if (w + 1 < w1) prep_a(w + 1);  // next list's A while this list's MMAs run
                 const uint32_t lw = li0 + static_cast<uint32_t>(w - w0);  // (waited for by prep_a(w))
                 const WorkItem wi = lslot_wi(lw);
-                const int cutv = live ? cut_n : 0;
-                if (w + 1 < w1) cut_n = P.cut ? P.cut[(w + 1) * kRows + row] : P.work[w + 1].ext;
+                const int cutv = live ? (P.cut ? lslot_cut(lw)[row] : wi.ext) : 0;
                 // both column parts of this lane quadrant have prepared lists w and w + 1: the
                 // row's |q - r_p|^2 is the sum of their two halves (slot w & 3; a part runs at
                 // most one list ahead of its partner, so slots are never overwritten early)
