@@ -72,7 +72,7 @@ constexpr int kMaxSlots = kParts * kMaxSplit;  // candidate slots per query (col
 template <int NP>
 struct S2Cfg {
     static constexpr int kN = NP == 1 ? 256 : 128;   // UMMA N per chunk
-    static constexpr int kStages = NP == 1 ? 4 : 3;  // B ring depth
+    static constexpr int kStages = 3;                // B ring depth (B traffic is not the bound)
     static constexpr int kCols = kN / kParts;        // columns of each chunk per epilogue warp
     static constexpr int kKd = 64 * NP / kParts;     // A-operand dims per epilogue warp
     static constexpr int kStageBytes = kN * (NP * kP0 + kP1);
@@ -82,8 +82,13 @@ struct S2Cfg {
     // producer one list ahead so no role waits on a dependent global load at a list switch
     static constexpr int kRepStride = 64 * NP + 4;                        // floats per rep row
     static constexpr int kLSlotBytes = 32 + kRepStride * 4 + kRows * 4;  // WorkItem + rep row + row cutoffs
+    // NP = 1: the tile's query rows in shared memory (the A-operand preparation reads them per
+    // list; registers go to two TMEM loads in flight instead), stride 68 floats (conflict-free
+    // 16-byte loads of 32 consecutive rows)
+    static constexpr int kQStride = 68;
+    static constexpr int kQSmemFloats = NP == 1 ? kRows * kQStride : 0;
     static constexpr size_t kSmem = 1024 + kStages * kStageBytes + 2 * kABytes +
-                                    (kEpiWarps * kCols + 8 * kParts * kRows) * sizeof(float) +
+                                    (kEpiWarps * kCols + 8 * kParts * kRows + kQSmemFloats) * sizeof(float) +
                                     kLSlots * kLSlotBytes + 512;
 };
 
@@ -562,7 +567,8 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
     float *gbuf = reinterpret_cast<float *>(sA + 2 * kABytes);  // 8 epilogue warps x 128 (fallback column)
     float *s_dq = gbuf + kEpiWarps * kCols;  // [4 list slots][kParts][128] partial |q - r_p|^2
     float *s_da = s_dq + 4 * kParts * kRows;  // [4 list slots][kParts][128] partial |a - f16(a)|^2 (scaled)
-    uint8_t *lring = reinterpret_cast<uint8_t *>(s_da + 4 * kParts * kRows);  // [kLSlots] per-list data
+    float *sQ = s_da + 4 * kParts * kRows;  // NP = 1: [128][kQStride] the tile's query rows
+    uint8_t *lring = reinterpret_cast<uint8_t *>(sQ + Cfg::kQSmemFloats);  // [kLSlots] per-list data
     uint64_t *bars = reinterpret_cast<uint64_t *>(lring + kLSlots * Cfg::kLSlotBytes);
     uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + kAcc;
     uint64_t *afull = tempty + kAcc, *aempty = afull + 2, *tile_full = aempty + 2, *tile_empty = tile_full + 2;
@@ -754,19 +760,14 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             // this thread's quarter of the query row (rows padded to 64 floats with zeros)
             // (NP = 2: 64 floats per thread would not fit beside the epilogue's registers;
             // prep_a then re-reads the row from L1)
-            constexpr int kQv = NP == 1 ? kKd : 4;
-            float qv[kQv];
             const float4 *qsrc =
                 reinterpret_cast<const float4 *>(P.q64 + static_cast<int64_t>(live ? qi : 0) * (64 * NP) + part * kKd);
+            // NP = 1: this thread's part of its query row into shared memory (only this thread
+            // reads it back, in prep_a; the previous tile's reads by this thread are done)
+            float4 *qs4 = reinterpret_cast<float4 *>(sQ + row * Cfg::kQStride + part * kKd);
             if (NP == 1) {
 #pragma unroll
-                for (int c = 0; c < kQv / 4; ++c) {
-                    const float4 t = live ? __ldg(qsrc + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    qv[4 * c] = t.x;
-                    qv[4 * c + 1] = t.y;
-                    qv[4 * c + 2] = t.z;
-                    qv[4 * c + 3] = t.w;
-                }
+                for (int c = 0; c < kKd / 4; ++c) qs4[c] = live ? __ldg(qsrc + c) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             // A operand of list w: this thread's kKd * 2 bytes of row `row` (+ the aug columns, last part)
             auto prep_a = [&](int64_t w) {
@@ -804,8 +805,16 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 float da2 = 0.f;  // |a - f16(a)|^2 of this part (scaled units)
                 if constexpr (NP == 1) {
                     float4 rr4[kKd / 4];
+                    float qv[kKd];
 #pragma unroll
-                    for (int c = 0; c < kKd / 4; ++c) rr4[c] = rep4[c];
+                    for (int c = 0; c < kKd / 4; ++c) {
+                        rr4[c] = rep4[c];
+                        const float4 t = qs4[c];
+                        qv[4 * c] = t.x;
+                        qv[4 * c + 1] = t.y;
+                        qv[4 * c + 2] = t.z;
+                        qv[4 * c + 3] = t.w;
+                    }
                     // this part's share of |q - r_p|^2 (fp32; with the other part's, the A2 term of
                     // the error bound -- same (d + 2) 2^-24 relative error budget as kD1 / kUq)
                     {
