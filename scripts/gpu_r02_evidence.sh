@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 evidence run: full GPU suite, bench lines for every config (+ reference arm), ncu launch
 # lists and --set full captures of the dominant kernels.  Everything lands in gpurun_out/r02e/.
-O=gpurun_out/r02e; mkdir -p $O
+O=gpurun_out/${R02E:-r02e}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q --durations=10 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 tail -3 $O/pytest_gpu.log
@@ -22,7 +22,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
    python scripts/prof_search.py --config cfg2 --iters 2 > $O/ncu_cfg2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'simt_tile|collect_kernel' -c 3 \
    -o $O/ncu_cfg4 -f python scripts/prof_search.py --config cfg4 --iters 1 > $O/ncu_cfg4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'stage2_tc_kernel' -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage2_tc_kernel -s 3 -c 1 \
    -o $O/ncu_cfg3 -f python scripts/prof_search.py --config cfg3 --iters 1 > $O/ncu_cfg3.log 2>&1
 for r in ncu_cfg2 ncu_cfg4 ncu_cfg3; do python scripts/ncu_hot.py $O/$r.ncu-rep 25 > $O/${r}_summary.txt 2>&1; done
 ls -la $O
