@@ -20,9 +20,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on \
    -k regex:'stage[12]_tc_kernel|stage1_fixup|rerank|tile_fill' -s 6 -c 5 -o $O/ncu_cfg2 -f \
    python scripts/prof_search.py --config cfg2 --iters 2 > $O/ncu_cfg2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'simt_tile|collect_kernel' -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'simt_tile|collect_kernel' -c 4 \
    -o $O/ncu_cfg4 -f python scripts/prof_search.py --config cfg4 --iters 1 > $O/ncu_cfg4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage2_tc_kernel -s 3 -c 1 \
-   -o $O/ncu_cfg3 -f python scripts/prof_search.py --config cfg3 --iters 1 > $O/ncu_cfg3.log 2>&1
+   -o $O/ncu_cfg3 -f python scripts/prof_search.py --config cfg3 --iters 2 > $O/ncu_cfg3.log 2>&1
 for r in ncu_cfg2 ncu_cfg4 ncu_cfg3; do python scripts/ncu_hot.py $O/$r.ncu-rep 25 > $O/${r}_summary.txt 2>&1; done
 ls -la $O
