@@ -319,6 +319,7 @@ static int exact_create(const float *x, int64_t n, int32_t d, int32_t metric, co
     if (rc == RBC_OK && cudaGetLastError() != cudaSuccess) rc = fail(RBC_ECUDA, "index kernels");
     if (rc == RBC_OK) rc = tc_index_prepare(idx, st);
     if (rc == RBC_OK) rc = tc1_index_prepare(idx, st);
+    if (rc == RBC_OK) rc = simt_index_prepare(idx, st);
     if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "index sync");
     if (rc != RBC_OK) {
         rbc_index_destroy(idx);
@@ -589,6 +590,7 @@ int rbc_index_exact_create_local(const float *reps, const int64_t *rep_ids, int6
     if (rc == RBC_OK) rc = cudaGetDevice(&idx->device) == cudaSuccess ? RBC_OK : fail(RBC_ECUDA, "device");
     if (rc == RBC_OK) rc = tc_index_prepare(idx, st);
     if (rc == RBC_OK) rc = tc1_index_prepare(idx, st);
+    if (rc == RBC_OK) rc = simt_index_prepare(idx, st);
     if (rc == RBC_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(RBC_ECUDA, "shard index sync");
     if (rc != RBC_OK) {
         rbc_index_destroy(idx);

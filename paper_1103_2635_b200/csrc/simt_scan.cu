@@ -69,6 +69,9 @@ struct SimtParams {
     int64_t nqc;             // dense: query chunks
     int64_t np;              // dense: point rows
     int64_t pchunk;          // dense: rows per split (< 2^31)
+    const int32_t *qcut;     // segment items: rows of the item each position scans (nullptr: all)
+    const int64_t *qout;     // segment items: output row of each position (nullptr: its query)
+    const float *qthr;       // segment items: initial fp32 bound of each position (nullptr: none)
     int k;
     int qpt;                 // queries per lane (host side: selects the instantiation)
     uint64_t *out;           // [split][nq][k]
@@ -159,10 +162,12 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
     uint32_t *qs_r = reinterpret_cast<uint32_t *>(qs_s + kQLen * kT);  // [kQLen][kT] (u << 28) | row
     const float *qg[QPT];
     float2 qv[QPT][DMAX / 2];
+    int lim[QPT];  // rows this position scans (segment items: its list's cutoff)
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
         const int pos = 32 * u + lane < qcnt ? 32 * u + lane : 0;  // a missing query repeats the first
         const int64_t qi = P.qorder ? P.qorder[qbeg + pos] : qbeg + pos;
+        lim[u] = P.qcut ? P.qcut[qbeg + pos] : pcnt;
         qg[u] = P.q + qi * d;
 #pragma unroll
         for (int c = 0; c < DMAX / 2; ++c)
@@ -174,7 +179,8 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
     uint64_t ek[QPT][KT];
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
-        T[u] = __int_as_float(0x7f800000);
+        const int pos = 32 * u + lane < qcnt ? 32 * u + lane : 0;
+        T[u] = P.qthr ? P.qthr[qbeg + pos] : __int_as_float(0x7f800000);
 #pragma unroll
         for (int j = 0; j < KT; ++j) {
             sv[u][j] = __int_as_float(0x7f800000);
@@ -262,8 +268,9 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
 #pragma unroll
                 for (int u = 0; u < QPT; ++u) {
                     const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
-                    if (S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
-                    if (S <= T[u]) {
+                    const bool in = t0 + j + rr * kW < lim[u];  // segment items: inside its cutoff
+                    if (in && S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
+                    if (in && S <= T[u]) {
                         qs_s[qn * kT + tid] = S;
                         qs_r[qn * kT + tid] = (static_cast<uint32_t>(u) << 28) | static_cast<uint32_t>(t0 + j + rr * kW);
                         ++qn;
@@ -305,7 +312,7 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
                 if (key >= best[KT - 1]) break;  // each warp's list ascends
                 sorted_insert<KT>(best, key);
             }
-        const int64_t qi = P.qorder ? P.qorder[qbeg + qp] : qbeg + qp;
+        const int64_t qi = P.qout ? P.qout[qbeg + qp] : (P.qorder ? P.qorder[qbeg + qp] : qbeg + qp);
         uint64_t *outq = P.out + (slot * P.nq + qi) * k;
 #pragma unroll
         for (int j = 0; j < KT; ++j)
@@ -362,17 +369,96 @@ __global__ void near_items_kernel(const int32_t *__restrict__ cnt, const int32_t
     if (r == nr - 1) *nitems = istart[r] + nc;
 }
 
+// ---- exact-search stage 2 on the SIMT filter (search.py:183-186): surviving segments grouped by list --
+__global__ void seg_query_kernel(const int64_t *__restrict__ seg_off, const int32_t *__restrict__ nseg, int64_t nq,
+                                 const int32_t *__restrict__ seg_list, int32_t *__restrict__ seg_q,
+                                 uint32_t *__restrict__ key, int32_t *__restrict__ val) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nq) return;
+    for (int64_t s = seg_off[i], e = s + nseg[i]; s < e; ++s) {
+        seg_q[s] = static_cast<int32_t>(i);
+        key[s] = static_cast<uint32_t>(seg_list[s]);
+        val[s] = static_cast<int32_t>(s);
+    }
+}
+
+__global__ void seg_hist_kernel(const uint32_t *__restrict__ skey, int64_t total, int32_t *__restrict__ cnt) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < total) atomicAdd(&cnt[skey[t]], 1);
+}
+
+// items of list p: its segments (sorted positions [start[p], start[p] + cnt[p])) in chunks of qb;
+// each item scans the list's rows up to the largest cutoff among its segments
+__global__ void seg_items_kernel(const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
+                                 const int32_t *__restrict__ istart, int64_t nr, const int64_t *__restrict__ offsets,
+                                 const int32_t *__restrict__ sval, const int32_t *__restrict__ seg_len, int qb,
+                                 ScanItem *__restrict__ items, int32_t *__restrict__ nitems) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p >= nr) return;
+    const int c = cnt[p];
+    const int nc = (c + qb - 1) / qb;
+    for (int j = 0; j < nc; ++j) {
+        ScanItem it;
+        it.qbeg = start[p] + j * qb;
+        it.qcnt = min(qb, c - j * qb);
+        int m = 0;
+        for (int e = 0; e < it.qcnt; ++e) m = max(m, seg_len[sval[it.qbeg + e]]);
+        it.pbeg = static_cast<int32_t>(offsets[p]);
+        it.pcnt = m;
+        items[istart[p] + j] = it;
+    }
+    if (p == nr - 1) *nitems = istart[p] + nc;
+}
+
+// positions in list order: query, cutoff, output row, and the initial bound from the query's
+// gamma_k (the k nearest representatives are points of X, so the k-th neighbour lies within
+// gamma_k: S <= gamma^p fac, as in select.cu, keeps every possible member of the answer)
+__global__ void seg_positions_kernel(const int32_t *__restrict__ sval, int64_t total, const int32_t *__restrict__ seg_q,
+                                     const int32_t *__restrict__ seg_len, const float *__restrict__ gamma, int d,
+                                     int metric, int32_t *__restrict__ qorder, int32_t *__restrict__ qcut,
+                                     int64_t *__restrict__ qout, float *__restrict__ qthr) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= total) return;
+    const int32_t s = sval[t];
+    const int32_t qi = seg_q[s];
+    qorder[t] = qi;
+    qcut[t] = seg_len[s];
+    qout[t] = s;
+    const float g = gamma[qi];
+    const float fac = 1.0f + static_cast<float>(4 * d + 16) * (1.0f / 16777216.0f);
+    const float gp = metric == RBC_L2 ? g * g * (1.0f + 1.0f / 8388608.0f) : g;
+    qthr[t] = fmaf(gp, fac, static_cast<float>(d) * 1e-35f);
+}
+
+// per query: the k smallest keys over its segments' k-key rows (ascending; empty = ~0)
+template <int KT>
+__global__ void seg_merge_kernel(const uint64_t *__restrict__ seg_keys, const int64_t *__restrict__ seg_off,
+                                 const int32_t *__restrict__ nseg, int64_t nq, int k, uint64_t *__restrict__ out) {
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= nq) return;
+    uint64_t best[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+    const uint64_t *src = seg_keys + seg_off[i] * k;
+    for (int64_t t = lane, e = static_cast<int64_t>(nseg[i]) * k; t < e; t += 32) {
+        const uint64_t key = src[t];
+        if (key < best[KT - 1]) sorted_insert<KT>(best, key);
+    }
+    warp_merge_sorted<KT>(best, k, out + i * k);
+}
+
 int simt_dmax(int d) { return d <= 24 ? 24 : d <= 64 ? 64 : 128; }
 int simt_kt(int k) { return k <= 1 ? 1 : k <= 4 ? 4 : k <= 16 ? 16 : 32; }
 // queries per lane: each shared-memory row read serves QPT queries, as registers allow
 // (grouped items with small groups use one: a lane slot left empty costs a full scan)
-int simt_qpt(int d, int k) { return d <= 64 && k <= 16 ? 2 : 1; }
+int simt_qpt(int d, int k) { return d <= 64 && k <= 4 ? 2 : 1; }  // (k > 4: the k-best registers spill at two)
 // grouped items: enough queries per lane that one chunk holds a typical group (every chunk of a
 // group scans the whole s-list, so an almost empty second chunk costs as much as a full one)
 int simt_qpt_grouped(int d, int k, int64_t nq, int64_t nr) {
     const int64_t mean = (nq + nr - 1) / (nr > 0 ? nr : 1);
     // (three queries per lane for ~69-query groups measured slower at cfg4: 1.26 vs 1.06 ms)
-    return d <= 64 && k <= 16 && mean > 96 ? 2 : 1;
+    return d <= 64 && k <= 4 && mean > 96 ? 2 : 1;
 }
 int simt_tp(int d4) { return d4 <= 32 ? 128 : 64; }
 
@@ -407,7 +493,10 @@ template <int METRIC, int DMAX>
 int launch_dmax(const SimtParams &P, unsigned grid, cudaStream_t st) {
     if (P.k > 16) return launch_kt<METRIC, DMAX, 32, 1>(P, grid, st);
     if constexpr (DMAX <= 64) {
-        if (P.qpt == 2) return launch_qpt<METRIC, DMAX, 2>(P, grid, st);
+        if (P.qpt == 2) {  // k <= 4
+            if (simt_kt(P.k) == 1) return launch_kt<METRIC, DMAX, 1, 2>(P, grid, st);
+            return launch_kt<METRIC, DMAX, 4, 2>(P, grid, st);
+        }
     }
     return launch_qpt<METRIC, DMAX, 1>(P, grid, st);
 }
@@ -555,16 +644,119 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
     return simt_launch(P, idx->metric, max_items, st);
 }
 
+bool simt_exact_supported(const rbc_index *idx, int64_t nq, int k) {
+    return idx->kind == 0 && idx->x4 != nullptr && simt_supported(idx->d, k) && idx->n_local < (int64_t(1) << 31) &&
+           nq < (int64_t(1) << 31) && nq * idx->nr >= simt_min_pairs();
+}
+
+// Exact-search stage 2 (search.py:183-186) on the SIMT filter: every query's surviving segments
+// (list p, cutoff) regrouped by list -- one item per (list, chunk of its segments) scanning the
+// list's rows up to the chunk's largest cutoff, each position stopping at its own -- then the
+// per-segment k-key rows merged per query.
+int simt_exact_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const int64_t *seg_off,
+                      const int32_t *nseg, const int32_t *seg_list, const int32_t *seg_len, const float *gamma,
+                      int64_t total, uint64_t *keys, cudaStream_t st) {
+    if (nq == 0) return RBC_OK;
+    if (total >= (int64_t(1) << 31)) return fail(RBC_EINVAL, "simt stage 2: too many segments");
+    const int64_t nr = idx->nr;
+    const int64_t T = total > 0 ? total : 1;
+    DevBuf<int32_t> seg_q, val, sval, cnt, start, nchunk, istart, nitems, qorder, qcut;
+    DevBuf<float> qthr;
+    DevBuf<uint32_t> key, skey;
+    DevBuf<int64_t> qout;
+    DevBuf<ScanItem> items;
+    DevBuf<uint64_t> seg_keys;
+    RBC_CHECK(seg_q.alloc(T, st));
+    RBC_CHECK(key.alloc(T, st));
+    RBC_CHECK(skey.alloc(T, st));
+    RBC_CHECK(val.alloc(T, st));
+    RBC_CHECK(sval.alloc(T, st));
+    RBC_CHECK(cnt.alloc(nr, st));
+    RBC_CHECK(start.alloc(nr, st));
+    RBC_CHECK(nchunk.alloc(nr, st));
+    RBC_CHECK(istart.alloc(nr, st));
+    RBC_CHECK(nitems.alloc(1, st));
+    RBC_CHECK(qorder.alloc(T, st));
+    RBC_CHECK(qcut.alloc(T, st));
+    RBC_CHECK(qout.alloc(T, st));
+    RBC_CHECK(qthr.alloc(T, st));
+    RBC_CHECK(seg_keys.alloc(T * k, st));
+    seg_query_kernel<<<grid_for(nq, 256), 256, 0, st>>>(seg_off, nseg, nq, seg_list, seg_q.get(), key.get(), val.get());
+    RBC_LAUNCHED();
+    int kb = 1;
+    while ((int64_t(1) << kb) < nr) ++kb;
+    size_t tb = 0, tb2 = 0, tb3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key.get(), skey.get(), val.get(), sval.get(), total, 0, kb, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt.get(), start.get(), nr, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb3, nchunk.get(), istart.get(), nr, st);
+    DevBuf<unsigned char> tmp;
+    RBC_CHECK(tmp.alloc(std::max(tb, std::max(tb2, tb3)), st));
+    if (total > 0) {
+        RBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, key.get(), skey.get(), val.get(), sval.get(), total, 0,
+                                                 kb, st));
+        note_launch();
+    }
+    const int qpt = simt_qpt(idx->d, k);
+    const int qb = 32 * qpt;
+    RBC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * nr, st));
+    seg_hist_kernel<<<grid_for(T, 256), 256, 0, st>>>(skey.get(), total, cnt.get());
+    RBC_LAUNCHED();
+    near_chunks_kernel<<<grid_for(nr, 256), 256, 0, st>>>(cnt.get(), nr, qb, nchunk.get());
+    RBC_LAUNCHED();
+    RBC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb2, cnt.get(), start.get(), nr, st));
+    RBC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb3, nchunk.get(), istart.get(), nr, st));
+    note_launch(2);
+    const int64_t max_items = std::min<int64_t>(nr, T) + T / qb + 1;
+    RBC_CHECK(items.alloc(max_items, st));
+    seg_items_kernel<<<grid_for(nr, 256), 256, 0, st>>>(cnt.get(), start.get(), istart.get(), nr, idx->offsets,
+                                                       sval.get(), seg_len, qb, items.get(), nitems.get());
+    RBC_LAUNCHED();
+    seg_positions_kernel<<<grid_for(T, 256), 256, 0, st>>>(sval.get(), total, seg_q.get(), seg_len, gamma, idx->d,
+                                                          idx->metric, qorder.get(), qcut.get(), qout.get(), qthr.get());
+    RBC_LAUNCHED();
+    SimtParams P{};
+    P.q = q;
+    P.nq = T;
+    P.d = idx->d;
+    P.qorder = qorder.get();
+    P.items = items.get();
+    P.nitems = nitems.get();
+    P.p = idx->x4;
+    P.pid = idx->perm;
+    P.qcut = qcut.get();
+    P.qout = qout.get();
+    P.qthr = qthr.get();
+    P.k = k;
+    P.qpt = qpt;
+    P.out = seg_keys.get();
+    if (total > 0) RBC_CHECK(simt_launch(P, idx->metric, max_items, st));
+    const unsigned mgrid = grid_for(nq * 32, 256);
+    const int kt = simt_kt(k);
+    if (kt == 1) seg_merge_kernel<1><<<mgrid, 256, 0, st>>>(seg_keys.get(), seg_off, nseg, nq, k, keys);
+    else if (kt == 4) seg_merge_kernel<4><<<mgrid, 256, 0, st>>>(seg_keys.get(), seg_off, nseg, nq, k, keys);
+    else if (kt == 16) seg_merge_kernel<16><<<mgrid, 256, 0, st>>>(seg_keys.get(), seg_off, nseg, nq, k, keys);
+    else seg_merge_kernel<32><<<mgrid, 256, 0, st>>>(seg_keys.get(), seg_off, nseg, nq, k, keys);
+    RBC_LAUNCHED();
+    return RBC_OK;
+}
+
 // padded SIMT operands of an index: the representatives (both kinds) and, one-shot, the
-// s-lists' rows gathered per list
+// s-lists' rows gathered per list; exact L1 indexes: the list-ordered rows (stage 2)
 int simt_index_prepare(rbc_index *idx, cudaStream_t st) {
-    if (idx->d > 128) return RBC_OK;
+    if (idx->d > 128 || (idx->kind == 0 && idx->metric != RBC_L1)) return RBC_OK;
     const int d4 = (idx->d + 3) & ~3;
     if (cudaMalloc(&idx->reps4, sizeof(float) * idx->nr * d4) != cudaSuccess)
         return fail(RBC_ENOMEM, "simt operands (representatives)");
     idx->bytes += sizeof(float) * idx->nr * d4;
     RBC_CHECK(simt_pad_rows(idx->reps, nullptr, idx->nr, idx->d, idx->reps4, st));
-    if (idx->kind == 1) {
+    if (idx->kind == 0) {
+        // exact indexes: L1 only (L2 stage 2 runs on the tensor cores)
+        if (idx->metric != RBC_L1 || idx->n_local == 0 || idx->n_local >= (int64_t(1) << 31)) return RBC_OK;
+        if (cudaMalloc(&idx->x4, sizeof(float) * idx->n_local * d4) != cudaSuccess)
+            return fail(RBC_ENOMEM, "simt operands (list-ordered rows)");
+        idx->bytes += sizeof(float) * idx->n_local * d4;
+        RBC_CHECK(simt_pad_rows(idx->xp, nullptr, idx->n_local, idx->d, idx->x4, st));
+    } else {
         const int64_t rows = idx->nr * static_cast<int64_t>(idx->s);
         if (rows >= (int64_t(1) << 31)) return RBC_OK;
         if (cudaMalloc(&idx->x4, sizeof(float) * rows * d4) != cudaSuccess)

@@ -79,6 +79,9 @@ int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const P
         }
     }
     last_overflow_count() = 0;
+    if (!force_exact_engine() && simt_exact_supported(idx, nq, k))
+        return simt_exact_stage2(idx, q, nq, k, po.seg_off.get(), po.nseg.get(), po.seg_list.get(), po.seg_len.get(),
+                                 po.gamma.get(), po.total_segs, keys, st);
     return stage2_exact(idx, q, nq, k, po, keys, st);
 }
 

@@ -72,6 +72,12 @@ bool simt_one_shot_supported(const rbc_index *idx, int64_t nq, int k);
 int simt_dense_topk(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k,
                     const int32_t *pid, uint64_t *keys, cudaStream_t st, const float *x4 = nullptr);
 int simt_index_prepare(rbc_index *idx, cudaStream_t st);
+// exact-search stage 2 on the SIMT filter (L1 exact indexes): the surviving segments (CSR per
+// query: seg_off, nseg; per segment its list and cutoff; `total` segments) -> k keys per query
+bool simt_exact_supported(const rbc_index *idx, int64_t nq, int k);
+int simt_exact_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const int64_t *seg_off,
+                      const int32_t *nseg, const int32_t *seg_list, const int32_t *seg_len, const float *gamma,
+                      int64_t total, uint64_t *keys, cudaStream_t st);
 int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const uint64_t *near, uint64_t *keys,
                        cudaStream_t st);
 

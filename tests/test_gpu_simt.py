@@ -209,3 +209,20 @@ def test_simt_one_shot_large_groups(rbc, oracle, metric, k):
     want = oracle.one_shot_query(x, idx.reps.rep_ids, lists, q, k, metric)
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("d", [3, 21, 64, 100])
+@pytest.mark.parametrize("k", [1, 4, 10, 32])
+def test_simt_exact_l1_search_vs_oracle(rbc, oracle, d, k):
+    # exact L1 search: stage 2 (the surviving segments, search.py:183-186) regrouped by list on the
+    # SIMT filter, per-segment rows merged per query; results and every stats field equal the oracle
+    full = oracle.gen_clusters(20_000 + 1500, d, 70 + d, n_clusters=10, cluster_sigma=0.05)
+    x, q = full[:20_000], full[20_000:]
+    idx = rbc.build_exact(rbc.DataMatrix(x), 150, rbc.MetricSpec("l1", d), seed=6)
+    li, off, ld, radii = oracle.build_exact(x, idx.reps.rep_ids, "l1")
+    c0 = _calls()
+    got = rbc.exact_query_arrays(idx, q, k)
+    assert _calls() > c0, "the SIMT filter did not run"
+    want = oracle.exact_query(x, idx.reps.rep_ids, li, off, ld, radii, q, k, "l1")
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g).astype(np.asarray(w).dtype), w)
