@@ -645,7 +645,8 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
 }
 
 bool simt_exact_supported(const rbc_index *idx, int64_t nq, int k) {
-    return idx->kind == 0 && idx->x4 != nullptr && simt_supported(idx->d, k) && idx->n_local < (int64_t(1) << 31) &&
+    // (a list's rows are encoded in 28 bits in the candidate queues: n_local < 2^28 bounds every list)
+    return idx->kind == 0 && idx->x4 != nullptr && simt_supported(idx->d, k) && idx->n_local < (int64_t(1) << 28) &&
            nq < (int64_t(1) << 31) && nq * idx->nr >= simt_min_pairs();
 }
 
