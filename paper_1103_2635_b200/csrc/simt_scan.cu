@@ -69,12 +69,15 @@ struct SimtParams {
     int64_t nqc;             // dense: query chunks
     int64_t np;              // dense: point rows
     int64_t pchunk;          // dense: rows per split (< 2^31)
-    const int32_t *qcut;     // segment items: rows of the item each position scans (nullptr: all)
-    const int64_t *qout;     // segment items: output row of each position (nullptr: its query)
-    const float *qthr;       // segment items: initial fp32 bound of each position (nullptr: none)
     int k;
     int qpt;                 // queries per lane (host side: selects the instantiation)
     uint64_t *out;           // [split][nq][k]
+};
+// segment items (simt_seg_kernel only; a separate parameter block keeps simt_tile_kernel's as it was)
+struct SimtSegParams : SimtParams {
+    const int32_t *qcut;     // rows of the item each position scans (nullptr: not segment items)
+    const int64_t *qout;     // output row of each position
+    const float *qthr;       // initial fp32 bound of each position
 };
 
 // packed fp32 pairs (FADD2 / FFMA2 on sm_100)
@@ -162,12 +165,10 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
     uint32_t *qs_r = reinterpret_cast<uint32_t *>(qs_s + kQLen * kT);  // [kQLen][kT] (u << 28) | row
     const float *qg[QPT];
     float2 qv[QPT][DMAX / 2];
-    int lim[QPT];  // rows this position scans (segment items: its list's cutoff)
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
         const int pos = 32 * u + lane < qcnt ? 32 * u + lane : 0;  // a missing query repeats the first
         const int64_t qi = P.qorder ? P.qorder[qbeg + pos] : qbeg + pos;
-        lim[u] = P.qcut ? P.qcut[qbeg + pos] : pcnt;
         qg[u] = P.q + qi * d;
 #pragma unroll
         for (int c = 0; c < DMAX / 2; ++c)
@@ -179,8 +180,7 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
     uint64_t ek[QPT][KT];
 #pragma unroll
     for (int u = 0; u < QPT; ++u) {
-        const int pos = 32 * u + lane < qcnt ? 32 * u + lane : 0;
-        T[u] = P.qthr ? P.qthr[qbeg + pos] : __int_as_float(0x7f800000);
+        T[u] = __int_as_float(0x7f800000);
 #pragma unroll
         for (int j = 0; j < KT; ++j) {
             sv[u][j] = __int_as_float(0x7f800000);
@@ -268,9 +268,8 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
 #pragma unroll
                 for (int u = 0; u < QPT; ++u) {
                     const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
-                    const bool in = t0 + j + rr * kW < lim[u];  // segment items: inside its cutoff
-                    if (in && S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
-                    if (in && S <= T[u]) {
+                    if (S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
+                    if (S <= T[u]) {
                         qs_s[qn * kT + tid] = S;
                         qs_r[qn * kT + tid] = (static_cast<uint32_t>(u) << 28) | static_cast<uint32_t>(t0 + j + rr * kW);
                         ++qn;
@@ -312,7 +311,202 @@ __global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_tile_kernel
                 if (key >= best[KT - 1]) break;  // each warp's list ascends
                 sorted_insert<KT>(best, key);
             }
-        const int64_t qi = P.qout ? P.qout[qbeg + qp] : (P.qorder ? P.qorder[qbeg + qp] : qbeg + qp);
+        const int64_t qi = P.qorder ? P.qorder[qbeg + qp] : qbeg + qp;
+        uint64_t *outq = P.out + (slot * P.nq + qi) * k;
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+            if (j < k) outq[j] = best[j];
+    }
+}
+
+// The same scan over segment items (exact-search stage 2, simt_exact_stage2): per-position
+// cutoffs, output rows and gamma-seeded bounds.  A separate kernel: folding these into
+// simt_tile_kernel changed its code generation and cost the dense and one-shot scans ~10%.
+template <int METRIC, int DMAX, int KT, int QPT>
+__global__ void __launch_bounds__(kT, DMAX * QPT <= 64 ? 2 : 1) simt_seg_kernel(const SimtSegParams P) {
+    constexpr bool SEG = true;
+    extern __shared__ __align__(16) float smem[];
+    int64_t qbeg, pbeg;
+    int qcnt, pcnt;
+    int64_t slot = 0;
+    if (P.items) {
+        if (static_cast<int>(blockIdx.x) >= *P.nitems) return;
+        const ScanItem it = P.items[blockIdx.x];
+        qbeg = it.qbeg;
+        qcnt = it.qcnt;
+        pbeg = it.pbeg;
+        pcnt = it.pcnt;
+    } else {
+        const int64_t chunk = blockIdx.x % P.nqc;
+        slot = blockIdx.x / P.nqc;
+        qbeg = chunk * 32 * QPT;
+        qcnt = static_cast<int>(min(static_cast<int64_t>(32 * QPT), P.nq - qbeg));
+        pbeg = slot * P.pchunk;
+        pcnt = static_cast<int>(min(P.pchunk, P.np - pbeg));
+    }
+    const int d = P.d, d4 = P.d4, tp = P.tp, k = P.k;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float *tiles = smem;                                            // [2][tp][d4]
+    float *tsh = smem + 2 * tp * d4;                                // [kW][32 QPT] published bounds
+    float *qs_s = tsh + kW * 32 * QPT;                              // [kQLen][kT] queued sums
+    uint32_t *qs_r = reinterpret_cast<uint32_t *>(qs_s + kQLen * kT);  // [kQLen][kT] (u << 28) | row
+    const float *qg[QPT];
+    float2 qv[QPT][DMAX / 2];
+    int lim[SEG ? QPT : 1];  // segment items: rows each position scans (its list's cutoff)
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) {
+        const int pos = 32 * u + lane < qcnt ? 32 * u + lane : 0;  // a missing query repeats the first
+        const int64_t qi = P.qorder ? P.qorder[qbeg + pos] : qbeg + pos;
+        if constexpr (SEG) lim[u] = P.qcut[qbeg + pos];
+        qg[u] = P.q + qi * d;
+#pragma unroll
+        for (int c = 0; c < DMAX / 2; ++c)
+            qv[u][c] = make_float2(2 * c < d ? __ldg(qg[u] + 2 * c) : 0.f, 2 * c + 1 < d ? __ldg(qg[u] + 2 * c + 1) : 0.f);
+    }
+    const float fac = 1.0f + static_cast<float>(4 * d + 16) * (1.0f / 16777216.0f);
+    const float absl = static_cast<float>(d) * 1e-35f;
+    float sv[QPT][KT], T[QPT];
+    uint64_t ek[QPT][KT];
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) {
+        T[u] = __int_as_float(0x7f800000);
+        if constexpr (SEG) T[u] = P.qthr[qbeg + (32 * u + lane < qcnt ? 32 * u + lane : 0)];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            sv[u][j] = __int_as_float(0x7f800000);
+            ek[u][j] = kEmptyKey;
+        }
+    }
+    int qn = 0;
+    // exact fp64 evaluation of the queued points that still qualify
+    auto drain = [&]() {
+        for (int e = 0; e < qn; ++e) {
+            const float sq = qs_s[e * kT + tid];
+            const uint32_t rw = qs_r[e * kT + tid];
+            const int u = static_cast<int>(rw >> 28);
+            float Tu = T[0];
+            const float *qq = qg[0];
+#pragma unroll
+            for (int v = 1; v < QPT; ++v)
+                if (u == v) {
+                    Tu = T[v];
+                    qq = qg[v];
+                }
+            if (sq <= Tu) {
+                const int64_t row = pbeg + static_cast<int64_t>(rw & 0x0FFFFFFFu);
+                const uint32_t id = P.pid ? static_cast<uint32_t>(P.pid[row]) : static_cast<uint32_t>(row);
+                const uint64_t key = pack_key(exact_dist<METRIC>(qq, P.p + row * d4, d), id);
+#pragma unroll
+                for (int v = 0; v < QPT; ++v)
+                    if (u == v && key < ek[v][KT - 1]) sorted_insert<KT>(ek[v], key);
+            }
+        }
+        qn = 0;
+    };
+    // tile copies: the tile's rows are contiguous and 16-byte aligned (padded stride d4)
+    auto tile_rows = [&](int t0) { return min(t0 == 0 ? 2 * kW : tp, pcnt - t0); };
+    auto issue = [&](int t0, int buf) {
+        const int tn = tile_rows(t0);
+        const float4 *src = reinterpret_cast<const float4 *>(P.p + (pbeg + t0) * d4);
+        float4 *dst = reinterpret_cast<float4 *>(tiles + buf * tp * d4);
+        for (int e = tid; e < tn * (d4 >> 2); e += kT) cp_async16(dst + e, src + e);
+        cp_async_commit();
+    };
+
+    // tiles: a short first one (two rows per warp: after its bound exchange every query
+    // starts from the best of 16 rows, so the later tiles rarely queue a candidate), then
+    // tp rows each
+    int t = 0;
+    if (pcnt > 0) issue(0, 0);
+    for (int t0 = 0; t0 < pcnt; t0 += tile_rows(t0), ++t) {
+        const int buf = t & 1, tn = tile_rows(t0);
+        if (t0 + tn < pcnt) {
+            issue(t0 + tn, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *tile = tiles + buf * tp * d4;
+        // kRows tile rows per step (a warp's rows j, j + kW, ...): every row's loads are issued
+        // before any arithmetic (independent registers, predicated instead of branched), so the
+        // shared-memory latency overlaps across rows and chunks
+        constexpr int kRowsStep = DMAX * (QPT + 2) <= 128 ? 2 : 1;
+        for (int j = warp; j < tn; j += kRowsStep * kW) {
+            float4 xs[kRowsStep][DMAX / 4];
+#pragma unroll
+            for (int rr = 0; rr < kRowsStep; ++rr) {
+                const int jr = j + rr * kW < tn ? j + rr * kW : j;
+                const float4 *xr = reinterpret_cast<const float4 *>(tile + jr * d4);
+#pragma unroll
+                for (int c = 0; c < DMAX / 4; ++c) xs[rr][c] = 4 * c < d ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int rr = 0; rr < kRowsStep; ++rr) {
+                if (j + rr * kW >= tn) break;  // warp-uniform
+                float2 acc[QPT][2];
+#pragma unroll
+                for (int u = 0; u < QPT; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < DMAX / 4; ++c) {
+#pragma unroll
+                    for (int u = 0; u < QPT; ++u) {
+                        acc2<METRIC>(qv[u][2 * c], make_float2(xs[rr][c].x, xs[rr][c].y), acc[u][0]);
+                        acc2<METRIC>(qv[u][2 * c + 1], make_float2(xs[rr][c].z, xs[rr][c].w), acc[u][1]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < QPT; ++u) {
+                    const float S = (acc[u][0].x + acc[u][1].x) + (acc[u][0].y + acc[u][1].y);
+                    if constexpr (SEG) {  // past its cutoff: the row is not a candidate of this position
+                        if (t0 + j + rr * kW >= lim[u]) continue;
+                    }
+                    if (S < sv[u][KT - 1]) T[u] = fminf(T[u], topk_push<KT>(sv[u], S, k, fac, absl));
+                    if (S <= T[u]) {
+                        qs_s[qn * kT + tid] = S;
+                        qs_r[qn * kT + tid] = (static_cast<uint32_t>(u) << 28) | static_cast<uint32_t>(t0 + j + rr * kW);
+                        ++qn;
+                    }
+                }
+                if (__any_sync(0xffffffffu, qn > kQLen - QPT)) drain();
+            }
+        }
+        // bound exchange: every warp adopts the smallest published bound of each query
+#pragma unroll
+        for (int u = 0; u < QPT; ++u) tsh[warp * 32 * QPT + 32 * u + lane] = T[u];
+        __syncthreads();  // (also: the buffer is refilled by the next issue)
+#pragma unroll
+        for (int u = 0; u < QPT; ++u) {
+            float m = T[u];
+#pragma unroll
+            for (int w = 0; w < kW; ++w) m = fminf(m, tsh[w * 32 * QPT + 32 * u + lane]);
+            T[u] = m;
+        }
+        drain();
+    }
+    // merge the warps' exact lists: mk[w][pos][k] (the tiles are done)
+    __syncthreads();
+    uint64_t *mk = reinterpret_cast<uint64_t *>(smem);
+#pragma unroll
+    for (int u = 0; u < QPT; ++u)
+        if (32 * u + lane < qcnt)
+#pragma unroll
+            for (int j = 0; j < KT; ++j)
+                if (j < k) mk[(static_cast<int64_t>(warp) * qcnt + 32 * u + lane) * k + j] = ek[u][j];
+    __syncthreads();
+    for (int qp = tid; qp < qcnt; qp += kT) {
+        uint64_t best[KT];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) best[j] = kEmptyKey;
+        for (int w = 0; w < kW; ++w)
+            for (int j = 0; j < k; ++j) {
+                const uint64_t key = mk[(static_cast<int64_t>(w) * qcnt + qp) * k + j];
+                if (key >= best[KT - 1]) break;  // each warp's list ascends
+                sorted_insert<KT>(best, key);
+            }
+        int64_t qi;
+        if constexpr (SEG) qi = P.qout[qbeg + qp];
+        else qi = P.qorder ? P.qorder[qbeg + qp] : qbeg + qp;
         uint64_t *outq = P.out + (slot * P.nq + qi) * k;
 #pragma unroll
         for (int j = 0; j < KT; ++j)
@@ -470,18 +664,29 @@ size_t simt_smem(int d4, int k, int qpt) {
 }
 
 template <int METRIC, int DMAX, int KT, int QPT>
-int launch_kt(const SimtParams &P, unsigned grid, cudaStream_t st) {
+int launch_kt(const SimtSegParams &P, unsigned grid, cudaStream_t st) {
     const size_t smem = simt_smem(P.d4, P.k, QPT);
+    if (P.qcut) {  // segment items: exact L1 stage 2 only (L2 stage 2 runs on the tensor cores)
+        if constexpr (METRIC == RBC_L1 && QPT == 1) {
+            auto *fn = simt_seg_kernel<METRIC, DMAX, KT, QPT>;
+            if (smem > 48 * 1024)
+                RBC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            fn<<<grid, kT, smem, st>>>(P);
+            RBC_LAUNCHED();
+            return RBC_OK;
+        }
+        return fail(RBC_EINVAL, "simt segment scan: L1, one query per lane");
+    }
     auto *fn = simt_tile_kernel<METRIC, DMAX, KT, QPT>;
     if (smem > 48 * 1024)
         RBC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    fn<<<grid, kT, smem, st>>>(P);
+    fn<<<grid, kT, smem, st>>>(static_cast<const SimtParams &>(P));
     RBC_LAUNCHED();
     return RBC_OK;
 }
 
 template <int METRIC, int DMAX, int QPT>
-int launch_qpt(const SimtParams &P, unsigned grid, cudaStream_t st) {
+int launch_qpt(const SimtSegParams &P, unsigned grid, cudaStream_t st) {
     switch (simt_kt(P.k)) {
         case 1: return launch_kt<METRIC, DMAX, 1, QPT>(P, grid, st);
         case 4: return launch_kt<METRIC, DMAX, 4, QPT>(P, grid, st);
@@ -490,7 +695,7 @@ int launch_qpt(const SimtParams &P, unsigned grid, cudaStream_t st) {
 }
 
 template <int METRIC, int DMAX>
-int launch_dmax(const SimtParams &P, unsigned grid, cudaStream_t st) {
+int launch_dmax(const SimtSegParams &P, unsigned grid, cudaStream_t st) {
     if (P.k > 16) return launch_kt<METRIC, DMAX, 32, 1>(P, grid, st);
     if constexpr (DMAX <= 64) {
         if (P.qpt == 2) {  // k <= 4
@@ -502,7 +707,7 @@ int launch_dmax(const SimtParams &P, unsigned grid, cudaStream_t st) {
 }
 
 template <int METRIC>
-int launch_metric(const SimtParams &P, unsigned grid, cudaStream_t st) {
+int launch_metric(const SimtSegParams &P, unsigned grid, cudaStream_t st) {
     switch (simt_dmax(P.d)) {
         case 24: return launch_dmax<METRIC, 24>(P, grid, st);
         case 64: return launch_dmax<METRIC, 64>(P, grid, st);
@@ -512,7 +717,7 @@ int launch_metric(const SimtParams &P, unsigned grid, cudaStream_t st) {
 
 std::atomic<int64_t> g_simt_calls{0};
 
-int simt_launch(SimtParams P, int metric, int64_t grid, cudaStream_t st) {
+int simt_launch(SimtSegParams P, int metric, int64_t grid, cudaStream_t st) {
     g_simt_calls.fetch_add(1);
     if (grid > 0x7FFFFFFF) return fail(RBC_EINVAL, "simt scan: too many queries for one call");
     P.d4 = (P.d + 3) & ~3;
@@ -572,7 +777,7 @@ int simt_dense_topk(const float *q, int64_t nq, const float *x, int64_t n, int d
     splits = (n + pchunk - 1) / pchunk;
     DevBuf<uint64_t> part;
     if (splits > 1) RBC_CHECK(part.alloc(splits * nq * k, st));
-    SimtParams P{};
+    SimtSegParams P{};
     P.q = q;
     P.nq = nq;
     P.d = d;
@@ -629,7 +834,7 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
     near_items_kernel<<<grid_for(nr, 256), 256, 0, st>>>(cnt.get(), start.get(), istart.get(), nr, idx->s, qb,
                                                         items.get(), nitems.get());
     RBC_LAUNCHED();
-    SimtParams P{};
+    SimtSegParams P{};
     P.q = q;
     P.nq = nq;
     P.d = idx->d;
@@ -646,7 +851,7 @@ int simt_one_shot_scan(const rbc_index *idx, const float *q, int64_t nq, int k, 
 
 bool simt_exact_supported(const rbc_index *idx, int64_t nq, int k) {
     // (a list's rows are encoded in 28 bits in the candidate queues: n_local < 2^28 bounds every list)
-    return idx->kind == 0 && idx->x4 != nullptr && simt_supported(idx->d, k) && idx->n_local < (int64_t(1) << 28) &&
+    return idx->kind == 0 && idx->metric == RBC_L1 && idx->x4 != nullptr && simt_supported(idx->d, k) && idx->n_local < (int64_t(1) << 28) &&
            nq < (int64_t(1) << 31) && nq * idx->nr >= simt_min_pairs();
 }
 
@@ -697,7 +902,7 @@ int simt_exact_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, c
                                                  kb, st));
         note_launch();
     }
-    const int qpt = simt_qpt(idx->d, k);
+    const int qpt = 1;  // (simt_seg_kernel: one segment per lane)
     const int qb = 32 * qpt;
     RBC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * nr, st));
     seg_hist_kernel<<<grid_for(T, 256), 256, 0, st>>>(skey.get(), total, cnt.get());
@@ -715,7 +920,7 @@ int simt_exact_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, c
     seg_positions_kernel<<<grid_for(T, 256), 256, 0, st>>>(sval.get(), total, seg_q.get(), seg_len, gamma, idx->d,
                                                           idx->metric, qorder.get(), qcut.get(), qout.get(), qthr.get());
     RBC_LAUNCHED();
-    SimtParams P{};
+    SimtSegParams P{};
     P.q = q;
     P.nq = T;
     P.d = idx->d;
