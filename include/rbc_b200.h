@@ -95,6 +95,11 @@ int64_t rbc_simt_scan_calls(void);
  * (diagnostic). */
 int64_t rbc_select_calls(void);
 int64_t rbc_select_fallbacks(void);
+/* Query batches of the exact search whose stage 1 + pruning ran the filtered engine
+ * (filter_stage1.cu: d > 64 or L1), and the batches it handed back to the exact
+ * |Q| x |R| path (diagnostic). */
+int64_t rbc_filter_stage1_calls(void);
+int64_t rbc_filter_stage1_fallbacks(void);
 
 /* metric.py:57-76 pairwise_distances (and brute_force.py:220-251
  * distance_rows): out[m,p] = dist(a[i], b[j]), bit-exact. */

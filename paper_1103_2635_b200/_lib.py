@@ -98,6 +98,8 @@ EXPORTS = {
     "rbc_simt_scan_calls": ([], _i64),
     "rbc_select_calls": ([], _i64),
     "rbc_select_fallbacks": ([], _i64),
+    "rbc_filter_stage1_calls": ([], _i64),
+    "rbc_filter_stage1_fallbacks": ([], _i64),
     "rbc_index_exact_create_local": ([_p, _p, _i64, _p, _i64, _i32, _i32, _p, _p, _p, _p, _i64, ctypes.POINTER(_p), _p],
                                      ctypes.c_int),
     "rbc_local_list_radii": ([_p, _p, _i64, _i64, _p, _p], ctypes.c_int),

@@ -437,7 +437,7 @@ int rbc_bf_search(const float *q, int64_t nq, const float *x, int64_t n, int32_t
         // large scan: partition the points once, then the tcgen05 scan over every list
         rbc_index *bf = nullptr;
         RBC_CHECK(bf_prepare(x, n, d, metric, &bf, st));
-        const int rc = bf->tc ? tc_bf_index_search(bf, q, nq, k, keys.get(), st)
+        const int rc = bf->tc && tc_range_ok(q, nq * d, st) ? tc_bf_index_search(bf, q, nq, k, keys.get(), st)
                               : bf_search_keys(q, nq, x, n, d, metric, k, keys.get(), st);
         cudaStreamSynchronize(st);
         rbc_index_destroy(bf);
@@ -460,7 +460,7 @@ int rbc_bf_search_prepared(const rbc_index *bf, const float *q, int64_t nq, int3
     cudaStream_t st = as_stream(stream);
     DevBuf<uint64_t> keys;
     RBC_CHECK(keys.alloc(nq * k, st));
-    if (bf->tc && k <= 32 && !force_exact_engine())
+    if (bf->tc && k <= 32 && !force_exact_engine() && tc_range_ok(q, nq * bf->d, st))
         RBC_CHECK(tc_bf_index_search(bf, q, nq, k, keys.get(), st));
     else
         RBC_CHECK(bf_search_keys(q, nq, bf->x, bf->n, bf->d, bf->metric, k, keys.get(), st));

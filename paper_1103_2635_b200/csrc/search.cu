@@ -518,6 +518,7 @@ int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, i
     if (chunk < 1) chunk = 1;
     if (chunk > nq) chunk = nq;
     DevBuf<float> d1;
+    DevBuf<int32_t> lenbuf;
     for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
         const int64_t m = nq - q0 < chunk ? nq - q0 : chunk;
         const float *qc = q + q0 * idx->d;
@@ -576,11 +577,23 @@ int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, i
             po->pr = pr;
             po->p3 = p3;
             if (!d1.get()) RBC_CHECK(d1.alloc(chunk * idx->nr, st));
-            {
+            bool filtered = false;
+            if (filter_stage1_supported(idx, k)) {
+                // fp32 SIMT bounds + exact fp64 where a decision needs it (filter_stage1.cu)
+                if (!lenbuf.get()) RBC_CHECK(lenbuf.alloc(chunk * idx->nr, st));
                 ProfScope ps(kPhaseStage1, st);
-                RBC_CHECK(stage1_distances(idx, qc, m, d1.get(), st));
+                RBC_CHECK(filter_stage1(idx, qc, m, k, d1.get(), lenbuf.get(), *po, filtered, st));
+                if (!filtered) {
+                    po.reset(new PruneOut());
+                    po->pr = pr;
+                    po->p3 = p3;
+                }
             }
-            {
+            if (!filtered) {
+                {
+                    ProfScope ps(kPhaseStage1, st);
+                    RBC_CHECK(stage1_distances(idx, qc, m, d1.get(), st));
+                }
                 ProfScope ps(kPhasePrune, st);
                 RBC_CHECK(prune(idx, d1.get(), m, k, *po, st));
             }
@@ -628,7 +641,7 @@ int one_shot_search_keys(const rbc_index *idx, const float *q, int64_t nq, int k
         RBC_LAUNCHED();
     }
     ProfScope ps(kPhaseScan, st);
-    if (!force_exact_engine() && tc_one_shot_supported(idx, nq, k))
+    if (!force_exact_engine() && tc_one_shot_supported(idx, nq, k) && tc_range_ok(q, nq * idx->d, st))
         return tc_one_shot_scan(idx, q, nq, k, nearest.get(), keys, st);
     if (!force_exact_engine() && simt_one_shot_supported(idx, nq, k))
         return simt_one_shot_scan(idx, q, nq, k, nearest.get(), keys, st);

@@ -1,5 +1,7 @@
 // tc_scan.cu -- dispatch of the hot scans between the tensor-core engine and
 // the exact SIMT kernels.
+#include <cstring>
+
 #include "common.cuh"
 #include "index.cuh"
 #include "kernels.cuh"
@@ -23,9 +25,41 @@ int64_t tc_min_pairs() { return g_engine == 2 ? 0 : g_engine == 3 ? INT64_MAX : 
 // sequence cost ~20 us)
 int64_t simt_min_pairs() { return g_engine >= 2 ? 0 : (int64_t(1) << 22); }
 
+static unsigned __float_as_uint_host(float f) {
+    unsigned u;
+    std::memcpy(&u, &f, sizeof(u));
+    return u;
+}
+
+__global__ void maxabs_kernel(const float *__restrict__ a, int64_t count, unsigned *__restrict__ out) {
+    unsigned m = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        m = max(m, __float_as_uint(a[i]) & 0x7FFFFFFFu);  // |a| bits; nan sorts above inf
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+bool tc_range_ok(const float *a, int64_t count, cudaStream_t st) {
+    if (count <= 0) return true;
+    DevBuf<unsigned> m;
+    if (m.alloc(1, st) != RBC_OK) return false;
+    unsigned h = 0xFFFFFFFFu;
+    if (cudaMemsetAsync(m.get(), 0, sizeof(unsigned), st) != cudaSuccess) return false;
+    maxabs_kernel<<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(a, count, m.get());
+    note_launch();
+    if (cudaMemcpyAsync(&h, m.get(), sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return false;
+    return h <= __float_as_uint_host(kTcMaxAbs);
+}
+
 int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, uint64_t *keys,
                  cudaStream_t st, const float *x4) {
-    if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, 1)) return tc_bf_keys(q, nq, x, n, d, 1, keys, st);
+    if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, 1) && tc_range_ok(q, nq * d, st) &&
+        tc_range_ok(x, n * d, st))
+        return tc_bf_keys(q, nq, x, n, d, 1, keys, st);
     if (!force_exact_engine() && simt_supported(d, 1) && nq * n >= simt_min_pairs())
         return simt_dense_topk(q, nq, x, n, d, metric, 1, nullptr, keys, st, x4);
     AllSrc src{x, n, d};
@@ -34,7 +68,9 @@ int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, i
 
 int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
                    cudaStream_t st) {
-    if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, k)) return tc_bf_keys(q, nq, x, n, d, k, keys, st);
+    if (!force_exact_engine() && tc_bf_supported(nq, n, d, metric, k) && tc_range_ok(q, nq * d, st) &&
+        tc_range_ok(x, n * d, st))
+        return tc_bf_keys(q, nq, x, n, d, k, keys, st);
     if (!force_exact_engine() && simt_supported(d, k) && nq * n >= simt_min_pairs())
         return simt_dense_topk(q, nq, x, n, d, metric, k, nullptr, keys, st);
     if (!force_exact_engine() && select_large_supported(nq, n, d, k))
@@ -64,7 +100,7 @@ void stage2_note_work(const rbc_index *idx, int64_t nq, int64_t needed) {
 
 int stage2_scan(const rbc_index *idx, const float *q, int64_t nq, int k, const PruneOut &po, uint64_t *keys,
                 cudaStream_t st) {
-    if (!force_exact_engine() && tc_stage2_supported(idx, k)) {
+    if (!force_exact_engine() && tc_stage2_supported(idx, k) && tc_range_ok(q, nq * idx->d, st)) {
         DevBuf<int64_t> status;
         RBC_CHECK(status.alloc(2, st));
         for (int attempt = 0; attempt < 2; ++attempt) {

@@ -20,8 +20,24 @@ int nearest_rows(const float *q, int64_t nq, const float *x, int64_t n, int d, i
 int bf_search_keys(const float *q, int64_t nq, const float *x, int64_t n, int d, int metric, int k, uint64_t *keys,
                    cudaStream_t st);
 
+// Range guard of the tensor-core engines: their fp32 bounds (squared norms, the error terms)
+// stay finite only while every coordinate is at most kTcMaxAbs in magnitude (d <= 128:
+// 512 kTcMaxAbs^2 << FLT_MAX).  Index operands are checked when they are prepared, queries per
+// call (synchronising: one max-reduce); out-of-range data takes the SIMT / exact engines,
+// which accumulate in fp64 or treat an overflowed fp32 bound as undecided.
+constexpr float kTcMaxAbs = 1e15f;
+bool tc_range_ok(const float *a, int64_t count, cudaStream_t st);
+
 // stage 1 of the searches: bit-exact dist(q_i, r_p) -> d1[nq, nr]
 int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1, cudaStream_t st);
+
+// filtered stage 1 + pruning (filter_stage1.cu) for indexes without the tensor-core stage 1
+// (d > 64, L1): fp32 SIMT bounds for every (q, r), exact fp64 only where a decision needs it.
+// d1 [nq, nr] and len [nq, nr] are scratch; ok = false (a query with too many gamma
+// candidates): nothing usable was produced and the caller runs stage1_distances + prune.
+bool filter_stage1_supported(const rbc_index *idx, int k);
+int filter_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, float *d1, int32_t *len, PruneOut &out,
+                  bool &ok, cudaStream_t st);
 
 // stage 2 of the exact search over the pruned segments (synchronising wrapper
 // around tc_stage2 / stage2_exact)

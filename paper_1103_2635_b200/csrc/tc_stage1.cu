@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
         const float4 *pb = reinterpret_cast<const float4 *>(reps64 + static_cast<int64_t>(pilots[jB]) * 64) + 4 * t4;
         const float4 *xa = reinterpret_cast<const float4 *>(qa) + 4 * t4;
         const float4 *xb = reinterpret_cast<const float4 *>(qb) + 4 * t4;
-        float sa = 0.f, sb = 0.f;
+        float sa = 0.f, sb = 0.f, mx = 0.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const float4 u = __ldg(xa + c), v = __ldg(pa + c), w = __ldg(xb + c), z = __ldg(pb + c);
@@ -411,7 +411,15 @@ __global__ void __launch_bounds__(kPilotWarps * 32) pilot_key_kernel(const float
             const float b0 = w.x - z.x, b1 = w.y - z.y, b2 = w.z - z.z, b3 = w.w - z.w;
             sa = fmaf(a0, a0, fmaf(a1, a1, fmaf(a2, a2, fmaf(a3, a3, sa))));
             sb = fmaf(b0, b0, fmaf(b1, b1, fmaf(b2, b2, fmaf(b3, b3, sb))));
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(u.x), fabsf(u.y)), fmaxf(fabsf(u.z), fabsf(u.w))));
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w))));
+            if (u.x != u.x || u.y != u.y || u.z != u.z || u.w != u.w || w.x != w.x || w.y != w.y || w.z != w.z ||
+                w.w != w.w)
+                mx = __int_as_float(0x7f800000);
         }
+        // the tensor-core bounds' range (tc_scan.cuh kTcMaxAbs): larger queries -> exact path
+        // (hist[2 kPilots]; pilot_scatter_kernel turns it into stage 1's failure flag)
+        if (!(mx <= kTcMaxAbs)) atomicOr(hist + 2 * kPilots, 1u);
 #pragma unroll
         for (int o = 1; o < 4; o <<= 1) {
             sa += __shfl_xor_sync(0xffffffffu, sa, o);
@@ -451,7 +459,8 @@ __global__ void __launch_bounds__(128) pilot_scatter_kernel(const uint32_t *__re
     // (no memset nodes; every writer of them runs after this kernel)
     if (blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2) *zero64 = 0ull;
-    if (blockIdx.x == 0 && threadIdx.x >= 4 && threadIdx.x < 6) fail2[threadIdx.x - 4] = 0;
+    if (blockIdx.x == 0 && threadIdx.x >= 4 && threadIdx.x < 6)  // [0]: queries beyond the tensor-core range
+        fail2[threadIdx.x - 4] = threadIdx.x == 4 && cursor[kPilots] != 0u ? 1 : 0;
     if (threadIdx.x == 0) {
         unsigned run = 0;
         for (int j = 0; j < npilot; ++j) {
@@ -1264,6 +1273,7 @@ inline size_t s1_smem_bytes(int64_t nr) {
 
 int tc1_index_prepare(rbc_index *idx, cudaStream_t st) {
     if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 64 || idx->nr > kMaxRepsSmem) return RBC_OK;
+    if (!tc_range_ok(idx->reps, idx->nr * idx->d, st)) return RBC_OK;  // (queries: pilot_key_kernel)
     Tc1Index *t = new Tc1Index();
     t->plane1 = idx->d > 62;
     const int64_t nchunks = (idx->nr + kN - 1) / kN;
@@ -1375,8 +1385,8 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     const int npilot = static_cast<int>(idx->nr < kPilots ? idx->nr : kPilots);
     RBC_CHECK(qorder.alloc(nq, st));
     RBC_CHECK(pkey.alloc(nq, st));
-    RBC_CHECK(phist.alloc(2 * kPilots, st));
-    RBC_CUDA(cudaMemsetAsync(phist.get(), 0, 2 * kPilots * sizeof(unsigned), st));
+    RBC_CHECK(phist.alloc(2 * kPilots + 1, st));  // + the query range flag
+    RBC_CUDA(cudaMemsetAsync(phist.get(), 0, (2 * kPilots + 1) * sizeof(unsigned), st));
     RBC_CHECK(pd2.alloc(nq, st));
     pilot_key_kernel<<<grid_for(nq, kPilotWarps * 16), kPilotWarps * 32, 0, st>>>(
         q64, nq, t->prow, t->pnorm, npilot, t->reps64, t->pilots, pkey.get(), phist.get(), pd2.get());

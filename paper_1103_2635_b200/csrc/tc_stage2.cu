@@ -1460,6 +1460,8 @@ static int tc_lists_build(const float *xp, const float *reps, const int64_t *off
 int tc_index_prepare(rbc_index *idx, cudaStream_t st) {
     if (idx->kind != 0 || idx->metric != RBC_L2 || idx->d > 128 || idx->n_local == 0) return RBC_OK;
     if (idx->n_local + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 work offsets
+    if (!tc_range_ok(idx->xp, idx->n_local * idx->d, st) || !tc_range_ok(idx->reps, idx->nr * idx->d, st))
+        return RBC_OK;  // coordinates beyond the fp32 bounds' range: SIMT / exact engines
     std::vector<int64_t> off(idx->nr + 1);
     RBC_CUDA(cudaMemcpyAsync(off.data(), idx->offsets, sizeof(int64_t) * (idx->nr + 1), cudaMemcpyDeviceToHost, st));
     RBC_CUDA(cudaStreamSynchronize(st));
@@ -2223,6 +2225,7 @@ int tc_one_shot_prepare(rbc_index *idx, const float *xp_lists, cudaStream_t st) 
     if (idx->kind != 1 || idx->metric != RBC_L2 || idx->d > 128) return RBC_OK;
     const int64_t total = idx->nr * static_cast<int64_t>(idx->s);
     if (total + kTailRows >= (int64_t(1) << 31)) return RBC_OK;  // int32 positions
+    if (!tc_range_ok(xp_lists, total * idx->d, st) || !tc_range_ok(idx->reps, idx->nr * idx->d, st)) return RBC_OK;
     std::vector<int64_t> off(idx->nr + 1);
     for (int64_t p = 0; p <= idx->nr; ++p) off[p] = p * idx->s;
     one_shot_offsets_kernel<<<grid_for(idx->nr + 1, 256), 256, 0, st>>>(idx->nr, idx->s, idx->offsets);

@@ -1,4 +1,4 @@
-"""Per-kernel device timeline of cfg2 exact searches via torch.profiler (CUPTI), no replay/serialisation:
+"""Per-kernel device timeline of exact searches (cfg2 by default; args: nq k config) via torch.profiler (CUPTI), no replay/serialisation:
 kernel durations, start offsets and the idle gaps between kernels inside one search."""
 import ctypes
 import os
@@ -51,7 +51,7 @@ def main():
     # split into searches at the pilot kernel
     runs, cur = [], []
     for e in ev:
-        if "pilot_key" in e.name and cur:
+        if ("pilot_key" in e.name or "s1_filter" in e.name or "pairwise_kernel" in e.name) and cur:
             runs.append(cur)
             cur = []
         cur.append(e)
