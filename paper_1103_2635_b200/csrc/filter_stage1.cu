@@ -69,7 +69,7 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 template <int METRIC, bool VEC>
 __global__ void __launch_bounds__(256) s1_filter_kernel(const float *__restrict__ q, int64_t m,
                                                         const float *__restrict__ r, int64_t nr, int d,
-                                                        float *__restrict__ S) {
+                                                        float *__restrict__ S, int64_t ld) {
     __shared__ __align__(16) float qs[kFc][kQs];
     __shared__ __align__(16) float rs[kFc][kRs];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) s1_filter_kernel(const float *__restrict_
     for (int u = 0; u < 4; ++u) {
         const int64_t i = i0 + 4 * ty + u;
         if (i >= m) continue;
-        float *row = S + i * nr;
+        float *row = S + i * ld;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int64_t j = j0 + (v < 2 ? 4 * tx + 2 * v : 64 + 4 * tx + 2 * (v - 2));
@@ -187,6 +187,9 @@ __device__ __forceinline__ float sdom(float t, bool &valid) {
     return t2;
 }
 
+// (a variant staging each warp's S~ row in shared memory once, 4 warps per block, measured
+// slower at cfg5: 476 vs 351 us -- the kernel's time is the latency of the exact distances,
+// which then had a third of the warps to hide it)
 template <int METRIC, int KT>
 __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *__restrict__ q, int64_t m,
                                                                const float *__restrict__ reps, int64_t nr, int d,
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
                                                                const int64_t *__restrict__ offsets,
                                                                const float *__restrict__ list_dists,
                                                                float *__restrict__ d1, int32_t *__restrict__ len_out,
-                                                               CountOut out) {
+                                                               int64_t ld, CountOut out) {
     __shared__ int32_t s_cp[kWarps][kCap];
     __shared__ float s_cd[kWarps][kCap];
     __shared__ int32_t s_work[kWarps][kWork];
@@ -202,8 +205,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
     const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarps + w;
     if (i >= m) return;
     const float inf = __int_as_float(0x7f800000);
-    float *srow = d1 + i * nr;
-    int32_t *lrow = len_out + i * nr;
+    float *srow = d1 + i * ld;
+    int32_t *lrow = len_out + i * ld;
+    const float *rd = srow;
     const float *qi = q + i * d;
     const int64_t nw = (nr + 31) >> 5;
     uint32_t *mrow = out.mask + i * nw;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int64_t p = p0 + 32 * u + lane;
-            sv[u] = p < nr ? srow[p] : inf;
+            sv[u] = p < nr ? rd[p] : inf;
         }
         if (++step > 1 && (step & (step - 1)) == 0) {
             float v = best[0];  // bitonic sort of the lane minima, ascending
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int64_t p = p0 + 32 * u + lane;
-            sv[u] = p < nr ? srow[p] : 0.f;
+            sv[u] = p < nr ? rd[p] : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
         return;
     }
     __syncwarp();
-    for (int j = lane; j < nc; j += 32) s_cd[w][j] = exact_dist<METRIC>(qi, reps + static_cast<int64_t>(s_cp[w][j]) * d, d);
+    for (int j = lane; j < nc; j += 32) s_cd[w][j] = exact_dist<METRIC, 8>(qi, reps + static_cast<int64_t>(s_cp[w][j]) * d, d);
     __syncwarp();
     // gamma_k = k-th smallest exact candidate distance; nearest rep = the first (ties: lowest position)
     unsigned removed = 0;  // bit t: entry lane + 32 t taken
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
     auto drain = [&](int cnt) {  // entries 0 .. cnt-1 (cnt <= 32), one per lane
         if (lane < cnt) {
             const int32_t p = s_work[w][lane];
-            const float dist = exact_dist<METRIC>(qi, reps + static_cast<int64_t>(p) * d, d);
+            const float dist = exact_dist<METRIC, 8>(qi, reps + static_cast<int64_t>(p) * d, d);
             const float rad = radii[p];
             pr += pruned_radius(dist, rad, g) ? 1 : 0;
             p3 += pruned_3gamma(dist, g) ? 1 : 0;
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int64_t p = p0 + 32 * u + lane;
-            sv[u] = p < nr ? srow[p] : 0.f;
+            sv[u] = p < nr ? rd[p] : 0.f;
             rv[u] = p < nr ? radii[p] : 0.f;
         }
 #pragma unroll
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) s1_count_kernel(const float *_
 // ---- fill: segment bits -> segments, ascending rep position -------------------------
 __global__ void __launch_bounds__(256) s1_fill_kernel(const uint32_t *__restrict__ mask, const int32_t *__restrict__ len,
                                                       const float *__restrict__ d1, int64_t m, int64_t nr,
-                                                      const int64_t *__restrict__ offsets,
+                                                      int64_t ld, const int64_t *__restrict__ offsets,
                                                       const int64_t *__restrict__ seg_off,
                                                       int64_t *__restrict__ seg_start, int32_t *__restrict__ seg_len,
                                                       int32_t *__restrict__ seg_list, float *__restrict__ seg_d1) {
@@ -444,9 +448,9 @@ __global__ void __launch_bounds__(256) s1_fill_kernel(const uint32_t *__restrict
             bits &= bits - 1;
             const int64_t p = ((t0 + lane) << 5) + b;
             seg_start[at] = offsets[p];
-            seg_len[at] = len[i * nr + p];
+            seg_len[at] = len[i * ld + p];
             seg_list[at] = static_cast<int32_t>(p);
-            seg_d1[at] = d1[i * nr + p];
+            seg_d1[at] = d1[i * ld + p];
             ++at;
         }
         base += __shfl_sync(0xffffffffu, incl, 31);
@@ -461,6 +465,8 @@ struct ToI64 {
 
 }  // namespace
 
+int64_t filter_stage1_stride(int64_t nr) { return (nr + 3) & ~int64_t(3); }
+
 bool filter_stage1_supported(const rbc_index *idx, int k) {
     return !force_exact_engine() && k >= 1 && k <= 16 && idx->nr >= k && idx->nr <= int64_t(65535) * kFr &&
            (idx->metric == RBC_L2 || idx->metric == RBC_L1);
@@ -471,6 +477,7 @@ int filter_stage1(const rbc_index *idx, const float *q, int64_t m, int k, float 
     ok = false;
     g_calls.fetch_add(1);
     const int64_t nr = idx->nr;
+    const int64_t ld = filter_stage1_stride(nr);
     const int d = idx->d;
     RBC_CHECK(out.gamma.alloc(m, st));
     RBC_CHECK(out.nseg.alloc(m, st));
@@ -485,11 +492,11 @@ int filter_stage1(const rbc_index *idx, const float *q, int64_t m, int k, float 
         const dim3 grid(grid_for(m, kFq, 0x7FFFFFFF), grid_for(nr, kFr, 65535));  // nr <= 65535 * kFr (supported)
         const bool vec = (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(idx->reps)) & 15) == 0;
         if (idx->metric == RBC_L2) {
-            if (vec) s1_filter_kernel<RBC_L2, true><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1);
-            else s1_filter_kernel<RBC_L2, false><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1);
+            if (vec) s1_filter_kernel<RBC_L2, true><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1, ld);
+            else s1_filter_kernel<RBC_L2, false><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1, ld);
         } else {
-            if (vec) s1_filter_kernel<RBC_L1, true><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1);
-            else s1_filter_kernel<RBC_L1, false><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1);
+            if (vec) s1_filter_kernel<RBC_L1, true><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1, ld);
+            else s1_filter_kernel<RBC_L1, false><<<grid, 256, 0, st>>>(q, m, idx->reps, nr, d, d1, ld);
         }
         RBC_LAUNCHED();
     }
@@ -504,10 +511,10 @@ int filter_stage1(const rbc_index *idx, const float *q, int64_t m, int k, float 
     RBC_CHECK(mask.alloc(m * ((nr + 31) >> 5), st));
     CountOut co{out.gamma.get(), out.nseg.get(), out.cand.get(), out.pr, out.p3, out.order_key.get(), mask.get(),
                 flag.get()};
-    const unsigned cgrid = grid_for(m, kWarps);
 #define RBC_S1_COUNT(M, KT)                                                                                          \
-    s1_count_kernel<M, KT><<<cgrid, kWarps * 32, 0, st>>>(q, m, idx->reps, nr, d, k, bd, idx->radii, idx->offsets,   \
-                                                          idx->list_dists, d1, len, co)
+    s1_count_kernel<M, KT><<<grid_for(m, kWarps), kWarps * 32, 0, st>>>(q, m, idx->reps, nr, d, k, bd, idx->radii,  \
+                                                                       idx->offsets, idx->list_dists, d1, len, ld,  \
+                                                                       co)
     if (idx->metric == RBC_L2) {
         if (k == 1) RBC_S1_COUNT(RBC_L2, 1);
         else if (k <= 4) RBC_S1_COUNT(RBC_L2, 4);
@@ -541,7 +548,7 @@ int filter_stage1(const rbc_index *idx, const float *q, int64_t m, int k, float 
     RBC_CHECK(out.seg_len.alloc(total, st));
     RBC_CHECK(out.seg_list.alloc(total, st));
     RBC_CHECK(out.seg_d1.alloc(total, st));
-    s1_fill_kernel<<<grid_for(m * 32, 256), 256, 0, st>>>(mask.get(), len, d1, m, nr, idx->offsets, out.seg_off.get(),
+    s1_fill_kernel<<<grid_for(m * 32, 256), 256, 0, st>>>(mask.get(), len, d1, m, nr, ld, idx->offsets, out.seg_off.get(),
                                                           out.seg_start.get(), out.seg_len.get(), out.seg_list.get(),
                                                           out.seg_d1.get());
     RBC_LAUNCHED();

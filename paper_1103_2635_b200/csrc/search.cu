@@ -576,11 +576,11 @@ int exact_search_keys_direct(const rbc_index *idx, const float *q, int64_t nq, i
             po.reset(new PruneOut());
             po->pr = pr;
             po->p3 = p3;
-            if (!d1.get()) RBC_CHECK(d1.alloc(chunk * idx->nr, st));
+            if (!d1.get()) RBC_CHECK(d1.alloc(chunk * filter_stage1_stride(idx->nr), st));
             bool filtered = false;
             if (filter_stage1_supported(idx, k)) {
                 // fp32 SIMT bounds + exact fp64 where a decision needs it (filter_stage1.cu)
-                if (!lenbuf.get()) RBC_CHECK(lenbuf.alloc(chunk * idx->nr, st));
+                if (!lenbuf.get()) RBC_CHECK(lenbuf.alloc(chunk * filter_stage1_stride(idx->nr), st));
                 ProfScope ps(kPhaseStage1, st);
                 RBC_CHECK(filter_stage1(idx, qc, m, k, d1.get(), lenbuf.get(), *po, filtered, st));
                 if (!filtered) {

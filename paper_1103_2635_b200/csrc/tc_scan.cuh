@@ -36,6 +36,7 @@ int stage1_distances(const rbc_index *idx, const float *q, int64_t nq, float *d1
 // d1 [nq, nr] and len [nq, nr] are scratch; ok = false (a query with too many gamma
 // candidates): nothing usable was produced and the caller runs stage1_distances + prune.
 bool filter_stage1_supported(const rbc_index *idx, int k);
+int64_t filter_stage1_stride(int64_t nr);  // row stride of d1 / len (16-byte rows)
 int filter_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, float *d1, int32_t *len, PruneOut &out,
                   bool &ok, cudaStream_t st);
 

@@ -24,5 +24,11 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'sim
    -o $O/ncu_cfg4 -f python scripts/prof_search.py --config cfg4 --iters 1 > $O/ncu_cfg4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage2_tc_kernel -s 3 -c 1 \
    -o $O/ncu_cfg3 -f python scripts/prof_search.py --config cfg3 --iters 2 > $O/ncu_cfg3.log 2>&1
-for r in ncu_cfg2 ncu_cfg4 ncu_cfg3; do python scripts/ncu_hot.py $O/$r.ncu-rep 25 > $O/${r}_summary.txt 2>&1; done
+timeout 800 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_cfg5.csv \
+   python scripts/prof_search.py --config cfg5 --iters 2 > $O/launches_cfg5.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'s1_filter|s1_count|s1_fill|stage2_tc_kernel' \
+   -s 5 -c 4 -o $O/ncu_cfg5 -f python scripts/prof_search.py --config cfg5 --iters 3 > $O/ncu_cfg5.log 2>&1
+timeout 300 python scripts/kernel_timeline.py 10000 10 cfg5 > $O/timeline_cfg5.txt 2>&1
+timeout 300 python scripts/kernel_timeline.py > $O/timeline_cfg2.txt 2>&1
+for r in ncu_cfg2 ncu_cfg4 ncu_cfg3 ncu_cfg5; do python scripts/ncu_hot.py $O/$r.ncu-rep 25 > $O/${r}_summary.txt 2>&1; done
 ls -la $O
