@@ -60,7 +60,16 @@ constexpr int kNmax = 256;       // largest UMMA N per chunk (N = 256 keeps the 
 constexpr int kAcc = 2;          // TMEM accumulator stages (2 x 256 columns)
 constexpr int kParts = 2;        // epilogue warps per TMEM lane quadrant (column halves / K halves)
 constexpr int kEpiWarps = 4 * kParts;
-constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 16 epilogue warps
+// warp group 0: producer (warp 0), MMA issuer (warp 1), two idle warps; warp groups 1-2: the
+// epilogue.  Launched at 168 registers per thread (384 threads, 1 CTA/SM); warp group 0 gives
+// registers back (setmaxnreg.dec to kRegsCtl) and the epilogue takes them (setmaxnreg.inc to
+// kRegsEpi) so two TMEM loads can be in flight per epilogue thread without spills.  Per SMSP:
+// warps {w, w + 4, w + 8} hold kRegsCtl + 2 kRegsEpi <= 512 registers per lane.
+constexpr int kEpiWarp0 = 4;
+constexpr int kThreads = 32 * kEpiWarp0 + 32 * kEpiWarps;
+constexpr int kRegsCtl = 56;
+constexpr int kRegsEpi = 224;
+static_assert(kRegsCtl + 2 * kRegsEpi <= 512, "per-SMSP register file");
 constexpr int kTailRows = kNmax; // zero rows after the last list (bulk copies may overrun)
 constexpr int kP0 = 128;         // plane-0 row bytes: 64 f16, SWIZZLE_128B
 constexpr int kP1 = 32;          // plane-1 row bytes: 16 f16, SWIZZLE_32B (aug columns when d > 62)
@@ -629,6 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
 
     if (warp == 0) {
         // ===== scheduler + producer =====
+        sm100::setmaxnreg_dec<kRegsCtl>();
         if (lane == 0) {
             uint32_t bi = 0, li = 0;
             // list data of work item w into the next ring slot (the epilogue prepares list w + 1's
@@ -690,6 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         }
     } else if (warp == 1) {
         // ===== MMA issuer =====
+        sm100::setmaxnreg_dec<kRegsCtl>();
         if (lane == 0) {
             uint32_t bi = 0, ti = 0, ai = 0, li = 0;
             for (uint32_t it = 0;; ++it) {
@@ -736,14 +747,17 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                 }
             }
         }
+    } else if (warp < kEpiWarp0) {
+        sm100::setmaxnreg_dec<kRegsCtl>();  // idle warps of warp group 0
     } else {
         // ===== epilogue warps (kParts per TMEM lane quadrant): A prep + filter + candidate buffer =====
+        sm100::setmaxnreg_inc<kRegsEpi>();
         // warp (quad, part): rows quad*32 .. +31, columns [part*kCols, +kCols) of every 256-column
         // chunk (two 32-column halves), K range [part*kKd, +kKd) of the A operand.
         const int quad = warp & 3;
-        const int part = (warp - 2) >> 2;
+        const int part = (warp - kEpiWarp0) >> 2;
         const int row = quad * 32 + lane;
-        float *g = gbuf + (warp - 2) * kCols;
+        float *g = gbuf + (warp - kEpiWarp0) * kCols;
         uint32_t ti = 0, ai = 0, li0 = 0;  // li0: ring position of the tile's first list
         for (uint32_t it = 0;; ++it) {
             const uint32_t slot = it & 1;
@@ -1052,17 +1066,16 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                     const int wlim = __reduce_max_sync(0xffffffffu, max(lim, 0));
 #endif
                     const uint32_t tbase = tmem + tb * kN + hb + (static_cast<uint32_t>(quad * 32) << 16);
-                    for (int c0 = 0; c0 < wlim; c0 += 32) {
-                        uint32_t ra[32];
-                        sm100::tmem_ld32_async(tbase + c0, ra);
-                        sm100::tmem_wait_ld(ra);
+                    // one 32-column block of this warp's columns: max tree against the running
+                    // bound, candidate groups buffered on the slow path
+                    auto block = [&](uint32_t (&ra)[32], const int c0) {
 #if defined(RBC_S2_LEVEL) && RBC_S2_LEVEL == 1
                         if (P.cut) {  // diagnostic: TMEM loads only (search only)
                             uint32_t x = 0;
 #pragma unroll
                             for (int j = 0; j < 32; ++j) x ^= ra[j];
                             if (x == 0x12345u) count += 1;
-                            continue;
+                            return;
                         }
 #endif
                         float va[32];
@@ -1090,7 +1103,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
 #if defined(RBC_S2_LEVEL) && RBC_S2_LEVEL == 2
                         if (P.cut) {  // diagnostic: loads + reductions, no candidates (search only)
                             if (ma == 1234.5f) count += 1;
-                            continue;
+                            return;
                         }
 #endif
                         if (ma >= T) {
@@ -1100,7 +1113,44 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                             for (int s = 0; s < 4; ++s)
                                 if (m8[s] >= T) push8(va + 8 * s, m8[s], base + 8 * s, llim, c0 + 32 <= lim);
                         }
+                    };
+#if defined(RBC_S2_X64)
+                    // diagnostic variant: one 64-column TMEM round trip per two blocks
+                    for (int c0 = 0; c0 < wlim; c0 += 64) {
+                        uint32_t r64[64];
+                        sm100::tmem_ld64_wait(tbase + c0, r64);
+                        block(*reinterpret_cast<uint32_t(*)[32]>(r64), c0);
+                        if (c0 + 32 < wlim) block(*reinterpret_cast<uint32_t(*)[32]>(r64 + 32), c0 + 32);
                     }
+#elif defined(RBC_S2_PIPE)
+                    // diagnostic variant: block b + 1's TMEM load in flight while block b is reduced
+                    // (measured slower: cfg2 stage 2 0.51 -> 0.70 ms)
+                    uint32_t ra[32], rb[32];
+                    if (wlim > 0) {
+                        sm100::tmem_ld32_async(tbase, ra);
+                        sm100::tmem_wait_ld(ra);
+                    }
+#pragma unroll 1
+                    for (int c0 = 0; c0 < wlim; c0 += 64) {
+                        const bool n1 = c0 + 32 < wlim, n2 = c0 + 64 < wlim;
+                        if (n1) sm100::tmem_ld32_async(tbase + c0 + 32, rb);
+                        block(ra, c0);
+                        __syncwarp();
+                        if (!n1) break;
+                        sm100::tmem_wait_ld(rb);
+                        if (n2) sm100::tmem_ld32_async(tbase + c0 + 64, ra);
+                        block(rb, c0 + 32);
+                        __syncwarp();
+                        if (n2) sm100::tmem_wait_ld(ra);
+                    }
+#else
+                    for (int c0 = 0; c0 < wlim; c0 += 32) {
+                        uint32_t ra[32];
+                        sm100::tmem_ld32_async(tbase + c0, ra);
+                        sm100::tmem_wait_ld(ra);
+                        block(ra, c0);
+                    }
+#endif
                     sm100::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) sm100::mbar_arrive(&tempty[tb]);
@@ -1132,7 +1182,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
         }
     }
 #ifdef RBC_S2_TIMING
-    if (P.timing && lane == 0 && (warp <= 1 || warp == 2)) {
+    if (P.timing && lane == 0 && (warp <= 1 || warp == kEpiWarp0)) {
         // warp 0: producer, warp 1: MMA, warp 2: one epilogue warp (wait slots 0..5, 6 = role busy-until-exit)
         tw[6] = clock64() - t_start;
         for (int j = 0; j < 12; ++j)
