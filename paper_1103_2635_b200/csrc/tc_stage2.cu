@@ -57,7 +57,6 @@ namespace {
 
 constexpr int kRows = 128;       // queries per tile = UMMA M = TMEM lanes
 constexpr int kNmax = 256;       // largest UMMA N per chunk (N = 256 keeps the single MMA thread compute-bound)
-constexpr int kAcc = 2;          // TMEM accumulator stages (2 x 256 columns)
 constexpr int kParts = 2;        // epilogue warps per TMEM lane quadrant (column halves / K halves)
 constexpr int kEpiWarps = 4 * kParts;
 // warp group 0: producer (warp 0), MMA issuer (warp 1), two idle warps; warp groups 1-2: the
@@ -80,13 +79,20 @@ constexpr int kMaxSlots = kParts * kMaxSplit;  // candidate slots per query (col
 // planes, 128-column chunks and a 3-stage ring so the A/B buffers fit in shared memory).
 template <int NP>
 struct S2Cfg {
-    static constexpr int kN = NP == 1 ? 256 : 128;   // UMMA N per chunk
-    static constexpr int kStages = 3;                // B ring depth (B traffic is not the bound)
+#ifndef RBC_S2_N1
+#define RBC_S2_N1 256
+#endif
+#ifndef RBC_S2_ACC2
+#define RBC_S2_ACC2 4
+#endif
+    static constexpr int kN = NP == 1 ? RBC_S2_N1 : 128;  // UMMA N per chunk
+    static constexpr int kAcc = NP == 1 ? 512 / RBC_S2_N1 : RBC_S2_ACC2;  // TMEM accumulator stages
+    static constexpr int kStages = 3 * 256 / kN / NP;     // B ring depth (B traffic is not the bound)
     static constexpr int kCols = kN / kParts;        // columns of each chunk per epilogue warp
     static constexpr int kKd = 64 * NP / kParts;     // A-operand dims per epilogue warp
     static constexpr int kStageBytes = kN * (NP * kP0 + kP1);
     static constexpr int kABytes = kRows * (NP * kP0 + kP1);
-    static constexpr int kTmemCols = 2 * kN;         // kAcc accumulators
+    static constexpr int kTmemCols = kAcc * kN;      // kAcc accumulators
     // per-list data ring (work item + representative row + its B rounding error), staged by the
     // producer one list ahead so no role waits on a dependent global load at a list switch
     static constexpr int kRepStride = 64 * NP + 4;                        // floats per rep row
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(1024) split_plan_kernel(const int32_t *__restr
 template <int KT, int NP>
 __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P) {
     using Cfg = S2Cfg<NP>;
-    constexpr int kN = Cfg::kN, kStages = Cfg::kStages, kCols = Cfg::kCols, kKd = Cfg::kKd;
+    constexpr int kN = Cfg::kN, kStages = Cfg::kStages, kCols = Cfg::kCols, kKd = Cfg::kKd, kAcc = Cfg::kAcc;
     constexpr int kStageBytes = Cfg::kStageBytes, kABytes = Cfg::kABytes;
     constexpr float kAccErrNP = kAccErr * NP;
     if (static_cast<int64_t>(*P.work_total) > P.cap_work) return;  // work arrays incomplete (see tile_fill_kernel)
@@ -616,9 +622,11 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
             sm100::mbar_init(&full[s], 1);
             sm100::mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kAcc; ++b) {
             sm100::mbar_init(&tfull[b], 1);
             sm100::mbar_init(&tempty[b], kEpiWarps);
+        }
+        for (int b = 0; b < 2; ++b) {
             sm100::mbar_init(&afull[b], kEpiWarps);
             sm100::mbar_init(&aempty[b], 1);
             sm100::mbar_init(&tile_full[b], 1);
