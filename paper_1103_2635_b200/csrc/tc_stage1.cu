@@ -1470,6 +1470,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     if (k == 1) launch(stage1_tc_kernel<1>);
     else if (k <= 4) launch(stage1_tc_kernel<4>);
     else if (k <= 8) launch(stage1_tc_kernel<8>);
+    else if (k <= 10) launch(stage1_tc_kernel<10>);
     else launch(stage1_tc_kernel<16>);
     RBC_LAUNCHED();
 #ifdef RBC_S1_TIMING
@@ -1496,6 +1497,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     if (k == 1) RBC_FIXUP(1);
     else if (k <= 4) RBC_FIXUP(4);
     else if (k <= 8) RBC_FIXUP(8);
+    else if (k <= 10) RBC_FIXUP(10);
     else RBC_FIXUP(16);
 #undef RBC_FIXUP
     RBC_LAUNCHED();

@@ -32,5 +32,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'s1_
    -s 5 -c 4 -o $NR/ncu_cfg5 -f python scripts/prof_search.py --config cfg5 --iters 3 > $O/ncu_cfg5.log 2>&1
 timeout 300 python scripts/kernel_timeline.py 10000 10 cfg5 > $O/timeline_cfg5.txt 2>&1
 timeout 300 python scripts/kernel_timeline.py > $O/timeline_cfg2.txt 2>&1
+timeout 300 python scripts/kernel_timeline.py 100000 10 cfg2 > $O/timeline_cfg2_k10.txt 2>&1
+timeout 300 python scripts/kernel_timeline.py 100000 10 cfg3 > $O/timeline_cfg3.txt 2>&1
 for r in ncu_cfg2 ncu_cfg4 ncu_cfg3 ncu_cfg5; do python scripts/ncu_hot.py $NR/$r.ncu-rep 25 > $O/${r}_summary.txt 2>&1; done
 ls -la $O
