@@ -1004,8 +1004,12 @@ __device__ __forceinline__ uint64_t group_min_u64(uint64_t v) {
     return v;
 }
 
+#ifndef RBC_FIX_MB10
+#define RBC_FIX_MB10 3
+#endif
 template <int KT>
-__global__ void __launch_bounds__(kFixQueries * kFixLanes, KT == 1 ? 5 : (KT <= 8 ? 4 : 2)) stage1_fixup_kernel(
+__global__ void __launch_bounds__(kFixQueries * kFixLanes,
+                                  KT == 1 ? 5 : (KT <= 8 ? 4 : (KT <= 10 ? RBC_FIX_MB10 : 2))) stage1_fixup_kernel(
     const float *__restrict__ q64, const int32_t *__restrict__ qorder, const float *__restrict__ reps64, int64_t nq,
     int k, const float *__restrict__ radii, const int64_t *__restrict__ offsets, const float *__restrict__ list_dists,
     const float *__restrict__ lskip, const float *__restrict__ c1_lb, const int32_t *__restrict__ c1_p, int cap1,

@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1103_2635_b200/librbc_b200.so"
-WANT = ["UTCHMMA", "UTCBAR", "LDTM", "UBLKCP", "SYNCS", "FADD2", "FFMA2", "FMNMX3", "DADD", "LDGSTS", "REDUX"]
+WANT = ["UTCHMMA", "UTCBAR", "LDTM", "UBLKCP", "SYNCS", "FADD2", "FFMA2", "FMNMX3", "DADD", "LDGSTS", "REDUX", "USETMAXREG"]
 
 
 def demangle(n):
@@ -33,7 +33,7 @@ for line in out.splitlines():
                 counts[fn][w] += 1
 print(f"# static SASS counts per kernel, {LIB} (sm_100a); UTCHMMA = tcgen05.mma, LDTM = tcgen05.ld,")
 print("# UBLKCP = cp.async.bulk, FADD2/FFMA2 = packed fp32 (SIMT filter), FMNMX3 = 3-input max,")
-print("# DADD = fp64 add (exact re-rank, reference arithmetic), LDGSTS = cp.async")
+print("# DADD = fp64 add (exact re-rank, reference arithmetic), LDGSTS = cp.async, USETMAXREG = setmaxnreg")
 rows = [(demangle(f), c) for f, c in counts.items() if any(c[w] for w in ("UTCHMMA", "LDTM", "UBLKCP", "FADD2", "FFMA2"))]
 for name, c in sorted(rows):
     print(f"{name:60s} " + " ".join(f"{w}={c[w]}" for w in WANT if c[w]))
