@@ -188,6 +188,11 @@ struct S2Params {
 __device__ __forceinline__ int roundup16(int x) { return (x + 15) & ~15; }
 
 constexpr int kSegBatch = 8;  // per-row segment entries loaded together in the tile kernels
+#ifndef RBC_FILL_WAYS
+#define RBC_FILL_WAYS 4
+#endif
+constexpr int kFillWays = RBC_FILL_WAYS;          // tile_fill_kernel threads per row
+constexpr int kFillThreads = kFillWays * kRows;
 
 // Entries a[s .. s + min(rem, 8)) of a 32-bit array (the rest = fill): 16-byte vector
 // loads where the address is aligned and the quad lies inside the row, so a thread
@@ -330,7 +335,7 @@ __global__ void group_key_kernel(const uint64_t *__restrict__ order_key, int64_t
 
 // union of the tile's surviving lists: work items, per-row cutoffs and stage-1
 // distances, and the tile's total work (for the LPT order)
-__global__ void __launch_bounds__(kRows) tile_fill_kernel(
+__global__ void __launch_bounds__(kFillThreads) tile_fill_kernel(
     const int32_t *__restrict__ order, int64_t nq, int64_t *__restrict__ nwork, int64_t *__restrict__ work_off,
     unsigned long long *__restrict__ work_total, int32_t *__restrict__ tile_ids, const int64_t *__restrict__ seg_off, const int32_t *__restrict__ seg_cnt,
     const int32_t *__restrict__ seg_list, const int32_t *__restrict__ seg_len, const float *__restrict__ seg_d1,
@@ -344,7 +349,9 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     int32_t *maxlen = sm;           // [nr]
     int32_t *maxd1 = sm + nr;       // [nr] float bits (non-negative)
     int32_t *nearcnt = sm + 2 * nr; // [nr]
-    typedef cub::BlockScan<int, kRows> Scan;
+    typedef cub::BlockScan<int, kFillThreads> Scan;
+    // kFillWays threads per row: `way` takes every kFillWays-th batch of the row's segments
+    const int row = threadIdx.x & (kRows - 1), way = threadIdx.x / kRows;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned long long s_work, s_off;
     __shared__ int s_lists;
@@ -354,11 +361,11 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         s_lists = 0;
     }
     __syncthreads();
-    const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
+    const int64_t tq = static_cast<int64_t>(blockIdx.x) * kRows + row;
     // stage 2's per-query group counts and its two counters start at zero (in place of two
     // memset nodes; unconditional: the re-rank reads the counts even when stage 2 bails out)
     if (tq < nq)
-        for (int h = 0; h < nslot; ++h) cand_count[nslot * tq + h] = 0;
+        for (int h = way; h < nslot; h += kFillWays) cand_count[nslot * tq + h] = 0;
     if (blockIdx.x == 0 && threadIdx.x < 2) counters[threadIdx.x] = 0;
     const int32_t qi = tq < nq ? order[tq] : -1;
     const int64_t s0 = qi >= 0 ? seg_off[qi] : 0;
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         // Each row's segments are read kSegBatch at a time (independent loads in flight).
         const int lane = threadIdx.x & 31;
         const int wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
-        for (int it0 = 0; it0 < wmax; it0 += kSegBatch) {
+        for (int it0 = way * kSegBatch; it0 < wmax; it0 += kFillWays * kSegBatch) {
             uint32_t pu[kSegBatch], lb[kSegBatch], db[kSegBatch];
             const int rem = max(cnt - it0, 0);
             load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, rem, pu, 0xFFFFFFFFu);
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         }
         const int32_t nr_near = qi >= 0 ? static_cast<int32_t>(order_key[qi] & 0xFFFFFF) : -1;
         const unsigned grp = __match_any_sync(0xffffffffu, nr_near);
-        if (qi >= 0 && lane == __ffs(grp) - 1) atomicAdd(&nearcnt[nr_near], __popc(grp));
+        if (way == 0 && qi >= 0 && lane == __ffs(grp) - 1) atomicAdd(&nearcnt[nr_near], __popc(grp));
     }
     __syncthreads();
     // one pass over this thread's contiguous range of lists: the tile's total work (LPT
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     __shared__ int s_nf;
     if (threadIdx.x == 0) s_nf = 0;
     __syncthreads();
-    const int64_t per = (nr + kRows - 1) / kRows;
+    const int64_t per = (nr + kFillThreads - 1) / kFillThreads;
     const int64_t pa = threadIdx.x * per, pe = min(nr, pa + per);
     unsigned long long wsum = 0;
     int nl = 0, c = 0;
@@ -447,7 +454,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
     if (wbase + wn > cap_work) return;  // capacity exceeded: the caller re-runs with the exact size
     const int64_t w0 = wbase + ((warm && wn > 0) ? 1 : 0);
     // zero this thread's cutoff column of the tile's work items (its own later writes win)
-    for (int64_t w = wbase; w < wbase + wn; ++w) cut[w * kRows + threadIdx.x] = 0;
+    for (int64_t w = wbase + way; w < wbase + wn; w += kFillWays) cut[w * kRows + row] = 0;
     // positions (nearcnt is reused as list -> work index): F lists by rank, then the others
     const int nf = s_nf;
     for (int64_t p = pa; p < pe; ++p)
@@ -479,13 +486,13 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
         }
     }
     __syncthreads();
-    for (int it0 = 0; it0 < cnt; it0 += kSegBatch) {
+    for (int it0 = way * kSegBatch; it0 < cnt; it0 += kFillWays * kSegBatch) {
         uint32_t pb[kSegBatch], lb[kSegBatch];
         load8_u32(reinterpret_cast<const uint32_t *>(seg_list), s0 + it0, cnt - it0, pb, 0u);
         load8_u32(reinterpret_cast<const uint32_t *>(seg_len), s0 + it0, cnt - it0, lb, 0u);
 #pragma unroll
         for (int j = 0; j < kSegBatch; ++j)
-            if (it0 + j < cnt) cut[(w0 + nearcnt[pb[j]]) * kRows + threadIdx.x] = static_cast<int32_t>(lb[j]);
+            if (it0 + j < cnt) cut[(w0 + nearcnt[pb[j]]) * kRows + row] = static_cast<int32_t>(lb[j]);
     }
     if (w0 > wbase) {
         __syncthreads();
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(kRows) tile_fill_kernel(
             it.csr = -1;  // max-only marker
             work[wbase] = it;
         }
-        cut[wbase * kRows + threadIdx.x] = cut[w0 * kRows + threadIdx.x];
+        if (way == 0) cut[wbase * kRows + row] = cut[w0 * kRows + row];
     }
     // LPT: heavier tiles first
     if (threadIdx.x == 0) {
@@ -1635,7 +1642,7 @@ int tc_stage2(const rbc_index *idx, const float *q, int64_t nq, int k, const Pru
     RBC_CHECK(counters.alloc(2, st));              // (overflow count, tile counter), zeroed by tile_fill_kernel
     RBC_CHECK(work.alloc(total_work, st));
     RBC_CHECK(cut.alloc(total_work * kRows, st));
-    tile_fill_kernel<<<ntiles, kRows, smem3, st>>>(order, nq, nwork.get(), work_off.get(), work_total, tids.get(),
+    tile_fill_kernel<<<ntiles, kFillThreads, smem3, st>>>(order, nq, nwork.get(), work_off.get(), work_total, tids.get(),
                                                    po.seg_off.get(),
                                                    po.nseg.get(), po.seg_list.get(),
                                                    po.seg_len.get(), po.seg_d1.get(), po.order_key.get(), nr, tc->sB,
