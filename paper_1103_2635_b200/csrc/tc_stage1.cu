@@ -803,10 +803,12 @@ __global__ void __launch_bounds__(kThreads, 2) stage1_tc_kernel(const S1Params P
                             }
                         }
                         if (KT > 1 && take) {
-                            float kth = ubk[0];
+                            float kth = ubk[KT - 1];  // KT = 10 serves k = 10 only
+                            if (KT != 10) {
 #pragma unroll
-                            for (int t = 0; t < KT; ++t)
-                                if (t == P.k - 1) kth = ubk[t];
+                                for (int t = 0; t < KT; ++t)
+                                    if (t == P.k - 1) kth = ubk[t];
+                            }
                             U = fminf(U, kth);
                             T = threshold();
                         }
@@ -1474,7 +1476,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     if (k == 1) launch(stage1_tc_kernel<1>);
     else if (k <= 4) launch(stage1_tc_kernel<4>);
     else if (k <= 8) launch(stage1_tc_kernel<8>);
-    else if (k <= 10) launch(stage1_tc_kernel<10>);
+    else if (k == 10) launch(stage1_tc_kernel<10>);  // the k of cfg3/cfg5: no k-th select
     else launch(stage1_tc_kernel<16>);
     RBC_LAUNCHED();
 #ifdef RBC_S1_TIMING
@@ -1501,7 +1503,7 @@ int tc_stage1(const rbc_index *idx, const float *q, int64_t nq, int k, PruneOut 
     if (k == 1) RBC_FIXUP(1);
     else if (k <= 4) RBC_FIXUP(4);
     else if (k <= 8) RBC_FIXUP(8);
-    else if (k <= 10) RBC_FIXUP(10);
+    else if (k == 10) RBC_FIXUP(10);
     else RBC_FIXUP(16);
 #undef RBC_FIXUP
     RBC_LAUNCHED();

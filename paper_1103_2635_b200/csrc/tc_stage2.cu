@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1) stage2_tc_kernel(const S2Params P
                                 x = hi;
                             }
                             float kth = ubk[KT - 1];
-                            if (P.k != KT) {
+                            if (KT != 10 && P.k != KT) {  // (KT = 10 serves k = 10 only)
 #pragma unroll
                                 for (int t = 0; t < KT; ++t)
                                     if (t == P.k - 1) kth = ubk[t];
