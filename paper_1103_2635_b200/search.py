@@ -110,9 +110,12 @@ def exact_query_batch(index: RbcExactIndex, queries, k: int = 1, workers: int | 
         resolve_workers(workers)
     ids, dists, gamma, prr, p3, cand = exact_query_arrays(index, queries, k)
     n_reps = index.reps.size
-    results = [NeighborList(i, ids[i], dists[i]) for i in range(ids.shape[0])]
+    # per-query objects from bulk conversions (tolist, row iteration): the same values as
+    # float(gamma[i]) / int(...) per element, at a fraction of the per-query cost
+    results = [NeighborList(i, r_ids, r_d) for i, (r_ids, r_d) in enumerate(zip(ids, dists))]
     stats = [
-        SearchStats(float(gamma[i]), n_reps, int(prr[i]), int(p3[i]), int(cand[i]), n_reps) for i in range(ids.shape[0])
+        SearchStats(g, n_reps, a, b, c, n_reps)
+        for g, a, b, c in zip(gamma.tolist(), prr.tolist(), p3.tolist(), cand.tolist())
     ]
     return results, stats
 
@@ -149,8 +152,8 @@ def one_shot_query_batch(index: RbcOneShotIndex, queries, k: int = 1, workers: i
         resolve_workers(workers)
     ids, dists, gamma = one_shot_query_arrays(index, queries, k)
     n_reps = index.reps.size
-    results = [NeighborList(i, ids[i], dists[i]) for i in range(ids.shape[0])]
-    stats = [SearchStats(float(gamma[i]), n_reps, 0, 0, index.s, n_reps) for i in range(ids.shape[0])]
+    results = [NeighborList(i, r_ids, r_d) for i, (r_ids, r_d) in enumerate(zip(ids, dists))]
+    stats = [SearchStats(g, n_reps, 0, 0, index.s, n_reps) for g in gamma.tolist()]
     return results, stats
 
 
